@@ -1,0 +1,101 @@
+"""ctypes binding of the C-ABI library ``libb2s.so`` (declared in include/b2s.h).
+
+This is the only way the package reaches its CUDA kernels. There is no CPU
+fallback: if the library is missing the import of any op raises
+:class:`NativeLibraryMissing` instead of silently computing on the host.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+from ctypes import POINTER, c_char_p, c_int, c_int32, c_int64, c_uint64, c_void_p, c_float
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libb2s.so")
+HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "b2s.h")
+
+B2S_OK = 0
+B2S_EINVAL = -1
+B2S_ERANGE = -2
+B2S_ECUDA = -3
+B2S_EUNSUPPORTED = -4
+
+
+class NativeLibraryMissing(RuntimeError):
+    """libb2s.so was not built; run ``__graft_entry__.build()``."""
+
+
+class B2SError(RuntimeError):
+    """A C-ABI call returned a non-zero status."""
+
+    def __init__(self, fn: str, code: int, msg: str):
+        super().__init__(f"{fn} failed ({code}): {msg}")
+        self.code = code
+
+
+_lib = None
+
+# Argument signatures of every exported function, keyed by name. `p` = pointer
+# (device or host; passed as int), `i` = int, `l` = int64, `u` = uint64, `f` = float.
+_SIGS = {
+    "b2s_abi_version": "",
+    "b2s_token_width_for_vocab": "up",
+    "b2s_sample_count": "ulp",
+    "b2s_splitmix64": "uup",
+    "b2s_make_permutation": "uup",
+    "b2s_chunk_bounds": "uup",
+    "b2s_gather_samples": "piupilpppp",
+}
+
+_CT = {"p": c_void_p, "i": c_int, "l": c_int64, "u": c_uint64, "f": c_float}
+
+
+def load():
+    """Load libb2s.so once and attach argtypes. Raises if the library is absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise NativeLibraryMissing(
+            f"{LIB_PATH} not found: the CUDA path has no fallback; build it with "
+            "`python -c 'import __graft_entry__ as g; g.build()'`"
+        )
+    lib = ctypes.CDLL(LIB_PATH)
+    lib.b2s_last_error.restype = c_char_p
+    lib.b2s_last_error.argtypes = []
+    for name, sig in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.restype = c_int
+        fn.argtypes = [_CT[c] for c in sig]
+    _lib = lib
+    return lib
+
+
+def call(name: str, *args) -> None:
+    """Invoke ``name``; raise :class:`B2SError` on a non-zero status."""
+    lib = load()
+    rc = getattr(lib, name)(*args)
+    if rc != B2S_OK:
+        raise B2SError(name, rc, lib.b2s_last_error().decode(errors="replace"))
+
+
+def last_error() -> str:
+    return load().b2s_last_error().decode(errors="replace")
+
+
+def declared_symbols() -> list[str]:
+    """Function names declared in include/b2s.h (used by the ABI export test)."""
+    with open(HEADER_PATH) as f:
+        text = f.read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(b2s_[a-z0-9_]+)\s*\(", text)))
+
+
+def stream_ptr(stream=None) -> int:
+    """cudaStream_t of ``stream`` (default: torch's current stream) as an int."""
+    import torch
+
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
