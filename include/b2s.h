@@ -76,6 +76,23 @@ int b2s_gather_samples(const void* d_payload, int width, uint64_t token_count,
                        int64_t* d_inputs, int64_t* d_targets, int32_t* d_status,
                        b2s_stream_t stream);
 
+
+/* ------------------------------------------------------------------ */
+/* Dense contractions (K5): tcgen05 + TMEM + TMA, persistent           */
+/* ------------------------------------------------------------------ */
+
+/* C[M,N] = epi( sum_k A(m,k) B(n,k) ), bf16 operands, fp32 accumulation.
+ * A: a_mn_major=0 -> row-major [M][lda] (K contiguous); 1 -> [K][lda] (M contiguous).
+ * B: b_mn_major=0 -> row-major [N][ldb];                 1 -> [K][ldb] (N contiguous).
+ * C: row-major [M][ldc], fp32 if c_f32 else bf16; accumulate!=0 adds into C.
+ * d_bias: optional bf16 [N] added before the activation.
+ * act: 0 none; 1 GELU-tanh (pre-activation written to d_aux as bf16);
+ *      2 multiply by GELU-tanh'(d_aux) (fused activation backward).
+ * Strides must keep rows 16-byte aligned (multiples of 8 bf16). */
+int b2s_gemm(const void* d_A, int a_mn_major, int64_t lda, const void* d_B, int b_mn_major,
+             int64_t ldb, void* d_C, int64_t ldc, int c_f32, int M, int N, int K, int accumulate,
+             const void* d_bias, int act, void* d_aux, int64_t ld_aux, b2s_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

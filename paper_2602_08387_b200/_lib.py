@@ -47,6 +47,7 @@ _SIGS = {
     "b2s_make_permutation": "uup",
     "b2s_chunk_bounds": "uup",
     "b2s_gather_samples": "piupilpppp",
+    "b2s_gemm": "pilpilpliiiiipiplp",
 }
 
 _CT = {"p": c_void_p, "i": c_int, "l": c_int64, "u": c_uint64, "f": c_float}

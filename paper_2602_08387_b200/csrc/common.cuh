@@ -1,5 +1,6 @@
 // Shared helpers for the b2s C-ABI library (sm_100a only).
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <stdint.h>
@@ -89,3 +90,13 @@ inline unsigned ceil_div(uint64_t a, uint64_t b) { return (unsigned)((a + b - 1)
       return (code);                      \
     }                                     \
   } while (0)
+
+namespace b2s {
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+int encode_tma_2d(CUtensorMap* map, const void* base, int elem_bytes, uint64_t inner,
+                  uint64_t outer, uint64_t row_stride_bytes, uint32_t box_inner,
+                  uint32_t box_outer, int swizzle_bytes);
+}  // namespace b2s

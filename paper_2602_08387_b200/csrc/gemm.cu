@@ -1,0 +1,408 @@
+// Persistent warp-specialised tcgen05 GEMM for sm_100a (K5).
+//
+//   C[M,N] = epilogue( sum_k A(m,k) * B(n,k) )
+//
+// A and B are bf16 and each may be K-major (row-major [M][K] / [N][K]) or
+// MN-major ([K][M] / [K][N]); that covers forward (X W^T), dgrad (dY W) and
+// wgrad (dY^T X) of a row-major nn.Linear without any transpose kernel.
+//
+// Roles (192 threads): warp0 = TMA producer, warp1 = TMEM owner + MMA issuer,
+// warps 2..5 = epilogue. Operand tiles are staged by TMA into 128B-swizzled
+// shared memory (kStages-deep ring of full/empty mbarriers); the fp32
+// accumulator lives in TMEM, double-buffered so the epilogue of tile i
+// overlaps the MMAs of tile i+1. The epilogue moves 32x32 sub-tiles
+// TMEM -> registers (bias / GELU / dGELU applied there) -> swizzled smem ->
+// TMA store (or TMA add-reduce when accumulating), so global writes are
+// full-line and asynchronous. Grid = #SMs, tiles strided over CTAs.
+#include <mutex>
+#include "common.cuh"
+#include "sm100.cuh"
+
+namespace b2s {
+using namespace sm100;
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+// 2-D tensor map over a row-major [outer][inner] array (row stride in bytes).
+// Resolved through the runtime so the library needs no -lcuda at link time.
+int encode_tma_2d(CUtensorMap* map, const void* base, int elem_bytes, uint64_t inner,
+                  uint64_t outer, uint64_t row_stride_bytes, uint32_t box_inner,
+                  uint32_t box_outer, int swizzle_bytes) {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  if (!fn) { set_error("cuTensorMapEncodeTiled unavailable"); return B2S_ECUDA; }
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {row_stride_bytes};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUtensorMapSwizzle sw = swizzle_bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                        : swizzle_bytes == 64  ? CU_TENSOR_MAP_SWIZZLE_64B
+                        : swizzle_bytes == 32  ? CU_TENSOR_MAP_SWIZZLE_32B
+                                               : CU_TENSOR_MAP_SWIZZLE_NONE;
+  CUtensorMapDataType dt = elem_bytes == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  CUresult r = fn(map, dt, 2, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) { set_error("cuTensorMapEncodeTiled failed (%d)", (int)r); return B2S_ECUDA; }
+  return B2S_OK;
+}
+
+namespace gemm {
+
+constexpr int BM = 128;
+constexpr int BK = 64;  // 64 bf16 = 128 B = one swizzle row
+constexpr int UMMA_K = 16;
+constexpr int kThreads = 192;
+constexpr int kEpiWarps = 4;
+constexpr int kStageSlot = 4096;  // one 32x32 fp32 (or bf16) staging sub-tile
+constexpr int kEpiSmem = kEpiWarps * 2 * kStageSlot;
+
+struct Epi {
+  int out_f32;                // 1: fp32 output, 0: bf16
+  int accumulate;             // C += result (TMA add-reduce)
+  const __nv_bfloat16* bias;  // [N] or null
+  int act;                    // 0 none, 1 gelu-tanh (aux <- pre-activation), 2 x gelu'(aux)
+  const __nv_bfloat16* aux_in;  // act=2: [M, ld_aux]
+  int64_t ld_aux;
+};
+
+__device__ __forceinline__ float gelu_tanh(float x) {
+  const float k0 = 0.7978845608028654f, k1 = 0.044715f;
+  float u = k0 * (x + k1 * x * x * x);
+  return 0.5f * x * (1.f + tanhf(u));
+}
+__device__ __forceinline__ float gelu_tanh_grad(float x) {
+  const float k0 = 0.7978845608028654f, k1 = 0.044715f;
+  float x2 = x * x;
+  float u = k0 * (x + k1 * x2 * x);
+  float t = tanhf(u);
+  return 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * k0 * (1.f + 3.f * k1 * x2);
+}
+
+template <int BN>
+struct Cfg {
+  static constexpr int kABytes = BM * BK * 2;
+  static constexpr int kBBytes = BN * BK * 2;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kStages = (BN == 256) ? 4 : 6;
+  static constexpr int kTmemCols = 2 * BN;  // double-buffered accumulator
+  static constexpr int kSmem = kStages * kStageBytes + kEpiSmem + 1024 /*align*/ + 256 /*barriers*/;
+  static_assert(kSmem <= 227 * 1024, "smem budget");
+};
+
+// Stage one 32x32 sub-tile (row `lane` of this warp) into swizzled smem.
+// bf16 rows are 64 B (TMA SWIZZLE_64B), fp32 rows 128 B (SWIZZLE_128B); the
+// XOR below is the same address permutation the tensor map applies.
+__device__ __forceinline__ void stage_bf16(uint8_t* buf, int lane, const float* v) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    uint4 w;
+    w.x = pack_bf16x2(v[8 * c + 0], v[8 * c + 1]);
+    w.y = pack_bf16x2(v[8 * c + 2], v[8 * c + 3]);
+    w.z = pack_bf16x2(v[8 * c + 4], v[8 * c + 5]);
+    w.w = pack_bf16x2(v[8 * c + 6], v[8 * c + 7]);
+    const int pc = c ^ ((lane >> 1) & 3);
+    *reinterpret_cast<uint4*>(buf + lane * 64 + pc * 16) = w;
+  }
+}
+__device__ __forceinline__ void stage_f32(uint8_t* buf, int lane, const float* v) {
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const int pc = c ^ (lane & 7);
+    *reinterpret_cast<float4*>(buf + lane * 128 + pc * 16) =
+        make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+  }
+}
+
+template <int BN, bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmAux,
+                int M, int N, int K, int splits, Epi epi) {
+  using C_ = Cfg<BN>;
+  constexpr uint32_t kIdesc = make_idesc_bf16(BM, BN, A_MN, B_MN);
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* epi_smem = smem + C_::kStages * C_::kStageBytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(epi_smem + kEpiSmem);
+  uint64_t* empty = full + C_::kStages;
+  uint64_t* tfull = empty + C_::kStages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int num_m = (M + BM - 1) / BM, num_n = (N + BN - 1) / BN;
+  const int num_tiles = num_m * num_n * splits;  // split-K tiles add-reduce into C
+  const int num_kb_all = (K + BK - 1) / BK;
+  const int kb_per = (num_kb_all + splits - 1) / splits;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    tma_prefetch(&tmC);
+    for (int s = 0; s < C_::kStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], kEpiWarps); }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<C_::kTmemCols>(tmem_base_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_base_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------ TMA producer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int mn = tile % (num_m * num_n), ks = tile / (num_m * num_n);
+        const int m0 = (mn % num_m) * BM, n0 = (mn / num_m) * BN;
+        const int kb0 = ks * kb_per, kb1 = min(num_kb_all, kb0 + kb_per);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * C_::kStageBytes;
+          uint8_t* sb = sa + C_::kABytes;
+          const int k0 = kb * BK;
+          if constexpr (A_MN) {
+#pragma unroll
+            for (int j = 0; j < BM / 64; ++j) tma_load_2d(sa + j * (64 * BK * 2), &tmA, &full[stage], m0 + 64 * j, k0);
+          } else {
+            tma_load_2d(sa, &tmA, &full[stage], k0, m0);
+          }
+          if constexpr (B_MN) {
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j) tma_load_2d(sb + j * (64 * BK * 2), &tmB, &full[stage], n0 + 64 * j, k0);
+          } else {
+            tma_load_2d(sb, &tmB, &full[stage], k0, n0);
+          }
+          mbar_arrive_expect_tx(&full[stage], C_::kStageBytes);
+          if (++stage == C_::kStages) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        const int ks = tile / (num_m * num_n);
+        const int kb0 = ks * kb_per, kb1 = min(num_kb_all, kb0 + kb_per);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * C_::kStageBytes);
+          const uint32_t sb = sa + C_::kABytes;
+#pragma unroll
+          for (int kk = 0; kk < BK / UMMA_K; ++kk) {
+            uint64_t ad, bd;
+            if constexpr (A_MN) ad = make_sdesc(sa + kk * (UMMA_K * 128), 64 * BK * 2, 1024);
+            else ad = make_sdesc(sa + kk * (UMMA_K * 2), 16, 1024);
+            if constexpr (B_MN) bd = make_sdesc(sb + kk * (UMMA_K * 128), 64 * BK * 2, 1024);
+            else bd = make_sdesc(sb + kk * (UMMA_K * 2), 16, 1024);
+            mma_bf16_ss(d_tmem, ad, bd, kIdesc, (kb > kb0 || kk) ? 1u : 0u);
+          }
+          mma_commit(&empty[stage]);  // frees the smem slot once these MMAs retire
+          if (++stage == C_::kStages) { stage = 0; phase ^= 1; }
+        }
+        mma_commit(&tfull[acc]);  // accumulator ready for the epilogue
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+    __syncwarp();
+  } else {
+    // ------------------------------------------------ epilogue warps 2..5
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    uint8_t* ring = epi_smem + (warp - 2) * 2 * kStageSlot;
+    int slot = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    // Hand the next staging slot to this warp: the bulk store issued from it
+    // two jobs ago must have finished reading smem.
+    auto next_slot = [&]() -> uint8_t* {
+      if (lane == 0) bulk_wait_read<1>();
+      __syncwarp();
+      uint8_t* b = ring + slot * kStageSlot;
+      slot ^= 1;
+      return b;
+    };
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      const int mn = tile % (num_m * num_n);
+      const int m0 = (mn % num_m) * BM, n0 = (mn / num_m) * BN;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const int rbase = m0 + q * 32;
+      const int row = rbase + lane;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        const int col0 = n0 + c * 32;
+        uint32_t r[32];
+        tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, r);
+        tmem_wait_ld();
+        if (c == BN / 32 - 1) {  // accumulator fully read: release it to the MMA warp
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[acc]);
+        }
+        if (rbase >= M || col0 >= N) continue;  // warp-uniform
+        float v[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+        if (epi.bias) {
+#pragma unroll
+          for (int i = 0; i < 32; i += 8) {
+            if (col0 + i < N) {
+              float bb[8];
+              unpack8(*reinterpret_cast<const bf16x8*>(epi.bias + col0 + i), bb);
+#pragma unroll
+              for (int j = 0; j < 8; ++j) v[i + j] += bb[j];
+            }
+          }
+        }
+        if (epi.act == 1) {
+          uint8_t* b = next_slot();
+          stage_bf16(b, lane, v);
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) { tma_store_2d(&tmAux, b, col0, rbase); bulk_commit(); }
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = gelu_tanh(__bfloat162float(__float2bfloat16_rn(v[i])));
+        } else if (epi.act == 2 && row < M) {
+          const __nv_bfloat16* ap = epi.aux_in + (int64_t)row * epi.ld_aux + col0;
+#pragma unroll
+          for (int i = 0; i < 32; i += 8) {
+            if (col0 + i < N) {
+              float h[8];
+              unpack8(*reinterpret_cast<const bf16x8*>(ap + i), h);
+#pragma unroll
+              for (int j = 0; j < 8; ++j) v[i + j] *= gelu_tanh_grad(h[j]);
+            }
+          }
+        }
+        uint8_t* b = next_slot();
+        if (epi.out_f32) stage_f32(b, lane, v);
+        else stage_bf16(b, lane, v);
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          if (epi.accumulate) tma_reduce_add_2d(&tmC, b, col0, rbase);
+          else tma_store_2d(&tmC, b, col0, rbase);
+          bulk_commit();
+        }
+      }
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+    if (lane == 0) bulk_wait<0>();
+    __syncwarp();
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<C_::kTmemCols>(tmem_base);
+  }
+}
+
+template <int BN, bool A_MN, bool B_MN>
+static int launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc,
+                  const CUtensorMap& tx, int M, int N, int K, int splits, const Epi& e, cudaStream_t st) {
+  using C_ = Cfg<BN>;
+  auto kern = gemm_kernel<BN, A_MN, B_MN>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::kSmem);
+    attr_set = true;
+  }
+  const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN) * splits;
+  const int grid = tiles < kNumSMs ? tiles : kNumSMs;
+  kern<<<grid, kThreads, C_::kSmem, st>>>(ta, tb, tc, tx, M, N, K, splits, e);
+  return check_launch("gemm");
+}
+
+template <int BN>
+static int dispatch(bool amn, bool bmn, const CUtensorMap& ta, const CUtensorMap& tb,
+                    const CUtensorMap& tc, const CUtensorMap& tx, int M, int N, int K,
+                    int splits, const Epi& e, cudaStream_t st) {
+  if (!amn && !bmn) return launch<BN, false, false>(ta, tb, tc, tx, M, N, K, splits, e, st);
+  if (!amn && bmn) return launch<BN, false, true>(ta, tb, tc, tx, M, N, K, splits, e, st);
+  if (amn && !bmn) return launch<BN, true, false>(ta, tb, tc, tx, M, N, K, splits, e, st);
+  return launch<BN, true, true>(ta, tb, tc, tx, M, N, K, splits, e, st);
+}
+
+// Pick the N tile: 256 unless 128 fills the 148 SMs' last wave much better.
+static int pick_bn(int M, int N) {
+  auto eff = [&](int bn) {
+    long t = (long)((M + BM - 1) / BM) * ((N + bn - 1) / bn);
+    long waves = (t + kNumSMs - 1) / kNumSMs;
+    double pad = (double)N / (double)(((N + bn - 1) / bn) * bn);
+    return pad * (double)t / (double)(waves * kNumSMs);
+  };
+  return eff(128) > eff(256) * 1.08 ? 128 : 256;
+}
+
+}  // namespace gemm
+}  // namespace b2s
+
+extern "C" int b2s_gemm(const void* d_A, int a_mn_major, int64_t lda, const void* d_B,
+                        int b_mn_major, int64_t ldb, void* d_C, int64_t ldc, int c_f32, int M,
+                        int N, int K, int accumulate, const void* d_bias, int act, void* d_aux,
+                        int64_t ld_aux, b2s_stream_t stream) {
+  using namespace b2s;
+  B2S_REQUIRE(M > 0 && N > 0 && K > 0, B2S_EINVAL, "gemm: empty shape %d x %d x %d", M, N, K);
+  B2S_REQUIRE(d_A && d_B && d_C, B2S_EINVAL, "gemm: null operand");
+  B2S_REQUIRE((lda * 2) % 16 == 0 && (ldb * 2) % 16 == 0, B2S_EUNSUPPORTED,
+              "gemm: operand row strides must be multiples of 8 elements");
+  B2S_REQUIRE(((uintptr_t)d_A % 16) == 0 && ((uintptr_t)d_B % 16) == 0 && ((uintptr_t)d_C % 16) == 0,
+              B2S_EUNSUPPORTED, "gemm: operands must be 16-byte aligned");
+  B2S_REQUIRE((ldc * (c_f32 ? 4 : 2)) % 16 == 0 && N % 8 == 0, B2S_EUNSUPPORTED,
+              "gemm: N and ldc must keep output rows 16B aligned");
+  B2S_REQUIRE(act == 0 || ((act == 1 || act == 2) && d_aux && !c_f32 && (ld_aux * 2) % 16 == 0 &&
+                           ((uintptr_t)d_aux % 16) == 0),
+              B2S_EINVAL, "gemm: activation epilogue needs an aligned bf16 aux buffer and bf16 output");
+  B2S_REQUIRE(!(accumulate && act == 1), B2S_EINVAL, "gemm: accumulate with GELU is not supported");
+  const int bn = gemm::pick_bn(M, N);
+  CUtensorMap ta, tb, tc, tx;
+  int rc;
+  if (a_mn_major) rc = encode_tma_2d(&ta, d_A, 2, (uint64_t)M, (uint64_t)K, (uint64_t)lda * 2, 64, gemm::BK, 128);
+  else rc = encode_tma_2d(&ta, d_A, 2, (uint64_t)K, (uint64_t)M, (uint64_t)lda * 2, gemm::BK, gemm::BM, 128);
+  if (rc) return rc;
+  if (b_mn_major) rc = encode_tma_2d(&tb, d_B, 2, (uint64_t)N, (uint64_t)K, (uint64_t)ldb * 2, 64, gemm::BK, 128);
+  else rc = encode_tma_2d(&tb, d_B, 2, (uint64_t)K, (uint64_t)N, (uint64_t)ldb * 2, gemm::BK, (uint32_t)bn, 128);
+  if (rc) return rc;
+  if (c_f32) rc = encode_tma_2d(&tc, d_C, 4, (uint64_t)N, (uint64_t)M, (uint64_t)ldc * 4, 32, 32, 128);
+  else rc = encode_tma_2d(&tc, d_C, 2, (uint64_t)N, (uint64_t)M, (uint64_t)ldc * 2, 32, 32, 64);
+  if (rc) return rc;
+  if (act == 1) rc = encode_tma_2d(&tx, d_aux, 2, (uint64_t)N, (uint64_t)M, (uint64_t)ld_aux * 2, 32, 32, 64);
+  else tx = tc;
+  if (rc) return rc;
+  gemm::Epi e{c_f32, accumulate, (const __nv_bfloat16*)d_bias, act, (const __nv_bfloat16*)d_aux, ld_aux};
+  cudaStream_t st = (cudaStream_t)stream;
+  // Split K when the output has too few tiles to fill the GPU; only legal when
+  // accumulating (the partial sums add-reduce into C through TMA).
+  int splits = 1;
+  if (accumulate && !d_bias && act == 0) {
+    const long tiles = (long)((M + gemm::BM - 1) / gemm::BM) * ((N + bn - 1) / bn);
+    const int nkb = (K + gemm::BK - 1) / gemm::BK;
+    while (tiles * splits * 2 <= 2L * kNumSMs && nkb / (splits * 2) >= 8) splits *= 2;
+  }
+  if (bn == 256) return gemm::dispatch<256>(a_mn_major, b_mn_major, ta, tb, tc, tx, M, N, K, splits, e, st);
+  return gemm::dispatch<128>(a_mn_major, b_mn_major, ta, tb, tc, tx, M, N, K, splits, e, st);
+}

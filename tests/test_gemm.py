@@ -1,0 +1,68 @@
+"""tcgen05 GEMM (K5) vs a plain PyTorch fp32 reference of the same contraction."""
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _ref(a, b, a_mn, b_mn):
+    A = a.float().t() if a_mn else a.float()
+    B = b.float() if b_mn else b.float().t()
+    return A @ B
+
+
+SHAPES = [(128, 128, 64), (256, 512, 128), (200, 136, 72), (1000, 776, 264), (384, 2304, 768),
+          (130, 256, 4096), (64, 64, 8)]
+
+
+@pytest.mark.parametrize("a_mn", [False, True])
+@pytest.mark.parametrize("b_mn", [False, True])
+@pytest.mark.parametrize("shape", SHAPES)
+def test_gemm_layouts(cuda, a_mn, b_mn, shape):
+    from paper_2602_08387_b200 import ops
+
+    M, N, K = shape
+    if a_mn and M % 8:
+        pytest.skip("MN-major A needs M % 8 == 0 (row stride alignment)")
+    g = torch.Generator(device="cuda").manual_seed(M * 7 + N * 3 + K)
+    a = torch.randn((K, M) if a_mn else (M, K), device=cuda, generator=g).bfloat16()
+    b = torch.randn((K, N) if b_mn else (N, K), device=cuda, generator=g).bfloat16()
+    ref = _ref(a, b, a_mn, b_mn)
+    c32 = ops.gemm(a, b, a_mn=a_mn, b_mn=b_mn, M=M, N=N, K=K, out_f32=True)
+    torch.testing.assert_close(c32, ref, rtol=1e-4, atol=1e-3 * K ** 0.5)
+    c16 = ops.gemm(a, b, a_mn=a_mn, b_mn=b_mn, M=M, N=N, K=K)
+    torch.testing.assert_close(c16.float(), ref, rtol=1e-2, atol=1e-2 * K ** 0.5)
+
+
+def test_gemm_epilogues(cuda):
+    from paper_2602_08387_b200 import ops
+
+    M, N, K = 300, 520, 192
+    x = torch.randn(M, K, device=cuda).bfloat16()
+    w = torch.randn(N, K, device=cuda).bfloat16() * 0.1
+    bias = torch.randn(N, device=cuda).bfloat16()
+    pre = torch.empty(M, N, device=cuda, dtype=torch.bfloat16)
+    y = ops.linear(x, w, bias=bias, act=1, aux=pre)
+    ref_pre = x.float() @ w.float().t() + bias.float()
+    torch.testing.assert_close(pre.float(), ref_pre, rtol=1e-2, atol=2e-2)
+    torch.testing.assert_close(y.float(), torch.nn.functional.gelu(pre.float(), approximate="tanh"),
+                               rtol=1e-2, atol=2e-2)
+    # dgelu epilogue: dh = (dy @ w2) * gelu'(pre)
+    w2 = torch.randn(K, N, device=cuda).bfloat16() * 0.1
+    dy = torch.randn(M, K, device=cuda).bfloat16()
+    dh = ops.linear_dgrad(dy, w2, act=2, aux=pre)
+    p = pre.float().requires_grad_()
+    torch.nn.functional.gelu(p, approximate="tanh").backward(dy.float() @ w2.float())
+    torch.testing.assert_close(dh.float(), p.grad, rtol=2e-2, atol=5e-2)
+    # accumulate (fp32 and bf16) and wgrad
+    acc = torch.randn(N, K, device=cuda)
+    ref = acc + dy.new_tensor(0).float() + (torch.randn(0, device=cuda).sum())
+    dw = acc.clone()
+    dyy = torch.randn(M, N, device=cuda).bfloat16()
+    ops.linear_wgrad(dyy, x, out=dw, accumulate=True)
+    torch.testing.assert_close(dw, acc + dyy.float().t() @ x.float(), rtol=1e-4, atol=1e-2)
+    res = torch.randn(M, N, device=cuda).bfloat16()
+    out = res.clone()
+    ops.linear(x, w, out=out, accumulate=True)
+    torch.testing.assert_close(out.float(), res.float() + x.float() @ w.float().t(), rtol=1e-2, atol=3e-2)
