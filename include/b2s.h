@@ -93,6 +93,72 @@ int b2s_gemm(const void* d_A, int a_mn_major, int64_t lda, const void* d_B, int 
              int64_t ldb, void* d_C, int64_t ldc, int c_f32, int M, int N, int K, int accumulate,
              const void* d_bias, int act, void* d_aux, int64_t ld_aux, b2s_stream_t stream);
 
+/* ------------------------------------------------------------------ */
+/* Bandwidth-bound kernels (K2-K4, K8-K11); no reference counterpart    */
+/* ------------------------------------------------------------------ */
+/* Hidden sizes D in {128, 768, 1024, 2048, 4096}. x is the fp32 residual
+ * stream [M, D]; normalised outputs are bf16. d_x_copy (optional) receives a
+ * copy of x (forwarding the residual into the next stream buffer). */
+int b2s_layernorm_fwd(const float* d_x, const void* d_g, const void* d_b, void* d_y, float* d_mean,
+                      float* d_rstd, float* d_x_copy, int64_t M, int D, float eps, b2s_stream_t stream);
+int b2s_rmsnorm_fwd(const float* d_x, const void* d_g, void* d_y, float* d_rstd, float* d_x_copy,
+                    int64_t M, int D, float eps, b2s_stream_t stream);
+/* dx (fp32) += norm backward of dy (bf16); d_dx_bf16 (optional) <- bf16(dx);
+ * d_dg / d_db (fp32 [D], optional) += parameter grads. d_work holds
+ * b2s_norm_work_floats(D) floats. */
+int b2s_layernorm_bwd(const float* d_x, const void* d_dy, const void* d_g, const float* d_mean,
+                      const float* d_rstd, float* d_dx, void* d_dx_bf16, float* d_dg, float* d_db,
+                      float* d_work, int64_t M, int D, b2s_stream_t stream);
+int b2s_rmsnorm_bwd(const float* d_x, const void* d_dy, const void* d_g, const float* d_rstd, float* d_dx,
+                    void* d_dx_bf16, float* d_dg, float* d_work, int64_t M, int D, b2s_stream_t stream);
+int64_t b2s_norm_work_floats(int D);
+
+/* d_out[c] (fp32) += sum_r x[r, c] over M rows of a bf16 (x_f32=0) or fp32
+ * [M, ld] array (bias gradients). d_work: b2s_colsum_work_floats(N) floats. */
+int b2s_colsum_accumulate(const void* d_x, int x_f32, int64_t M, int N, int64_t ld, float* d_out,
+                          float* d_work, b2s_stream_t stream);
+int64_t b2s_colsum_work_floats(int N);
+
+/* x[m] = wte[tok[m]] (+ wpe[m % T]) -> fp32 [M, D]; backward scatters dx
+ * into fp32 dwte (atomics) and sums positions into dwpe (optional). */
+int b2s_embedding_fwd(const int64_t* d_tok, const void* d_wte, const void* d_wpe, float* d_x, int64_t M,
+                      int T, int D, b2s_stream_t stream);
+int b2s_embedding_bwd(const int64_t* d_tok, const float* d_dx, float* d_dwte, float* d_dwpe, int B, int T,
+                      int D, b2s_stream_t stream);
+
+/* Rotary embedding in place on the first `nheads` heads (dh wide) of each
+ * [M, ld] bf16 row; rotate-half pairing; tables [T, dh/2] fp32; inverse=1
+ * applies the transposed rotation (backward). */
+int b2s_rope(void* d_qkv, int64_t M, int T, int64_t ld, int nheads, int dh, const float* d_cos,
+             const float* d_sin, int inverse, b2s_stream_t stream);
+
+/* h = silu(gate) * up with gu = [gate | up] (bf16 [M, 2F]); backward writes [dgate | dup]. */
+int b2s_swiglu_fwd(const void* d_gu, void* d_h, int64_t M, int F, b2s_stream_t stream);
+int b2s_swiglu_bwd(const void* d_gu, const void* d_dh, void* d_dgu, int64_t M, int F, b2s_stream_t stream);
+
+/* Per-row softmax cross-entropy over the first V of ld bf16 logits:
+ * d_loss_rows[m] = logsumexp - logit[target]; if write_grad, the logits are
+ * overwritten by (softmax - onehot) * grad_scale (padding columns zeroed). */
+int b2s_cross_entropy(void* d_logits, int64_t ld, int V, const int64_t* d_target, float* d_loss_rows,
+                      float grad_scale, int64_t M, int write_grad, b2s_stream_t stream);
+
+/* d_out[0] = scale * sum(x or x^2), single block, deterministic. */
+int b2s_sum(const float* d_x, int64_t n, int squares, float* d_out, float scale, b2s_stream_t stream);
+/* d_part[b] = partial sum of squares (b < nparts), deterministic stage 1. */
+int b2s_sumsq_partial(const float* d_x, int64_t n, float* d_part, int nparts, b2s_stream_t stream);
+
+/* Fused AdamW over a flat fp32 shard (K10). Gradient clipping by the global
+ * norm is applied on the device: clip = min(1, max_norm/(sqrt(*d_gn2)+1e-6))
+ * (d_gn2 = all-reduced squared grad norm; null or max_norm<=0 disables).
+ * Writes the updated bf16 copy of p (the next all-gather source). d_wd_mask:
+ * per-element u8 (1 = decay) or null (decay all). step is 1-based. */
+int b2s_adamw(float* d_p, float* d_m, float* d_v, const float* d_g, void* d_p_bf16, const uint8_t* d_wd_mask,
+              int64_t n, const float* d_gn2, float max_norm, float lr, float beta1, float beta2, float eps,
+              float wd, int step, b2s_stream_t stream);
+
+int b2s_f32_to_bf16(const float* d_x, void* d_y, int64_t n, float scale, b2s_stream_t stream);
+int b2s_scale_f32(float* d_x, int64_t n, float scale, b2s_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

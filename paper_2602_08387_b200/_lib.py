@@ -48,7 +48,25 @@ _SIGS = {
     "b2s_chunk_bounds": "uup",
     "b2s_gather_samples": "piupilpppp",
     "b2s_gemm": "pilpilpliiiiipiplp",
+    "b2s_layernorm_fwd": "ppppppplifp",
+    "b2s_rmsnorm_fwd": "ppppplifp",
+    "b2s_layernorm_bwd": "pppppppppplip",
+    "b2s_rmsnorm_bwd": "pppppppplip",
+    "b2s_colsum_accumulate": "pililppp",
+    "b2s_embedding_fwd": "ppppliip",
+    "b2s_embedding_bwd": "ppppiiip",
+    "b2s_rope": "pliliippip",
+    "b2s_swiglu_fwd": "pplip",
+    "b2s_swiglu_bwd": "ppplip",
+    "b2s_cross_entropy": "plippflip",
+    "b2s_sum": "plipfp",
+    "b2s_sumsq_partial": "plpip",
+    "b2s_adamw": "pppppplpffffffip",
+    "b2s_f32_to_bf16": "pplfp",
+    "b2s_scale_f32": "plfp",
 }
+# functions returning int64 sizes (not statuses): name -> argument signature
+_SIZE_FNS = {"b2s_norm_work_floats": "i", "b2s_colsum_work_floats": "i"}
 
 _CT = {"p": c_void_p, "i": c_int, "l": c_int64, "u": c_uint64, "f": c_float}
 
@@ -69,6 +87,10 @@ def load():
     for name, sig in _SIGS.items():
         fn = getattr(lib, name)
         fn.restype = c_int
+        fn.argtypes = [_CT[c] for c in sig]
+    for name, sig in _SIZE_FNS.items():
+        fn = getattr(lib, name)
+        fn.restype = c_int64
         fn.argtypes = [_CT[c] for c in sig]
     _lib = lib
     return lib

@@ -1,0 +1,647 @@
+// Bandwidth-bound kernels of the training step (K2-K4, K8-K11): embedding,
+// LayerNorm / RMSNorm, RoPE, SwiGLU, cross-entropy, column sums, AdamW,
+// grad-norm, casts. All HBM-bound: 16-byte vector accesses, one warp per row
+// for the row-wise ops with the hidden size a compile-time constant (so the
+// row lives in registers), warp-shuffle reductions, deterministic two-stage
+// column reductions (no floating-point atomics except the embedding scatter).
+#include "common.cuh"
+
+namespace b2s {
+namespace ew {
+
+constexpr int kRowThreads = 256;  // 8 warps, one row per warp at a time
+
+__device__ __forceinline__ float4 ld4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+__device__ __forceinline__ void st4(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
+__device__ __forceinline__ void ld_bf4(const __nv_bfloat16* p, float* f) {
+  uint2 u = *reinterpret_cast<const uint2*>(p);
+  float2 a = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&u.x));
+  float2 b = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&u.y));
+  f[0] = a.x; f[1] = a.y; f[2] = b.x; f[3] = b.y;
+}
+__device__ __forceinline__ void st_bf4(__nv_bfloat16* p, const float* f) {
+  uint2 u;
+  u.x = pack_bf16x2(f[0], f[1]);
+  u.y = pack_bf16x2(f[2], f[3]);
+  *reinterpret_cast<uint2*>(p) = u;
+}
+
+
+// ------------------------------------------------------------------ norms
+// y = (x - mean) * rstd * g (+ b)  [LayerNorm]   or   y = x * rstd * g  [RMSNorm]
+// x fp32 [M, D] (the residual stream), y bf16; optional x_copy (forward the
+// residual into the next stream buffer while it is in registers).
+// TPR threads cooperate on a row (32 = one warp for D <= 1024, 256 = the whole
+// block for D >= 2048) so the row stays in registers at every hidden size.
+template <int TPR>
+__device__ __forceinline__ float row_sum(float v, float* scratch) {
+  if constexpr (TPR == 32) return warp_sum(v);
+  else return block_sum(v, scratch);
+}
+
+template <int D, int TPR, bool RMS>
+__global__ void __launch_bounds__(kRowThreads) norm_fwd_kernel(
+    const float* __restrict__ x, const __nv_bfloat16* __restrict__ g, const __nv_bfloat16* __restrict__ b,
+    __nv_bfloat16* __restrict__ y, float* __restrict__ mean_out, float* __restrict__ rstd_out,
+    float* __restrict__ x_copy, int64_t M, float eps) {
+  constexpr int V = D / (TPR * 4);  // float4 vectors per thread
+  static_assert(V * TPR * 4 == D, "hidden size must tile the row threads");
+  __shared__ float scratch[32];
+  const int t = threadIdx.x % TPR;
+  const int64_t r0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / TPR;
+  const int64_t nr = ((int64_t)gridDim.x * blockDim.x) / TPR;
+  float gv[V][4], bv[V][4];
+#pragma unroll
+  for (int j = 0; j < V; ++j) {
+    ld_bf4(g + t * 4 + j * TPR * 4, gv[j]);
+    if (!RMS) ld_bf4(b + t * 4 + j * TPR * 4, bv[j]);
+  }
+  for (int64_t row = r0; row < M; row += nr) {
+    const float* xr = x + row * D;
+    float4 xv[V];
+    float s = 0.f, ss = 0.f;
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      xv[j] = ld4(xr + t * 4 + j * TPR * 4);
+      s += xv[j].x + xv[j].y + xv[j].z + xv[j].w;
+    }
+    if (x_copy) {
+#pragma unroll
+      for (int j = 0; j < V; ++j) st4(x_copy + row * D + t * 4 + j * TPR * 4, xv[j]);
+    }
+    float mean = 0.f;
+    if (!RMS) mean = row_sum<TPR>(s, scratch) * (1.f / D);
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      float a = xv[j].x - mean, c = xv[j].y - mean, d = xv[j].z - mean, e = xv[j].w - mean;
+      ss += a * a + c * c + d * d + e * e;
+    }
+    const float rstd = rsqrtf(row_sum<TPR>(ss, scratch) * (1.f / D) + eps);
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      float o[4] = {(xv[j].x - mean) * rstd, (xv[j].y - mean) * rstd, (xv[j].z - mean) * rstd,
+                    (xv[j].w - mean) * rstd};
+#pragma unroll
+      for (int u = 0; u < 4; ++u) o[u] = RMS ? o[u] * gv[j][u] : o[u] * gv[j][u] + bv[j][u];
+      st_bf4(y + row * D + t * 4 + j * TPR * 4, o);
+    }
+    if (t == 0) {
+      if (!RMS) mean_out[row] = mean;
+      rstd_out[row] = rstd;
+    }
+  }
+}
+
+// Backward. dy bf16 [M,D]; dx fp32 accumulated in place (dx += ...), with a
+// bf16 copy of the updated dx (the next GEMM operand) when dx_bf16 != null.
+// dg/db partial sums per block into part[blockIdx][2][D] (db only for LN).
+template <int D, int TPR, bool RMS>
+__global__ void __launch_bounds__(kRowThreads) norm_bwd_kernel(
+    const float* __restrict__ x, const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ g,
+    const float* __restrict__ mean_in, const float* __restrict__ rstd_in, float* __restrict__ dx,
+    __nv_bfloat16* __restrict__ dx_bf16, float* __restrict__ part, int64_t M) {
+  constexpr int V = D / (TPR * 4);
+  constexpr int kGroups = kRowThreads / TPR;  // rows processed concurrently by the block
+  constexpr int kChunk = 1024;                // columns reduced per smem pass
+  __shared__ float red[kGroups][kChunk];
+  __shared__ float scratch[32];
+  const int t = threadIdx.x % TPR, grp = threadIdx.x / TPR;
+  const int64_t r0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / TPR;
+  const int64_t nr = ((int64_t)gridDim.x * blockDim.x) / TPR;
+  float gv[V][4], dg[V][4], db[V][4];
+#pragma unroll
+  for (int j = 0; j < V; ++j) {
+    ld_bf4(g + t * 4 + j * TPR * 4, gv[j]);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) { dg[j][u] = 0.f; db[j][u] = 0.f; }
+  }
+  // rows per group are equal for every group except the tail; loop bound must
+  // be uniform across the block when TPR spans the block (block_sum syncs)
+  for (int64_t row = r0; row < M; row += nr) {
+    const float mean = RMS ? 0.f : mean_in[row];
+    const float rstd = rstd_in[row];
+    float xh[V][4], dyg[V][4];
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      float4 xv = ld4(x + row * D + t * 4 + j * TPR * 4);
+      float d4[4];
+      ld_bf4(dy + row * D + t * 4 + j * TPR * 4, d4);
+      xh[j][0] = (xv.x - mean) * rstd; xh[j][1] = (xv.y - mean) * rstd;
+      xh[j][2] = (xv.z - mean) * rstd; xh[j][3] = (xv.w - mean) * rstd;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        dyg[j][u] = d4[u] * gv[j][u];
+        s1 += dyg[j][u];
+        s2 += dyg[j][u] * xh[j][u];
+        dg[j][u] += d4[u] * xh[j][u];
+        db[j][u] += d4[u];
+      }
+    }
+    s2 = row_sum<TPR>(s2, scratch) * (1.f / D);
+    if (!RMS) s1 = row_sum<TPR>(s1, scratch) * (1.f / D);
+    else s1 = 0.f;
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      float* dxp = dx + row * D + t * 4 + j * TPR * 4;
+      float4 o = ld4(dxp);
+      o.x += rstd * (dyg[j][0] - s1 - xh[j][0] * s2);
+      o.y += rstd * (dyg[j][1] - s1 - xh[j][1] * s2);
+      o.z += rstd * (dyg[j][2] - s1 - xh[j][2] * s2);
+      o.w += rstd * (dyg[j][3] - s1 - xh[j][3] * s2);
+      st4(dxp, o);
+      if (dx_bf16) {
+        float f[4] = {o.x, o.y, o.z, o.w};
+        st_bf4(dx_bf16 + row * D + t * 4 + j * TPR * 4, f);
+      }
+    }
+  }
+  // block-level reduction of dg (then db) over the row groups -> part[block]
+  for (int pass = 0; pass < (RMS ? 1 : 2); ++pass) {
+    for (int c0 = 0; c0 < D; c0 += kChunk) {
+      __syncthreads();
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        const int col = t * 4 + j * TPR * 4;
+        if (col >= c0 && col < c0 + kChunk) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) red[grp][col - c0 + u] = pass == 0 ? dg[j][u] : db[j][u];
+        }
+      }
+      __syncthreads();
+      for (int c = threadIdx.x; c < kChunk && c0 + c < D; c += blockDim.x) {
+        float acc = 0.f;
+#pragma unroll
+        for (int w = 0; w < kGroups; ++w) acc += red[w][c];
+        part[((int64_t)blockIdx.x * 2 + pass) * D + c0 + c] = acc;
+      }
+    }
+  }
+}
+
+// out[c] += sum_b part[b][which][c]  (deterministic second stage)
+__global__ void reduce_parts_kernel(const float* __restrict__ part, int nblocks, int D, int which,
+                                    float* __restrict__ out) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < D; c += gridDim.x * blockDim.x) {
+    float acc = 0.f;
+    for (int b = 0; b < nblocks; ++b) acc += part[((int64_t)b * 2 + which) * D + c];
+    out[c] += acc;
+  }
+}
+
+// ------------------------------------------------------------------ column sums
+// part[blockIdx.y][c] = sum over this block's rows of x[r][c] (bf16 or fp32 x).
+template <typename T>
+__global__ void colsum_kernel(const T* __restrict__ x, int64_t M, int N, int64_t ld, int rows_per,
+                              float* __restrict__ part) {
+  const int c = (blockIdx.x * blockDim.x + threadIdx.x) * 2;
+  if (c >= N) return;
+  const int64_t r0 = (int64_t)blockIdx.y * rows_per;
+  const int64_t r1 = min(M, r0 + rows_per);
+  float a0 = 0.f, a1 = 0.f;
+  for (int64_t r = r0; r < r1; ++r) {
+    if constexpr (sizeof(T) == 2) {
+      float2 v = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(x + r * ld + c));
+      a0 += v.x; a1 += v.y;
+    } else {
+      float2 v = *reinterpret_cast<const float2*>(x + r * ld + c);
+      a0 += v.x; a1 += v.y;
+    }
+  }
+  part[(int64_t)blockIdx.y * N + c] = a0;
+  if (c + 1 < N) part[(int64_t)blockIdx.y * N + c + 1] = a1;
+}
+__global__ void colsum_final_kernel(const float* __restrict__ part, int nparts, int N, float* __restrict__ out) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < N; c += gridDim.x * blockDim.x) {
+    float acc = 0.f;
+    for (int p = 0; p < nparts; ++p) acc += part[(int64_t)p * N + c];
+    out[c] += acc;
+  }
+}
+
+// ------------------------------------------------------------------ embedding
+// x[m, :] = wte[tok[m], :] (+ wpe[m % T, :]), fp32 out.
+__global__ void embed_fwd_kernel(const int64_t* __restrict__ tok, const __nv_bfloat16* __restrict__ wte,
+                                 const __nv_bfloat16* __restrict__ wpe, float* __restrict__ x, int64_t M,
+                                 int T, int D) {
+  const int vec = D / 4;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < M * vec;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t m = i / vec;
+    const int c = (int)(i - m * vec) * 4;
+    float f[4];
+    ld_bf4(wte + tok[m] * D + c, f);
+    if (wpe) {
+      float p[4];
+      ld_bf4(wpe + (int64_t)(m % T) * D + c, p);
+      f[0] += p[0]; f[1] += p[1]; f[2] += p[2]; f[3] += p[3];
+    }
+    st4(x + m * D + c, make_float4(f[0], f[1], f[2], f[3]));
+  }
+}
+// dwte[tok[m]] += dx[m]  (fp32 atomics: rows collide only on repeated tokens)
+__global__ void embed_bwd_tok_kernel(const int64_t* __restrict__ tok, const float* __restrict__ dx,
+                                     float* __restrict__ dwte, int64_t M, int D) {
+  const int vec = D / 4;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < M * vec;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t m = i / vec;
+    const int c = (int)(i - m * vec) * 4;
+    float4 v = ld4(dx + m * D + c);
+    float* o = dwte + tok[m] * D + c;
+    atomicAdd(reinterpret_cast<float4*>(o), v);
+  }
+}
+// dwpe[t] += sum_b dx[b*T + t]  (deterministic)
+__global__ void embed_bwd_pos_kernel(const float* __restrict__ dx, float* __restrict__ dwpe, int B, int T, int D) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (int64_t)T * D;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = i / D;
+    const int c = (int)(i - t * D);
+    float acc = 0.f;
+    for (int b = 0; b < B; ++b) acc += dx[((int64_t)b * T + t) * D + c];
+    dwpe[i] += acc;
+  }
+}
+
+// ------------------------------------------------------------------ RoPE
+// In place on the q and k heads of a [M, ld] bf16 buffer, rotate-half pairing
+// (i, i + dh/2) as in Llama: (a, b) -> (a cos - b sin, b cos + a sin).
+// inverse=1 applies the transpose rotation (backward).
+__global__ void rope_kernel(__nv_bfloat16* __restrict__ qkv, int64_t M, int T, int64_t ld, int nheads,
+                            int dh, const float* __restrict__ cos_t, const float* __restrict__ sin_t,
+                            int inverse) {
+  const int half = dh / 2;
+  const int64_t per_row = (int64_t)nheads * half;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < M * per_row;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t m = i / per_row;
+    const int r = (int)(i - m * per_row);
+    const int h = r / half, j = r - h * half;
+    const int t = (int)(m % T);
+    const float c = cos_t[t * half + j], s = inverse ? -sin_t[t * half + j] : sin_t[t * half + j];
+    __nv_bfloat16* p = qkv + m * ld + (int64_t)h * dh;
+    const float a = bf2f(p[j]), b = bf2f(p[j + half]);
+    p[j] = f2bf(a * c - b * s);
+    p[j + half] = f2bf(b * c + a * s);
+  }
+}
+
+// ------------------------------------------------------------------ SwiGLU
+// gu [M, 2F] (gate | up), h [M, F] = silu(gate) * up
+__global__ void swiglu_fwd_kernel(const __nv_bfloat16* __restrict__ gu, __nv_bfloat16* __restrict__ h,
+                                  int64_t M, int F) {
+  const int vec = F / 8;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < M * vec;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t m = i / vec;
+    const int c = (int)(i - m * vec) * 8;
+    float g[8], u[8], o[8];
+    unpack8(*reinterpret_cast<const bf16x8*>(gu + m * 2 * F + c), g);
+    unpack8(*reinterpret_cast<const bf16x8*>(gu + m * 2 * F + F + c), u);
+#pragma unroll
+    for (int t = 0; t < 8; ++t) o[t] = g[t] / (1.f + __expf(-g[t])) * u[t];
+    *reinterpret_cast<bf16x8*>(h + m * F + c) = pack8(o);
+  }
+}
+// dgu = [dgate | dup] from dh and the saved gu
+__global__ void swiglu_bwd_kernel(const __nv_bfloat16* __restrict__ gu, const __nv_bfloat16* __restrict__ dh,
+                                  __nv_bfloat16* __restrict__ dgu, int64_t M, int F) {
+  const int vec = F / 8;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < M * vec;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t m = i / vec;
+    const int c = (int)(i - m * vec) * 8;
+    float g[8], u[8], d[8], dg[8], du[8];
+    unpack8(*reinterpret_cast<const bf16x8*>(gu + m * 2 * F + c), g);
+    unpack8(*reinterpret_cast<const bf16x8*>(gu + m * 2 * F + F + c), u);
+    unpack8(*reinterpret_cast<const bf16x8*>(dh + m * F + c), d);
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const float sg = 1.f / (1.f + __expf(-g[t]));
+      const float silu = g[t] * sg;
+      du[t] = d[t] * silu;
+      dg[t] = d[t] * u[t] * sg * (1.f + g[t] * (1.f - sg));
+    }
+    *reinterpret_cast<bf16x8*>(dgu + m * 2 * F + c) = pack8(dg);
+    *reinterpret_cast<bf16x8*>(dgu + m * 2 * F + F + c) = pack8(du);
+  }
+}
+
+// ------------------------------------------------------------------ cross-entropy
+// One block per row of bf16 logits [M, ld] (first V columns valid). Writes
+// loss[m] = logsumexp - logit[target] (fp32) and, in place over the logits,
+// dlogits = (softmax - onehot) * gscale (columns >= V zeroed).
+__global__ void __launch_bounds__(512) xent_kernel(__nv_bfloat16* __restrict__ logits, int64_t ld, int V,
+                                                   const int64_t* __restrict__ target, float* __restrict__ loss,
+                                                   float gscale, int64_t M, int write_grad) {
+  __shared__ float scratch[32];
+  const int64_t m = blockIdx.x;
+  __nv_bfloat16* row = logits + m * ld;
+  const int nvec = V / 8;  // full 8-wide vectors
+  float mx = -INFINITY;
+  for (int i = threadIdx.x; i < nvec; i += blockDim.x) {
+    float f[8];
+    unpack8(*reinterpret_cast<const bf16x8*>(row + i * 8), f);
+#pragma unroll
+    for (int t = 0; t < 8; ++t) mx = fmaxf(mx, f[t]);
+  }
+  for (int c = nvec * 8 + threadIdx.x; c < V; c += blockDim.x) mx = fmaxf(mx, bf2f(row[c]));
+  mx = block_max(mx, scratch);
+  float se = 0.f;
+  for (int i = threadIdx.x; i < nvec; i += blockDim.x) {
+    float f[8];
+    unpack8(*reinterpret_cast<const bf16x8*>(row + i * 8), f);
+#pragma unroll
+    for (int t = 0; t < 8; ++t) se += __expf(f[t] - mx);
+  }
+  for (int c = nvec * 8 + threadIdx.x; c < V; c += blockDim.x) se += __expf(bf2f(row[c]) - mx);
+  se = block_sum(se, scratch);
+  const float lse = mx + __logf(se);
+  const int64_t tgt = target[m];
+  const float xt = bf2f(row[tgt]);
+  __syncthreads();
+  if (threadIdx.x == 0) loss[m] = lse - xt;
+  if (!write_grad) return;
+  const float inv = 1.f / se;
+  for (int i = threadIdx.x; i < nvec; i += blockDim.x) {
+    float f[8];
+    unpack8(*reinterpret_cast<const bf16x8*>(row + i * 8), f);
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const int c = i * 8 + t;
+      f[t] = (__expf(f[t] - mx) * inv - (c == tgt ? 1.f : 0.f)) * gscale;
+    }
+    *reinterpret_cast<bf16x8*>(row + i * 8) = pack8(f);
+  }
+  for (int c = nvec * 8 + threadIdx.x; c < ld; c += blockDim.x) {
+    float g = 0.f;
+    if (c < V) g = (__expf(bf2f(row[c]) - mx) * inv - (c == tgt ? 1.f : 0.f)) * gscale;
+    row[c] = f2bf(g);
+  }
+}
+
+// ------------------------------------------------------------------ reductions
+// Deterministic sum of n floats (optionally of squares) into out[0] (overwrite).
+__global__ void __launch_bounds__(1024) sum_kernel(const float* __restrict__ x, int64_t n, int squares,
+                                                   float* __restrict__ out, float scale) {
+  __shared__ float scratch[32];
+  float acc = 0.f;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) acc += squares ? x[i] * x[i] : x[i];
+  acc = block_sum(acc, scratch);
+  if (threadIdx.x == 0) out[0] = acc * scale;
+}
+// Stage 1 of a deterministic large sum of squares: part[block] = sum x^2.
+__global__ void __launch_bounds__(256) sumsq_part_kernel(const float* __restrict__ x, int64_t n,
+                                                         float* __restrict__ part) {
+  __shared__ float scratch[32];
+  float acc = 0.f;
+  const int64_t nv = n / 4;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += (int64_t)gridDim.x * blockDim.x) {
+    float4 v = ld4(x + i * 4);
+    acc += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+  }
+  for (int64_t i = nv * 4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    acc += x[i] * x[i];
+  acc = block_sum(acc, scratch);
+  if (threadIdx.x == 0) part[blockIdx.x] = acc;
+}
+
+// ------------------------------------------------------------------ AdamW
+// Fused over one flat shard: fp32 master p, m, v, grad g; writes the bf16
+// copy of p (the next step's all-gather source). The global clip factor is
+// computed on the device from the all-reduced grad-norm^2 (no host sync):
+//   clip = min(1, max_norm / (sqrt(gn2) + 1e-6)).
+// Weight decay is applied where wd_mask (per-element u8, or null = all) is set.
+__global__ void __launch_bounds__(256) adamw_kernel(
+    float* __restrict__ p, float* __restrict__ m, float* __restrict__ v, const float* __restrict__ g,
+    __nv_bfloat16* __restrict__ p_bf16, const uint8_t* __restrict__ wd_mask, int64_t n,
+    const float* __restrict__ gn2, float max_norm, float lr, float beta1, float beta2, float eps,
+    float wd, float bc1, float bc2) {
+  float clip = 1.f;
+  if (gn2 && max_norm > 0.f) clip = fminf(1.f, max_norm / (sqrtf(gn2[0]) + 1e-6f));
+  const int64_t nv = n / 4;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += (int64_t)gridDim.x * blockDim.x) {
+    float4 pp = ld4(p + 4 * i), mm = ld4(m + 4 * i), vv = ld4(v + 4 * i), gg = ld4(g + 4 * i);
+    float P[4] = {pp.x, pp.y, pp.z, pp.w}, Mv[4] = {mm.x, mm.y, mm.z, mm.w};
+    float Vv[4] = {vv.x, vv.y, vv.z, vv.w}, G[4] = {gg.x, gg.y, gg.z, gg.w};
+    uint32_t mask = wd_mask ? *reinterpret_cast<const uint32_t*>(wd_mask + 4 * i) : 0x01010101u;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const float gt = G[t] * clip;
+      Mv[t] = beta1 * Mv[t] + (1.f - beta1) * gt;
+      Vv[t] = beta2 * Vv[t] + (1.f - beta2) * gt * gt;
+      const float dec = ((mask >> (8 * t)) & 0xff) ? wd : 0.f;
+      P[t] = P[t] - lr * dec * P[t];
+      P[t] = P[t] - lr * (Mv[t] / bc1) / (sqrtf(Vv[t] / bc2) + eps);
+    }
+    st4(p + 4 * i, make_float4(P[0], P[1], P[2], P[3]));
+    st4(m + 4 * i, make_float4(Mv[0], Mv[1], Mv[2], Mv[3]));
+    st4(v + 4 * i, make_float4(Vv[0], Vv[1], Vv[2], Vv[3]));
+    st_bf4(p_bf16 + 4 * i, P);
+  }
+  for (int64_t i = nv * 4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const float gt = g[i] * clip;
+    const float mi = beta1 * m[i] + (1.f - beta1) * gt;
+    const float vi = beta2 * v[i] + (1.f - beta2) * gt * gt;
+    float pi = p[i];
+    const float dec = (wd_mask ? wd_mask[i] : 1) ? wd : 0.f;
+    pi = pi - lr * dec * pi;
+    pi = pi - lr * (mi / bc1) / (sqrtf(vi / bc2) + eps);
+    p[i] = pi; m[i] = mi; v[i] = vi;
+    p_bf16[i] = f2bf(pi);
+  }
+}
+
+// ------------------------------------------------------------------ casts / scale
+__global__ void f32_to_bf16_kernel(const float* __restrict__ x, __nv_bfloat16* __restrict__ y, int64_t n, float scale) {
+  const int64_t nv = n / 4;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += (int64_t)gridDim.x * blockDim.x) {
+    float4 v = ld4(x + 4 * i);
+    float f[4] = {v.x * scale, v.y * scale, v.z * scale, v.w * scale};
+    st_bf4(y + 4 * i, f);
+  }
+  for (int64_t i = nv * 4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = f2bf(x[i] * scale);
+}
+__global__ void scale_f32_kernel(float* __restrict__ x, int64_t n, float scale) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    x[i] *= scale;
+}
+
+static unsigned flat_grid(int64_t n, int per_thread = 4) {
+  int64_t blocks = (n / per_thread + 255) / 256;
+  if (blocks < 1) blocks = 1;
+  int64_t cap = (int64_t)kNumSMs * 16;
+  return (unsigned)(blocks < cap ? blocks : cap);
+}
+
+template <bool RMS>
+static int norm_fwd(const float* x, const void* g, const void* b, void* y, float* mean, float* rstd,
+                    float* x_copy, int64_t M, int D, float eps, cudaStream_t st) {
+  auto go = [&](auto kern, int tpr) {
+    int64_t blocks = (M * tpr + kRowThreads - 1) / kRowThreads;
+    const int64_t cap = (int64_t)kNumSMs * 8;
+    kern<<<(unsigned)(blocks < cap ? blocks : cap), kRowThreads, 0, st>>>(
+        x, (const __nv_bfloat16*)g, (const __nv_bfloat16*)b, (__nv_bfloat16*)y, mean, rstd, x_copy, M, eps);
+    return check_launch("norm_fwd");
+  };
+  switch (D) {
+    case 128: return go(norm_fwd_kernel<128, 32, RMS>, 32);
+    case 768: return go(norm_fwd_kernel<768, 32, RMS>, 32);
+    case 1024: return go(norm_fwd_kernel<1024, 32, RMS>, 32);
+    case 2048: return go(norm_fwd_kernel<2048, 256, RMS>, 256);
+    case 4096: return go(norm_fwd_kernel<4096, 256, RMS>, 256);
+  }
+  set_error("norm: unsupported hidden size %d", D);
+  return B2S_EUNSUPPORTED;
+}
+
+template <bool RMS>
+static int norm_bwd(const float* x, const void* dy, const void* g, const float* mean, const float* rstd,
+                    float* dx, void* dx_bf16, float* dg, float* db, float* work, int64_t M, int D,
+                    cudaStream_t st) {
+  unsigned grid = 0;
+  auto go = [&](auto kern, int tpr) {
+    int64_t blocks = (M * tpr + kRowThreads - 1) / kRowThreads;
+    grid = (unsigned)(blocks < kNumSMs ? blocks : kNumSMs);  // partial buffer: grid * 2 * D floats
+    kern<<<grid, kRowThreads, 0, st>>>(x, (const __nv_bfloat16*)dy, (const __nv_bfloat16*)g, mean, rstd, dx,
+                                       (__nv_bfloat16*)dx_bf16, work, M);
+    return check_launch("norm_bwd");
+  };
+  int rc;
+  switch (D) {
+    case 128: rc = go(norm_bwd_kernel<128, 32, RMS>, 32); break;
+    case 768: rc = go(norm_bwd_kernel<768, 32, RMS>, 32); break;
+    case 1024: rc = go(norm_bwd_kernel<1024, 32, RMS>, 32); break;
+    case 2048: rc = go(norm_bwd_kernel<2048, 256, RMS>, 256); break;
+    case 4096: rc = go(norm_bwd_kernel<4096, 256, RMS>, 256); break;
+    default:
+      set_error("norm_bwd: unsupported hidden size %d", D);
+      return B2S_EUNSUPPORTED;
+  }
+  if (rc) return rc;
+  const unsigned g2 = (D + 255) / 256;
+  if (dg) reduce_parts_kernel<<<g2, 256, 0, st>>>(work, grid, D, 0, dg);
+  if (!RMS && db) reduce_parts_kernel<<<g2, 256, 0, st>>>(work, grid, D, 1, db);
+  return check_launch("norm_bwd_reduce");
+}
+
+}  // namespace ew
+}  // namespace b2s
+
+using namespace b2s;
+
+extern "C" {
+
+int b2s_layernorm_fwd(const float* d_x, const void* d_g, const void* d_b, void* d_y, float* d_mean,
+                      float* d_rstd, float* d_x_copy, int64_t M, int D, float eps, b2s_stream_t stream) {
+  return ew::norm_fwd<false>(d_x, d_g, d_b, d_y, d_mean, d_rstd, d_x_copy, M, D, eps, (cudaStream_t)stream);
+}
+int b2s_rmsnorm_fwd(const float* d_x, const void* d_g, void* d_y, float* d_rstd, float* d_x_copy,
+                    int64_t M, int D, float eps, b2s_stream_t stream) {
+  return ew::norm_fwd<true>(d_x, d_g, nullptr, d_y, nullptr, d_rstd, d_x_copy, M, D, eps, (cudaStream_t)stream);
+}
+int b2s_layernorm_bwd(const float* d_x, const void* d_dy, const void* d_g, const float* d_mean,
+                      const float* d_rstd, float* d_dx, void* d_dx_bf16, float* d_dg, float* d_db,
+                      float* d_work, int64_t M, int D, b2s_stream_t stream) {
+  return ew::norm_bwd<false>(d_x, d_dy, d_g, d_mean, d_rstd, d_dx, d_dx_bf16, d_dg, d_db, d_work, M, D,
+                             (cudaStream_t)stream);
+}
+int b2s_rmsnorm_bwd(const float* d_x, const void* d_dy, const void* d_g, const float* d_rstd, float* d_dx,
+                    void* d_dx_bf16, float* d_dg, float* d_work, int64_t M, int D, b2s_stream_t stream) {
+  return ew::norm_bwd<true>(d_x, d_dy, d_g, nullptr, d_rstd, d_dx, d_dx_bf16, d_dg, nullptr, d_work, M, D,
+                            (cudaStream_t)stream);
+}
+int64_t b2s_norm_work_floats(int D) { return (int64_t)kNumSMs * 2 * D; }
+
+int b2s_colsum_accumulate(const void* d_x, int x_f32, int64_t M, int N, int64_t ld, float* d_out,
+                          float* d_work, b2s_stream_t stream) {
+  B2S_REQUIRE(N % 2 == 0 && ld % 2 == 0, B2S_EUNSUPPORTED, "colsum: N and ld must be even");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int nparts = 64;
+  const int rows_per = (int)((M + nparts - 1) / nparts);
+  dim3 grid((N / 2 + 127) / 128, nparts);
+  if (x_f32) ew::colsum_kernel<float><<<grid, 128, 0, st>>>((const float*)d_x, M, N, ld, rows_per, d_work);
+  else ew::colsum_kernel<__nv_bfloat16><<<grid, 128, 0, st>>>((const __nv_bfloat16*)d_x, M, N, ld, rows_per, d_work);
+  ew::colsum_final_kernel<<<(N + 255) / 256, 256, 0, st>>>(d_work, nparts, N, d_out);
+  return check_launch("colsum");
+}
+int64_t b2s_colsum_work_floats(int N) { return 64LL * N; }
+
+int b2s_embedding_fwd(const int64_t* d_tok, const void* d_wte, const void* d_wpe, float* d_x, int64_t M,
+                      int T, int D, b2s_stream_t stream) {
+  B2S_REQUIRE(D % 4 == 0, B2S_EUNSUPPORTED, "embedding: D %% 4 != 0");
+  ew::embed_fwd_kernel<<<ew::flat_grid(M * D), 256, 0, (cudaStream_t)stream>>>(
+      d_tok, (const __nv_bfloat16*)d_wte, (const __nv_bfloat16*)d_wpe, d_x, M, T, D);
+  return check_launch("embedding_fwd");
+}
+int b2s_embedding_bwd(const int64_t* d_tok, const float* d_dx, float* d_dwte, float* d_dwpe, int B, int T,
+                      int D, b2s_stream_t stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t M = (int64_t)B * T;
+  ew::embed_bwd_tok_kernel<<<ew::flat_grid(M * D), 256, 0, st>>>(d_tok, d_dx, d_dwte, M, D);
+  if (d_dwpe) ew::embed_bwd_pos_kernel<<<ew::flat_grid((int64_t)T * D, 1), 256, 0, st>>>(d_dx, d_dwpe, B, T, D);
+  return check_launch("embedding_bwd");
+}
+
+int b2s_rope(void* d_qkv, int64_t M, int T, int64_t ld, int nheads, int dh, const float* d_cos,
+             const float* d_sin, int inverse, b2s_stream_t stream) {
+  ew::rope_kernel<<<ew::flat_grid(M * nheads * dh / 2, 1), 256, 0, (cudaStream_t)stream>>>(
+      (__nv_bfloat16*)d_qkv, M, T, ld, nheads, dh, d_cos, d_sin, inverse);
+  return check_launch("rope");
+}
+
+int b2s_swiglu_fwd(const void* d_gu, void* d_h, int64_t M, int F, b2s_stream_t stream) {
+  B2S_REQUIRE(F % 8 == 0, B2S_EUNSUPPORTED, "swiglu: F %% 8 != 0");
+  ew::swiglu_fwd_kernel<<<ew::flat_grid(M * F, 8), 256, 0, (cudaStream_t)stream>>>(
+      (const __nv_bfloat16*)d_gu, (__nv_bfloat16*)d_h, M, F);
+  return check_launch("swiglu_fwd");
+}
+int b2s_swiglu_bwd(const void* d_gu, const void* d_dh, void* d_dgu, int64_t M, int F, b2s_stream_t stream) {
+  B2S_REQUIRE(F % 8 == 0, B2S_EUNSUPPORTED, "swiglu: F %% 8 != 0");
+  ew::swiglu_bwd_kernel<<<ew::flat_grid(M * F, 8), 256, 0, (cudaStream_t)stream>>>(
+      (const __nv_bfloat16*)d_gu, (const __nv_bfloat16*)d_dh, (__nv_bfloat16*)d_dgu, M, F);
+  return check_launch("swiglu_bwd");
+}
+
+int b2s_cross_entropy(void* d_logits, int64_t ld, int V, const int64_t* d_target, float* d_loss_rows,
+                      float grad_scale, int64_t M, int write_grad, b2s_stream_t stream) {
+  B2S_REQUIRE(ld % 8 == 0 && V <= ld, B2S_EUNSUPPORTED, "cross_entropy: ld must be a multiple of 8 >= V");
+  ew::xent_kernel<<<(unsigned)M, 512, 0, (cudaStream_t)stream>>>((__nv_bfloat16*)d_logits, ld, V, d_target,
+                                                                 d_loss_rows, grad_scale, M, write_grad);
+  return check_launch("cross_entropy");
+}
+
+int b2s_sum(const float* d_x, int64_t n, int squares, float* d_out, float scale, b2s_stream_t stream) {
+  ew::sum_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(d_x, n, squares, d_out, scale);
+  return check_launch("sum");
+}
+int b2s_sumsq_partial(const float* d_x, int64_t n, float* d_part, int nparts, b2s_stream_t stream) {
+  ew::sumsq_part_kernel<<<nparts, 256, 0, (cudaStream_t)stream>>>(d_x, n, d_part);
+  return check_launch("sumsq_partial");
+}
+
+int b2s_adamw(float* d_p, float* d_m, float* d_v, const float* d_g, void* d_p_bf16, const uint8_t* d_wd_mask,
+              int64_t n, const float* d_gn2, float max_norm, float lr, float beta1, float beta2, float eps,
+              float wd, int step, b2s_stream_t stream) {
+  B2S_REQUIRE(((uintptr_t)d_p | (uintptr_t)d_m | (uintptr_t)d_v | (uintptr_t)d_g) % 16 == 0 &&
+                  ((uintptr_t)d_p_bf16 % 8) == 0 && (!d_wd_mask || ((uintptr_t)d_wd_mask % 4) == 0),
+              B2S_EUNSUPPORTED, "adamw: misaligned shard");
+  const float bc1 = 1.f - powf(beta1, (float)step), bc2 = 1.f - powf(beta2, (float)step);
+  ew::adamw_kernel<<<ew::flat_grid(n), 256, 0, (cudaStream_t)stream>>>(
+      d_p, d_m, d_v, d_g, (__nv_bfloat16*)d_p_bf16, d_wd_mask, n, d_gn2, max_norm, lr, beta1, beta2, eps, wd,
+      bc1, bc2);
+  return check_launch("adamw");
+}
+
+int b2s_f32_to_bf16(const float* d_x, void* d_y, int64_t n, float scale, b2s_stream_t stream) {
+  ew::f32_to_bf16_kernel<<<ew::flat_grid(n), 256, 0, (cudaStream_t)stream>>>(d_x, (__nv_bfloat16*)d_y, n, scale);
+  return check_launch("f32_to_bf16");
+}
+int b2s_scale_f32(float* d_x, int64_t n, float scale, b2s_stream_t stream) {
+  ew::scale_f32_kernel<<<ew::flat_grid(n, 1), 256, 0, (cudaStream_t)stream>>>(d_x, n, scale);
+  return check_launch("scale_f32");
+}
+
+}  // extern "C"

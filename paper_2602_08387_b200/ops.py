@@ -72,3 +72,134 @@ def linear_wgrad(dy, x, out=None, accumulate=False, out_f32=True):
     K = x.shape[1]
     return gemm(dy, x, a_mn=True, b_mn=True, M=N, N=K, K=M, out=out, out_f32=out_f32,
                 accumulate=accumulate)
+
+
+# ---------------------------------------------------------------------------- norms
+
+
+def _f32(M, D, dev):
+    return torch.empty(M, D, device=dev, dtype=torch.float32)
+
+
+_work_cache: dict = {}
+
+
+def _work(n_floats: int, device):
+    """Reusable per-device scratch for the deterministic reductions."""
+    key = (device.index, "work")
+    buf = _work_cache.get(key)
+    if buf is None or buf.numel() < n_floats:
+        buf = torch.empty(max(n_floats, 1 << 20), device=device, dtype=torch.float32)
+        _work_cache[key] = buf
+    return buf
+
+
+def layernorm_fwd(x, g, b, eps=1e-5, y=None, mean=None, rstd=None, x_copy=None):
+    _dev(x)
+    M, D = x.shape
+    y = torch.empty(M, D, device=x.device, dtype=torch.bfloat16) if y is None else y
+    mean = torch.empty(M, device=x.device) if mean is None else mean
+    rstd = torch.empty(M, device=x.device) if rstd is None else rstd
+    _call("b2s_layernorm_fwd", x.data_ptr(), g.data_ptr(), b.data_ptr(), y.data_ptr(), mean.data_ptr(),
+          rstd.data_ptr(), _ptr(x_copy), M, D, eps, _sp())
+    return y, mean, rstd
+
+
+def rmsnorm_fwd(x, g, eps=1e-5, y=None, rstd=None, x_copy=None):
+    _dev(x)
+    M, D = x.shape
+    y = torch.empty(M, D, device=x.device, dtype=torch.bfloat16) if y is None else y
+    rstd = torch.empty(M, device=x.device) if rstd is None else rstd
+    _call("b2s_rmsnorm_fwd", x.data_ptr(), g.data_ptr(), y.data_ptr(), rstd.data_ptr(), _ptr(x_copy), M, D,
+          eps, _sp())
+    return y, rstd
+
+
+def layernorm_bwd(x, dy, g, mean, rstd, dx, dx_bf16=None, dg=None, db=None):
+    """dx += LN backward; dg/db (fp32) accumulated."""
+    M, D = x.shape
+    work = _work(_lib.load().b2s_norm_work_floats(D), x.device)
+    _call("b2s_layernorm_bwd", x.data_ptr(), dy.data_ptr(), g.data_ptr(), mean.data_ptr(), rstd.data_ptr(),
+          dx.data_ptr(), _ptr(dx_bf16), _ptr(dg), _ptr(db), work.data_ptr(), M, D, _sp())
+
+
+def rmsnorm_bwd(x, dy, g, rstd, dx, dx_bf16=None, dg=None):
+    M, D = x.shape
+    work = _work(_lib.load().b2s_norm_work_floats(D), x.device)
+    _call("b2s_rmsnorm_bwd", x.data_ptr(), dy.data_ptr(), g.data_ptr(), rstd.data_ptr(), dx.data_ptr(),
+          _ptr(dx_bf16), _ptr(dg), work.data_ptr(), M, D, _sp())
+
+
+def colsum_accumulate(x, out):
+    """out[c] += sum_r x[r, c]   (bias gradient)."""
+    M, N = x.shape
+    work = _work(_lib.load().b2s_colsum_work_floats(N), x.device)
+    _call("b2s_colsum_accumulate", x.data_ptr(), int(x.dtype == torch.float32), M, N, x.stride(0),
+          out.data_ptr(), work.data_ptr(), _sp())
+
+
+# ---------------------------------------------------------------------------- misc
+
+
+def embedding_fwd(tok, wte, wpe, T, out=None):
+    M = tok.numel()
+    D = wte.shape[1]
+    out = torch.empty(M, D, device=tok.device) if out is None else out
+    _call("b2s_embedding_fwd", tok.data_ptr(), wte.data_ptr(), _ptr(wpe), out.data_ptr(), M, T, D, _sp())
+    return out
+
+
+def embedding_bwd(tok, dx, dwte, dwpe, B, T):
+    _call("b2s_embedding_bwd", tok.data_ptr(), dx.data_ptr(), dwte.data_ptr(), _ptr(dwpe), B, T, dx.shape[1],
+          _sp())
+
+
+def rope(qkv, T, nheads, dh, cos, sin, inverse=False):
+    M = qkv.shape[0]
+    _call("b2s_rope", qkv.data_ptr(), M, T, qkv.stride(0), nheads, dh, cos.data_ptr(), sin.data_ptr(),
+          int(inverse), _sp())
+
+
+def swiglu_fwd(gu, h=None):
+    M, F2 = gu.shape
+    h = torch.empty(M, F2 // 2, device=gu.device, dtype=torch.bfloat16) if h is None else h
+    _call("b2s_swiglu_fwd", gu.data_ptr(), h.data_ptr(), M, F2 // 2, _sp())
+    return h
+
+
+def swiglu_bwd(gu, dh, dgu=None):
+    M, F2 = gu.shape
+    dgu = torch.empty_like(gu) if dgu is None else dgu
+    _call("b2s_swiglu_bwd", gu.data_ptr(), dh.data_ptr(), dgu.data_ptr(), M, F2 // 2, _sp())
+    return dgu
+
+
+def cross_entropy(logits, V, target, loss_rows=None, grad_scale=1.0, write_grad=True):
+    M = logits.shape[0]
+    loss_rows = torch.empty(M, device=logits.device) if loss_rows is None else loss_rows
+    _call("b2s_cross_entropy", logits.data_ptr(), logits.stride(0), V, target.data_ptr(), loss_rows.data_ptr(),
+          grad_scale, M, int(write_grad), _sp())
+    return loss_rows
+
+
+def sum_(x, out, squares=False, scale=1.0):
+    _call("b2s_sum", x.data_ptr(), x.numel(), int(squares), out.data_ptr(), scale, _sp())
+    return out
+
+
+def sumsq_partial(x, part):
+    _call("b2s_sumsq_partial", x.data_ptr(), x.numel(), part.data_ptr(), part.numel(), _sp())
+
+
+def adamw(p, m, v, g, p_bf16, step, lr, beta1, beta2, eps, wd, gn2=None, max_norm=0.0, wd_mask=None):
+    _call("b2s_adamw", p.data_ptr(), m.data_ptr(), v.data_ptr(), g.data_ptr(), p_bf16.data_ptr(), _ptr(wd_mask),
+          p.numel(), _ptr(gn2), max_norm, lr, beta1, beta2, eps, wd, step, _sp())
+
+
+def f32_to_bf16(x, y, scale=1.0):
+    _call("b2s_f32_to_bf16", x.data_ptr(), y.data_ptr(), x.numel(), scale, _sp())
+    return y
+
+
+def scale_f32(x, scale):
+    _call("b2s_scale_f32", x.data_ptr(), x.numel(), scale, _sp())

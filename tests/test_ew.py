@@ -1,0 +1,160 @@
+"""Bandwidth-bound kernels vs plain PyTorch fp32 references of the same ops."""
+
+import math
+
+import pytest
+import torch
+import torch.nn.functional as F
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("D", [128, 768, 2048, 4096])
+@pytest.mark.parametrize("rms", [False, True])
+def test_norm_fwd_bwd(cuda, D, rms):
+    from paper_2602_08387_b200 import ops
+
+    torch.manual_seed(D)
+    M = 777
+    x = torch.randn(M, D, device=cuda) * 3 + 1
+    g = (1 + 0.1 * torch.randn(D, device=cuda)).bfloat16()
+    b = (0.1 * torch.randn(D, device=cuda)).bfloat16()
+    xc = torch.empty_like(x)
+    if rms:
+        y, rstd = ops.rmsnorm_fwd(x, g, 1e-5, x_copy=xc)
+        xr = x.clone().requires_grad_()
+        ref = xr * torch.rsqrt(xr.pow(2).mean(-1, keepdim=True) + 1e-5) * g.float()
+    else:
+        y, mean, rstd = ops.layernorm_fwd(x, g, b, 1e-5, x_copy=xc)
+        xr = x.clone().requires_grad_()
+        ref = F.layer_norm(xr, (D,), g.float(), b.float(), 1e-5)
+    assert torch.equal(xc, x)
+    torch.testing.assert_close(y.float(), ref, rtol=1e-2, atol=2e-2)
+    dy = torch.randn(M, D, device=cuda).bfloat16()
+    gr = g.float().requires_grad_()
+    if rms:
+        ref2 = xr * torch.rsqrt(xr.pow(2).mean(-1, keepdim=True) + 1e-5) * gr
+        ref2.backward(dy.float())
+    else:
+        br = b.float().requires_grad_()
+        F.layer_norm(xr, (D,), gr, br, 1e-5).backward(dy.float())
+    dx0 = torch.randn(M, D, device=cuda)
+    dx = dx0.clone()
+    dxb = torch.empty(M, D, device=cuda, dtype=torch.bfloat16)
+    dg = torch.zeros(D, device=cuda)
+    if rms:
+        ops.rmsnorm_bwd(x, dy, g, rstd, dx, dxb, dg)
+    else:
+        db = torch.zeros(D, device=cuda)
+        ops.layernorm_bwd(x, dy, g, mean, rstd, dx, dxb, dg, db)
+        torch.testing.assert_close(db, br.grad, rtol=1e-4, atol=1e-3)
+    torch.testing.assert_close(dx, dx0 + xr.grad, rtol=1e-4, atol=1e-4)
+    torch.testing.assert_close(dxb.float(), dx, rtol=1e-2, atol=1e-2)
+    torch.testing.assert_close(dg, gr.grad, rtol=1e-4, atol=1e-3)
+
+
+def test_colsum_embedding(cuda):
+    from paper_2602_08387_b200 import ops
+
+    torch.manual_seed(0)
+    x = torch.randn(1000, 520, device=cuda).bfloat16()
+    out = torch.ones(520, device=cuda)
+    ops.colsum_accumulate(x, out)
+    torch.testing.assert_close(out, 1 + x.float().sum(0), rtol=1e-4, atol=1e-3)
+    B, T, V, D = 3, 17, 50, 128
+    tok = torch.randint(0, V, (B * T,), device=cuda)
+    wte = torch.randn(V, D, device=cuda).bfloat16()
+    wpe = torch.randn(T, D, device=cuda).bfloat16()
+    x = ops.embedding_fwd(tok, wte, wpe, T)
+    ref = wte.float()[tok] + wpe.float().repeat(B, 1)
+    torch.testing.assert_close(x, ref)
+    dx = torch.randn(B * T, D, device=cuda)
+    dwte = torch.zeros(V, D, device=cuda)
+    dwpe = torch.zeros(T, D, device=cuda)
+    ops.embedding_bwd(tok, dx, dwte, dwpe, B, T)
+    torch.testing.assert_close(dwte, torch.zeros(V, D, device=cuda).index_add_(0, tok, dx), rtol=1e-5, atol=1e-5)
+    torch.testing.assert_close(dwpe, dx.view(B, T, D).sum(0), rtol=1e-5, atol=1e-5)
+
+
+def test_rope_swiglu(cuda):
+    from paper_2602_08387_b200 import ops
+
+    torch.manual_seed(1)
+    B, T, Hq, Hkv, dh = 2, 16, 4, 2, 64
+    ld = (Hq + 2 * Hkv) * dh
+    qkv = torch.randn(B * T, ld, device=cuda).bfloat16()
+    inv = 1.0 / (500000.0 ** (torch.arange(0, dh, 2, device=cuda).float() / dh))
+    ang = torch.arange(T, device=cuda).float()[:, None] * inv[None]
+    cos, sin = ang.cos().contiguous(), ang.sin().contiguous()
+    out = qkv.clone()
+    ops.rope(out, T, Hq + Hkv, dh, cos, sin)
+    x = qkv.float().view(B, T, Hq + 2 * Hkv, dh)[:, :, : Hq + Hkv]
+    x1, x2 = x[..., : dh // 2], x[..., dh // 2:]
+    c, s = cos[None, :, None], sin[None, :, None]
+    ref = torch.cat([x1 * c - x2 * s, x2 * c + x1 * s], -1)
+    got = out.float().view(B, T, Hq + 2 * Hkv, dh)
+    torch.testing.assert_close(got[:, :, : Hq + Hkv], ref, rtol=1e-2, atol=2e-2)
+    assert torch.equal(got[:, :, Hq + Hkv:], qkv.float().view(B, T, -1, dh)[:, :, Hq + Hkv:])
+    back = out.clone()
+    ops.rope(back, T, Hq + Hkv, dh, cos, sin, inverse=True)
+    torch.testing.assert_close(back.float(), qkv.float(), rtol=2e-2, atol=3e-2)
+    # swiglu
+    M, Fh = 300, 256
+    gu = torch.randn(M, 2 * Fh, device=cuda).bfloat16()
+    h = ops.swiglu_fwd(gu)
+    g_, u_ = gu.float()[:, :Fh].requires_grad_(), gu.float()[:, Fh:].requires_grad_()
+    ref = F.silu(g_) * u_
+    torch.testing.assert_close(h.float(), ref, rtol=1e-2, atol=1e-2)
+    dh = torch.randn(M, Fh, device=cuda).bfloat16()
+    ref.backward(dh.float())
+    dgu = ops.swiglu_bwd(gu, dh)
+    torch.testing.assert_close(dgu.float()[:, :Fh], g_.grad, rtol=1e-2, atol=2e-2)
+    torch.testing.assert_close(dgu.float()[:, Fh:], u_.grad, rtol=1e-2, atol=2e-2)
+
+
+@pytest.mark.parametrize("V,ld", [(4096, 4096), (50257, 50304), (1000, 1008)])
+def test_cross_entropy(cuda, V, ld):
+    from paper_2602_08387_b200 import ops
+
+    torch.manual_seed(2)
+    M = 64
+    logits = (torch.randn(M, ld, device=cuda) * 2).bfloat16()
+    tgt = torch.randint(0, V, (M,), device=cuda)
+    lf = logits.float()[:, :V].requires_grad_()
+    ref = F.cross_entropy(lf, tgt, reduction="none")
+    ref.sum().div(M).backward()
+    work = logits.clone()
+    loss = ops.cross_entropy(work, V, tgt, grad_scale=1.0 / M)
+    torch.testing.assert_close(loss, ref, rtol=1e-4, atol=1e-4)
+    torch.testing.assert_close(work.float()[:, :V], lf.grad, rtol=1e-2, atol=1e-5)
+    assert torch.all(work[:, V:] == 0)
+
+
+def test_adamw_and_sums(cuda):
+    from paper_2602_08387_b200 import ops
+
+    torch.manual_seed(3)
+    n = 10_003
+    p = torch.randn(n, device=cuda)
+    g = torch.randn(n, device=cuda)
+    m = torch.zeros(n, device=cuda)
+    v = torch.zeros(n, device=cuda)
+    pb = torch.empty(n, device=cuda, dtype=torch.bfloat16)
+    mask = (torch.arange(n, device=cuda) % 3 != 0).to(torch.uint8)
+    ref_p = p.clone().requires_grad_()
+    opt = torch.optim.AdamW([ref_p], lr=1e-2, betas=(0.9, 0.95), eps=1e-8, weight_decay=0.0)
+    gn2 = torch.empty(1, device=cuda)
+    ops.sum_(g, gn2, squares=True)
+    torch.testing.assert_close(gn2, (g * g).sum().view(1), rtol=1e-5, atol=1e-3)
+    clip = min(1.0, 1.0 / (math.sqrt(gn2.item()) + 1e-6))
+    for step in range(1, 4):
+        ops.adamw(p, m, v, g, pb, step, 1e-2, 0.9, 0.95, 1e-8, 0.1, gn2=gn2, max_norm=1.0, wd_mask=mask)
+        with torch.no_grad():
+            ref_p.mul_(1 - 1e-2 * 0.1 * mask.float())
+        ref_p.grad = g * clip
+        opt.step()
+    torch.testing.assert_close(p, ref_p.detach(), rtol=1e-5, atol=1e-6)
+    torch.testing.assert_close(pb.float(), p, rtol=1e-2, atol=1e-2)
+    part = torch.empty(37, device=cuda)
+    ops.sumsq_partial(g, part)
+    torch.testing.assert_close(part.sum(), (g * g).sum(), rtol=1e-5, atol=1e-3)
