@@ -159,6 +159,22 @@ int b2s_adamw(float* d_p, float* d_m, float* d_v, const float* d_g, void* d_p_bf
 int b2s_f32_to_bf16(const float* d_x, void* d_y, int64_t n, float scale, b2s_stream_t stream);
 int b2s_scale_f32(float* d_x, int64_t n, float scale, b2s_stream_t stream);
 
+/* ------------------------------------------------------------------ */
+/* Causal attention (K7): tcgen05 + TMEM + TMA, head dim 64            */
+/* ------------------------------------------------------------------ */
+/* q/k/v read in place from the fused projection output d_qkv, bf16
+ * [B*T, (Hq + 2*Hkv)*dh] (q heads, then k heads, then v heads). Writes
+ * d_o bf16 [B*T, Hq*dh] and d_lse fp32 [B, Hq, T] (natural-log softmax
+ * normaliser of the scaled scores). T % 128 == 0, Hq % Hkv == 0. */
+int b2s_attn_fwd(const void* d_qkv, void* d_o, float* d_lse, int B, int T, int Hq, int Hkv, int dh,
+                 b2s_stream_t stream);
+/* Backward of b2s_attn_fwd: writes dq, dk, dv into d_dqkv (same layout as
+ * d_qkv). d_do: bf16 [B*T, Hq*dh]. d_work: b2s_attn_bwd_work_floats() floats
+ * (fp32 dQ accumulator + rowsum(dO*O)). */
+int b2s_attn_bwd(const void* d_qkv, const void* d_o, const void* d_do, const float* d_lse, void* d_dqkv,
+                 float* d_work, int B, int T, int Hq, int Hkv, int dh, b2s_stream_t stream);
+int64_t b2s_attn_bwd_work_floats(int B, int T, int Hq, int dh);
+
 #ifdef __cplusplus
 }
 #endif

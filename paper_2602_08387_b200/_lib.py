@@ -64,9 +64,11 @@ _SIGS = {
     "b2s_adamw": "pppppplpffffffip",
     "b2s_f32_to_bf16": "pplfp",
     "b2s_scale_f32": "plfp",
+    "b2s_attn_fwd": "pppiiiiip",
+    "b2s_attn_bwd": "ppppppiiiiip",
 }
 # functions returning int64 sizes (not statuses): name -> argument signature
-_SIZE_FNS = {"b2s_norm_work_floats": "i", "b2s_colsum_work_floats": "i"}
+_SIZE_FNS = {"b2s_norm_work_floats": "i", "b2s_colsum_work_floats": "i", "b2s_attn_bwd_work_floats": "iiii"}
 
 _CT = {"p": c_void_p, "i": c_int, "l": c_int64, "u": c_uint64, "f": c_float}
 

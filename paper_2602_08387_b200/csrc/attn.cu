@@ -1,0 +1,612 @@
+// Causal multi-head / grouped-query attention on tcgen05 (K7), head dim 64.
+//
+// Layout: q/k/v are read straight out of the fused QKV projection output
+// [B*T, (Hq + 2*Hkv) * dh] (bf16, head h of q at column h*dh, kv head j of k
+// at (Hq + j)*dh and of v at (Hq + Hkv + j)*dh) by 2-D TMA boxes of
+// 64 (dh) x 128 (tokens) -- no transpose/copy kernel. Output o is
+// [B*T, Hq*dh] bf16 (the O-projection GEMM's A operand) and the per-row
+// log-sum-exp lse[B, Hq, T] (fp32, natural log) is kept for the backward.
+//
+// Forward CTA = (batch, q head, 128-query tile); roles: warp0 TMA, warp1 MMA,
+// warps 2..5 softmax (one query row per thread, the row is a TMEM lane).
+//   S_j = Q K_j^T  -> TMEM (double-buffered, M=128 N=128 K=64)
+//   P_j = exp2(S_j * scale*log2e - m_j) -> bf16 -> swizzled smem
+//   PV_j = P_j V_j -> TMEM (M=128 N=64 K=128, V as an MN-major operand)
+//   O   = O * 2^(m_{j-1} - m_j) + PV_j   (fp32, registers)
+// S_{j+1} is issued before PV_j, so QK^T of the next block overlaps softmax.
+//
+// Backward CTA = (batch, kv head, 128-key tile), looping over the q heads of
+// its group and the causal query tiles: S^T = K Q^T, dP^T = V dO^T (TMEM),
+// P^T and dS^T = P^T (dP^T - D) to smem (thread = key row), then
+// dV += P^T dO, dK += dS^T Q (TMEM accumulators across the loop) and
+// dQ_i = dS K (TMEM) -> fp32 smem -> TMA add-reduce into a dQ accumulator.
+#include "common.cuh"
+#include "sm100.cuh"
+
+namespace b2s {
+using namespace sm100;
+namespace attn {
+
+constexpr int BQ = 128, BKV = 128, DH = 64;
+constexpr int kThreads = 192;
+constexpr int kTile = BQ * DH * 2;  // 16 KB bf16 128x64 tile
+constexpr int kStages = 2;
+constexpr float kLog2e = 1.4426950408889634f;
+
+// byte offset of 16-B chunk c of row r in a 128B-swizzled tile of 128-B rows
+__device__ __forceinline__ uint32_t swz(int r, int c) { return (uint32_t)(r * 128 + ((c ^ (r & 7)) << 4)); }
+
+__device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
+  return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
+}
+__device__ __forceinline__ void named_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+struct Params {
+  int B, T, Hq, Hkv, nqt;
+  float scale_log2;  // log2(e) / sqrt(dh)
+  float scale;       // 1 / sqrt(dh)
+  float* lse;        // [B, Hq, T]
+  const float* dsum; // bwd: D = rowsum(dO * O), [B, Hq, T]
+};
+
+// =====================================================================================
+// forward
+// =====================================================================================
+constexpr int kFwdSmem = 1024 + kTile /*Q*/ + 2 * kStages * kTile /*K,V*/ + 2 * kTile /*P*/ + 256;
+
+__global__ void __launch_bounds__(kThreads, 1)
+    attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_o,
+                    Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sQ = align1024(smem_raw);
+  uint8_t* sK = sQ + kTile;
+  uint8_t* sV = sK + kStages * kTile;
+  uint8_t* sP = sV + kStages * kTile;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + 2 * kTile);
+  uint64_t* q_full = bars;
+  uint64_t* k_full = bars + 1;
+  uint64_t* v_full = k_full + kStages;
+  uint64_t* kv_empty = v_full + kStages;
+  uint64_t* s_full = kv_empty + kStages;  // [2]
+  uint64_t* s_empty = s_full + 2;         // [2]
+  uint64_t* p_full = s_empty + 2;
+  uint64_t* o_full = p_full + 1;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(o_full + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nbh = p.B * p.Hq;
+  const int qt = p.nqt - 1 - (int)(blockIdx.x / nbh);  // longest (diagonal-most) tiles first
+  const int bh = blockIdx.x % nbh;
+  const int b = bh / p.Hq, h = bh % p.Hq;
+  const int kvh = h / (p.Hq / p.Hkv);
+  const int row0 = b * p.T + qt * BQ;
+  const int nkv = qt + 1;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tm_qkv);
+    mbar_init(q_full, 1);
+    for (int s = 0; s < kStages; ++s) { mbar_init(&k_full[s], 1); mbar_init(&v_full[s], 1); mbar_init(&kv_empty[s], 1); }
+    for (int s = 0; s < 2; ++s) { mbar_init(&s_full[s], 1); mbar_init(&s_empty[s], 4); }
+    mbar_init(p_full, 4);
+    mbar_init(o_full, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tslot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tslot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(q_full, kTile);
+      tma_load_2d(sQ, &tm_qkv, q_full, h * DH, row0);
+      for (int j = 0; j < nkv; ++j) {
+        const int s = j % kStages;
+        mbar_wait(&kv_empty[s], ((j / kStages) & 1) ^ 1);
+        const int r = b * p.T + j * BKV;
+        mbar_arrive_expect_tx(&k_full[s], kTile);
+        tma_load_2d(sK + s * kTile, &tm_qkv, &k_full[s], (p.Hq + kvh) * DH, r);
+        mbar_arrive_expect_tx(&v_full[s], kTile);
+        tma_load_2d(sV + s * kTile, &tm_qkv, &v_full[s], (p.Hq + p.Hkv + kvh) * DH, r);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idS = make_idesc_bf16(BQ, BKV, false, false);
+      constexpr uint32_t idO = make_idesc_bf16(BQ, DH, false, true);
+      const uint32_t tO = tbase + 256;
+      const uint32_t aQ = smem_u32(sQ), aK = smem_u32(sK), aV = smem_u32(sV), aP = smem_u32(sP);
+      mbar_wait(q_full, 0);
+      for (int j = 0; j <= nkv; ++j) {
+        if (j < nkv) {
+          const int s = j % kStages;
+          mbar_wait(&k_full[s], (j / kStages) & 1);
+          mbar_wait(&s_empty[j & 1], ((j >> 1) & 1) ^ 1);
+          tc_fence_after();
+#pragma unroll
+          for (int kk = 0; kk < DH / 16; ++kk)
+            mma_bf16_ss(tbase + (j & 1) * BKV, make_sdesc(aQ + kk * 32, 16, 1024),
+                        make_sdesc(aK + s * kTile + kk * 32, 16, 1024), idS, kk > 0);
+          mma_commit(&s_full[j & 1]);
+        }
+        if (j > 0) {
+          const int jj = j - 1, s = jj % kStages;
+          mbar_wait(&v_full[s], (jj / kStages) & 1);
+          mbar_wait(p_full, jj & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int kk = 0; kk < BKV / 16; ++kk)
+            mma_bf16_ss(tO, make_sdesc(aP + (kk >> 2) * kTile + (kk & 3) * 32, 16, 1024),
+                        make_sdesc(aV + s * kTile + kk * 2048, kTile, 1024), idO, kk > 0);
+          mma_commit(o_full);
+          mma_commit(&kv_empty[s]);
+        }
+      }
+    }
+    __syncwarp();
+  } else {
+    // ------------------------------------------------ softmax warps
+    const int q4 = warp & 3;
+    const int r = q4 * 32 + lane;
+    const int qi = qt * BQ + r;
+    const uint32_t lrow = (uint32_t)(q4 * 32) << 16;
+    float m = -INFINITY, l = 0.f;
+    float O[DH];
+#pragma unroll
+    for (int d = 0; d < DH; ++d) O[d] = 0.f;
+    for (int j = 0; j < nkv; ++j) {
+      mbar_wait(&s_full[j & 1], (j >> 1) & 1);
+      tc_fence_after();
+      const uint32_t tS = tbase + lrow + (j & 1) * BKV;
+      const bool diag = (j == qt);
+      // pass 1: row max
+      float mx = -INFINITY;
+#pragma unroll 1
+      for (int c = 0; c < BKV / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld32(tS + c * 32, v);
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          float x = __uint_as_float(v[i]) * p.scale_log2;
+          if (diag && c * 32 + i > r) x = -INFINITY;
+          mx = fmaxf(mx, x);
+        }
+      }
+      const float m_new = fmaxf(m, mx);
+      const float alpha = exp2f(m - m_new);
+      // pass 2: P = exp2(s - m_new) -> bf16 smem, row sum
+      float rs = 0.f;
+#pragma unroll 1
+      for (int c = 0; c < BKV / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld32(tS + c * 32, v);
+        tmem_wait_ld();
+        float pr[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          float x = __uint_as_float(v[i]) * p.scale_log2;
+          if (diag && c * 32 + i > r) x = -INFINITY;
+          pr[i] = exp2f(x - m_new);
+          rs += pr[i];
+        }
+#pragma unroll
+        for (int k8 = 0; k8 < 4; ++k8) {
+          const int kc = c * 4 + k8;  // 16-B chunk index along the 128 keys
+          uint4 w;
+          w.x = pack_bf16x2(pr[8 * k8 + 0], pr[8 * k8 + 1]);
+          w.y = pack_bf16x2(pr[8 * k8 + 2], pr[8 * k8 + 3]);
+          w.z = pack_bf16x2(pr[8 * k8 + 4], pr[8 * k8 + 5]);
+          w.w = pack_bf16x2(pr[8 * k8 + 6], pr[8 * k8 + 7]);
+          *reinterpret_cast<uint4*>(sP + (kc >> 3) * kTile + swz(r, kc & 7)) = w;
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s_empty[j & 1]);
+      l = l * alpha + rs;
+      m = m_new;
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p_full);
+      // accumulate PV_j
+      mbar_wait(o_full, j & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int c = 0; c < DH / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld32(tbase + lrow + 256 + c * 32, v);
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) O[c * 32 + i] = O[c * 32 + i] * alpha + __uint_as_float(v[i]);
+      }
+      tc_fence_before();
+    }
+    // epilogue: O / l -> bf16 -> sQ (free: every MMA has retired) -> TMA store
+    const float inv = 1.f / l;
+#pragma unroll
+    for (int c = 0; c < DH / 8; ++c) {
+      uint4 w;
+      w.x = pack_bf16x2(O[8 * c + 0] * inv, O[8 * c + 1] * inv);
+      w.y = pack_bf16x2(O[8 * c + 2] * inv, O[8 * c + 3] * inv);
+      w.z = pack_bf16x2(O[8 * c + 4] * inv, O[8 * c + 5] * inv);
+      w.w = pack_bf16x2(O[8 * c + 6] * inv, O[8 * c + 7] * inv);
+      *reinterpret_cast<uint4*>(sQ + swz(r, c)) = w;
+    }
+    p.lse[((size_t)b * p.Hq + h) * p.T + qi] = (m + log2f(l)) * (1.f / kLog2e);
+    fence_proxy_async_smem();
+    named_sync(1, 128);
+    if (warp == 2 && lane == 0) {
+      tma_store_2d(&tm_o, sQ, h * DH, row0);
+      bulk_commit();
+      bulk_wait<0>();
+    }
+    __syncwarp();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<512>(tbase);
+  }
+}
+
+
+// =====================================================================================
+// backward
+// =====================================================================================
+// D[b, h, q] = sum_d dO * O (row-wise), and zero the fp32 dQ accumulator.
+__global__ void attn_bwd_prep_kernel(const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ dout,
+                                     float* __restrict__ dsum, float* __restrict__ dq_acc, int B, int T, int Hq) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nrows = (int64_t)B * T * Hq;
+  for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nrows;
+       w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t row = w / Hq;
+    const int h = (int)(w - row * Hq);
+    const int64_t off = row * Hq * DH + h * DH + lane * 2;
+    float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(o + off));
+    float2 g = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(dout + off));
+    float acc = warp_sum(a.x * g.x + a.y * g.y);
+    *reinterpret_cast<float2*>(dq_acc + off) = make_float2(0.f, 0.f);
+    if (lane == 0) {
+      const int64_t b = row / T, t = row - b * T;
+      dsum[(b * Hq + h) * T + t] = acc;
+    }
+  }
+}
+
+// dqkv[:, q heads] = bf16(dq_acc)
+__global__ void attn_bwd_dq_kernel(const float* __restrict__ dq_acc, __nv_bfloat16* __restrict__ dqkv, int64_t M,
+                                   int Hq, int64_t ldq) {
+  const int width = Hq * DH;
+  const int64_t nvec = M * width / 4;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nvec; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = i * 4;
+    const int64_t row = e / width;
+    const int c = (int)(e - row * width);
+    float4 v = *reinterpret_cast<const float4*>(dq_acc + e);
+    uint2 u;
+    u.x = pack_bf16x2(v.x, v.y);
+    u.y = pack_bf16x2(v.z, v.w);
+    *reinterpret_cast<uint2*>(dqkv + row * ldq + c) = u;
+  }
+}
+
+// dQ's fp32 staging tile reuses the P^T buffer (free once dQ's MMA retired).
+constexpr int kBwdSmem = 1024 + 2 * kTile /*K,V*/ + 4 * kTile /*Q,dO x2*/ + 2 * kTile /*P^T*/ + 2 * kTile /*dS^T*/ +
+                         4 * BQ * 4 /*lse2, D x2*/ + 256;
+
+__global__ void __launch_bounds__(kThreads, 1)
+    attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
+                    const __grid_constant__ CUtensorMap tm_dq, const __grid_constant__ CUtensorMap tm_dkv, Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sK = align1024(smem_raw);
+  uint8_t* sV = sK + kTile;
+  uint8_t* sQ = sV + kTile;          // [2]
+  uint8_t* sdO = sQ + 2 * kTile;     // [2]
+  uint8_t* sP = sdO + 2 * kTile;     // P^T  [128 keys][128 q] as two 64-column atoms
+  uint8_t* sdS = sP + 2 * kTile;     // dS^T
+  uint8_t* sdQ = sP;                 // fp32 128 x 64 as two 32-column boxes (aliases P^T)
+  float* sLse = reinterpret_cast<float*>(sdS + 2 * kTile);  // [2][128] (log2 domain)
+  float* sD = sLse + 2 * BQ;                                 // [2][128]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sD + 2 * BQ);
+  uint64_t* kv_full = bars;
+  uint64_t* qd_full = bars + 1;   // [2]
+  uint64_t* qd_empty = bars + 3;  // [2]
+  uint64_t* st_full = bars + 5;
+  uint64_t* st_empty = bars + 6;
+  uint64_t* pds_full = bars + 7;
+  uint64_t* pds_empty = bars + 8;
+  uint64_t* dq_full = bars + 9;
+  uint64_t* dq_empty = bars + 10;
+  uint64_t* done = bars + 11;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 12);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nbk = p.B * p.Hkv;
+  const int kt = (int)(blockIdx.x / nbk);  // kt = 0 has the most query tiles: launched first
+  const int bk = blockIdx.x % nbk;
+  const int b = bk / p.Hkv, kvh = bk % p.Hkv;
+  const int G = p.Hq / p.Hkv;
+  const int nq = p.nqt - kt;  // query tiles i = kt .. nqt-1
+  const int nsteps = G * nq;
+  const int krow0 = b * p.T + kt * BKV;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tm_qkv);
+    tma_prefetch(&tm_do);
+    mbar_init(kv_full, 1);
+    for (int s = 0; s < 2; ++s) { mbar_init(&qd_full[s], 1); mbar_init(&qd_empty[s], 1); }
+    mbar_init(st_full, 1);
+    mbar_init(st_empty, 4);
+    mbar_init(pds_full, 4);
+    mbar_init(pds_empty, 1);
+    mbar_init(dq_full, 1);
+    mbar_init(dq_empty, 4);
+    mbar_init(done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tslot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tslot;
+  const uint32_t tS = tbase, tdP = tbase + 128, tdV = tbase + 256, tdK = tbase + 320, tdQ = tbase + 384;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(kv_full, 2 * kTile);
+      tma_load_2d(sK, &tm_qkv, kv_full, (p.Hq + kvh) * DH, krow0);
+      tma_load_2d(sV, &tm_qkv, kv_full, (p.Hq + p.Hkv + kvh) * DH, krow0);
+      for (int t = 0; t < nsteps; ++t) {
+        const int h = kvh * G + t / nq, i = kt + t % nq;
+        const int s = t & 1;
+        mbar_wait(&qd_empty[s], ((t >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&qd_full[s], 2 * kTile);
+        tma_load_2d(sQ + s * kTile, &tm_qkv, &qd_full[s], h * DH, b * p.T + i * BQ);
+        tma_load_2d(sdO + s * kTile, &tm_do, &qd_full[s], h * DH, b * p.T + i * BQ);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idSS = make_idesc_bf16(128, 128, false, false);  // S^T, dP^T
+      constexpr uint32_t idKM = make_idesc_bf16(128, DH, false, true);    // dV, dK
+      constexpr uint32_t idMM = make_idesc_bf16(128, DH, true, true);     // dQ
+      const uint32_t aK = smem_u32(sK), aV = smem_u32(sV), aQ = smem_u32(sQ), adO = smem_u32(sdO);
+      const uint32_t aP = smem_u32(sP), adS = smem_u32(sdS);
+      mbar_wait(kv_full, 0);
+      for (int t = 0; t < nsteps; ++t) {
+        const int s = t & 1;
+        const uint32_t q_ = aQ + s * kTile, do_ = adO + s * kTile;
+        mbar_wait(&qd_full[s], (t >> 1) & 1);
+        mbar_wait(st_empty, (t & 1) ^ 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < DH / 16; ++kk)
+          mma_bf16_ss(tS, make_sdesc(aK + kk * 32, 16, 1024), make_sdesc(q_ + kk * 32, 16, 1024), idSS, kk > 0);
+#pragma unroll
+        for (int kk = 0; kk < DH / 16; ++kk)
+          mma_bf16_ss(tdP, make_sdesc(aV + kk * 32, 16, 1024), make_sdesc(do_ + kk * 32, 16, 1024), idSS, kk > 0);
+        mma_commit(st_full);
+        mbar_wait(pds_full, t & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < BQ / 16; ++kk) {
+          const uint64_t a_p = make_sdesc(aP + (kk >> 2) * kTile + (kk & 3) * 32, 16, 1024);
+          const uint64_t a_ds = make_sdesc(adS + (kk >> 2) * kTile + (kk & 3) * 32, 16, 1024);
+          mma_bf16_ss(tdV, a_p, make_sdesc(do_ + kk * 2048, kTile, 1024), idKM, (t > 0 || kk > 0));
+          mma_bf16_ss(tdK, a_ds, make_sdesc(q_ + kk * 2048, kTile, 1024), idKM, (t > 0 || kk > 0));
+        }
+        mbar_wait(dq_empty, (t & 1) ^ 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < BKV / 16; ++kk)
+          mma_bf16_ss(tdQ, make_sdesc(adS + kk * 2048, kTile, 1024), make_sdesc(aK + kk * 2048, kTile, 1024), idMM,
+                      kk > 0);
+        mma_commit(&qd_empty[s]);
+        mma_commit(pds_empty);
+        mma_commit(dq_full);
+      }
+      mma_commit(done);
+    }
+    __syncwarp();
+  } else {
+    // ------------------------------------------------ compute warps (thread = key row, then q row)
+    const int ct = threadIdx.x - 64;  // 0..127
+    const int q4 = warp & 3;
+    const int r = q4 * 32 + lane;
+    const uint32_t lrow = (uint32_t)(q4 * 32) << 16;
+    for (int t = 0; t < nsteps; ++t) {
+      const int h = kvh * G + t / nq, i = kt + t % nq;
+      const bool diag = (i == kt);
+      float* lse2 = sLse + (t & 1) * BQ;
+      float* dd = sD + (t & 1) * BQ;
+      {
+        const size_t off = ((size_t)b * p.Hq + h) * p.T + (size_t)i * BQ + ct;
+        lse2[ct] = p.lse[off] * kLog2e;
+        dd[ct] = p.dsum[off];
+      }
+      named_sync(1, 128);
+      mbar_wait(st_full, t & 1);
+      mbar_wait(pds_empty, (t & 1) ^ 1);
+      tc_fence_after();
+#pragma unroll 1
+      for (int c = 0; c < BQ / 32; ++c) {
+        uint32_t sv[32], dv[32];
+        tmem_ld32(tS + lrow + c * 32, sv);
+        tmem_ld32(tdP + lrow + c * 32, dv);
+        tmem_wait_ld();
+        float pr[32], ds[32];
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          const int q = c * 32 + e;
+          float pv = exp2f(__uint_as_float(sv[e]) * p.scale_log2 - lse2[q]);
+          if (diag && q < r) pv = 0.f;  // query index below key index: masked
+          pr[e] = pv;
+          ds[e] = pv * (__uint_as_float(dv[e]) - dd[q]);
+        }
+#pragma unroll
+        for (int k8 = 0; k8 < 4; ++k8) {
+          const int kc = c * 4 + k8;
+          uint4 w, z;
+          w.x = pack_bf16x2(pr[8 * k8 + 0], pr[8 * k8 + 1]);
+          w.y = pack_bf16x2(pr[8 * k8 + 2], pr[8 * k8 + 3]);
+          w.z = pack_bf16x2(pr[8 * k8 + 4], pr[8 * k8 + 5]);
+          w.w = pack_bf16x2(pr[8 * k8 + 6], pr[8 * k8 + 7]);
+          z.x = pack_bf16x2(ds[8 * k8 + 0], ds[8 * k8 + 1]);
+          z.y = pack_bf16x2(ds[8 * k8 + 2], ds[8 * k8 + 3]);
+          z.z = pack_bf16x2(ds[8 * k8 + 4], ds[8 * k8 + 5]);
+          z.w = pack_bf16x2(ds[8 * k8 + 6], ds[8 * k8 + 7]);
+          const uint32_t off = (kc >> 3) * kTile + swz(r, kc & 7);
+          *reinterpret_cast<uint4*>(sP + off) = w;
+          *reinterpret_cast<uint4*>(sdS + off) = z;
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(st_empty);
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(pds_full);
+      // dQ_i = scale * dS K  (TMEM lane = query row)
+      mbar_wait(dq_full, t & 1);
+      tc_fence_after();
+      uint32_t qv[DH];
+      tmem_ld32(tdQ + lrow, qv);
+      tmem_ld32(tdQ + lrow + 32, qv + 32);
+      tmem_wait_ld();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(dq_empty);
+#pragma unroll
+      for (int c = 0; c < DH / 4; ++c) {
+        const int box = c >> 3, cc = c & 7;
+        *reinterpret_cast<float4*>(sdQ + box * (2 * kTile) + swz(r, cc)) =
+            make_float4(__uint_as_float(qv[4 * c]) * p.scale, __uint_as_float(qv[4 * c + 1]) * p.scale,
+                        __uint_as_float(qv[4 * c + 2]) * p.scale, __uint_as_float(qv[4 * c + 3]) * p.scale);
+      }
+      fence_proxy_async_smem();
+      named_sync(3, 128);
+      if (ct == 0) {
+        tma_reduce_add_2d(&tm_dq, sdQ, h * DH, b * p.T + i * BQ);
+        tma_reduce_add_2d(&tm_dq, sdQ + 2 * kTile, h * DH + 32, b * p.T + i * BQ);
+        bulk_commit();
+        bulk_wait_read<0>();
+      }
+    }
+    // dK (scaled) and dV -> bf16 -> smem (Q stages are free) -> TMA store into dqkv
+    mbar_wait(done, 0);
+    tc_fence_after();
+    uint32_t kv[DH], vv[DH];
+    tmem_ld32(tdK + lrow, kv);
+    tmem_ld32(tdK + lrow + 32, kv + 32);
+    tmem_ld32(tdV + lrow, vv);
+    tmem_ld32(tdV + lrow + 32, vv + 32);
+    tmem_wait_ld();
+#pragma unroll
+    for (int c = 0; c < DH / 8; ++c) {
+      uint4 w, z;
+      w.x = pack_bf16x2(__uint_as_float(kv[8 * c + 0]) * p.scale, __uint_as_float(kv[8 * c + 1]) * p.scale);
+      w.y = pack_bf16x2(__uint_as_float(kv[8 * c + 2]) * p.scale, __uint_as_float(kv[8 * c + 3]) * p.scale);
+      w.z = pack_bf16x2(__uint_as_float(kv[8 * c + 4]) * p.scale, __uint_as_float(kv[8 * c + 5]) * p.scale);
+      w.w = pack_bf16x2(__uint_as_float(kv[8 * c + 6]) * p.scale, __uint_as_float(kv[8 * c + 7]) * p.scale);
+      z.x = pack_bf16x2(__uint_as_float(vv[8 * c + 0]), __uint_as_float(vv[8 * c + 1]));
+      z.y = pack_bf16x2(__uint_as_float(vv[8 * c + 2]), __uint_as_float(vv[8 * c + 3]));
+      z.z = pack_bf16x2(__uint_as_float(vv[8 * c + 4]), __uint_as_float(vv[8 * c + 5]));
+      z.w = pack_bf16x2(__uint_as_float(vv[8 * c + 6]), __uint_as_float(vv[8 * c + 7]));
+      *reinterpret_cast<uint4*>(sQ + swz(r, c)) = w;
+      *reinterpret_cast<uint4*>(sQ + kTile + swz(r, c)) = z;
+    }
+    fence_proxy_async_smem();
+    named_sync(1, 128);
+    if (ct == 0) {
+      tma_store_2d(&tm_dkv, sQ, (p.Hq + kvh) * DH, krow0);
+      tma_store_2d(&tm_dkv, sQ + kTile, (p.Hq + p.Hkv + kvh) * DH, krow0);
+      bulk_commit();
+      bulk_wait<0>();
+    }
+    __syncwarp();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<512>(tbase);
+  }
+}
+
+}  // namespace attn
+}  // namespace b2s
+
+using namespace b2s;
+
+extern "C" int b2s_attn_fwd(const void* d_qkv, void* d_o, float* d_lse, int B, int T, int Hq, int Hkv, int dh,
+                            b2s_stream_t stream) {
+  B2S_REQUIRE(dh == attn::DH, B2S_EUNSUPPORTED, "attention: head dim %d not implemented (64 only)", dh);
+  B2S_REQUIRE(T % attn::BQ == 0 && T > 0, B2S_EUNSUPPORTED, "attention: T must be a multiple of 128");
+  B2S_REQUIRE(Hkv > 0 && Hq % Hkv == 0, B2S_EINVAL, "attention: Hq must be a multiple of Hkv");
+  const int ldq = (Hq + 2 * Hkv) * dh;
+  CUtensorMap tq, to;
+  int rc = encode_tma_2d(&tq, d_qkv, 2, (uint64_t)ldq, (uint64_t)B * T, (uint64_t)ldq * 2, 64, 128, 128);
+  if (rc) return rc;
+  rc = encode_tma_2d(&to, d_o, 2, (uint64_t)Hq * dh, (uint64_t)B * T, (uint64_t)Hq * dh * 2, 64, 128, 128);
+  if (rc) return rc;
+  attn::Params p{B, T, Hq, Hkv, T / attn::BQ, attn::kLog2e / sqrtf((float)dh), 1.f / sqrtf((float)dh), d_lse,
+                 nullptr};
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(attn::attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, attn::kFwdSmem);
+    attr = true;
+  }
+  const unsigned grid = (unsigned)(B * Hq * (T / attn::BQ));
+  attn::attn_fwd_kernel<<<grid, attn::kThreads, attn::kFwdSmem, (cudaStream_t)stream>>>(tq, to, p);
+  return check_launch("attn_fwd");
+}
+
+extern "C" int64_t b2s_attn_bwd_work_floats(int B, int T, int Hq, int dh) {
+  return (int64_t)B * T * Hq * dh + (int64_t)B * Hq * T;
+}
+
+extern "C" int b2s_attn_bwd(const void* d_qkv, const void* d_o, const void* d_do, const float* d_lse, void* d_dqkv,
+                            float* d_work, int B, int T, int Hq, int Hkv, int dh, b2s_stream_t stream) {
+  B2S_REQUIRE(dh == attn::DH, B2S_EUNSUPPORTED, "attention: head dim %d not implemented (64 only)", dh);
+  B2S_REQUIRE(T % attn::BQ == 0 && T > 0, B2S_EUNSUPPORTED, "attention: T must be a multiple of 128");
+  B2S_REQUIRE(Hkv > 0 && Hq % Hkv == 0, B2S_EINVAL, "attention: Hq must be a multiple of Hkv");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int ldq = (Hq + 2 * Hkv) * dh;
+  const int64_t M = (int64_t)B * T;
+  float* dq_acc = d_work;
+  float* dsum = d_work + M * Hq * dh;
+  attn::attn_bwd_prep_kernel<<<kNumSMs * 8, 256, 0, st>>>((const __nv_bfloat16*)d_o, (const __nv_bfloat16*)d_do,
+                                                          dsum, dq_acc, B, T, Hq);
+  int rc = check_launch("attn_bwd_prep");
+  if (rc) return rc;
+  CUtensorMap tq, tdo, tdq, tdkv;
+  rc = encode_tma_2d(&tq, d_qkv, 2, (uint64_t)ldq, (uint64_t)M, (uint64_t)ldq * 2, 64, 128, 128);
+  if (rc) return rc;
+  rc = encode_tma_2d(&tdo, d_do, 2, (uint64_t)Hq * dh, (uint64_t)M, (uint64_t)Hq * dh * 2, 64, 128, 128);
+  if (rc) return rc;
+  rc = encode_tma_2d(&tdq, dq_acc, 4, (uint64_t)Hq * dh, (uint64_t)M, (uint64_t)Hq * dh * 4, 32, 128, 128);
+  if (rc) return rc;
+  rc = encode_tma_2d(&tdkv, d_dqkv, 2, (uint64_t)ldq, (uint64_t)M, (uint64_t)ldq * 2, 64, 128, 128);
+  if (rc) return rc;
+  attn::Params p{B, T, Hq, Hkv, T / attn::BQ, attn::kLog2e / sqrtf((float)dh), 1.f / sqrtf((float)dh),
+                 const_cast<float*>(d_lse), dsum};
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(attn::attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, attn::kBwdSmem);
+    attr = true;
+  }
+  const unsigned grid = (unsigned)(B * Hkv * (T / attn::BQ));
+  attn::attn_bwd_kernel<<<grid, attn::kThreads, attn::kBwdSmem, st>>>(tq, tdo, tdq, tdkv, p);
+  rc = check_launch("attn_bwd");
+  if (rc) return rc;
+  attn::attn_bwd_dq_kernel<<<kNumSMs * 8, 256, 0, st>>>(dq_acc, (__nv_bfloat16*)d_dqkv, M, Hq, ldq);
+  return check_launch("attn_bwd_dq");
+}

@@ -203,3 +203,25 @@ def f32_to_bf16(x, y, scale=1.0):
 
 def scale_f32(x, scale):
     _call("b2s_scale_f32", x.data_ptr(), x.numel(), scale, _sp())
+
+
+# ---------------------------------------------------------------------------- attention
+
+
+def attn_fwd(qkv, B, T, Hq, Hkv, dh, o=None, lse=None):
+    """Causal attention over the fused [B*T, (Hq+2Hkv)*dh] projection output."""
+    _dev(qkv)
+    o = torch.empty(B * T, Hq * dh, device=qkv.device, dtype=torch.bfloat16) if o is None else o
+    lse = torch.empty(B, Hq, T, device=qkv.device, dtype=torch.float32) if lse is None else lse
+    _call("b2s_attn_fwd", qkv.data_ptr(), o.data_ptr(), lse.data_ptr(), B, T, Hq, Hkv, dh, _sp())
+    return o, lse
+
+
+def attn_bwd(qkv, o, do, lse, B, T, Hq, Hkv, dh, dqkv=None, work=None):
+    """dq/dk/dv of causal attention, written into a [B*T, (Hq+2Hkv)*dh] buffer."""
+    dqkv = torch.empty_like(qkv) if dqkv is None else dqkv
+    n = _lib.load().b2s_attn_bwd_work_floats(B, T, Hq, dh)
+    work = _work(n, qkv.device) if work is None else work
+    _call("b2s_attn_bwd", qkv.data_ptr(), o.data_ptr(), do.data_ptr(), lse.data_ptr(), dqkv.data_ptr(),
+          work.data_ptr(), B, T, Hq, Hkv, dh, _sp())
+    return dqkv

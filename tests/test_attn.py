@@ -1,0 +1,54 @@
+"""tcgen05 causal attention vs a plain PyTorch fp32 reference (same bf16 inputs)."""
+
+import math
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _ref(qkv, B, T, Hq, Hkv, dh):
+    x = qkv.float().view(B, T, Hq + 2 * Hkv, dh)
+    q = x[:, :, :Hq].transpose(1, 2)
+    k = x[:, :, Hq:Hq + Hkv].transpose(1, 2).repeat_interleave(Hq // Hkv, 1)
+    v = x[:, :, Hq + Hkv:].transpose(1, 2).repeat_interleave(Hq // Hkv, 1)
+    s = q @ k.transpose(-1, -2) / math.sqrt(dh)
+    mask = torch.ones(T, T, device=qkv.device, dtype=torch.bool).tril()
+    s = s.masked_fill(~mask, float("-inf"))
+    lse = torch.logsumexp(s, -1)
+    o = torch.softmax(s, -1) @ v
+    return o.transpose(1, 2).reshape(B * T, Hq * dh), lse
+
+
+@pytest.mark.parametrize("B,T,Hq,Hkv", [(1, 128, 1, 1), (2, 256, 4, 2), (1, 512, 3, 3), (2, 384, 8, 2)])
+def test_attn_fwd(cuda, B, T, Hq, Hkv):
+    from paper_2602_08387_b200 import ops
+
+    dh = 64
+    torch.manual_seed(B * T + Hq)
+    qkv = torch.randn(B * T, (Hq + 2 * Hkv) * dh, device=cuda).bfloat16()
+    o, lse = ops.attn_fwd(qkv, B, T, Hq, Hkv, dh)
+    ro, rl = _ref(qkv, B, T, Hq, Hkv, dh)
+    torch.testing.assert_close(lse, rl, rtol=1e-3, atol=1e-3)
+    torch.testing.assert_close(o.float(), ro, rtol=2e-2, atol=2e-2)
+
+
+@pytest.mark.parametrize("B,T,Hq,Hkv", [(1, 128, 1, 1), (2, 256, 4, 2), (1, 512, 3, 3), (2, 384, 8, 2)])
+def test_attn_bwd(cuda, B, T, Hq, Hkv):
+    from paper_2602_08387_b200 import ops
+
+    dh = 64
+    torch.manual_seed(B * T + Hq + 1)
+    qkv = torch.randn(B * T, (Hq + 2 * Hkv) * dh, device=cuda).bfloat16()
+    o, lse = ops.attn_fwd(qkv, B, T, Hq, Hkv, dh)
+    do = torch.randn(B * T, Hq * dh, device=cuda).bfloat16()
+    dqkv = ops.attn_bwd(qkv, o, do, lse, B, T, Hq, Hkv, dh)
+    x = qkv.float().requires_grad_()
+    ro, _ = _ref(x, B, T, Hq, Hkv, dh)
+    ro.backward(do.float())
+    ref = x.grad
+    err = (dqkv.float() - ref).abs().max().item()
+    scale = ref.abs().max().item()
+    assert err <= 2e-2 * scale + 2e-2, (err, scale)
+    torch.testing.assert_close(dqkv.float(), ref, rtol=5e-2, atol=5e-2)
