@@ -76,6 +76,12 @@ int b2s_gather_samples(const void* d_payload, int width, uint64_t token_count,
                        int64_t* d_inputs, int64_t* d_targets, int32_t* d_status,
                        b2s_stream_t stream);
 
+/* Same widening split for `batch` host-staged windows of seq_len+1 tokens
+ * stored back to back in d_windows (window b starts at token b*(seq_len+1)):
+ * the end-to-end feed that copies each step's windows from host memory. */
+int b2s_unpack_windows(const void* d_windows, int width, int batch, int64_t seq_len, int64_t* d_inputs,
+                       int64_t* d_targets, b2s_stream_t stream);
+
 
 /* ------------------------------------------------------------------ */
 /* Dense contractions (K5): tcgen05 + TMEM + TMA, persistent           */

@@ -488,6 +488,8 @@ static int norm_fwd(const float* x, const void* g, const void* b, void* y, float
   };
   switch (D) {
     case 128: return go(norm_fwd_kernel<128, 32, RMS>, 32);
+    case 256: return go(norm_fwd_kernel<256, 32, RMS>, 32);
+    case 512: return go(norm_fwd_kernel<512, 32, RMS>, 32);
     case 768: return go(norm_fwd_kernel<768, 32, RMS>, 32);
     case 1024: return go(norm_fwd_kernel<1024, 32, RMS>, 32);
     case 2048: return go(norm_fwd_kernel<2048, 256, RMS>, 256);
@@ -512,6 +514,8 @@ static int norm_bwd(const float* x, const void* dy, const void* g, const float* 
   int rc;
   switch (D) {
     case 128: rc = go(norm_bwd_kernel<128, 32, RMS>, 32); break;
+    case 256: rc = go(norm_bwd_kernel<256, 32, RMS>, 32); break;
+    case 512: rc = go(norm_bwd_kernel<512, 32, RMS>, 32); break;
     case 768: rc = go(norm_bwd_kernel<768, 32, RMS>, 32); break;
     case 1024: rc = go(norm_bwd_kernel<1024, 32, RMS>, 32); break;
     case 2048: rc = go(norm_bwd_kernel<2048, 256, RMS>, 256); break;

@@ -32,10 +32,12 @@ __device__ __forceinline__ int64_t load_token(const uint8_t* __restrict__ p, uin
 // input/target arrays and stores each pair as one 16-byte vector. The payload
 // read for output (b,t) is token s_b*L+t (+1 for targets): consecutive threads
 // read consecutive tokens, so loads and stores are both coalesced.
+// Sample s starts at token s * stride: stride = L for the packed stream
+// (consecutive samples overlap by one token), L + 1 for staged windows.
 template <int W>
 __global__ void __launch_bounds__(256) gather_samples_kernel(
     const uint8_t* __restrict__ payload, uint64_t nsamples, const uint64_t* __restrict__ ids,
-    int batch, int64_t L, int64_t* __restrict__ inputs, int64_t* __restrict__ targets,
+    int batch, int64_t L, int64_t stride, int64_t* __restrict__ inputs, int64_t* __restrict__ targets,
     int32_t* __restrict__ status) {
   const uint64_t total = (uint64_t)batch * (uint64_t)L;
   const uint64_t npairs = (total + 1) / 2;
@@ -48,12 +50,12 @@ __global__ void __launch_bounds__(256) gather_samples_kernel(
       const uint64_t idx = 2 * p + e;
       if (idx >= total) break;
       const uint64_t b = idx / (uint64_t)L, t = idx - b * (uint64_t)L;
-      const uint64_t s = __ldg(ids + b);
+      const uint64_t s = ids ? __ldg(ids + b) : b;
       if (s >= nsamples) {
         if (t == 0) atomicExch(status, 1);
         continue;
       }
-      const uint64_t base = s * (uint64_t)L + t;  // 64-bit token offset
+      const uint64_t base = s * (uint64_t)stride + t;  // 64-bit token offset
       in2[e] = load_token<W>(payload, base);
       tg2[e] = load_token<W>(payload, base + 1);
       ok[e] = true;
@@ -166,11 +168,31 @@ int b2s_gather_samples(const void* d_payload, int width, uint64_t token_count,
   cudaStream_t st = (cudaStream_t)stream;
   const uint8_t* p = (const uint8_t*)d_payload;
   switch (width) {
-    case 1: b2s::gather_samples_kernel<1><<<grid, 256, 0, st>>>(p, nsamples, d_sample_ids, batch, seq_len, d_inputs, d_targets, d_status); break;
-    case 2: b2s::gather_samples_kernel<2><<<grid, 256, 0, st>>>(p, nsamples, d_sample_ids, batch, seq_len, d_inputs, d_targets, d_status); break;
-    default: b2s::gather_samples_kernel<4><<<grid, 256, 0, st>>>(p, nsamples, d_sample_ids, batch, seq_len, d_inputs, d_targets, d_status); break;
+    case 1: b2s::gather_samples_kernel<1><<<grid, 256, 0, st>>>(p, nsamples, d_sample_ids, batch, seq_len, seq_len, d_inputs, d_targets, d_status); break;
+    case 2: b2s::gather_samples_kernel<2><<<grid, 256, 0, st>>>(p, nsamples, d_sample_ids, batch, seq_len, seq_len, d_inputs, d_targets, d_status); break;
+    default: b2s::gather_samples_kernel<4><<<grid, 256, 0, st>>>(p, nsamples, d_sample_ids, batch, seq_len, seq_len, d_inputs, d_targets, d_status); break;
   }
   return b2s::check_launch("gather_samples");
+}
+
+int b2s_unpack_windows(const void* d_windows, int width, int batch, int64_t seq_len, int64_t* d_inputs,
+                       int64_t* d_targets, b2s_stream_t stream) {
+  B2S_REQUIRE(width == 1 || width == 2 || width == 4, B2S_EINVAL, "token width must be 1, 2 or 4, got %d", width);
+  B2S_REQUIRE(seq_len >= 1 && batch >= 0, B2S_EINVAL, "bad shape");
+  if (batch == 0) return B2S_OK;
+  B2S_REQUIRE(((uintptr_t)d_inputs % 16) == 0 && ((uintptr_t)d_targets % 16) == 0, B2S_EINVAL,
+              "inputs/targets must be 16-byte aligned");
+  const uint64_t npairs = ((uint64_t)batch * (uint64_t)seq_len + 1) / 2;
+  unsigned grid = b2s::ceil_div(npairs, 256);
+  if (grid > b2s::kNumSMs * 16) grid = b2s::kNumSMs * 16;
+  cudaStream_t st = (cudaStream_t)stream;
+  const uint8_t* p = (const uint8_t*)d_windows;
+  switch (width) {
+    case 1: b2s::gather_samples_kernel<1><<<grid, 256, 0, st>>>(p, batch, nullptr, batch, seq_len, seq_len + 1, d_inputs, d_targets, nullptr); break;
+    case 2: b2s::gather_samples_kernel<2><<<grid, 256, 0, st>>>(p, batch, nullptr, batch, seq_len, seq_len + 1, d_inputs, d_targets, nullptr); break;
+    default: b2s::gather_samples_kernel<4><<<grid, 256, 0, st>>>(p, batch, nullptr, batch, seq_len, seq_len + 1, d_inputs, d_targets, nullptr); break;
+  }
+  return b2s::check_launch("unpack_windows");
 }
 
 }  // extern "C"

@@ -1,0 +1,233 @@
+"""Fully-sharded data parallelism over flat per-unit buffers (FSDP2 semantics, B200 layout).
+
+Each FSDP unit (embedding, each transformer block or group of g blocks,
+final norm/head) owns one flat parameter space of `padded` elements, split
+into W equal shards. Per rank and unit (sizes for the shard S = padded / W):
+
+  master  fp32 [S]   optimizer's copy of the parameters       (sharded)
+  m, v    fp32 [S]   AdamW moments                            (sharded)
+  p16     bf16 [S]   AdamW's bf16 output = all-gather source   (sharded)
+  g       fp32 [S]   reduce-scatter destination (averaged)    (sharded)
+  full    bf16 [W*S] all-gather destination: the compute weights
+  gfull   fp32 [W*S] the backward's weight-gradient accumulator
+
+With 180 GB per GPU the unsharded buffers stay resident (no re-gather in the
+backward): per step each unit does one NCCL all-gather (before its forward,
+prefetched on a side stream) and one reduce-scatter (as soon as its backward
+is done, on the same side stream), overlapping the compute of other units.
+At W = 1 the shard IS the full buffer and no collective is issued.
+`comm_planner.plan_unit_size` picks how many blocks form a unit.
+"""
+
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+from .model import ALIGN, UnitSpec
+
+
+class FlatUnit:
+    def __init__(self, specs: list, rank: int, world: int, device):
+        self.specs = specs  # one or more model UnitSpecs grouped into this FSDP unit
+        self.rank, self.world = rank, world
+        self.offsets = {}
+        off = 0
+        for s in specs:
+            for p in s.params:
+                self.offsets[(s.name, p.name)] = (off + s.offsets[p.name], tuple(p.shape), p.decay)
+            off += s.numel
+        self.numel = off
+        per = -(-off // world)
+        self.shard = -(-per // ALIGN) * ALIGN
+        self.padded = self.shard * world
+        bf, f32 = torch.bfloat16, torch.float32
+        self.full = torch.zeros(self.padded, device=device, dtype=bf)
+        self.gfull = torch.zeros(self.padded, device=device, dtype=f32)
+        lo = rank * self.shard
+        if world == 1:
+            self.p16 = self.full
+            self.g = self.gfull
+        else:
+            self.p16 = torch.zeros(self.shard, device=device, dtype=bf)
+            self.g = torch.zeros(self.shard, device=device, dtype=f32)
+        self.master = torch.zeros(self.shard, device=device, dtype=f32)
+        self.m = torch.zeros(self.shard, device=device, dtype=f32)
+        self.v = torch.zeros(self.shard, device=device, dtype=f32)
+        mask = torch.zeros(self.padded, dtype=torch.uint8)
+        for (_, _), (o, shape, decay) in self.offsets.items():
+            n = int(torch.Size(shape).numel())
+            if decay:
+                mask[o:o + n] = 1
+        self.wd_mask = mask[lo:lo + self.shard].to(device)
+
+    def load_full_fp32(self, get) -> None:
+        """Fill this rank's master shard (and bf16 copies); get('unit.param') -> full fp32 tensor."""
+        full = torch.zeros(self.padded, dtype=torch.float32, device=self.master.device)
+        for (u, p), (o, shape, _) in self.offsets.items():
+            t = get(f"{u}.{p}")
+            full[o:o + t.numel()] = t.reshape(-1).to(full.device, torch.float32)
+        lo = self.rank * self.shard
+        self.master.copy_(full[lo:lo + self.shard])
+        self.p16.copy_(self.master)
+        self.full.copy_(full)  # initial gather done locally (every rank has the same init)
+
+    def view(self, buf, unit: str, name: str):
+        o, shape, _ = self.offsets[(unit, name)]
+        return buf[o:o + int(torch.Size(shape).numel())].view(shape)
+
+
+class UnitView:
+    """The parameters / gradients of one *model* unit inside its FSDP unit."""
+
+    def __init__(self, flat: FlatUnit, name: str):
+        self.flat, self.name = flat, name
+
+    def p(self, pname):
+        return self.flat.view(self.flat.full, self.name, pname)
+
+    def g(self, pname):
+        return self.flat.view(self.flat.gfull, self.name, pname)
+
+
+class FlatParams:
+    """All FSDP units of a model; ``unit(i)`` addresses the i-th *model* unit."""
+
+    def __init__(self, unit_specs: list, rank: int, world: int, device, blocks_per_unit: int = 1):
+        self.model_units = unit_specs
+        groups, cur = [], []
+        # embedding and head are units of their own; blocks are grouped g at a time
+        for s in unit_specs:
+            if s.name.startswith("block"):
+                cur.append(s)
+                if len(cur) == blocks_per_unit:
+                    groups.append(cur)
+                    cur = []
+            else:
+                if cur:
+                    groups.append(cur)
+                    cur = []
+                groups.append([s])
+        if cur:
+            groups.append(cur)
+        self.flat = [FlatUnit(g, rank, world, device) for g in groups]
+        self.owner = {}
+        self.first_model_unit = {}
+        self.last_model_unit = {}
+        mi = 0
+        for fi, g in enumerate(groups):
+            self.first_model_unit[fi] = mi
+            for _ in g:
+                self.owner[mi] = fi
+                mi += 1
+            self.last_model_unit[fi] = mi - 1
+        self._views = [UnitView(self.flat[self.owner[i]], s.name) for i, s in enumerate(unit_specs)]
+
+    def unit(self, i: int) -> UnitView:
+        return self._views[i]
+
+    def load(self, tensors) -> None:
+        """tensors: dict 'unit.param' -> fp32 tensor, or a callable with the same contract."""
+        get = tensors if callable(tensors) else tensors.__getitem__
+        for f in self.flat:
+            f.load_full_fp32(get)
+
+    def gather_full_fp32(self) -> dict:
+        """fp32 copies of the current parameters keyed 'unit.param' (from the bf16 compute copy)."""
+        out = {}
+        for f in self.flat:
+            for (u, p), (o, shape, _) in f.offsets.items():
+                out[f"{u}.{p}"] = f.full[o:o + int(torch.Size(shape).numel())].view(shape).float().cpu()
+        return out
+
+    def master_full_fp32(self, group=None) -> dict:
+        """fp32 master parameters keyed 'unit.param' (all-gathered when sharded)."""
+        out = {}
+        for f in self.flat:
+            if f.world > 1:
+                full = torch.empty(f.padded, device=f.master.device)
+                dist.all_gather_into_tensor(full, f.master, group=group)
+            else:
+                full = f.master
+            for (u, p), (o, shape, _) in f.offsets.items():
+                out[f"{u}.{p}"] = full[o:o + int(torch.Size(shape).numel())].view(shape).cpu().clone()
+        return out
+
+    def grads_full_fp32(self) -> dict:
+        """Unsharded fp32 gradients of the last backward (before the reduce-scatter)."""
+        out = {}
+        for f in self.flat:
+            for (u, p), (o, shape, _) in f.offsets.items():
+                out[f"{u}.{p}"] = f.gfull[o:o + int(torch.Size(shape).numel())].view(shape).cpu().clone()
+        return out
+
+
+class Engine:
+    """Issues the per-unit collectives on a side stream and fences them against compute.
+
+    before_forward(i): compute waits for the all-gather of model unit i's FSDP unit.
+    after_backward(i): when the last model unit of an FSDP unit finished its
+    backward, its gradient reduce-scatter is queued on the comm stream.
+    """
+
+    def __init__(self, params: FlatParams, group=None, world: int = 1, prefetch: int = 2):
+        self.P = params
+        self.group = group
+        self.world = world
+        self.prefetch = prefetch
+        self.comm = torch.cuda.Stream() if world > 1 else None
+        n = len(params.flat)
+        self.ag_done = [torch.cuda.Event() for _ in range(n)]
+        self.rs_done = [torch.cuda.Event() for _ in range(n)]
+        self._issued = 0
+        self.bytes_ag = sum(f.padded * 2 for f in params.flat)
+        self.bytes_rs = sum(f.padded * 4 for f in params.flat)
+
+    # ------------------------------------------------------------------ step
+    def begin_step(self) -> None:
+        for f in self.P.flat:
+            f.gfull.zero_()
+        self._issued = 0
+        if self.world > 1:
+            ready = torch.cuda.Event()
+            ready.record()  # after the previous optimizer step wrote p16
+            self.comm.wait_event(ready)
+            self._issue_until(min(len(self.P.flat), self.prefetch))
+
+    def _issue_until(self, k: int) -> None:
+        with torch.cuda.stream(self.comm):
+            while self._issued < k:
+                f = self.P.flat[self._issued]
+                dist.all_gather_into_tensor(f.full, f.p16, group=self.group)
+                self.ag_done[self._issued].record(self.comm)
+                self._issued += 1
+
+    def before_forward(self, model_unit: int) -> None:
+        if self.world == 1:
+            return
+        fi = self.P.owner[model_unit]
+        if self.P.first_model_unit[fi] != model_unit:
+            return
+        self._issue_until(min(len(self.P.flat), fi + 1 + self.prefetch))
+        torch.cuda.current_stream().wait_event(self.ag_done[fi])
+
+    def after_backward(self, model_unit: int) -> None:
+        if self.world == 1:
+            return
+        fi = self.P.owner[model_unit]
+        if self.P.first_model_unit[fi] != model_unit:
+            return  # the unit's gradients are complete once its first model unit is done
+        done = torch.cuda.Event()
+        done.record()
+        self.comm.wait_event(done)
+        f = self.P.flat[fi]
+        with torch.cuda.stream(self.comm):
+            dist.reduce_scatter_tensor(f.g, f.gfull, op=dist.ReduceOp.AVG, group=self.group)
+            self.rs_done[fi].record(self.comm)
+
+    def end_backward(self) -> None:
+        if self.world == 1:
+            return
+        cur = torch.cuda.current_stream()
+        for e in self.rs_done:
+            cur.wait_event(e)

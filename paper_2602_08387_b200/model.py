@@ -1,0 +1,405 @@
+"""GPT-2 / Llama-style decoder with an explicit, buffer-planned forward+backward.
+
+The reference fixes the model interface to ``nn.Module`` and has
+no model code, so this module is the B200-native decoder the
+registered ``model`` component builds. It is an ``nn.Module`` for the
+interface, but the training step does not run autograd: ``forward_backward``
+is a fixed sequence of C-ABI kernel launches over activation buffers that are
+allocated once per (batch, seq) shape, which keeps the step CUDA-graph
+capturable and lets the backward write weight gradients straight into the
+FSDP flat gradient buffers (see fsdp.py).
+
+Numerics: bf16 weights/activations into tcgen05 GEMMs and attention with
+fp32 accumulation; the residual stream, its gradient, norm statistics, the
+loss and all parameter gradients are fp32.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field, replace
+
+import torch
+
+from . import ops
+
+ALIGN = 64  # parameter offsets inside a flat unit, in elements (128 B of bf16)
+
+
+@dataclass(frozen=True)
+class ModelConfig:
+    arch: str  # "gpt2" | "llama"
+    n_layer: int
+    d_model: int
+    n_head: int
+    n_kv_head: int
+    d_ff: int
+    vocab_size: int
+    max_seq_len: int
+    tie_embeddings: bool = True
+    norm_eps: float = 1e-5
+    rope_theta: float = 500000.0
+    init_std: float = 0.02
+
+    def __post_init__(self):
+        if self.arch not in ("gpt2", "llama"):
+            raise ValueError(f"arch must be gpt2 or llama, got {self.arch!r}")
+        if self.d_model % self.n_head or self.n_head % self.n_kv_head:
+            raise ValueError("d_model % n_head and n_head % n_kv_head must be 0")
+        if self.arch == "gpt2" and self.n_kv_head != self.n_head:
+            raise ValueError("gpt2 uses multi-head attention (n_kv_head == n_head)")
+
+    @property
+    def head_dim(self) -> int:
+        return self.d_model // self.n_head
+
+    @property
+    def padded_vocab(self) -> int:
+        return (self.vocab_size + 127) // 128 * 128
+
+    @property
+    def qkv_dim(self) -> int:
+        return (self.n_head + 2 * self.n_kv_head) * self.head_dim
+
+    def matmul_params(self) -> int:
+        """Parameters that take part in matmuls (incl. the LM head, excl. embeddings/norms)."""
+        d, f = self.d_model, self.d_ff
+        per = d * self.qkv_dim + d * d + (2 if self.arch == "gpt2" else 3) * d * f
+        return self.n_layer * per + d * self.vocab_size
+
+    def flops_per_token(self, seq_len: int) -> float:
+        """Training FLOPs per token: 6 * N_matmul + 12 * L * d * T (PaLM/nanoGPT convention)."""
+        return 6.0 * self.matmul_params() + 12.0 * self.n_layer * self.d_model * seq_len
+
+    def num_params(self) -> int:
+        """Trainable parameters (padded vocabulary rows excluded)."""
+        n = sum(int(torch.Size(p.shape).numel()) for u in unit_specs(self) for p in u.params)
+        pad_rows = (self.padded_vocab - self.vocab_size) * self.d_model
+        return n - pad_rows * (1 if self.tie_embeddings else 2)
+
+
+PRESETS = {
+    # BASELINE.json configs[0]: the CPU-runnable oracle case
+    "tiny-gpt2": ModelConfig("gpt2", 2, 128, 4, 4, 512, 4096, 256),
+    # GPU parity configs (head dim 64, the attention kernel's tile): tiny GPT-2 / tiny Llama
+    "tiny-gpt2-dh64": ModelConfig("gpt2", 2, 256, 4, 4, 1024, 4096, 256),
+    "tiny-llama": ModelConfig("llama", 2, 256, 4, 2, 512, 4096, 256),
+    # configs[1]
+    "gpt2-124m": ModelConfig("gpt2", 12, 768, 12, 12, 3072, 50257, 2048),
+    # configs[2]: Llama-3.2-1B-like (tied head, GQA 32/8, dh 64)
+    "llama-1b": ModelConfig("llama", 16, 2048, 32, 8, 8192, 128256, 4096),
+    # configs[3]: Llama-3-8B-like (untied head, GQA 32/8, dh 128)
+    "llama-8b": ModelConfig("llama", 32, 4096, 32, 8, 14336, 128256, 4096, tie_embeddings=False),
+}
+
+
+@dataclass(frozen=True)
+class ParamSpec:
+    name: str
+    shape: tuple
+    init: str  # normal | resid | zeros | ones
+    decay: bool
+
+
+@dataclass
+class UnitSpec:
+    name: str
+    params: list
+    offsets: dict = field(default_factory=dict)
+    numel: int = 0
+
+    def layout(self):
+        off = 0
+        for p in self.params:
+            self.offsets[p.name] = off
+            n = int(torch.Size(p.shape).numel())
+            off += (n + ALIGN - 1) // ALIGN * ALIGN
+        self.numel = off
+        return self
+
+
+def unit_specs(cfg: ModelConfig) -> list:
+    """FSDP units in execution order: embedding, one per block, final norm (+ head)."""
+    d, f, Vp = cfg.d_model, cfg.d_ff, cfg.padded_vocab
+    units = []
+    emb = [ParamSpec("wte", (Vp, d), "normal", True)]
+    if cfg.arch == "gpt2":
+        emb.append(ParamSpec("wpe", (cfg.max_seq_len, d), "normal", True))
+    units.append(UnitSpec("embed", emb))
+    for i in range(cfg.n_layer):
+        if cfg.arch == "gpt2":
+            ps = [ParamSpec("ln1_g", (d,), "ones", False), ParamSpec("ln1_b", (d,), "zeros", False),
+                  ParamSpec("qkv_w", (cfg.qkv_dim, d), "normal", True), ParamSpec("qkv_b", (cfg.qkv_dim,), "zeros", False),
+                  ParamSpec("proj_w", (d, d), "resid", True), ParamSpec("proj_b", (d,), "zeros", False),
+                  ParamSpec("ln2_g", (d,), "ones", False), ParamSpec("ln2_b", (d,), "zeros", False),
+                  ParamSpec("fc_w", (f, d), "normal", True), ParamSpec("fc_b", (f,), "zeros", False),
+                  ParamSpec("fc2_w", (d, f), "resid", True), ParamSpec("fc2_b", (d,), "zeros", False)]
+        else:
+            ps = [ParamSpec("attn_norm", (d,), "ones", False),
+                  ParamSpec("wqkv", (cfg.qkv_dim, d), "normal", True),
+                  ParamSpec("wo", (d, cfg.n_head * cfg.head_dim), "resid", True),
+                  ParamSpec("mlp_norm", (d,), "ones", False),
+                  ParamSpec("w13", (2 * f, d), "normal", True),
+                  ParamSpec("w2", (d, f), "resid", True)]
+        units.append(UnitSpec(f"block{i}", ps))
+    head = [ParamSpec("lnf_g", (d,), "ones", False)]
+    if cfg.arch == "gpt2":
+        head.append(ParamSpec("lnf_b", (d,), "zeros", False))
+    if not cfg.tie_embeddings:
+        head.append(ParamSpec("lm_head", (Vp, d), "normal", True))
+    units.append(UnitSpec("head", head))
+    return [u.layout() for u in units]
+
+
+def init_params(cfg: ModelConfig, seed: int = 0) -> dict:
+    """fp32 CPU initial weights, generated in unit/param order from one seeded generator.
+
+    N(0, std) for matrices, N(0, std/sqrt(2L)) for residual output projections,
+    ones/zeros for norms and biases; padded vocabulary rows are zero.
+    """
+    g = torch.Generator().manual_seed(seed)
+    out = {}
+    resid_std = cfg.init_std / math.sqrt(2 * cfg.n_layer)
+    for u in unit_specs(cfg):
+        for p in u.params:
+            key = f"{u.name}.{p.name}"
+            if p.init == "ones":
+                t = torch.ones(p.shape)
+            elif p.init == "zeros":
+                t = torch.zeros(p.shape)
+            else:
+                t = torch.empty(p.shape).normal_(0.0, resid_std if p.init == "resid" else cfg.init_std, generator=g)
+            if p.name in ("wte", "lm_head") and cfg.padded_vocab > cfg.vocab_size:
+                t[cfg.vocab_size:] = 0
+            out[key] = t
+    return out
+
+
+def param_initializer(cfg: ModelConfig, seed: int = 0, device="cpu"):
+    """Returns get(key) -> fp32 initial tensor for 'unit.param'.
+
+    device='cpu' replays init_params (one sequential CPU generator: the oracle
+    reproduces it exactly). Any other device generates each tensor on that
+    device from its own generator seeded by (seed, crc32(key)) -- identical on
+    every rank, no host-memory copy of the whole model (used for 1B/8B).
+    """
+    if str(device) == "cpu":
+        tensors = init_params(cfg, seed)
+        return tensors.__getitem__
+    import zlib
+
+    specs = {f"{u.name}.{p.name}": p for u in unit_specs(cfg) for p in u.params}
+    resid_std = cfg.init_std / math.sqrt(2 * cfg.n_layer)
+
+    def get(key):
+        p = specs[key]
+        if p.init == "ones":
+            return torch.ones(p.shape, device=device)
+        if p.init == "zeros":
+            return torch.zeros(p.shape, device=device)
+        g = torch.Generator(device=device).manual_seed((seed * 1_000_003 + zlib.crc32(key.encode())) & 0x7FFFFFFF)
+        t = torch.empty(p.shape, device=device).normal_(0.0, resid_std if p.init == "resid" else cfg.init_std,
+                                                        generator=g)
+        if p.name in ("wte", "lm_head") and cfg.padded_vocab > cfg.vocab_size:
+            t[cfg.vocab_size:] = 0
+        return t
+
+    return get
+
+
+def rope_tables(cfg: ModelConfig, T: int, device):
+    dh = cfg.head_dim
+    inv = 1.0 / (cfg.rope_theta ** (torch.arange(0, dh, 2, dtype=torch.float64) / dh))
+    ang = torch.arange(T, dtype=torch.float64)[:, None] * inv[None]
+    return ang.cos().float().contiguous().to(device), ang.sin().float().contiguous().to(device)
+
+
+class _Acts:
+    """Activation buffers for one (B, T): saved forward tensors + backward scratch."""
+
+    def __init__(self, cfg: ModelConfig, B: int, T: int, device):
+        M, d, f, L = B * T, cfg.d_model, cfg.d_ff, cfg.n_layer
+        bf, f32 = torch.bfloat16, torch.float32
+        e = lambda *s, dt=bf: torch.empty(*s, device=device, dtype=dt)  # noqa: E731
+        self.B, self.T, self.M = B, T, M
+        # residual stream: xs[2i] enters block i's attention, xs[2i+1] its MLP, xs[2L] the head
+        self.xs = [e(M, d, dt=f32) for _ in range(2 * L + 1)]
+        self.ln = [e(M, d) for _ in range(2 * L + 1)]
+        self.mean = [e(M, dt=f32) for _ in range(2 * L + 1)]
+        self.rstd = [e(M, dt=f32) for _ in range(2 * L + 1)]
+        self.qkv = [e(M, cfg.qkv_dim) for _ in range(L)]
+        self.o = [e(M, cfg.n_head * cfg.head_dim) for _ in range(L)]
+        self.lse = [e(B, cfg.n_head, T, dt=f32) for _ in range(L)]
+        if cfg.arch == "gpt2":
+            self.hpre = [e(M, f) for _ in range(L)]
+            self.h = [e(M, f) for _ in range(L)]
+        else:
+            self.gu = [e(M, 2 * f) for _ in range(L)]
+            self.h = [e(M, f) for _ in range(L)]
+        self.logits = e(M, cfg.padded_vocab)
+        self.loss_rows = e(M, dt=f32)
+        self.loss = e(1, dt=f32)
+        # backward scratch (reused across layers)
+        self.dx = e(M, d, dt=f32)
+        self.dxb = e(M, d)
+        self.dln = e(M, d)
+        self.do = e(M, cfg.n_head * cfg.head_dim)
+        self.dqkv = e(M, cfg.qkv_dim)
+        self.dh = e(M, f)
+        if cfg.arch == "llama":
+            self.dgu = e(M, 2 * f)
+        self.attn_work = e(ops._lib.load().b2s_attn_bwd_work_floats(B, T, cfg.n_head, cfg.head_dim), dt=f32)
+
+
+class DecoderLM(torch.nn.Module):
+    """Decoder-only LM whose parameters live in FSDP flat units (see fsdp.FlatParams)."""
+
+    def __init__(self, cfg: ModelConfig):
+        super().__init__()
+        self.cfg = cfg
+        self.units = unit_specs(cfg)
+        self._acts = {}
+        self._rope = {}
+        self.params = None  # fsdp.FlatParams, attached by the trainer
+
+    def attach(self, flat_params) -> None:
+        self.params = flat_params
+
+    def acts(self, B, T, device) -> _Acts:
+        key = (B, T)
+        if key not in self._acts:
+            self._acts.clear()
+            self._acts[key] = _Acts(self.cfg, B, T, device)
+        return self._acts[key]
+
+    def rope(self, T, device):
+        if T not in self._rope:
+            self._rope[T] = rope_tables(self.cfg, T, device)
+        return self._rope[T]
+
+    # ------------------------------------------------------------------ step
+    def forward_backward(self, tokens, targets, hooks=None, compute_grad: bool = True):
+        """One training forward + backward over int64 tokens/targets [B, T].
+
+        Writes fp32 parameter gradients into the flat grad buffers (accumulated;
+        the caller zeroes them) and returns the device scalar mean loss.
+        ``hooks`` (fsdp.Engine) is told when each unit's parameters are needed
+        and when each unit's gradients are complete.
+        """
+        cfg, P = self.cfg, self.params
+        B, T = tokens.shape
+        dev = tokens.device
+        A = self.acts(B, T, dev)
+        M, d, L = A.M, cfg.d_model, cfg.n_layer
+        H, Hkv, dh = cfg.n_head, cfg.n_kv_head, cfg.head_dim
+        gpt2 = cfg.arch == "gpt2"
+        tok = tokens.reshape(-1)
+        tgt = targets.reshape(-1)
+        hk = hooks
+        pre = (lambda u: hk.before_forward(u)) if hk else (lambda u: None)
+        post = (lambda u: hk.after_backward(u)) if hk else (lambda u: None)
+        eps = cfg.norm_eps
+        if not gpt2:
+            cos, sin = self.rope(T, dev)
+
+        # ---------------- forward
+        pre(0)
+        E = P.unit(0)
+        ops.embedding_fwd(tok, E.p("wte"), E.p("wpe") if gpt2 else None, T, out=A.xs[0])
+        for i in range(L):
+            pre(i + 1)
+            U = P.unit(i + 1)
+            a, b = 2 * i, 2 * i + 1
+            if gpt2:
+                ops.layernorm_fwd(A.xs[a], U.p("ln1_g"), U.p("ln1_b"), eps, A.ln[a], A.mean[a], A.rstd[a], x_copy=A.xs[b])
+                ops.linear(A.ln[a], U.p("qkv_w"), bias=U.p("qkv_b"), out=A.qkv[i])
+            else:
+                ops.rmsnorm_fwd(A.xs[a], U.p("attn_norm"), eps, A.ln[a], A.rstd[a], x_copy=A.xs[b])
+                ops.linear(A.ln[a], U.p("wqkv"), out=A.qkv[i])
+                ops.rope(A.qkv[i], T, H + Hkv, dh, cos, sin)
+            ops.attn_fwd(A.qkv[i], B, T, H, Hkv, dh, o=A.o[i], lse=A.lse[i])
+            # residual: xs[b] (= copy of xs[a]) += o @ Wo^T (+ bias)  (fp32 TMA add-reduce)
+            ops.gemm(A.o[i], U.p("proj_w" if gpt2 else "wo"), a_mn=False, b_mn=False, M=M, N=d, K=H * dh,
+                     out=A.xs[b], accumulate=True, bias=U.p("proj_b") if gpt2 else None)
+            nxt = b + 1
+            if gpt2:
+                ops.layernorm_fwd(A.xs[b], U.p("ln2_g"), U.p("ln2_b"), eps, A.ln[b], A.mean[b], A.rstd[b],
+                                  x_copy=A.xs[nxt])
+                ops.linear(A.ln[b], U.p("fc_w"), bias=U.p("fc_b"), out=A.h[i], act=1, aux=A.hpre[i])
+                ops.gemm(A.h[i], U.p("fc2_w"), a_mn=False, b_mn=False, M=M, N=d, K=cfg.d_ff, out=A.xs[nxt],
+                         accumulate=True, bias=U.p("fc2_b"))
+            else:
+                ops.rmsnorm_fwd(A.xs[b], U.p("mlp_norm"), eps, A.ln[b], A.rstd[b], x_copy=A.xs[nxt])
+                ops.linear(A.ln[b], U.p("w13"), out=A.gu[i])
+                ops.swiglu_fwd(A.gu[i], A.h[i])
+                ops.gemm(A.h[i], U.p("w2"), a_mn=False, b_mn=False, M=M, N=d, K=cfg.d_ff, out=A.xs[nxt],
+                         accumulate=True)
+        pre(L + 1)
+        Hd = P.unit(L + 1)
+        f_ = 2 * L
+        if gpt2:
+            ops.layernorm_fwd(A.xs[f_], Hd.p("lnf_g"), Hd.p("lnf_b"), eps, A.ln[f_], A.mean[f_], A.rstd[f_])
+        else:
+            ops.rmsnorm_fwd(A.xs[f_], Hd.p("lnf_g"), eps, A.ln[f_], A.rstd[f_])
+        w_head = E.p("wte") if cfg.tie_embeddings else Hd.p("lm_head")
+        ops.linear(A.ln[f_], w_head, out=A.logits)
+        ops.cross_entropy(A.logits, cfg.vocab_size, tgt, A.loss_rows, grad_scale=1.0 / M, write_grad=compute_grad)
+        ops.sum_(A.loss_rows, A.loss, scale=1.0 / M)
+        if not compute_grad:
+            return A.loss
+
+        # ---------------- backward
+        # head: dlogits (in A.logits) -> d ln_f, dW_head
+        g_head = E.g("wte") if cfg.tie_embeddings else Hd.g("lm_head")
+        ops.linear_wgrad(A.logits, A.ln[f_], out=g_head, accumulate=True)
+        ops.linear_dgrad(A.logits, w_head, out=A.dln)
+        A.dx.zero_()
+        if gpt2:
+            ops.layernorm_bwd(A.xs[f_], A.dln, Hd.p("lnf_g"), A.mean[f_], A.rstd[f_], A.dx, A.dxb,
+                              Hd.g("lnf_g"), Hd.g("lnf_b"))
+        else:
+            ops.rmsnorm_bwd(A.xs[f_], A.dln, Hd.p("lnf_g"), A.rstd[f_], A.dx, A.dxb, Hd.g("lnf_g"))
+        post(L + 1)
+        for i in reversed(range(L)):
+            U = P.unit(i + 1)
+            a, b = 2 * i, 2 * i + 1
+            # --- MLP (its output gradient is the residual gradient dx, bf16 copy in dxb)
+            if gpt2:
+                ops.colsum_accumulate(A.dxb, U.g("fc2_b"))
+                ops.linear_wgrad(A.dxb, A.h[i], out=U.g("fc2_w"), accumulate=True)
+                ops.linear_dgrad(A.dxb, U.p("fc2_w"), out=A.dh, act=2, aux=A.hpre[i])
+                ops.colsum_accumulate(A.dh, U.g("fc_b"))
+                ops.linear_wgrad(A.dh, A.ln[b], out=U.g("fc_w"), accumulate=True)
+                ops.linear_dgrad(A.dh, U.p("fc_w"), out=A.dln)
+                ops.layernorm_bwd(A.xs[b], A.dln, U.p("ln2_g"), A.mean[b], A.rstd[b], A.dx, A.dxb,
+                                  U.g("ln2_g"), U.g("ln2_b"))
+            else:
+                ops.linear_wgrad(A.dxb, A.h[i], out=U.g("w2"), accumulate=True)
+                ops.linear_dgrad(A.dxb, U.p("w2"), out=A.dh)
+                ops.swiglu_bwd(A.gu[i], A.dh, A.dgu)
+                ops.linear_wgrad(A.dgu, A.ln[b], out=U.g("w13"), accumulate=True)
+                ops.linear_dgrad(A.dgu, U.p("w13"), out=A.dln)
+                ops.rmsnorm_bwd(A.xs[b], A.dln, U.p("mlp_norm"), A.rstd[b], A.dx, A.dxb, U.g("mlp_norm"))
+            # --- attention
+            wo = "proj_w" if gpt2 else "wo"
+            if gpt2:
+                ops.colsum_accumulate(A.dxb, U.g("proj_b"))
+            ops.linear_wgrad(A.dxb, A.o[i], out=U.g(wo), accumulate=True)
+            ops.linear_dgrad(A.dxb, U.p(wo), out=A.do)
+            ops.attn_bwd(A.qkv[i], A.o[i], A.do, A.lse[i], B, T, H, Hkv, dh, dqkv=A.dqkv, work=A.attn_work)
+            if not gpt2:
+                ops.rope(A.dqkv, T, H + Hkv, dh, cos, sin, inverse=True)
+            wq = "qkv_w" if gpt2 else "wqkv"
+            if gpt2:
+                ops.colsum_accumulate(A.dqkv, U.g("qkv_b"))
+            ops.linear_wgrad(A.dqkv, A.ln[a], out=U.g(wq), accumulate=True)
+            ops.linear_dgrad(A.dqkv, U.p(wq), out=A.dln)
+            if gpt2:
+                ops.layernorm_bwd(A.xs[a], A.dln, U.p("ln1_g"), A.mean[a], A.rstd[a], A.dx, A.dxb,
+                                  U.g("ln1_g"), U.g("ln1_b"))
+            else:
+                ops.rmsnorm_bwd(A.xs[a], A.dln, U.p("attn_norm"), A.rstd[a], A.dx, A.dxb, U.g("attn_norm"))
+            post(i + 1)
+        ops.embedding_bwd(tok, A.dx, E.g("wte"), E.g("wpe") if gpt2 else None, B, T)
+        post(0)
+        return A.loss

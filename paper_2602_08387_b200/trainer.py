@@ -1,0 +1,102 @@
+"""The SPMD training driver (the paper's "gym") as a registered component.
+
+One process per GPU (torchrun style: RANK / LOCAL_RANK / WORLD_SIZE /
+MASTER_ADDR from the environment), NCCL over NVLink for the FSDP
+collectives. A step is:
+
+  dataloader.batch(step)            H2D of the step's sample ids/windows + K1 gather
+  engine.begin_step()               zero grads, queue all-gathers on the comm stream
+  model.forward_backward(...)       tcgen05 GEMMs / attention + bandwidth kernels;
+                                    reduce-scatters queued per unit during backward
+  engine.end_backward()             compute waits for the reduce-scatters
+  optimizer.step(...)               grad-norm all-reduce + fused sharded AdamW
+  all_reduce(loss, AVG)             for logging (D2H only when the caller asks)
+"""
+
+from __future__ import annotations
+
+import os
+import time
+
+import torch
+import torch.distributed as dist
+
+from .data import PackedDataLoader
+from .fsdp import Engine, FlatParams
+from .model import DecoderLM, param_initializer
+from .optim import AdamWConfig, FusedAdamW
+
+
+def init_distributed():
+    """(rank, world, local_rank, device), initialising NCCL when launched with WORLD_SIZE > 1."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if not torch.cuda.is_available():
+        raise RuntimeError("the training step runs on B200 GPUs only (no CPU fallback)")
+    device = torch.device("cuda", local)
+    torch.cuda.set_device(device)
+    if world > 1 and not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=device)
+    return rank, world, local, device
+
+
+class SPMDTrainer:
+    def __init__(self, model: DecoderLM, optimizer, dataloader: PackedDataLoader, steps: int = 20,
+                 seed: int = 0, blocks_per_unit: int = 1, init_device: str = "cpu", log_every: int = 0):
+        self.model = model
+        self.opt_cfg = optimizer if isinstance(optimizer, AdamWConfig) else optimizer.cfg
+        self.dataloader = dataloader
+        self.steps = steps
+        self.seed = seed
+        self.blocks_per_unit = blocks_per_unit
+        self.init_device = init_device
+        self.log_every = log_every
+        self._ready = False
+
+    def setup(self) -> "SPMDTrainer":
+        if self._ready:
+            return self
+        self.rank, self.world, self.local_rank, self.device = init_distributed()
+        self.group = dist.group.WORLD if self.world > 1 else None
+        cfg = self.model.cfg
+        self.params = FlatParams(self.model.units, self.rank, self.world, self.device, self.blocks_per_unit)
+        init_dev = "cpu" if self.init_device == "cpu" else self.device
+        self.params.load(param_initializer(cfg, self.seed, init_dev))
+        self.model.attach(self.params)
+        self.engine = Engine(self.params, self.group, self.world)
+        self.optimizer = FusedAdamW(self.opt_cfg)
+        self.dataloader.bind(self.rank, self.world, self.device)
+        if self.dataloader.seq_len > cfg.max_seq_len:
+            raise ValueError(f"seq_len {self.dataloader.seq_len} exceeds the model's {cfg.max_seq_len}")
+        self._loss = torch.zeros(1, device=self.device)
+        self._ready = True
+        return self
+
+    def train_step(self, step: int, compute_only: bool = False):
+        """One optimizer step on global batch `step`; returns the device loss (mean over all ranks)."""
+        inputs, targets = self.dataloader.batch(step)
+        return self.step_on(inputs, targets)
+
+    def step_on(self, inputs, targets):
+        self.engine.begin_step()
+        loss = self.model.forward_backward(inputs, targets, hooks=self.engine)
+        self.engine.end_backward()
+        self.optimizer.step(self.params, self.group, self.world)
+        self._loss.copy_(loss)
+        if self.world > 1:
+            dist.all_reduce(self._loss, op=dist.ReduceOp.AVG, group=self.group)
+        return self._loss
+
+    def run(self) -> list:
+        """Train `steps` steps; returns the per-step mean losses (host floats)."""
+        self.setup()
+        losses = []
+        t0 = time.perf_counter()
+        for g in range(self.steps):
+            loss = self.train_step(g)
+            losses.append(float(loss.item()))
+            if self.log_every and self.rank == 0 and (g % self.log_every == 0 or g == self.steps - 1):
+                print(f"step {g:5d}  loss {losses[-1]:.4f}  {time.perf_counter() - t0:.1f}s", flush=True)
+        return losses
