@@ -1,0 +1,304 @@
+"""Training-step throughput on B200: tokens/s (whole job), tokens/s/GPU and MFU.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config gpt2-124m]
+    torchrun --nproc-per-node N bench.py --gpus N ...          (N > 1; one rank per GPU, NCCL)
+
+Workload (BASELINE.json configs[1]): GPT-2 small 124M, FSDP bf16, seq 2048,
+8 sequences per GPU per step (weak scaling), random-init weights, synthetic
+CFPKD001 token data. A step = gather the step's samples from the packed stream,
+forward, backward, reduce-scatter, AdamW. Prints ONE JSON line on rank 0.
+
+`value` is timed with CUDA events on the compute stream (inputs resident in
+HBM), max over ranks. `e2e` repeats the measurement through the public API
+with host buffers: each step's token windows are copied from the host memory
+map into pinned memory and H2D, and the step's loss is read back D2H.
+`--impl reference` times the CPU fp32 oracle of the same step (oracle/) on
+the host cores -- the reference itself has no training step.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "tokens/sec/GPU and MFU, GPT-2/Llama FSDP2 bf16 at 1/2/4/8 B200"
+UNIT = "tokens/s"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return {"hbm_gbs": p["hbm_gbs"], "bf16": p["bf16_tflops"], "bf16_sust": p.get("bf16_tflops_sustained",
+                                                                                         p["bf16_tflops"]),
+                "src": "measured"}
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16": 1590.0, "bf16_sust": 1400.0, "src": "fallback"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                vals = [v.strip() for v in out.stdout.strip().split(",")]
+                if len(vals) == 6:
+                    self.rows.append(vals)
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = sorted(float(r[0]) for r in self.rows)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() in ("active", "1")})
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": float(self.rows[0][1]), "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def _data_path(cfg, n_tokens):
+    from paper_2602_08387_b200.data import synthetic_path
+
+    return synthetic_path(os.path.join(ROOT, ".bench_data"), n_tokens, cfg.vocab_size, kind="uniform", seed=0)
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2602_08387_b200 import _lib, ops
+    from paper_2602_08387_b200.data import PackedDataLoader, Sampler
+    from paper_2602_08387_b200.model import PRESETS, DecoderLM
+    from paper_2602_08387_b200.optim import AdamWConfig
+    from paper_2602_08387_b200.packed import open_packed
+    from paper_2602_08387_b200.trainer import SPMDTrainer
+
+    cfg = PRESETS[args.config]
+    B, T = args.batch, args.seq
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    steps_needed = args.warmup + 2 * args.steps + 2
+    n_tokens = max(1 << 22, (steps_needed * world * B + 4) * T + 1)
+    rank = int(os.environ.get("RANK", "0"))
+    # rank 0 writes the synthetic corpus; the others wait (file name is content-addressed)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    path = None
+    if rank == 0:
+        path = _data_path(cfg, n_tokens)
+    tr = SPMDTrainer(DecoderLM(cfg), AdamWConfig(), None, steps=0, seed=0,
+                     blocks_per_unit=args.blocks_per_unit, init_device="cuda")
+    # distributed init happens in setup(); make sure the data file exists first
+    from paper_2602_08387_b200.trainer import init_distributed
+
+    rank, world, local, device = init_distributed()
+    if world > 1:
+        dist.barrier()
+    path = _data_path(cfg, n_tokens)
+    reader = open_packed(path)
+    tr.dataloader = PackedDataLoader(reader, B, T, Sampler(shuffle=True, seed=0), feed="resident")
+    tr.setup()
+    peaks = _peaks()
+
+    def barrier_sync():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    step = 0
+    for _ in range(args.warmup):
+        tr.train_step(step)
+        step += 1
+    barrier_sync()
+    launches0 = _lib.load().b2s_launch_count()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk, ops.KernelTimer() as kt:
+        start.record()
+        for _ in range(args.steps):
+            tr.train_step(step)
+            step += 1
+        end.record()
+        barrier_sync()
+    launches = _lib.load().b2s_launch_count() - launches0
+    ms = start.elapsed_time(end) / args.steps
+    t = torch.tensor([ms], device=device)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    kern = kt.summary()
+    loss_dev = float(tr._loss.item())
+
+    # ---- end to end through the public API with host buffers (staged windows, loss D2H each step)
+    e2e_dl = PackedDataLoader(reader, B, T, Sampler(shuffle=True, seed=0), feed="staged")
+    e2e_dl.bind(rank, world, device)
+    tr.dataloader = e2e_dl
+    for _ in range(2):
+        tr.train_step(step)
+        step += 1
+    barrier_sync()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        inputs, targets = e2e_dl.batch(step)
+        loss = tr.step_on(inputs, targets)
+        _ = float(loss.item())  # D2H read of the step's result
+        step += 1
+    barrier_sync()
+    e2e_ms = (time.perf_counter() - t0) * 1000 / args.steps
+    te = torch.tensor([e2e_ms], device=device)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_ms = float(te.item())
+
+    if rank != 0:
+        return None
+    tokens_step = world * B * T
+    value = tokens_step / (ms / 1000)
+    per_gpu = value / world
+    fpt = cfg.flops_per_token(T)
+    mfu = per_gpu * fpt / (peaks["bf16"] * 1e12)
+    g = kern.get("gemm", {"flops": 0, "ms": 1e-9, "launches": 0})
+    gemm_tf = g["flops"] / (g["ms"] / 1000) / 1e12 if g["ms"] > 0 else 0.0
+    per_kernel = {k: {"launches_per_step": v["launches"] // args.steps,
+                      "ms_per_step": round(v["ms"] / args.steps, 3),
+                      "tflops": round(v["flops"] / (v["ms"] / 1000) / 1e12, 1) if v["ms"] > 0 else None}
+                  for k, v in kern.items()}
+    out = {
+        "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (uniform token ids, CFPKD001 packed file); "
+                                                          "random-init weights",
+        "config": {"workload": f"{args.config} FSDP training step (fwd+bwd+AdamW), seq {T}, "
+                               f"{B} seqs/GPU", "model": args.config, "global_batch": world * B, "seq_len": T,
+                   "parallelism": f"fsdp{world}", "blocks_per_unit": args.blocks_per_unit,
+                   "l2": "working set (weights + activations) >> 126 MB L2; no explicit flush"},
+        "tokens_per_sec_per_gpu": round(per_gpu, 1),
+        "mfu": round(mfu, 4),
+        "mfu_vs_sustained_peak": round(per_gpu * fpt / (peaks["bf16_sust"] * 1e12), 4),
+        "flops_per_token": fpt,
+        "loss_last": round(loss_dev, 4),
+        "roofline": {"bound": "tensor", "kernel": "b2s gemm (tcgen05)", "achieved": round(gemm_tf, 1),
+                     "peak": peaks["bf16_sust"], "unit": "TFLOP/s", "frac": round(gemm_tf / peaks["bf16_sust"], 3),
+                     "traffic": None, "peak_src": f"{peaks['src']} bf16 sustained (kernel timed inside a long step)",
+                     "launches_per_step": g["launches"] // max(1, args.steps)},
+        "kernels": per_kernel,
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+        "e2e": {"value": round(tokens_step / (e2e_ms / 1000), 1), "unit": UNIT,
+                "ms_per_step": round(e2e_ms, 3),
+                "h2d_bytes_per_step": e2e_dl.h2d_bytes_per_step(), "d2h_bytes_per_step": 4},
+    }
+    if args.cpu_baseline and world == 1:
+        out["cpu_baseline"] = cpu_baseline(cfg, T, args)
+    elif world > 1:
+        out["cpu_baseline"] = None
+    return out
+
+
+def _oracle_step_timer(cfg, T, B, steps, warmup):
+    """Time OracleTrainer steps (CPU fp32) on synthetic samples; returns (tokens/s, threads, secs)."""
+    import torch
+
+    from oracle.model_oracle import OracleTrainer
+    from paper_2602_08387_b200.model import init_params
+
+    torch.manual_seed(0)
+    tr = OracleTrainer(cfg, init_params(cfg, 0))
+    gen = torch.Generator().manual_seed(0)
+    x = torch.randint(0, cfg.vocab_size, (B, T + 1), generator=gen)
+    for _ in range(warmup):
+        tr.step(x[:, :T], x[:, 1:])
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        tr.step(x[:, :T], x[:, 1:])
+    dt = time.perf_counter() - t0
+    return B * T * steps / dt, torch.get_num_threads(), dt
+
+
+def cpu_baseline(cfg, T, args):
+    tps, threads, dt = _oracle_step_timer(cfg, T, 1, 1, 0)
+    return {"value": round(tps, 2), "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"CPU fp32 oracle (oracle/model_oracle.py) of the same {args.config} step: 1 sequence x {T} "
+                      f"tokens, 1 step ({dt:.1f} s), torch threads={threads}, "
+                      f"host cpus={len(os.sched_getaffinity(0))}"}
+
+
+def run_reference(args):
+    from paper_2602_08387_b200.model import PRESETS
+
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return None
+    cfg = PRESETS[args.config]
+    T = args.seq
+    warm = min(args.warmup, 1)
+    tps, threads, dt = _oracle_step_timer(cfg, T, 1, args.steps, warm)
+    return {"metric": METRIC, "value": round(tps, 2), "unit": UNIT, "n_gpus": int(os.environ.get("WORLD_SIZE", 1)),
+            "steps": args.steps, "warmup": warm, "ms_per_step": round(dt * 1000 / args.steps, 1),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic token ids; random-init weights", "impl": "reference",
+            "config": {"workload": f"{args.config} training step (fwd+bwd+AdamW), seq {T}, 1 seq/step sample",
+                       "model": args.config, "global_batch": 1, "seq_len": T, "parallelism": "cpu"},
+            "cpu_baseline": {"value": round(tps, 2), "unit": UNIT, "cores": threads, "kind": "port",
+                             "sample": f"{args.steps} steps of 1 x {T} tokens after {warm} warm-up; the reference "
+                                       "has no training step (SPEC.md:12), so its arm is the CPU fp32 oracle"},
+            "e2e": {"value": round(tps, 2), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="gpt2-124m")
+    ap.add_argument("--batch", type=int, default=8, help="sequences per GPU per step")
+    ap.add_argument("--seq", type=int, default=2048)
+    ap.add_argument("--blocks-per-unit", type=int, default=1)
+    ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    out = run_reference(args) if args.impl == "reference" else run_ours(args)
+    if out is not None:
+        print(json.dumps(out), flush=True)
+    if args.impl == "ours" and int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        import torch.distributed as dist
+
+        if dist.is_initialized():
+            dist.barrier()
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

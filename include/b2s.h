@@ -41,6 +41,8 @@ enum {
 
 const char* b2s_last_error(void);
 int b2s_abi_version(void);
+/* Number of CUDA kernels this library has launched since it was loaded. */
+uint64_t b2s_launch_count(void);
 
 /* ------------------------------------------------------------------ */
 /* Packed data path (CFPKD001)                                         */

@@ -69,7 +69,7 @@ _SIGS = {
     "b2s_attn_bwd": "ppppppiiiiip",
 }
 # functions returning int64 sizes (not statuses): name -> argument signature
-_SIZE_FNS = {"b2s_norm_work_floats": "i", "b2s_colsum_work_floats": "i", "b2s_attn_bwd_work_floats": "iiii"}
+_SIZE_FNS = {"b2s_launch_count": "", "b2s_norm_work_floats": "i", "b2s_colsum_work_floats": "i", "b2s_attn_bwd_work_floats": "iiii"}
 
 _CT = {"p": c_void_p, "i": c_int, "l": c_int64, "u": c_uint64, "f": c_float}
 

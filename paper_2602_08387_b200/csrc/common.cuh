@@ -16,8 +16,11 @@ namespace b2s {
 
 // Thread-local error text behind b2s_last_error().
 void set_error(const char* fmt, ...);
+// Kernels launched by this library since load (b2s_launch_count()).
+void count_launches(int n);
 
-inline int check_launch(const char* what) {
+inline int check_launch(const char* what, int nlaunched = 1) {
+  count_launches(nlaunched);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error("%s: %s", what, cudaGetErrorString(e));

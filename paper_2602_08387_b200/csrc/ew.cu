@@ -526,9 +526,10 @@ static int norm_bwd(const float* x, const void* dy, const void* g, const float* 
   }
   if (rc) return rc;
   const unsigned g2 = (D + 255) / 256;
-  if (dg) reduce_parts_kernel<<<g2, 256, 0, st>>>(work, grid, D, 0, dg);
-  if (!RMS && db) reduce_parts_kernel<<<g2, 256, 0, st>>>(work, grid, D, 1, db);
-  return check_launch("norm_bwd_reduce");
+  int n = 0;
+  if (dg) { reduce_parts_kernel<<<g2, 256, 0, st>>>(work, grid, D, 0, dg); ++n; }
+  if (!RMS && db) { reduce_parts_kernel<<<g2, 256, 0, st>>>(work, grid, D, 1, db); ++n; }
+  return check_launch("norm_bwd_reduce", n);
 }
 
 }  // namespace ew
@@ -569,7 +570,7 @@ int b2s_colsum_accumulate(const void* d_x, int x_f32, int64_t M, int N, int64_t 
   if (x_f32) ew::colsum_kernel<float><<<grid, 128, 0, st>>>((const float*)d_x, M, N, ld, rows_per, d_work);
   else ew::colsum_kernel<__nv_bfloat16><<<grid, 128, 0, st>>>((const __nv_bfloat16*)d_x, M, N, ld, rows_per, d_work);
   ew::colsum_final_kernel<<<(N + 255) / 256, 256, 0, st>>>(d_work, nparts, N, d_out);
-  return check_launch("colsum");
+  return check_launch("colsum", 2);
 }
 int64_t b2s_colsum_work_floats(int N) { return 64LL * N; }
 
@@ -586,7 +587,7 @@ int b2s_embedding_bwd(const int64_t* d_tok, const float* d_dx, float* d_dwte, fl
   const int64_t M = (int64_t)B * T;
   ew::embed_bwd_tok_kernel<<<ew::flat_grid(M * D), 256, 0, st>>>(d_tok, d_dx, d_dwte, M, D);
   if (d_dwpe) ew::embed_bwd_pos_kernel<<<ew::flat_grid((int64_t)T * D, 1), 256, 0, st>>>(d_dx, d_dwpe, B, T, D);
-  return check_launch("embedding_bwd");
+  return check_launch("embedding_bwd", d_dwpe ? 2 : 1);
 }
 
 int b2s_rope(void* d_qkv, int64_t M, int T, int64_t ld, int nheads, int dh, const float* d_cos,

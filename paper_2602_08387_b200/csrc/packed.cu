@@ -7,12 +7,15 @@
 //   never runs the O(n) Python loop (packed_data.py:257-282, :322-333).
 #include <stdlib.h>
 #include <string.h>
+#include <atomic>
 #include <thread>
 #include "common.cuh"
 
 namespace b2s {
 
 static thread_local char g_err[512];
+static std::atomic<unsigned long long> g_launches{0};
+void count_launches(int n) { g_launches.fetch_add((unsigned long long)n, std::memory_order_relaxed); }
 
 void set_error(const char* fmt, ...) {
   va_list ap;
@@ -85,6 +88,7 @@ extern "C" {
 
 const char* b2s_last_error(void) { return b2s::g_err; }
 int b2s_abi_version(void) { return 1; }
+uint64_t b2s_launch_count(void) { return b2s::g_launches.load(); }
 
 int b2s_token_width_for_vocab(uint64_t vocab_size, int* h_width) {
   B2S_REQUIRE(h_width, B2S_EINVAL, "h_width is null");

@@ -15,6 +15,57 @@ _call = _lib.call
 _sp = _lib.stream_ptr
 
 
+class KernelTimer:
+    """CUDA-event timing of selected kernel classes on the launching stream.
+
+    While active (``with KernelTimer() as kt``), every gemm / attention launch
+    is bracketed by events and its algorithmic FLOPs recorded; ``summary()``
+    (after a synchronize) returns per-class launches, FLOPs and milliseconds.
+    """
+
+    active = None
+
+    def __init__(self):
+        self.records = []
+
+    def __enter__(self):
+        KernelTimer.active = self
+        return self
+
+    def __exit__(self, *exc):
+        KernelTimer.active = None
+
+    def start(self):
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        return e
+
+    def stop(self, kind, flops, start):
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        self.records.append((kind, flops, start, e))
+
+    def summary(self):
+        torch.cuda.synchronize()
+        out = {}
+        for kind, flops, s, e in self.records:
+            d = out.setdefault(kind, {"launches": 0, "flops": 0.0, "ms": 0.0})
+            d["launches"] += 1
+            d["flops"] += flops
+            d["ms"] += s.elapsed_time(e)
+        return out
+
+
+def _timed(kind, flops, fn):
+    kt = KernelTimer.active
+    if kt is None:
+        return fn()
+    s = kt.start()
+    r = fn()
+    kt.stop(kind, flops, s)
+    return r
+
+
 def _dev(*ts):
     for t in ts:
         if t is not None and not t.is_cuda:
@@ -44,9 +95,9 @@ def gemm(a, b, *, a_mn: bool, b_mn: bool, M: int, N: int, K: int, out=None, out_
     assert out.stride(-1) == 1 and a.stride(-1) == 1 and b.stride(-1) == 1
     lda, ldb, ldc = a.stride(0), b.stride(0), out.stride(0)
     ld_aux = aux.stride(0) if aux is not None else 0
-    _call("b2s_gemm", a.data_ptr(), int(a_mn), lda, b.data_ptr(), int(b_mn), ldb, out.data_ptr(), ldc,
-          int(out.dtype == torch.float32), M, N, K, int(accumulate), _ptr(bias), act, _ptr(aux), ld_aux,
-          _sp())
+    _timed("gemm", 2.0 * M * N * K, lambda: _call(
+        "b2s_gemm", a.data_ptr(), int(a_mn), lda, b.data_ptr(), int(b_mn), ldb, out.data_ptr(), ldc,
+        int(out.dtype == torch.float32), M, N, K, int(accumulate), _ptr(bias), act, _ptr(aux), ld_aux, _sp()))
     return out
 
 
@@ -213,7 +264,9 @@ def attn_fwd(qkv, B, T, Hq, Hkv, dh, o=None, lse=None):
     _dev(qkv)
     o = torch.empty(B * T, Hq * dh, device=qkv.device, dtype=torch.bfloat16) if o is None else o
     lse = torch.empty(B, Hq, T, device=qkv.device, dtype=torch.float32) if lse is None else lse
-    _call("b2s_attn_fwd", qkv.data_ptr(), o.data_ptr(), lse.data_ptr(), B, T, Hq, Hkv, dh, _sp())
+    flops = 4.0 * B * Hq * dh * T * T / 2  # algorithmic causal FLOPs: QK^T and PV, lower triangle
+    _timed("attn_fwd", flops, lambda: _call("b2s_attn_fwd", qkv.data_ptr(), o.data_ptr(), lse.data_ptr(), B, T,
+                                            Hq, Hkv, dh, _sp()))
     return o, lse
 
 
@@ -222,6 +275,8 @@ def attn_bwd(qkv, o, do, lse, B, T, Hq, Hkv, dh, dqkv=None, work=None):
     dqkv = torch.empty_like(qkv) if dqkv is None else dqkv
     n = _lib.load().b2s_attn_bwd_work_floats(B, T, Hq, dh)
     work = _work(n, qkv.device) if work is None else work
-    _call("b2s_attn_bwd", qkv.data_ptr(), o.data_ptr(), do.data_ptr(), lse.data_ptr(), dqkv.data_ptr(),
-          work.data_ptr(), B, T, Hq, Hkv, dh, _sp())
+    flops = 10.0 * B * Hq * dh * T * T / 2  # S, dP, dV, dK, dQ over the lower triangle
+    _timed("attn_bwd", flops, lambda: _call("b2s_attn_bwd", qkv.data_ptr(), o.data_ptr(), do.data_ptr(),
+                                            lse.data_ptr(), dqkv.data_ptr(), work.data_ptr(), B, T, Hq, Hkv, dh,
+                                            _sp()))
     return dqkv
