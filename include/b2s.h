@@ -112,13 +112,15 @@ int b2s_layernorm_fwd(const float* d_x, const void* d_g, const void* d_b, void* 
 int b2s_rmsnorm_fwd(const float* d_x, const void* d_g, void* d_y, float* d_rstd, float* d_x_copy,
                     int64_t M, int D, float eps, b2s_stream_t stream);
 /* dx (fp32) += norm backward of dy (bf16); d_dx_bf16 (optional) <- bf16(dx);
- * d_dg / d_db (fp32 [D], optional) += parameter grads. d_work holds
- * b2s_norm_work_floats(D) floats. */
+ * d_dg / d_db (fp32 [D], optional) += parameter grads; d_dxsum (optional)
+ * += column sums of the updated dx (the bias gradient of the linear layer
+ * whose output gradient dx is). d_work: b2s_norm_work_floats(D) floats. */
 int b2s_layernorm_bwd(const float* d_x, const void* d_dy, const void* d_g, const float* d_mean,
                       const float* d_rstd, float* d_dx, void* d_dx_bf16, float* d_dg, float* d_db,
-                      float* d_work, int64_t M, int D, b2s_stream_t stream);
+                      float* d_dxsum, float* d_work, int64_t M, int D, b2s_stream_t stream);
 int b2s_rmsnorm_bwd(const float* d_x, const void* d_dy, const void* d_g, const float* d_rstd, float* d_dx,
-                    void* d_dx_bf16, float* d_dg, float* d_work, int64_t M, int D, b2s_stream_t stream);
+                    void* d_dx_bf16, float* d_dg, float* d_dxsum, float* d_work, int64_t M, int D,
+                    b2s_stream_t stream);
 int64_t b2s_norm_work_floats(int D);
 
 /* d_out[c] (fp32) += sum_r x[r, c] over M rows of a bf16 (x_f32=0) or fp32

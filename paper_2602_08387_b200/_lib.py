@@ -51,8 +51,8 @@ _SIGS = {
     "b2s_gemm": "pilpilpliiiiipiplp",
     "b2s_layernorm_fwd": "ppppppplifp",
     "b2s_rmsnorm_fwd": "ppppplifp",
-    "b2s_layernorm_bwd": "pppppppppplip",
-    "b2s_rmsnorm_bwd": "pppppppplip",
+    "b2s_layernorm_bwd": "ppppppppppplip",
+    "b2s_rmsnorm_bwd": "ppppppppplip",
     "b2s_colsum_accumulate": "pililppp",
     "b2s_embedding_fwd": "ppppliip",
     "b2s_embedding_bwd": "ppppiiip",

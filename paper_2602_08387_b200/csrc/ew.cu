@@ -99,7 +99,7 @@ template <int D, int TPR, bool RMS>
 __global__ void __launch_bounds__(kRowThreads) norm_bwd_kernel(
     const float* __restrict__ x, const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ g,
     const float* __restrict__ mean_in, const float* __restrict__ rstd_in, float* __restrict__ dx,
-    __nv_bfloat16* __restrict__ dx_bf16, float* __restrict__ part, int64_t M) {
+    __nv_bfloat16* __restrict__ dx_bf16, float* __restrict__ part, int64_t M, int want_dxsum) {
   constexpr int V = D / (TPR * 4);
   constexpr int kGroups = kRowThreads / TPR;  // rows processed concurrently by the block
   constexpr int kChunk = 1024;                // columns reduced per smem pass
@@ -108,12 +108,12 @@ __global__ void __launch_bounds__(kRowThreads) norm_bwd_kernel(
   const int t = threadIdx.x % TPR, grp = threadIdx.x / TPR;
   const int64_t r0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / TPR;
   const int64_t nr = ((int64_t)gridDim.x * blockDim.x) / TPR;
-  float gv[V][4], dg[V][4], db[V][4];
+  float gv[V][4], dg[V][4], db[V][4], ds[V][4];
 #pragma unroll
   for (int j = 0; j < V; ++j) {
     ld_bf4(g + t * 4 + j * TPR * 4, gv[j]);
 #pragma unroll
-    for (int u = 0; u < 4; ++u) { dg[j][u] = 0.f; db[j][u] = 0.f; }
+    for (int u = 0; u < 4; ++u) { dg[j][u] = 0.f; db[j][u] = 0.f; ds[j][u] = 0.f; }
   }
   // rows per group are equal for every group except the tail; loop bound must
   // be uniform across the block when TPR spans the block (block_sum syncs)
@@ -150,14 +150,16 @@ __global__ void __launch_bounds__(kRowThreads) norm_bwd_kernel(
       o.z += rstd * (dyg[j][2] - s1 - xh[j][2] * s2);
       o.w += rstd * (dyg[j][3] - s1 - xh[j][3] * s2);
       st4(dxp, o);
+      ds[j][0] += o.x; ds[j][1] += o.y; ds[j][2] += o.z; ds[j][3] += o.w;
       if (dx_bf16) {
         float f[4] = {o.x, o.y, o.z, o.w};
         st_bf4(dx_bf16 + row * D + t * 4 + j * TPR * 4, f);
       }
     }
   }
-  // block-level reduction of dg (then db) over the row groups -> part[block]
-  for (int pass = 0; pass < (RMS ? 1 : 2); ++pass) {
+  // block-level reduction of dg, db, sum(dx) over the row groups -> part[block][pass]
+  for (int pass = 0; pass < 3; ++pass) {
+    if ((pass == 1 && RMS) || (pass == 2 && !want_dxsum)) continue;
     for (int c0 = 0; c0 < D; c0 += kChunk) {
       __syncthreads();
 #pragma unroll
@@ -165,7 +167,7 @@ __global__ void __launch_bounds__(kRowThreads) norm_bwd_kernel(
         const int col = t * 4 + j * TPR * 4;
         if (col >= c0 && col < c0 + kChunk) {
 #pragma unroll
-          for (int u = 0; u < 4; ++u) red[grp][col - c0 + u] = pass == 0 ? dg[j][u] : db[j][u];
+          for (int u = 0; u < 4; ++u) red[grp][col - c0 + u] = pass == 0 ? dg[j][u] : pass == 1 ? db[j][u] : ds[j][u];
         }
       }
       __syncthreads();
@@ -173,49 +175,89 @@ __global__ void __launch_bounds__(kRowThreads) norm_bwd_kernel(
         float acc = 0.f;
 #pragma unroll
         for (int w = 0; w < kGroups; ++w) acc += red[w][c];
-        part[((int64_t)blockIdx.x * 2 + pass) * D + c0 + c] = acc;
+        part[((int64_t)blockIdx.x * 3 + pass) * D + c0 + c] = acc;
       }
     }
   }
 }
 
-// out[c] += sum_b part[b][which][c]  (deterministic second stage)
-__global__ void reduce_parts_kernel(const float* __restrict__ part, int nblocks, int D, int which,
-                                    float* __restrict__ out) {
-  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < D; c += gridDim.x * blockDim.x) {
-    float acc = 0.f;
-    for (int b = 0; b < nblocks; ++b) acc += part[((int64_t)b * 2 + which) * D + c];
-    out[c] += acc;
+// out[c] += sum_b part[b][which][c]  (deterministic second stage): block =
+// 32 columns x 8 row groups, fixed summation order.
+__global__ void __launch_bounds__(256) reduce_parts_kernel(const float* __restrict__ part, int nblocks, int D,
+                                                           int which, float* __restrict__ out) {
+  __shared__ float red[8][33];
+  const int c = blockIdx.x * 32 + (threadIdx.x & 31), rg = threadIdx.x >> 5;
+  float acc = 0.f;
+  if (c < D)
+    for (int b = rg; b < nblocks; b += 8) acc += part[((int64_t)b * 3 + which) * D + c];
+  red[rg][threadIdx.x & 31] = acc;
+  __syncthreads();
+  if (rg == 0 && c < D) {
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += red[k][threadIdx.x & 31];
+    out[c] += s;
   }
 }
 
 // ------------------------------------------------------------------ column sums
 // part[blockIdx.y][c] = sum over this block's rows of x[r][c] (bf16 or fp32 x).
+// 8 warps stride the rows; each lane owns one 16-byte column vector, so a warp
+// reads 512 contiguous bytes per row. Requires N, ld multiples of the vector.
 template <typename T>
-__global__ void colsum_kernel(const T* __restrict__ x, int64_t M, int N, int64_t ld, int rows_per,
-                              float* __restrict__ part) {
-  const int c = (blockIdx.x * blockDim.x + threadIdx.x) * 2;
-  if (c >= N) return;
+__global__ void __launch_bounds__(256) colsum_kernel(const T* __restrict__ x, int64_t M, int N, int64_t ld,
+                                                     int rows_per, float* __restrict__ part) {
+  constexpr int VEC = 16 / sizeof(T);
+  constexpr int COLS = 32 * VEC;
+  __shared__ float red[8][COLS];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int c = blockIdx.x * COLS + lane * VEC;
   const int64_t r0 = (int64_t)blockIdx.y * rows_per;
   const int64_t r1 = min(M, r0 + rows_per);
-  float a0 = 0.f, a1 = 0.f;
-  for (int64_t r = r0; r < r1; ++r) {
-    if constexpr (sizeof(T) == 2) {
-      float2 v = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(x + r * ld + c));
-      a0 += v.x; a1 += v.y;
-    } else {
-      float2 v = *reinterpret_cast<const float2*>(x + r * ld + c);
-      a0 += v.x; a1 += v.y;
+  float acc[VEC];
+#pragma unroll
+  for (int i = 0; i < VEC; ++i) acc[i] = 0.f;
+  if (c < N) {
+    for (int64_t r = r0 + w; r < r1; r += 8) {
+      if constexpr (sizeof(T) == 2) {
+        float f[8];
+        unpack8(*reinterpret_cast<const bf16x8*>(x + r * ld + c), f);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i] += f[i];
+      } else {
+        float4 v = *reinterpret_cast<const float4*>(x + r * ld + c);
+        acc[0] += v.x; acc[1] += v.y; acc[2] += v.z; acc[3] += v.w;
+      }
     }
   }
-  part[(int64_t)blockIdx.y * N + c] = a0;
-  if (c + 1 < N) part[(int64_t)blockIdx.y * N + c + 1] = a1;
+#pragma unroll
+  for (int i = 0; i < VEC; ++i) red[w][lane * VEC + i] = acc[i];
+  __syncthreads();
+  for (int k = threadIdx.x; k < COLS; k += blockDim.x) {
+    const int cc = blockIdx.x * COLS + k;
+    if (cc < N) {
+      float s = 0.f;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) s += red[j][k];
+      part[(int64_t)blockIdx.y * N + cc] = s;
+    }
+  }
 }
-__global__ void colsum_final_kernel(const float* __restrict__ part, int nparts, int N, float* __restrict__ out) {
-  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < N; c += gridDim.x * blockDim.x) {
-    float acc = 0.f;
-    for (int p = 0; p < nparts; ++p) acc += part[(int64_t)p * N + c];
-    out[c] += acc;
+// out[c] += sum_p part[p][c]: 32 columns x 8 part-groups per block, fixed order.
+__global__ void __launch_bounds__(256) colsum_final_kernel(const float* __restrict__ part, int nparts, int N,
+                                                           float* __restrict__ out) {
+  __shared__ float red[8][33];
+  const int c = blockIdx.x * 32 + (threadIdx.x & 31), rg = threadIdx.x >> 5;
+  float acc = 0.f;
+  if (c < N)
+    for (int p = rg; p < nparts; p += 8) acc += part[(int64_t)p * N + c];
+  red[rg][threadIdx.x & 31] = acc;
+  __syncthreads();
+  if (rg == 0 && c < N) {
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += red[k][threadIdx.x & 31];
+    out[c] += s;
   }
 }
 
@@ -499,16 +541,19 @@ static int norm_fwd(const float* x, const void* g, const void* b, void* y, float
   return B2S_EUNSUPPORTED;
 }
 
+constexpr int kNormBwdMaxBlocks = kNumSMs * 4;
+
 template <bool RMS>
 static int norm_bwd(const float* x, const void* dy, const void* g, const float* mean, const float* rstd,
-                    float* dx, void* dx_bf16, float* dg, float* db, float* work, int64_t M, int D,
+                    float* dx, void* dx_bf16, float* dg, float* db, float* dxsum, float* work, int64_t M, int D,
                     cudaStream_t st) {
   unsigned grid = 0;
   auto go = [&](auto kern, int tpr) {
     int64_t blocks = (M * tpr + kRowThreads - 1) / kRowThreads;
-    grid = (unsigned)(blocks < kNumSMs ? blocks : kNumSMs);  // partial buffer: grid * 2 * D floats
+    const int64_t cap = tpr == 32 ? kNormBwdMaxBlocks : kNumSMs * 2;
+    grid = (unsigned)(blocks < cap ? blocks : cap);  // partial buffer: grid * 3 * D floats
     kern<<<grid, kRowThreads, 0, st>>>(x, (const __nv_bfloat16*)dy, (const __nv_bfloat16*)g, mean, rstd, dx,
-                                       (__nv_bfloat16*)dx_bf16, work, M);
+                                       (__nv_bfloat16*)dx_bf16, work, M, dxsum != nullptr);
     return check_launch("norm_bwd");
   };
   int rc;
@@ -525,10 +570,11 @@ static int norm_bwd(const float* x, const void* dy, const void* g, const float* 
       return B2S_EUNSUPPORTED;
   }
   if (rc) return rc;
-  const unsigned g2 = (D + 255) / 256;
+  const unsigned g2 = (D + 31) / 32;
   int n = 0;
   if (dg) { reduce_parts_kernel<<<g2, 256, 0, st>>>(work, grid, D, 0, dg); ++n; }
   if (!RMS && db) { reduce_parts_kernel<<<g2, 256, 0, st>>>(work, grid, D, 1, db); ++n; }
+  if (dxsum) { reduce_parts_kernel<<<g2, 256, 0, st>>>(work, grid, D, 2, dxsum); ++n; }
   return check_launch("norm_bwd_reduce", n);
 }
 
@@ -549,30 +595,36 @@ int b2s_rmsnorm_fwd(const float* d_x, const void* d_g, void* d_y, float* d_rstd,
 }
 int b2s_layernorm_bwd(const float* d_x, const void* d_dy, const void* d_g, const float* d_mean,
                       const float* d_rstd, float* d_dx, void* d_dx_bf16, float* d_dg, float* d_db,
-                      float* d_work, int64_t M, int D, b2s_stream_t stream) {
-  return ew::norm_bwd<false>(d_x, d_dy, d_g, d_mean, d_rstd, d_dx, d_dx_bf16, d_dg, d_db, d_work, M, D,
+                      float* d_dxsum, float* d_work, int64_t M, int D, b2s_stream_t stream) {
+  return ew::norm_bwd<false>(d_x, d_dy, d_g, d_mean, d_rstd, d_dx, d_dx_bf16, d_dg, d_db, d_dxsum, d_work, M, D,
                              (cudaStream_t)stream);
 }
 int b2s_rmsnorm_bwd(const float* d_x, const void* d_dy, const void* d_g, const float* d_rstd, float* d_dx,
-                    void* d_dx_bf16, float* d_dg, float* d_work, int64_t M, int D, b2s_stream_t stream) {
-  return ew::norm_bwd<true>(d_x, d_dy, d_g, nullptr, d_rstd, d_dx, d_dx_bf16, d_dg, nullptr, d_work, M, D,
-                            (cudaStream_t)stream);
+                    void* d_dx_bf16, float* d_dg, float* d_dxsum, float* d_work, int64_t M, int D,
+                    b2s_stream_t stream) {
+  return ew::norm_bwd<true>(d_x, d_dy, d_g, nullptr, d_rstd, d_dx, d_dx_bf16, d_dg, nullptr, d_dxsum, d_work, M,
+                            D, (cudaStream_t)stream);
 }
-int64_t b2s_norm_work_floats(int D) { return (int64_t)kNumSMs * 2 * D; }
+int64_t b2s_norm_work_floats(int D) { return (int64_t)ew::kNormBwdMaxBlocks * 3 * D; }
 
 int b2s_colsum_accumulate(const void* d_x, int x_f32, int64_t M, int N, int64_t ld, float* d_out,
                           float* d_work, b2s_stream_t stream) {
-  B2S_REQUIRE(N % 2 == 0 && ld % 2 == 0, B2S_EUNSUPPORTED, "colsum: N and ld must be even");
+  const int vec = x_f32 ? 4 : 8;
+  B2S_REQUIRE(N % vec == 0 && ld % vec == 0 && ((uintptr_t)d_x % 16) == 0, B2S_EUNSUPPORTED,
+              "colsum: N and ld must be multiples of %d and x 16-byte aligned", vec);
   cudaStream_t st = (cudaStream_t)stream;
-  const int nparts = 64;
+  const int cols = 32 * vec;
+  const int nblk = (N + cols - 1) / cols;
+  int nparts = (4 * kNumSMs + nblk - 1) / nblk;  // ~4 blocks per SM
+  if (nparts > 256) nparts = 256;
   const int rows_per = (int)((M + nparts - 1) / nparts);
-  dim3 grid((N / 2 + 127) / 128, nparts);
-  if (x_f32) ew::colsum_kernel<float><<<grid, 128, 0, st>>>((const float*)d_x, M, N, ld, rows_per, d_work);
-  else ew::colsum_kernel<__nv_bfloat16><<<grid, 128, 0, st>>>((const __nv_bfloat16*)d_x, M, N, ld, rows_per, d_work);
-  ew::colsum_final_kernel<<<(N + 255) / 256, 256, 0, st>>>(d_work, nparts, N, d_out);
+  dim3 grid(nblk, nparts);
+  if (x_f32) ew::colsum_kernel<float><<<grid, 256, 0, st>>>((const float*)d_x, M, N, ld, rows_per, d_work);
+  else ew::colsum_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>((const __nv_bfloat16*)d_x, M, N, ld, rows_per, d_work);
+  ew::colsum_final_kernel<<<(N + 31) / 32, 256, 0, st>>>(d_work, nparts, N, d_out);
   return check_launch("colsum", 2);
 }
-int64_t b2s_colsum_work_floats(int N) { return 64LL * N; }
+int64_t b2s_colsum_work_floats(int N) { return 256LL * N; }
 
 int b2s_embedding_fwd(const int64_t* d_tok, const void* d_wte, const void* d_wpe, float* d_x, int64_t M,
                       int T, int D, b2s_stream_t stream) {

@@ -6,8 +6,8 @@
 // MN-major ([K][M] / [K][N]); that covers forward (X W^T), dgrad (dY W) and
 // wgrad (dY^T X) of a row-major nn.Linear without any transpose kernel.
 //
-// Roles (192 threads): warp0 = TMA producer, warp1 = TMEM owner + MMA issuer,
-// warps 2..5 = epilogue. Operand tiles are staged by TMA into 128B-swizzled
+// Roles (320 threads): warp0 = TMA producer, warp1 = TMEM owner + MMA issuer,
+// warps 2..9 = epilogue. Operand tiles are staged by TMA into 128B-swizzled
 // shared memory (kStages-deep ring of full/empty mbarriers); the fp32
 // accumulator lives in TMEM, double-buffered so the epilogue of tile i
 // overlaps the MMAs of tile i+1. The epilogue moves 32x32 sub-tiles
@@ -62,8 +62,8 @@ namespace gemm {
 constexpr int BM = 128;
 constexpr int BK = 64;  // 64 bf16 = 128 B = one swizzle row
 constexpr int UMMA_K = 16;
-constexpr int kThreads = 192;
-constexpr int kEpiWarps = 4;
+constexpr int kEpiWarps = 8;  // two per TMEM lane quarter, splitting the tile's columns
+constexpr int kThreads = 64 + 32 * kEpiWarps;
 constexpr int kStageSlot = 4096;  // one 32x32 fp32 (or bf16) staging sub-tile
 constexpr int kEpiSmem = kEpiWarps * 2 * kStageSlot;
 
@@ -76,16 +76,21 @@ struct Epi {
   int64_t ld_aux;
 };
 
+__device__ __forceinline__ float tanh_fast(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 __device__ __forceinline__ float gelu_tanh(float x) {
   const float k0 = 0.7978845608028654f, k1 = 0.044715f;
   float u = k0 * (x + k1 * x * x * x);
-  return 0.5f * x * (1.f + tanhf(u));
+  return 0.5f * x * (1.f + tanh_fast(u));
 }
 __device__ __forceinline__ float gelu_tanh_grad(float x) {
   const float k0 = 0.7978845608028654f, k1 = 0.044715f;
   float x2 = x * x;
   float u = k0 * (x + k1 * x2 * x);
-  float t = tanhf(u);
+  float t = tanh_fast(u);
   return 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * k0 * (1.f + 3.f * k1 * x2);
 }
 
@@ -94,7 +99,7 @@ struct Cfg {
   static constexpr int kABytes = BM * BK * 2;
   static constexpr int kBBytes = BN * BK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kStages = (BN == 256) ? 4 : 6;
+  static constexpr int kStages = (BN == 256) ? 3 : 4;
   static constexpr int kTmemCols = 2 * BN;  // double-buffered accumulator
   static constexpr int kSmem = kStages * kStageBytes + kEpiSmem + 1024 /*align*/ + 256 /*barriers*/;
   static_assert(kSmem <= 227 * 1024, "smem budget");
@@ -138,7 +143,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* empty = full + C_::kStages;
   uint64_t* tfull = empty + C_::kStages;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* auxbar = tempty + 2;  // [kEpiWarps]: aux-tile TMA loads (dGELU epilogue)
+  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(auxbar + kEpiWarps);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int num_m = (M + BM - 1) / BM, num_n = (N + BN - 1) / BN;
@@ -152,6 +158,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch(&tmC);
     for (int s = 0; s < C_::kStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], kEpiWarps); }
+    for (int w = 0; w < kEpiWarps; ++w) mbar_init(&auxbar[w], 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<C_::kTmemCols>(tmem_base_slot);
@@ -228,12 +235,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     __syncwarp();
   } else {
-    // ------------------------------------------------ epilogue warps 2..5
+    // ------------------------------------------------ epilogue warps 2..9
     const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const int half = (warp - 2) >> 2;  // which alternate 32-column chunks this warp owns
     uint8_t* ring = epi_smem + (warp - 2) * 2 * kStageSlot;
     int slot = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
+    uint32_t aux_phase = 0;
     // Hand the next staging slot to this warp: the bulk store issued from it
     // two jobs ago must have finished reading smem.
     auto next_slot = [&]() -> uint8_t* {
@@ -249,19 +258,27 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const int rbase = m0 + q * 32;
-      const int row = rbase + lane;
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
+      for (int c = half; c < BN / 32; c += 2) {
         const int col0 = n0 + c * 32;
+        const bool live = rbase < M && col0 < N;  // warp-uniform
+        uint8_t* slot_b = nullptr;
+        if (epi.act == 2 && live) {  // dGELU: TMA the 32x32 pre-activation tile into the slot's upper half
+          slot_b = next_slot();
+          if (lane == 0) {
+            mbar_arrive_expect_tx(&auxbar[warp - 2], 2048);
+            tma_load_2d(slot_b + 2048, &tmAux, &auxbar[warp - 2], col0, rbase);
+          }
+        }
         uint32_t r[32];
         tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, r);
         tmem_wait_ld();
-        if (c == BN / 32 - 1) {  // accumulator fully read: release it to the MMA warp
+        if (c + 2 >= BN / 32) {  // this warp's last chunk read: release the accumulator
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&tempty[acc]);
         }
-        if (rbase >= M || col0 >= N) continue;  // warp-uniform
+        if (!live) continue;
         float v[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
@@ -284,19 +301,19 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (lane == 0) { tma_store_2d(&tmAux, b, col0, rbase); bulk_commit(); }
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] = gelu_tanh(__bfloat162float(__float2bfloat16_rn(v[i])));
-        } else if (epi.act == 2 && row < M) {
-          const __nv_bfloat16* ap = epi.aux_in + (int64_t)row * epi.ld_aux + col0;
+        } else if (epi.act == 2) {
+          mbar_wait(&auxbar[warp - 2], aux_phase);
+          aux_phase ^= 1;
+          const uint8_t* ap = slot_b + 2048;
 #pragma unroll
-          for (int i = 0; i < 32; i += 8) {
-            if (col0 + i < N) {
-              float h[8];
-              unpack8(*reinterpret_cast<const bf16x8*>(ap + i), h);
+          for (int c8 = 0; c8 < 4; ++c8) {
+            float h[8];
+            unpack8(*reinterpret_cast<const bf16x8*>(ap + lane * 64 + ((c8 ^ ((lane >> 1) & 3)) << 4)), h);
 #pragma unroll
-              for (int j = 0; j < 8; ++j) v[i + j] *= gelu_tanh_grad(h[j]);
-            }
+            for (int j = 0; j < 8; ++j) v[c8 * 8 + j] *= gelu_tanh_grad(h[j]);
           }
         }
-        uint8_t* b = next_slot();
+        uint8_t* b = slot_b ? slot_b : next_slot();
         if (epi.out_f32) stage_f32(b, lane, v);
         else stage_bf16(b, lane, v);
         fence_proxy_async_smem();
@@ -390,7 +407,7 @@ extern "C" int b2s_gemm(const void* d_A, int a_mn_major, int64_t lda, const void
   if (c_f32) rc = encode_tma_2d(&tc, d_C, 4, (uint64_t)N, (uint64_t)M, (uint64_t)ldc * 4, 32, 32, 128);
   else rc = encode_tma_2d(&tc, d_C, 2, (uint64_t)N, (uint64_t)M, (uint64_t)ldc * 2, 32, 32, 64);
   if (rc) return rc;
-  if (act == 1) rc = encode_tma_2d(&tx, d_aux, 2, (uint64_t)N, (uint64_t)M, (uint64_t)ld_aux * 2, 32, 32, 64);
+  if (act == 1 || act == 2) rc = encode_tma_2d(&tx, d_aux, 2, (uint64_t)N, (uint64_t)M, (uint64_t)ld_aux * 2, 32, 32, 64);
   else tx = tc;
   if (rc) return rc;
   gemm::Epi e{c_f32, accumulate, (const __nv_bfloat16*)d_bias, act, (const __nv_bfloat16*)d_aux, ld_aux};

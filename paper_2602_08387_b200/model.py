@@ -355,8 +355,9 @@ class DecoderLM(torch.nn.Module):
         ops.linear_dgrad(A.logits, w_head, out=A.dln)
         A.dx.zero_()
         if gpt2:
+            # the updated dx is the output gradient of the last block's fc2 -> its bias grad
             ops.layernorm_bwd(A.xs[f_], A.dln, Hd.p("lnf_g"), A.mean[f_], A.rstd[f_], A.dx, A.dxb,
-                              Hd.g("lnf_g"), Hd.g("lnf_b"))
+                              Hd.g("lnf_g"), Hd.g("lnf_b"), dxsum=P.unit(L).g("fc2_b"))
         else:
             ops.rmsnorm_bwd(A.xs[f_], A.dln, Hd.p("lnf_g"), A.rstd[f_], A.dx, A.dxb, Hd.g("lnf_g"))
         post(L + 1)
@@ -364,15 +365,14 @@ class DecoderLM(torch.nn.Module):
             U = P.unit(i + 1)
             a, b = 2 * i, 2 * i + 1
             # --- MLP (its output gradient is the residual gradient dx, bf16 copy in dxb)
-            if gpt2:
-                ops.colsum_accumulate(A.dxb, U.g("fc2_b"))
+            if gpt2:  # fc2_b's grad was summed by the norm backward that produced dx
                 ops.linear_wgrad(A.dxb, A.h[i], out=U.g("fc2_w"), accumulate=True)
                 ops.linear_dgrad(A.dxb, U.p("fc2_w"), out=A.dh, act=2, aux=A.hpre[i])
                 ops.colsum_accumulate(A.dh, U.g("fc_b"))
                 ops.linear_wgrad(A.dh, A.ln[b], out=U.g("fc_w"), accumulate=True)
                 ops.linear_dgrad(A.dh, U.p("fc_w"), out=A.dln)
                 ops.layernorm_bwd(A.xs[b], A.dln, U.p("ln2_g"), A.mean[b], A.rstd[b], A.dx, A.dxb,
-                                  U.g("ln2_g"), U.g("ln2_b"))
+                                  U.g("ln2_g"), U.g("ln2_b"), dxsum=U.g("proj_b"))
             else:
                 ops.linear_wgrad(A.dxb, A.h[i], out=U.g("w2"), accumulate=True)
                 ops.linear_dgrad(A.dxb, U.p("w2"), out=A.dh)
@@ -382,8 +382,6 @@ class DecoderLM(torch.nn.Module):
                 ops.rmsnorm_bwd(A.xs[b], A.dln, U.p("mlp_norm"), A.rstd[b], A.dx, A.dxb, U.g("mlp_norm"))
             # --- attention
             wo = "proj_w" if gpt2 else "wo"
-            if gpt2:
-                ops.colsum_accumulate(A.dxb, U.g("proj_b"))
             ops.linear_wgrad(A.dxb, A.o[i], out=U.g(wo), accumulate=True)
             ops.linear_dgrad(A.dxb, U.p(wo), out=A.do)
             ops.attn_bwd(A.qkv[i], A.o[i], A.do, A.lse[i], B, T, H, Hkv, dh, dqkv=A.dqkv, work=A.attn_work)
@@ -395,8 +393,9 @@ class DecoderLM(torch.nn.Module):
             ops.linear_wgrad(A.dqkv, A.ln[a], out=U.g(wq), accumulate=True)
             ops.linear_dgrad(A.dqkv, U.p(wq), out=A.dln)
             if gpt2:
+                prev_fc2_b = P.unit(i).g("fc2_b") if i > 0 else None
                 ops.layernorm_bwd(A.xs[a], A.dln, U.p("ln1_g"), A.mean[a], A.rstd[a], A.dx, A.dxb,
-                                  U.g("ln1_g"), U.g("ln1_b"))
+                                  U.g("ln1_g"), U.g("ln1_b"), dxsum=prev_fc2_b)
             else:
                 ops.rmsnorm_bwd(A.xs[a], A.dln, U.p("attn_norm"), A.rstd[a], A.dx, A.dxb, U.g("attn_norm"))
             post(i + 1)

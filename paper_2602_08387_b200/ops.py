@@ -40,15 +40,27 @@ class KernelTimer:
         e.record()
         return e
 
-    def stop(self, kind, flops, start):
+    def stop(self, kind, flops, start, detail=None):
         e = torch.cuda.Event(enable_timing=True)
         e.record()
-        self.records.append((kind, flops, start, e))
+        self.records.append((kind, flops, start, e, detail))
+
+    def detail(self):
+        """Per (kind, detail) launches / ms / TFLOP/s, sorted by time."""
+        torch.cuda.synchronize()
+        out = {}
+        for kind, flops, s, e, det in self.records:
+            d = out.setdefault((kind, det), [0, 0.0, 0.0])
+            d[0] += 1
+            d[1] += s.elapsed_time(e)
+            d[2] += flops
+        return sorted(((k, n, ms, fl / (ms / 1e3) / 1e12 if ms else 0) for k, (n, ms, fl) in out.items()),
+                      key=lambda r: -r[2])
 
     def summary(self):
         torch.cuda.synchronize()
         out = {}
-        for kind, flops, s, e in self.records:
+        for kind, flops, s, e, _ in self.records:
             d = out.setdefault(kind, {"launches": 0, "flops": 0.0, "ms": 0.0})
             d["launches"] += 1
             d["flops"] += flops
@@ -56,13 +68,13 @@ class KernelTimer:
         return out
 
 
-def _timed(kind, flops, fn):
+def _timed(kind, flops, fn, detail=None):
     kt = KernelTimer.active
     if kt is None:
         return fn()
     s = kt.start()
     r = fn()
-    kt.stop(kind, flops, s)
+    kt.stop(kind, flops, s, detail)
     return r
 
 
@@ -97,7 +109,9 @@ def gemm(a, b, *, a_mn: bool, b_mn: bool, M: int, N: int, K: int, out=None, out_
     ld_aux = aux.stride(0) if aux is not None else 0
     _timed("gemm", 2.0 * M * N * K, lambda: _call(
         "b2s_gemm", a.data_ptr(), int(a_mn), lda, b.data_ptr(), int(b_mn), ldb, out.data_ptr(), ldc,
-        int(out.dtype == torch.float32), M, N, K, int(accumulate), _ptr(bias), act, _ptr(aux), ld_aux, _sp()))
+        int(out.dtype == torch.float32), M, N, K, int(accumulate), _ptr(bias), act, _ptr(aux), ld_aux, _sp()),
+        detail=(M, N, K, "MN" if a_mn else "K", "MN" if b_mn else "K", "f32" if out.dtype == torch.float32 else "bf16",
+                "acc" if accumulate else "", "bias" if bias is not None else "", act))
     return out
 
 
@@ -166,19 +180,19 @@ def rmsnorm_fwd(x, g, eps=1e-5, y=None, rstd=None, x_copy=None):
     return y, rstd
 
 
-def layernorm_bwd(x, dy, g, mean, rstd, dx, dx_bf16=None, dg=None, db=None):
-    """dx += LN backward; dg/db (fp32) accumulated."""
+def layernorm_bwd(x, dy, g, mean, rstd, dx, dx_bf16=None, dg=None, db=None, dxsum=None):
+    """dx += LN backward; dg/db (fp32) accumulated; dxsum += colsum(updated dx)."""
     M, D = x.shape
     work = _work(_lib.load().b2s_norm_work_floats(D), x.device)
     _call("b2s_layernorm_bwd", x.data_ptr(), dy.data_ptr(), g.data_ptr(), mean.data_ptr(), rstd.data_ptr(),
-          dx.data_ptr(), _ptr(dx_bf16), _ptr(dg), _ptr(db), work.data_ptr(), M, D, _sp())
+          dx.data_ptr(), _ptr(dx_bf16), _ptr(dg), _ptr(db), _ptr(dxsum), work.data_ptr(), M, D, _sp())
 
 
-def rmsnorm_bwd(x, dy, g, rstd, dx, dx_bf16=None, dg=None):
+def rmsnorm_bwd(x, dy, g, rstd, dx, dx_bf16=None, dg=None, dxsum=None):
     M, D = x.shape
     work = _work(_lib.load().b2s_norm_work_floats(D), x.device)
     _call("b2s_rmsnorm_bwd", x.data_ptr(), dy.data_ptr(), g.data_ptr(), rstd.data_ptr(), dx.data_ptr(),
-          _ptr(dx_bf16), _ptr(dg), work.data_ptr(), M, D, _sp())
+          _ptr(dx_bf16), _ptr(dg), _ptr(dxsum), work.data_ptr(), M, D, _sp())
 
 
 def colsum_accumulate(x, out):

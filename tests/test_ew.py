@@ -42,12 +42,14 @@ def test_norm_fwd_bwd(cuda, D, rms):
     dx = dx0.clone()
     dxb = torch.empty(M, D, device=cuda, dtype=torch.bfloat16)
     dg = torch.zeros(D, device=cuda)
+    dsum = torch.ones(D, device=cuda)
     if rms:
-        ops.rmsnorm_bwd(x, dy, g, rstd, dx, dxb, dg)
+        ops.rmsnorm_bwd(x, dy, g, rstd, dx, dxb, dg, dxsum=dsum)
     else:
         db = torch.zeros(D, device=cuda)
-        ops.layernorm_bwd(x, dy, g, mean, rstd, dx, dxb, dg, db)
+        ops.layernorm_bwd(x, dy, g, mean, rstd, dx, dxb, dg, db, dxsum=dsum)
         torch.testing.assert_close(db, br.grad, rtol=1e-4, atol=1e-3)
+    torch.testing.assert_close(dsum, 1 + dx.sum(0), rtol=1e-4, atol=1e-2)
     torch.testing.assert_close(dx, dx0 + xr.grad, rtol=1e-4, atol=1e-4)
     torch.testing.assert_close(dxb.float(), dx, rtol=1e-2, atol=1e-2)
     torch.testing.assert_close(dg, gr.grad, rtol=1e-4, atol=1e-3)

@@ -35,3 +35,10 @@ n0 = _lib.load().b2s_launch_count()
 tr.train_step(W)
 torch.cuda.synchronize()
 print(f"launches_per_step {_lib.load().b2s_launch_count() - n0} loss {tr._loss.item():.4f}")
+if os.environ.get("KTIMER"):
+    from paper_2602_08387_b200 import ops
+
+    with ops.KernelTimer() as kt:
+        tr.train_step(W + 1)
+    for (kind, det), n, ms, tf in kt.detail():
+        print(f"{kind:9s} {str(det):70s} n={n:3d} {ms:8.3f} ms {tf:7.1f} TF/s")
