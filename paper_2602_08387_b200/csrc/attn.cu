@@ -28,7 +28,7 @@ using namespace sm100;
 namespace attn {
 
 constexpr int BQ = 128, BKV = 128, DH = 64;
-constexpr int kThreads = 192;
+
 constexpr int kTile = BQ * DH * 2;  // 16 KB bf16 128x64 tile
 constexpr int kStages = 2;
 constexpr float kLog2e = 1.4426950408889634f;
@@ -36,8 +36,12 @@ constexpr float kLog2e = 1.4426950408889634f;
 // byte offset of 16-B chunk c of row r in a 128B-swizzled tile of 128-B rows
 __device__ __forceinline__ uint32_t swz(int r, int c) { return (uint32_t)(r * 128 + ((c ^ (r & 7)) << 4)); }
 
+// Round a dynamic-smem pointer up to 1024 B by offsetting it (not via an
+// integer round trip), so the compiler keeps the shared address space and
+// emits STS/LDS instead of generic stores.
 __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
-  return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
+  const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(p));
+  return p + ((1024u - (a & 1023u)) & 1023u);
 }
 __device__ __forceinline__ void named_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
@@ -54,43 +58,68 @@ struct Params {
 // =====================================================================================
 // forward
 // =====================================================================================
-constexpr int kFwdSmem = 1024 + kTile /*Q*/ + 2 * kStages * kTile /*K,V*/ + 2 * kTile /*P*/ + 256;
+// CTA = (batch, q head, pair of 128-query tiles A = 2p, B = 2p+1). Two softmax
+// warpgroups (warps 2-5 -> tile A, warps 6-9 -> tile B) share each K/V block
+// and the MMA warp ping-pongs between them:
+//   S_A(0) S_B(0) | PV_A(j) S_A(j+1) PV_B(j) S_B(j+1) | ...
+// O accumulates in TMEM (PV MMAs chain with accumulate=1). A softmax thread
+// only rescales its O row (tcgen05.ld / st) when its running max grows by
+// more than 2^8 -- otherwise P is formed against the stale max and stays
+// <= 256 -- so the softmax loop never waits for the PV MMA it just enabled.
+// P is double-buffered in smem per tile so P(j+1) can be written while
+// PV(j) still reads P(j).
+constexpr int kFwdThreads = 320;
+constexpr int kFwdSmem = 1024 + 2 * kTile /*Q_A,Q_B*/ + 2 * kStages * kTile /*K,V*/ + 8 * kTile /*P: 2 tiles x 2 bufs*/ + 256;
+constexpr float kRescaleThresh = 8.0f;  // log2 units
 
-__global__ void __launch_bounds__(kThreads, 1)
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__global__ void __launch_bounds__(320, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_o,
                     Params p) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* sQ = align1024(smem_raw);
-  uint8_t* sK = sQ + kTile;
-  uint8_t* sV = sK + kStages * kTile;
-  uint8_t* sP = sV + kStages * kTile;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + 2 * kTile);
-  uint64_t* q_full = bars;
-  uint64_t* k_full = bars + 1;
-  uint64_t* v_full = k_full + kStages;
-  uint64_t* kv_empty = v_full + kStages;
-  uint64_t* s_full = kv_empty + kStages;  // [2]
-  uint64_t* s_empty = s_full + 2;         // [2]
-  uint64_t* p_full = s_empty + 2;
-  uint64_t* o_full = p_full + 1;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(o_full + 1);
+  uint8_t* sQ = align1024(smem_raw);          // [2] tiles A, B
+  uint8_t* sK = sQ + 2 * kTile;               // [kStages]
+  uint8_t* sV = sK + kStages * kTile;         // [kStages]
+  uint8_t* sP = sV + kStages * kTile;         // [tile][buf] x 32 KB (two 64-key atoms each)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + 8 * kTile);
+  uint64_t* q_full = bars;                    // 1
+  uint64_t* k_full = bars + 1;                // [kStages]
+  uint64_t* v_full = k_full + kStages;        // [kStages]
+  uint64_t* kv_empty = v_full + kStages;      // [kStages]
+  uint64_t* s_full = kv_empty + kStages;      // [2] per tile
+  uint64_t* s_empty = s_full + 2;             // [2]
+  uint64_t* p_full = s_empty + 2;             // [2]
+  uint64_t* p_empty = p_full + 2;             // [tile][buf]
+  uint64_t* o_done = p_empty + 4;             // [2] last PV of the tile retired
+  uint64_t* pv_done = o_done + 2;             // [2] each PV retired (rescale fence)
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(pv_done + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int npair = (p.nqt + 1) / 2;
   const int nbh = p.B * p.Hq;
-  const int qt = p.nqt - 1 - (int)(blockIdx.x / nbh);  // longest (diagonal-most) tiles first
+  const int pr = npair - 1 - (int)(blockIdx.x / nbh);  // heaviest pairs first
   const int bh = blockIdx.x % nbh;
   const int b = bh / p.Hq, h = bh % p.Hq;
   const int kvh = h / (p.Hq / p.Hkv);
-  const int row0 = b * p.T + qt * BQ;
-  const int nkv = qt + 1;
+  const int qtA = 2 * pr, qtB = 2 * pr + 1;
+  const bool hasB = qtB < p.nqt;
+  const int nA = qtA + 1, nB = hasB ? qtB + 1 : 0;
+  const int nkv = hasB ? nB : nA;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tm_qkv);
     mbar_init(q_full, 1);
     for (int s = 0; s < kStages; ++s) { mbar_init(&k_full[s], 1); mbar_init(&v_full[s], 1); mbar_init(&kv_empty[s], 1); }
-    for (int s = 0; s < 2; ++s) { mbar_init(&s_full[s], 1); mbar_init(&s_empty[s], 4); }
-    mbar_init(p_full, 4);
-    mbar_init(o_full, 1);
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(&s_full[t], 1); mbar_init(&s_empty[t], 4); mbar_init(&p_full[t], 4);
+      mbar_init(&o_done[t], 1); mbar_init(&pv_done[t], 1);
+      mbar_init(&p_empty[2 * t], 1); mbar_init(&p_empty[2 * t + 1], 1);
+    }
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<512>(tslot);
@@ -98,11 +127,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tslot;
+  // TMEM: S_A [0,128) S_B [128,256) O_A [256,320) O_B [320,384)
 
   if (warp == 0) {
     if (lane == 0) {
-      mbar_arrive_expect_tx(q_full, kTile);
-      tma_load_2d(sQ, &tm_qkv, q_full, h * DH, row0);
+      mbar_arrive_expect_tx(q_full, hasB ? 2 * kTile : kTile);
+      tma_load_2d(sQ, &tm_qkv, q_full, h * DH, b * p.T + qtA * BQ);
+      if (hasB) tma_load_2d(sQ + kTile, &tm_qkv, q_full, h * DH, b * p.T + qtB * BQ);
       for (int j = 0; j < nkv; ++j) {
         const int s = j % kStages;
         mbar_wait(&kv_empty[s], ((j / kStages) & 1) ^ 1);
@@ -118,132 +149,168 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       constexpr uint32_t idS = make_idesc_bf16(BQ, BKV, false, false);
       constexpr uint32_t idO = make_idesc_bf16(BQ, DH, false, true);
-      const uint32_t tO = tbase + 256;
       const uint32_t aQ = smem_u32(sQ), aK = smem_u32(sK), aV = smem_u32(sV), aP = smem_u32(sP);
+      auto issue_S = [&](int t, int j) {
+        const int s = j % kStages;
+        mbar_wait(&k_full[s], (j / kStages) & 1);
+        mbar_wait(&s_empty[t], (j & 1) ^ 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < DH / 16; ++kk)
+          mma_bf16_ss(tbase + t * BKV, make_sdesc(aQ + t * kTile + kk * 32, 16, 1024),
+                      make_sdesc(aK + s * kTile + kk * 32, 16, 1024), idS, kk > 0);
+        mma_commit(&s_full[t]);
+      };
+      auto issue_PV = [&](int t, int j, bool last) {
+        const int s = j % kStages;
+        mbar_wait(&v_full[s], (j / kStages) & 1);
+        mbar_wait(&p_full[t], j & 1);
+        tc_fence_after();
+        const uint32_t pbase = aP + (2 * t + (j & 1)) * 2 * kTile;
+#pragma unroll
+        for (int kk = 0; kk < BKV / 16; ++kk)
+          mma_bf16_ss(tbase + 256 + t * DH, make_sdesc(pbase + (kk >> 2) * kTile + (kk & 3) * 32, 16, 1024),
+                      make_sdesc(aV + s * kTile + kk * 2048, kTile, 1024), idO, (j > 0 || kk > 0) ? 1u : 0u);
+        mma_commit(&p_empty[2 * t + (j & 1)]);
+        mma_commit(&pv_done[t]);
+        if (last) mma_commit(&o_done[t]);
+      };
       mbar_wait(q_full, 0);
-      for (int j = 0; j <= nkv; ++j) {
-        if (j < nkv) {
-          const int s = j % kStages;
-          mbar_wait(&k_full[s], (j / kStages) & 1);
-          mbar_wait(&s_empty[j & 1], ((j >> 1) & 1) ^ 1);
-          tc_fence_after();
-#pragma unroll
-          for (int kk = 0; kk < DH / 16; ++kk)
-            mma_bf16_ss(tbase + (j & 1) * BKV, make_sdesc(aQ + kk * 32, 16, 1024),
-                        make_sdesc(aK + s * kTile + kk * 32, 16, 1024), idS, kk > 0);
-          mma_commit(&s_full[j & 1]);
-        }
-        if (j > 0) {
-          const int jj = j - 1, s = jj % kStages;
-          mbar_wait(&v_full[s], (jj / kStages) & 1);
-          mbar_wait(p_full, jj & 1);
-          tc_fence_after();
-#pragma unroll
-          for (int kk = 0; kk < BKV / 16; ++kk)
-            mma_bf16_ss(tO, make_sdesc(aP + (kk >> 2) * kTile + (kk & 3) * 32, 16, 1024),
-                        make_sdesc(aV + s * kTile + kk * 2048, kTile, 1024), idO, kk > 0);
-          mma_commit(o_full);
-          mma_commit(&kv_empty[s]);
-        }
+      issue_S(0, 0);
+      if (nB > 0) issue_S(1, 0);
+      for (int j = 0; j < nkv; ++j) {
+        if (j < nA) issue_PV(0, j, j + 1 == nA);
+        if (j + 1 < nA) issue_S(0, j + 1);
+        if (j < nB) issue_PV(1, j, j + 1 == nB);
+        if (j + 1 < nB) issue_S(1, j + 1);
+        mma_commit(&kv_empty[j % kStages]);  // K_j / V_j no longer read once these retire
       }
     }
     __syncwarp();
   } else {
-    // ------------------------------------------------ softmax warps
+    // ------------------------------------------------ softmax warpgroups
+    const int t = (warp - 2) >> 2;  // 0: tile A, 1: tile B
     const int q4 = warp & 3;
     const int r = q4 * 32 + lane;
-    const int qi = qt * BQ + r;
+    const int qt = t == 0 ? qtA : qtB;
+    const int nj = t == 0 ? nA : nB;
     const uint32_t lrow = (uint32_t)(q4 * 32) << 16;
+    const uint32_t tS = tbase + lrow + t * BKV;
+    const uint32_t tO = tbase + lrow + 256 + t * DH;
+    const float sl2 = p.scale_log2;
     float m = -INFINITY, l = 0.f;
-    float O[DH];
-#pragma unroll
-    for (int d = 0; d < DH; ++d) O[d] = 0.f;
-    for (int j = 0; j < nkv; ++j) {
-      mbar_wait(&s_full[j & 1], (j >> 1) & 1);
+    for (int j = 0; j < nj; ++j) {
+      mbar_wait(&s_full[t], j & 1);
       tc_fence_after();
-      const uint32_t tS = tbase + lrow + (j & 1) * BKV;
       const bool diag = (j == qt);
-      // pass 1: row max
+      // 10 warps/CTA puts 3 warps on some SMSPs: 168 registers per thread, so
+      // S is read from TMEM in two 64-column halves (max pass, then exp pass)
       float mx = -INFINITY;
-#pragma unroll 1
-      for (int c = 0; c < BKV / 32; ++c) {
-        uint32_t v[32];
-        tmem_ld32(tS + c * 32, v);
-        tmem_wait_ld();
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          float x = __uint_as_float(v[i]) * p.scale_log2;
-          if (diag && c * 32 + i > r) x = -INFINITY;
-          mx = fmaxf(mx, x);
+      for (int hf = 0; hf < 2; ++hf) {
+        uint32_t v[64];
+        tmem_ld32(tS + hf * 64, v);
+        tmem_ld32(tS + hf * 64 + 32, v + 32);
+        tmem_wait_ld();
+        if (diag) {
+#pragma unroll
+          for (int i = 0; i < 64; ++i)
+            if (hf * 64 + i <= r) mx = fmaxf(mx, __uint_as_float(v[i]));
+        } else {
+#pragma unroll
+          for (int i = 0; i < 64; ++i) mx = fmaxf(mx, __uint_as_float(v[i]));
         }
       }
-      const float m_new = fmaxf(m, mx);
-      const float alpha = exp2f(m - m_new);
-      // pass 2: P = exp2(s - m_new) -> bf16 smem, row sum
+      const float m_cand = mx * sl2;
+      // lazy rescale: keep the old max unless the new one exceeds it by > 2^8
+      float m_use = m;
+      bool resc = false;
+      if (m_cand > m + kRescaleThresh) { m_use = m_cand; resc = (j > 0); }
+      const float alpha = ex2(m - m_use);  // 0 on the first block (m = -inf)
+      if (__any_sync(0xffffffffu, resc)) {
+        // O must not be in flight: wait for the previous PV of this tile, then O *= alpha
+        mbar_wait(&pv_done[t], (j - 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int c = 0; c < DH / 16; ++c) {
+          uint32_t o[16];
+          tmem_ld16(tO + c * 16, o);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * (resc ? alpha : 1.f));
+          tmem_st16(tO + c * 16, o);
+        }
+        tmem_wait_st();
+      }
+      // P = 2^(s*sl2 - m_use) -> bf16 -> smem buffer (j & 1); row sum
+      const int pb = j & 1;
+      if (j >= 2) mbar_wait(&p_empty[2 * t + pb], ((j >> 1) - 1) & 1);
+      uint8_t* myP = sP + (2 * t + pb) * 2 * kTile;
       float rs = 0.f;
-#pragma unroll 1
-      for (int c = 0; c < BKV / 32; ++c) {
-        uint32_t v[32];
-        tmem_ld32(tS + c * 32, v);
-        tmem_wait_ld();
-        float pr[32];
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          float x = __uint_as_float(v[i]) * p.scale_log2;
-          if (diag && c * 32 + i > r) x = -INFINITY;
-          pr[i] = exp2f(x - m_new);
-          rs += pr[i];
+      for (int hf = 0; hf < 2; ++hf) {
+        uint32_t v[64];
+        tmem_ld32(tS + hf * 64, v);
+        tmem_ld32(tS + hf * 64 + 32, v + 32);
+        tmem_wait_ld();
+        if (hf == 1) {  // S fully consumed: the next QK^T may overwrite it
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&s_empty[t]);
         }
 #pragma unroll
-        for (int k8 = 0; k8 < 4; ++k8) {
-          const int kc = c * 4 + k8;  // 16-B chunk index along the 128 keys
+        for (int k8 = 0; k8 < 8; ++k8) {
+          float e[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int col = hf * 64 + k8 * 8 + i;
+            e[i] = (diag && col > r) ? 0.f : ex2(fmaf(__uint_as_float(v[k8 * 8 + i]), sl2, -m_use));
+            rs += e[i];
+          }
           uint4 w;
-          w.x = pack_bf16x2(pr[8 * k8 + 0], pr[8 * k8 + 1]);
-          w.y = pack_bf16x2(pr[8 * k8 + 2], pr[8 * k8 + 3]);
-          w.z = pack_bf16x2(pr[8 * k8 + 4], pr[8 * k8 + 5]);
-          w.w = pack_bf16x2(pr[8 * k8 + 6], pr[8 * k8 + 7]);
-          *reinterpret_cast<uint4*>(sP + (kc >> 3) * kTile + swz(r, kc & 7)) = w;
+          w.x = pack_bf16x2(e[0], e[1]);
+          w.y = pack_bf16x2(e[2], e[3]);
+          w.z = pack_bf16x2(e[4], e[5]);
+          w.w = pack_bf16x2(e[6], e[7]);
+          *reinterpret_cast<uint4*>(myP + hf * kTile + swz(r, k8)) = w;
         }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&s_empty[j & 1]);
       l = l * alpha + rs;
-      m = m_new;
+      m = m_use;
+      tc_fence_before();
       fence_proxy_async_smem();
       __syncwarp();
-      if (lane == 0) mbar_arrive(p_full);
-      // accumulate PV_j
-      mbar_wait(o_full, j & 1);
+      if (lane == 0) mbar_arrive(&p_full[t]);
+    }
+    if (nj > 0) {
+      // epilogue: O (TMEM) / l -> bf16 -> this tile's Q buffer (all MMAs retired) -> TMA store
+      mbar_wait(&o_done[t], 0);
       tc_fence_after();
+      uint8_t* sO = sQ + t * kTile;
+      const float inv = 1.f / l;
 #pragma unroll
       for (int c = 0; c < DH / 32; ++c) {
-        uint32_t v[32];
-        tmem_ld32(tbase + lrow + 256 + c * 32, v);
+        uint32_t o[32];
+        tmem_ld32(tO + c * 32, o);
         tmem_wait_ld();
 #pragma unroll
-        for (int i = 0; i < 32; ++i) O[c * 32 + i] = O[c * 32 + i] * alpha + __uint_as_float(v[i]);
+        for (int k8 = 0; k8 < 4; ++k8) {
+          uint4 w;
+          w.x = pack_bf16x2(__uint_as_float(o[8 * k8 + 0]) * inv, __uint_as_float(o[8 * k8 + 1]) * inv);
+          w.y = pack_bf16x2(__uint_as_float(o[8 * k8 + 2]) * inv, __uint_as_float(o[8 * k8 + 3]) * inv);
+          w.z = pack_bf16x2(__uint_as_float(o[8 * k8 + 4]) * inv, __uint_as_float(o[8 * k8 + 5]) * inv);
+          w.w = pack_bf16x2(__uint_as_float(o[8 * k8 + 6]) * inv, __uint_as_float(o[8 * k8 + 7]) * inv);
+          *reinterpret_cast<uint4*>(sO + swz(r, c * 4 + k8)) = w;
+        }
       }
-      tc_fence_before();
-    }
-    // epilogue: O / l -> bf16 -> sQ (free: every MMA has retired) -> TMA store
-    const float inv = 1.f / l;
-#pragma unroll
-    for (int c = 0; c < DH / 8; ++c) {
-      uint4 w;
-      w.x = pack_bf16x2(O[8 * c + 0] * inv, O[8 * c + 1] * inv);
-      w.y = pack_bf16x2(O[8 * c + 2] * inv, O[8 * c + 3] * inv);
-      w.z = pack_bf16x2(O[8 * c + 4] * inv, O[8 * c + 5] * inv);
-      w.w = pack_bf16x2(O[8 * c + 6] * inv, O[8 * c + 7] * inv);
-      *reinterpret_cast<uint4*>(sQ + swz(r, c)) = w;
-    }
-    p.lse[((size_t)b * p.Hq + h) * p.T + qi] = (m + log2f(l)) * (1.f / kLog2e);
-    fence_proxy_async_smem();
-    named_sync(1, 128);
-    if (warp == 2 && lane == 0) {
-      tma_store_2d(&tm_o, sQ, h * DH, row0);
-      bulk_commit();
-      bulk_wait<0>();
+      p.lse[((size_t)b * p.Hq + h) * p.T + qt * BQ + r] = (m + log2f(l)) * (1.f / kLog2e);
+      fence_proxy_async_smem();
+      named_sync(1 + t, 128);
+      if (q4 == 0 && lane == 0) {
+        tma_store_2d(&tm_o, sO, h * DH, b * p.T + qt * BQ);
+        bulk_commit();
+        bulk_wait<0>();
+      }
     }
     __syncwarp();
   }
@@ -254,7 +321,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     tmem_dealloc<512>(tbase);
   }
 }
-
 
 // =====================================================================================
 // backward
@@ -297,11 +363,19 @@ __global__ void attn_bwd_dq_kernel(const float* __restrict__ dq_acc, __nv_bfloat
   }
 }
 
-// dQ's fp32 staging tile reuses the P^T buffer (free once dQ's MMA retired).
+// Backward CTA = (batch, kv head, 128-key tile); 8 compute warps: warp w owns
+// key rows 32*(w&3).. (its TMEM lane quarter) and query columns
+// 64*((w-2)>>2).. of each 128x128 S^T / dP^T block. MMA order per step t:
+//   S(t+1), dP(t+1)  [as soon as the compute warps hold S(t), dP(t) in registers]
+//   dV += P^T dO, dK += dS^T Q, dQ[t&1] = dS K     [after P^T, dS^T(t) reach smem]
+// so the next step's QK^T / V dO^T overlap this step's exponentials, and dQ is
+// double-buffered in TMEM: the compute warps drain dQ(t-1) (TMA add-reduce
+// into the fp32 accumulator) after publishing P/dS(t).
+constexpr int kBwdThreads = 320;
 constexpr int kBwdSmem = 1024 + 2 * kTile /*K,V*/ + 4 * kTile /*Q,dO x2*/ + 2 * kTile /*P^T*/ + 2 * kTile /*dS^T*/ +
-                         4 * BQ * 4 /*lse2, D x2*/ + 256;
+                         2 * kTile /*dQ fp32 staging*/ + 4 * BQ * 4 /*lse2, D x2*/ + 256;
 
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(320, 1)
     attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
                     const __grid_constant__ CUtensorMap tm_dq, const __grid_constant__ CUtensorMap tm_dkv, Params p) {
   extern __shared__ uint8_t smem_raw[];
@@ -311,8 +385,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sdO = sQ + 2 * kTile;     // [2]
   uint8_t* sP = sdO + 2 * kTile;     // P^T  [128 keys][128 q] as two 64-column atoms
   uint8_t* sdS = sP + 2 * kTile;     // dS^T
-  uint8_t* sdQ = sP;                 // fp32 128 x 64 as two 32-column boxes (aliases P^T)
-  float* sLse = reinterpret_cast<float*>(sdS + 2 * kTile);  // [2][128] (log2 domain)
+  uint8_t* sdQ = sdS + 2 * kTile;    // fp32 128 x 64 as two 32-column boxes (16 KB each)
+  float* sLse = reinterpret_cast<float*>(sdQ + 2 * kTile);  // [2][128] (log2 domain)
   float* sD = sLse + 2 * BQ;                                 // [2][128]
   uint64_t* bars = reinterpret_cast<uint64_t*>(sD + 2 * BQ);
   uint64_t* kv_full = bars;
@@ -322,10 +396,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* st_empty = bars + 6;
   uint64_t* pds_full = bars + 7;
   uint64_t* pds_empty = bars + 8;
-  uint64_t* dq_full = bars + 9;
-  uint64_t* dq_empty = bars + 10;
-  uint64_t* done = bars + 11;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 12);
+  uint64_t* dq_full = bars + 9;   // [2]
+  uint64_t* dq_empty = bars + 11; // [2]
+  uint64_t* done = bars + 13;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 14);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nbk = p.B * p.Hkv;
@@ -341,13 +415,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch(&tm_qkv);
     tma_prefetch(&tm_do);
     mbar_init(kv_full, 1);
-    for (int s = 0; s < 2; ++s) { mbar_init(&qd_full[s], 1); mbar_init(&qd_empty[s], 1); }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&qd_full[s], 1); mbar_init(&qd_empty[s], 1); mbar_init(&dq_full[s], 1); mbar_init(&dq_empty[s], 8);
+    }
     mbar_init(st_full, 1);
-    mbar_init(st_empty, 4);
-    mbar_init(pds_full, 4);
+    mbar_init(st_empty, 8);
+    mbar_init(pds_full, 8);
     mbar_init(pds_empty, 1);
-    mbar_init(dq_full, 1);
-    mbar_init(dq_empty, 4);
     mbar_init(done, 1);
     fence_barrier_init();
   }
@@ -356,7 +430,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tslot;
-  const uint32_t tS = tbase, tdP = tbase + 128, tdV = tbase + 256, tdK = tbase + 320, tdQ = tbase + 384;
+  const uint32_t tS = tbase, tdP = tbase + 128, tdV = tbase + 256, tdK = tbase + 320, tdQ = tbase + 384;  // dQ: [2] x 64
 
   if (warp == 0) {
     if (lane == 0) {
@@ -380,13 +454,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       constexpr uint32_t idMM = make_idesc_bf16(128, DH, true, true);     // dQ
       const uint32_t aK = smem_u32(sK), aV = smem_u32(sV), aQ = smem_u32(sQ), adO = smem_u32(sdO);
       const uint32_t aP = smem_u32(sP), adS = smem_u32(sdS);
-      mbar_wait(kv_full, 0);
-      for (int t = 0; t < nsteps; ++t) {
+      auto issue_S = [&](int t) {
         const int s = t & 1;
-        const uint32_t q_ = aQ + s * kTile, do_ = adO + s * kTile;
         mbar_wait(&qd_full[s], (t >> 1) & 1);
-        mbar_wait(st_empty, (t & 1) ^ 1);
+        if (t > 0) mbar_wait(st_empty, (t - 1) & 1);
         tc_fence_after();
+        const uint32_t q_ = aQ + s * kTile, do_ = adO + s * kTile;
 #pragma unroll
         for (int kk = 0; kk < DH / 16; ++kk)
           mma_bf16_ss(tS, make_sdesc(aK + kk * 32, 16, 1024), make_sdesc(q_ + kk * 32, 16, 1024), idSS, kk > 0);
@@ -394,6 +467,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kk = 0; kk < DH / 16; ++kk)
           mma_bf16_ss(tdP, make_sdesc(aV + kk * 32, 16, 1024), make_sdesc(do_ + kk * 32, 16, 1024), idSS, kk > 0);
         mma_commit(st_full);
+      };
+      mbar_wait(kv_full, 0);
+      issue_S(0);
+      for (int t = 0; t < nsteps; ++t) {
+        const int s = t & 1;
+        const uint32_t q_ = aQ + s * kTile, do_ = adO + s * kTile;
+        if (t + 1 < nsteps) issue_S(t + 1);
         mbar_wait(pds_full, t & 1);
         tc_fence_after();
 #pragma unroll
@@ -403,114 +483,121 @@ __global__ void __launch_bounds__(kThreads, 1)
           mma_bf16_ss(tdV, a_p, make_sdesc(do_ + kk * 2048, kTile, 1024), idKM, (t > 0 || kk > 0));
           mma_bf16_ss(tdK, a_ds, make_sdesc(q_ + kk * 2048, kTile, 1024), idKM, (t > 0 || kk > 0));
         }
-        mbar_wait(dq_empty, (t & 1) ^ 1);
+        mbar_wait(&dq_empty[s], ((t >> 1) & 1) ^ 1);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < BKV / 16; ++kk)
-          mma_bf16_ss(tdQ, make_sdesc(adS + kk * 2048, kTile, 1024), make_sdesc(aK + kk * 2048, kTile, 1024), idMM,
-                      kk > 0);
+          mma_bf16_ss(tdQ + s * DH, make_sdesc(adS + kk * 2048, kTile, 1024), make_sdesc(aK + kk * 2048, kTile, 1024),
+                      idMM, kk > 0);
         mma_commit(&qd_empty[s]);
         mma_commit(pds_empty);
-        mma_commit(dq_full);
+        mma_commit(&dq_full[s]);
       }
       mma_commit(done);
     }
     __syncwarp();
   } else {
-    // ------------------------------------------------ compute warps (thread = key row, then q row)
-    const int ct = threadIdx.x - 64;  // 0..127
+    // ------------------------------------------------ compute warps
+    const int ct = threadIdx.x - 64;  // 0..255
     const int q4 = warp & 3;
-    const int r = q4 * 32 + lane;
+    const int half = (warp - 2) >> 2;
+    const int r = q4 * 32 + lane;  // key row (S^T / dP^T / dV / dK lanes) and query row (dQ lanes)
     const uint32_t lrow = (uint32_t)(q4 * 32) << 16;
-    for (int t = 0; t < nsteps; ++t) {
+    auto drain_dq = [&](int t) {  // dQ(t) (TMEM buffer t&1) -> fp32 smem -> TMA add-reduce
       const int h = kvh * G + t / nq, i = kt + t % nq;
+      mbar_wait(&dq_full[t & 1], (t >> 1) & 1);
+      tc_fence_after();
+      uint32_t qv[32];
+      tmem_ld32(tdQ + lrow + (t & 1) * DH + half * 32, qv);
+      tmem_wait_ld();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&dq_empty[t & 1]);
+      if (ct == 0) bulk_wait_read<0>();  // the previous add-reduce has finished reading sdQ
+      named_sync(2, 256);
+      uint8_t* box = sdQ + half * kTile;
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        *reinterpret_cast<float4*>(box + swz(r, c)) =
+            make_float4(__uint_as_float(qv[4 * c]) * p.scale, __uint_as_float(qv[4 * c + 1]) * p.scale,
+                        __uint_as_float(qv[4 * c + 2]) * p.scale, __uint_as_float(qv[4 * c + 3]) * p.scale);
+      fence_proxy_async_smem();
+      named_sync(3, 256);
+      if (ct == 0) {
+        tma_reduce_add_2d(&tm_dq, sdQ, h * DH, b * p.T + i * BQ);
+        tma_reduce_add_2d(&tm_dq, sdQ + kTile, h * DH + 32, b * p.T + i * BQ);
+        bulk_commit();
+      }
+    };
+    // lse / D of step t live in buffer t&1; step t+1's are loaded during step t
+    auto load_stats = [&](int t) {
+      const int h = kvh * G + t / nq, i = kt + t % nq;
+      const size_t off = ((size_t)b * p.Hq + h) * p.T + (size_t)i * BQ + (ct & 127);
+      if (ct < 128) sLse[(t & 1) * BQ + ct] = p.lse[off] * kLog2e;
+      else sD[(t & 1) * BQ + ct - 128] = p.dsum[off];
+    };
+    if (nsteps > 0) load_stats(0);
+    for (int t = 0; t < nsteps; ++t) {
+      const int i = kt + t % nq;
       const bool diag = (i == kt);
       float* lse2 = sLse + (t & 1) * BQ;
       float* dd = sD + (t & 1) * BQ;
-      {
-        const size_t off = ((size_t)b * p.Hq + h) * p.T + (size_t)i * BQ + ct;
-        lse2[ct] = p.lse[off] * kLog2e;
-        dd[ct] = p.dsum[off];
-      }
-      named_sync(1, 128);
+      named_sync(1, 256);  // stats of step t visible; everyone is done with step t-1's buffer
+      if (t + 1 < nsteps) load_stats(t + 1);
       mbar_wait(st_full, t & 1);
-      mbar_wait(pds_empty, (t & 1) ^ 1);
       tc_fence_after();
-#pragma unroll 1
-      for (int c = 0; c < BQ / 32; ++c) {
-        uint32_t sv[32], dv[32];
-        tmem_ld32(tS + lrow + c * 32, sv);
-        tmem_ld32(tdP + lrow + c * 32, dv);
-        tmem_wait_ld();
-        float pr[32], ds[32];
+      // 168 registers per thread (3 warps on some SMSPs): two 32-column passes
 #pragma unroll
-        for (int e = 0; e < 32; ++e) {
-          const int q = c * 32 + e;
-          float pv = exp2f(__uint_as_float(sv[e]) * p.scale_log2 - lse2[q]);
-          if (diag && q < r) pv = 0.f;  // query index below key index: masked
-          pr[e] = pv;
-          ds[e] = pv * (__uint_as_float(dv[e]) - dd[q]);
+      for (int qq = 0; qq < 2; ++qq) {
+        uint32_t sv[32], dv[32];
+        tmem_ld32(tS + lrow + half * 64 + qq * 32, sv);
+        tmem_ld32(tdP + lrow + half * 64 + qq * 32, dv);
+        tmem_wait_ld();
+        if (qq == 1) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(st_empty);  // the next step's S^T / dP^T may overwrite TMEM
         }
 #pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          const int q = half * 64 + qq * 32 + e;
+          float pv = ex2(fmaf(__uint_as_float(sv[e]), p.scale_log2, -lse2[q]));
+          if (diag && q < r) pv = 0.f;  // query index below key index: masked
+          sv[e] = __float_as_uint(pv);
+          dv[e] = __float_as_uint(pv * (__uint_as_float(dv[e]) - dd[q]));
+        }
+        if (qq == 0 && t > 0) mbar_wait(pds_empty, (t - 1) & 1);  // step t-1's MMAs released sP / sdS
+#pragma unroll
         for (int k8 = 0; k8 < 4; ++k8) {
-          const int kc = c * 4 + k8;
           uint4 w, z;
-          w.x = pack_bf16x2(pr[8 * k8 + 0], pr[8 * k8 + 1]);
-          w.y = pack_bf16x2(pr[8 * k8 + 2], pr[8 * k8 + 3]);
-          w.z = pack_bf16x2(pr[8 * k8 + 4], pr[8 * k8 + 5]);
-          w.w = pack_bf16x2(pr[8 * k8 + 6], pr[8 * k8 + 7]);
-          z.x = pack_bf16x2(ds[8 * k8 + 0], ds[8 * k8 + 1]);
-          z.y = pack_bf16x2(ds[8 * k8 + 2], ds[8 * k8 + 3]);
-          z.z = pack_bf16x2(ds[8 * k8 + 4], ds[8 * k8 + 5]);
-          z.w = pack_bf16x2(ds[8 * k8 + 6], ds[8 * k8 + 7]);
-          const uint32_t off = (kc >> 3) * kTile + swz(r, kc & 7);
+          w.x = pack_bf16x2(__uint_as_float(sv[8 * k8 + 0]), __uint_as_float(sv[8 * k8 + 1]));
+          w.y = pack_bf16x2(__uint_as_float(sv[8 * k8 + 2]), __uint_as_float(sv[8 * k8 + 3]));
+          w.z = pack_bf16x2(__uint_as_float(sv[8 * k8 + 4]), __uint_as_float(sv[8 * k8 + 5]));
+          w.w = pack_bf16x2(__uint_as_float(sv[8 * k8 + 6]), __uint_as_float(sv[8 * k8 + 7]));
+          z.x = pack_bf16x2(__uint_as_float(dv[8 * k8 + 0]), __uint_as_float(dv[8 * k8 + 1]));
+          z.y = pack_bf16x2(__uint_as_float(dv[8 * k8 + 2]), __uint_as_float(dv[8 * k8 + 3]));
+          z.z = pack_bf16x2(__uint_as_float(dv[8 * k8 + 4]), __uint_as_float(dv[8 * k8 + 5]));
+          z.w = pack_bf16x2(__uint_as_float(dv[8 * k8 + 6]), __uint_as_float(dv[8 * k8 + 7]));
+          const uint32_t off = half * kTile + swz(r, qq * 4 + k8);
           *reinterpret_cast<uint4*>(sP + off) = w;
           *reinterpret_cast<uint4*>(sdS + off) = z;
         }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(st_empty);
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(pds_full);
-      // dQ_i = scale * dS K  (TMEM lane = query row)
-      mbar_wait(dq_full, t & 1);
-      tc_fence_after();
-      uint32_t qv[DH];
-      tmem_ld32(tdQ + lrow, qv);
-      tmem_ld32(tdQ + lrow + 32, qv + 32);
-      tmem_wait_ld();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(dq_empty);
-#pragma unroll
-      for (int c = 0; c < DH / 4; ++c) {
-        const int box = c >> 3, cc = c & 7;
-        *reinterpret_cast<float4*>(sdQ + box * (2 * kTile) + swz(r, cc)) =
-            make_float4(__uint_as_float(qv[4 * c]) * p.scale, __uint_as_float(qv[4 * c + 1]) * p.scale,
-                        __uint_as_float(qv[4 * c + 2]) * p.scale, __uint_as_float(qv[4 * c + 3]) * p.scale);
-      }
-      fence_proxy_async_smem();
-      named_sync(3, 128);
-      if (ct == 0) {
-        tma_reduce_add_2d(&tm_dq, sdQ, h * DH, b * p.T + i * BQ);
-        tma_reduce_add_2d(&tm_dq, sdQ + 2 * kTile, h * DH + 32, b * p.T + i * BQ);
-        bulk_commit();
-        bulk_wait_read<0>();
-      }
+      if (t > 0) drain_dq(t - 1);
     }
+    if (nsteps > 0) drain_dq(nsteps - 1);
     // dK (scaled) and dV -> bf16 -> smem (Q stages are free) -> TMA store into dqkv
     mbar_wait(done, 0);
     tc_fence_after();
-    uint32_t kv[DH], vv[DH];
-    tmem_ld32(tdK + lrow, kv);
-    tmem_ld32(tdK + lrow + 32, kv + 32);
-    tmem_ld32(tdV + lrow, vv);
-    tmem_ld32(tdV + lrow + 32, vv + 32);
+    uint32_t kv[32], vv[32];
+    tmem_ld32(tdK + lrow + half * 32, kv);
+    tmem_ld32(tdV + lrow + half * 32, vv);
     tmem_wait_ld();
 #pragma unroll
-    for (int c = 0; c < DH / 8; ++c) {
+    for (int c = 0; c < 4; ++c) {
       uint4 w, z;
       w.x = pack_bf16x2(__uint_as_float(kv[8 * c + 0]) * p.scale, __uint_as_float(kv[8 * c + 1]) * p.scale);
       w.y = pack_bf16x2(__uint_as_float(kv[8 * c + 2]) * p.scale, __uint_as_float(kv[8 * c + 3]) * p.scale);
@@ -520,11 +607,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       z.y = pack_bf16x2(__uint_as_float(vv[8 * c + 2]), __uint_as_float(vv[8 * c + 3]));
       z.z = pack_bf16x2(__uint_as_float(vv[8 * c + 4]), __uint_as_float(vv[8 * c + 5]));
       z.w = pack_bf16x2(__uint_as_float(vv[8 * c + 6]), __uint_as_float(vv[8 * c + 7]));
-      *reinterpret_cast<uint4*>(sQ + swz(r, c)) = w;
-      *reinterpret_cast<uint4*>(sQ + kTile + swz(r, c)) = z;
+      *reinterpret_cast<uint4*>(sQ + swz(r, half * 4 + c)) = w;
+      *reinterpret_cast<uint4*>(sQ + kTile + swz(r, half * 4 + c)) = z;
     }
     fence_proxy_async_smem();
-    named_sync(1, 128);
+    named_sync(1, 256);
     if (ct == 0) {
       tma_store_2d(&tm_dkv, sQ, (p.Hq + kvh) * DH, krow0);
       tma_store_2d(&tm_dkv, sQ + kTile, (p.Hq + p.Hkv + kvh) * DH, krow0);
@@ -564,8 +651,8 @@ extern "C" int b2s_attn_fwd(const void* d_qkv, void* d_o, float* d_lse, int B, i
     cudaFuncSetAttribute(attn::attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, attn::kFwdSmem);
     attr = true;
   }
-  const unsigned grid = (unsigned)(B * Hq * (T / attn::BQ));
-  attn::attn_fwd_kernel<<<grid, attn::kThreads, attn::kFwdSmem, (cudaStream_t)stream>>>(tq, to, p);
+  const unsigned grid = (unsigned)(B * Hq * ((T / attn::BQ + 1) / 2));
+  attn::attn_fwd_kernel<<<grid, attn::kFwdThreads, attn::kFwdSmem, (cudaStream_t)stream>>>(tq, to, p);
   return check_launch("attn_fwd");
 }
 
@@ -604,7 +691,7 @@ extern "C" int b2s_attn_bwd(const void* d_qkv, const void* d_o, const void* d_do
     attr = true;
   }
   const unsigned grid = (unsigned)(B * Hkv * (T / attn::BQ));
-  attn::attn_bwd_kernel<<<grid, attn::kThreads, attn::kBwdSmem, st>>>(tq, tdo, tdq, tdkv, p);
+  attn::attn_bwd_kernel<<<grid, attn::kBwdThreads, attn::kBwdSmem, st>>>(tq, tdo, tdq, tdkv, p);
   rc = check_launch("attn_bwd");
   if (rc) return rc;
   attn::attn_bwd_dq_kernel<<<kNumSMs * 8, 256, 0, st>>>(dq_acc, (__nv_bfloat16*)d_dqkv, M, Hq, ldq);

@@ -137,7 +137,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   using C_ = Cfg<BN>;
   constexpr uint32_t kIdesc = make_idesc_bf16(BM, BN, A_MN, B_MN);
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // align by offsetting (keeps the shared address space: STS, not generic stores)
+  uint8_t* smem = smem_raw + ((1024u - (static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw)) & 1023u)) & 1023u);
   uint8_t* epi_smem = smem + C_::kStages * C_::kStageBytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(epi_smem + kEpiSmem);
   uint64_t* empty = full + C_::kStages;
