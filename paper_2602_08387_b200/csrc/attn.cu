@@ -328,18 +328,26 @@ __global__ void __launch_bounds__(320, 1)
 // D[b, h, q] = sum_d dO * O (row-wise), and zero the fp32 dQ accumulator.
 __global__ void attn_bwd_prep_kernel(const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ dout,
                                      float* __restrict__ dsum, float* __restrict__ dq_acc, int B, int T, int Hq) {
-  const int lane = threadIdx.x & 31;
+  // 8 lanes per (row, head): each lane a 16-byte vector of o and dO
+  const int sub = threadIdx.x & 7;
   const int64_t nrows = (int64_t)B * T * Hq;
-  for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nrows;
-       w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+  for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 3; w < nrows;
+       w += ((int64_t)gridDim.x * blockDim.x) >> 3) {
     const int64_t row = w / Hq;
     const int h = (int)(w - row * Hq);
-    const int64_t off = row * Hq * DH + h * DH + lane * 2;
-    float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(o + off));
-    float2 g = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(dout + off));
-    float acc = warp_sum(a.x * g.x + a.y * g.y);
-    *reinterpret_cast<float2*>(dq_acc + off) = make_float2(0.f, 0.f);
-    if (lane == 0) {
+    const int64_t off = row * Hq * DH + h * DH + sub * 8;
+    float a[8], g[8];
+    unpack8(*reinterpret_cast<const bf16x8*>(o + off), a);
+    unpack8(*reinterpret_cast<const bf16x8*>(dout + off), g);
+    float acc = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc += a[i] * g[i];
+    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+    *reinterpret_cast<float4*>(dq_acc + off) = make_float4(0.f, 0.f, 0.f, 0.f);
+    *reinterpret_cast<float4*>(dq_acc + off + 4) = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (sub == 0) {
       const int64_t b = row / T, t = row - b * T;
       dsum[(b * Hq + h) * T + t] = acc;
     }

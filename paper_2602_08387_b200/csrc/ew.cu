@@ -33,10 +33,23 @@ __device__ __forceinline__ void st_bf4(__nv_bfloat16* p, const float* f) {
 // residual into the next stream buffer while it is in registers).
 // TPR threads cooperate on a row (32 = one warp for D <= 1024, 256 = the whole
 // block for D >= 2048) so the row stays in registers at every hidden size.
+// Sum over the TPR threads sharing a row. TPR=64: two warps exchange through
+// double-buffered smem slots and a per-pair named barrier (ids 1..4).
 template <int TPR>
-__device__ __forceinline__ float row_sum(float v, float* scratch) {
-  if constexpr (TPR == 32) return warp_sum(v);
-  else return block_sum(v, scratch);
+__device__ __forceinline__ float row_sum(float v, float* scratch, int& toggle) {
+  if constexpr (TPR == 32) {
+    return warp_sum(v);
+  } else if constexpr (TPR == 64) {
+    v = warp_sum(v);
+    const int wid = threadIdx.x >> 5;
+    float* sl = scratch + toggle * 8;
+    if ((threadIdx.x & 31) == 0) sl[wid] = v;
+    asm volatile("bar.sync %0, 64;" ::"r"(1 + (wid >> 1)) : "memory");
+    toggle ^= 1;
+    return sl[wid & ~1] + sl[wid | 1];
+  } else {
+    return block_sum(v, scratch);
+  }
 }
 
 template <int D, int TPR, bool RMS>
@@ -47,6 +60,7 @@ __global__ void __launch_bounds__(kRowThreads) norm_fwd_kernel(
   constexpr int V = D / (TPR * 4);  // float4 vectors per thread
   static_assert(V * TPR * 4 == D, "hidden size must tile the row threads");
   __shared__ float scratch[32];
+  int tog = 0;
   const int t = threadIdx.x % TPR;
   const int64_t r0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / TPR;
   const int64_t nr = ((int64_t)gridDim.x * blockDim.x) / TPR;
@@ -70,13 +84,13 @@ __global__ void __launch_bounds__(kRowThreads) norm_fwd_kernel(
       for (int j = 0; j < V; ++j) st4(x_copy + row * D + t * 4 + j * TPR * 4, xv[j]);
     }
     float mean = 0.f;
-    if (!RMS) mean = row_sum<TPR>(s, scratch) * (1.f / D);
+    if (!RMS) mean = row_sum<TPR>(s, scratch, tog) * (1.f / D);
 #pragma unroll
     for (int j = 0; j < V; ++j) {
       float a = xv[j].x - mean, c = xv[j].y - mean, d = xv[j].z - mean, e = xv[j].w - mean;
       ss += a * a + c * c + d * d + e * e;
     }
-    const float rstd = rsqrtf(row_sum<TPR>(ss, scratch) * (1.f / D) + eps);
+    const float rstd = rsqrtf(row_sum<TPR>(ss, scratch, tog) * (1.f / D) + eps);
 #pragma unroll
     for (int j = 0; j < V; ++j) {
       float o[4] = {(xv[j].x - mean) * rstd, (xv[j].y - mean) * rstd, (xv[j].z - mean) * rstd,
@@ -105,6 +119,7 @@ __global__ void __launch_bounds__(kRowThreads) norm_bwd_kernel(
   constexpr int kChunk = 1024;                // columns reduced per smem pass
   __shared__ float red[kGroups][kChunk];
   __shared__ float scratch[32];
+  int tog = 0;
   const int t = threadIdx.x % TPR, grp = threadIdx.x / TPR;
   const int64_t r0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / TPR;
   const int64_t nr = ((int64_t)gridDim.x * blockDim.x) / TPR;
@@ -117,44 +132,47 @@ __global__ void __launch_bounds__(kRowThreads) norm_bwd_kernel(
   }
   // rows per group are equal for every group except the tail; loop bound must
   // be uniform across the block when TPR spans the block (block_sum syncs)
+  // Two passes per row keep register use low enough for 2 CTAs/SM: pass 1 forms
+  // the row statistics, pass 2 re-reads x and dy (L1-resident) with dx.
   for (int64_t row = r0; row < M; row += nr) {
     const float mean = RMS ? 0.f : mean_in[row];
     const float rstd = rstd_in[row];
-    float xh[V][4], dyg[V][4];
     float s1 = 0.f, s2 = 0.f;
 #pragma unroll
     for (int j = 0; j < V; ++j) {
-      float4 xv = ld4(x + row * D + t * 4 + j * TPR * 4);
+      const float4 xv = ld4(x + row * D + t * 4 + j * TPR * 4);
       float d4[4];
       ld_bf4(dy + row * D + t * 4 + j * TPR * 4, d4);
-      xh[j][0] = (xv.x - mean) * rstd; xh[j][1] = (xv.y - mean) * rstd;
-      xh[j][2] = (xv.z - mean) * rstd; xh[j][3] = (xv.w - mean) * rstd;
+      const float xs[4] = {xv.x, xv.y, xv.z, xv.w};
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        dyg[j][u] = d4[u] * gv[j][u];
-        s1 += dyg[j][u];
-        s2 += dyg[j][u] * xh[j][u];
-        dg[j][u] += d4[u] * xh[j][u];
-        db[j][u] += d4[u];
+        const float dyg = d4[u] * gv[j][u];
+        s1 += dyg;
+        s2 += dyg * (xs[u] - mean) * rstd;
       }
     }
-    s2 = row_sum<TPR>(s2, scratch) * (1.f / D);
-    if (!RMS) s1 = row_sum<TPR>(s1, scratch) * (1.f / D);
+    s2 = row_sum<TPR>(s2, scratch, tog) * (1.f / D);
+    if (!RMS) s1 = row_sum<TPR>(s1, scratch, tog) * (1.f / D);
     else s1 = 0.f;
 #pragma unroll
     for (int j = 0; j < V; ++j) {
-      float* dxp = dx + row * D + t * 4 + j * TPR * 4;
-      float4 o = ld4(dxp);
-      o.x += rstd * (dyg[j][0] - s1 - xh[j][0] * s2);
-      o.y += rstd * (dyg[j][1] - s1 - xh[j][1] * s2);
-      o.z += rstd * (dyg[j][2] - s1 - xh[j][2] * s2);
-      o.w += rstd * (dyg[j][3] - s1 - xh[j][3] * s2);
-      st4(dxp, o);
-      ds[j][0] += o.x; ds[j][1] += o.y; ds[j][2] += o.z; ds[j][3] += o.w;
-      if (dx_bf16) {
-        float f[4] = {o.x, o.y, o.z, o.w};
-        st_bf4(dx_bf16 + row * D + t * 4 + j * TPR * 4, f);
+      const int64_t off = row * D + t * 4 + j * TPR * 4;
+      const float4 xv = ld4(x + off);
+      float4 o = ld4(dx + off);
+      float d4[4];
+      ld_bf4(dy + off, d4);
+      const float xs[4] = {xv.x, xv.y, xv.z, xv.w};
+      float os[4] = {o.x, o.y, o.z, o.w};
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float xh = (xs[u] - mean) * rstd;
+        os[u] += rstd * (d4[u] * gv[j][u] - s1 - xh * s2);
+        dg[j][u] += d4[u] * xh;
+        db[j][u] += d4[u];
+        ds[j][u] += os[u];
       }
+      st4(dx + off, make_float4(os[0], os[1], os[2], os[3]));
+      if (dx_bf16) st_bf4(dx_bf16 + off, os);
     }
   }
   // block-level reduction of dg, db, sum(dx) over the row groups -> part[block][pass]
@@ -184,8 +202,12 @@ __global__ void __launch_bounds__(kRowThreads) norm_bwd_kernel(
 // out[c] += sum_b part[b][which][c]  (deterministic second stage): block =
 // 32 columns x 8 row groups, fixed summation order.
 __global__ void __launch_bounds__(256) reduce_parts_kernel(const float* __restrict__ part, int nblocks, int D,
-                                                           int which, float* __restrict__ out) {
+                                                           float* __restrict__ out0, float* __restrict__ out1,
+                                                           float* __restrict__ out2) {
   __shared__ float red[8][33];
+  const int which = blockIdx.y;
+  float* out = which == 0 ? out0 : which == 1 ? out1 : out2;
+  if (out == nullptr) return;
   const int c = blockIdx.x * 32 + (threadIdx.x & 31), rg = threadIdx.x >> 5;
   float acc = 0.f;
   if (c < D)
@@ -381,23 +403,30 @@ __global__ void __launch_bounds__(512) xent_kernel(__nv_bfloat16* __restrict__ l
   const int64_t m = blockIdx.x;
   __nv_bfloat16* row = logits + m * ld;
   const int nvec = V / 8;  // full 8-wide vectors
-  float mx = -INFINITY;
+  // one pass: per-thread online (max, sum of exp), then a block-wide merge
+  float mx = -INFINITY, se = 0.f;
   for (int i = threadIdx.x; i < nvec; i += blockDim.x) {
     float f[8];
     unpack8(*reinterpret_cast<const bf16x8*>(row + i * 8), f);
+    float lm = f[0];
 #pragma unroll
-    for (int t = 0; t < 8; ++t) mx = fmaxf(mx, f[t]);
-  }
-  for (int c = nvec * 8 + threadIdx.x; c < V; c += blockDim.x) mx = fmaxf(mx, bf2f(row[c]));
-  mx = block_max(mx, scratch);
-  float se = 0.f;
-  for (int i = threadIdx.x; i < nvec; i += blockDim.x) {
-    float f[8];
-    unpack8(*reinterpret_cast<const bf16x8*>(row + i * 8), f);
+    for (int t = 1; t < 8; ++t) lm = fmaxf(lm, f[t]);
+    const float mn = fmaxf(mx, lm);
+    float acc = 0.f;
 #pragma unroll
-    for (int t = 0; t < 8; ++t) se += __expf(f[t] - mx);
+    for (int t = 0; t < 8; ++t) acc += __expf(f[t] - mn);
+    se = se * __expf(mx - mn) + acc;
+    mx = mn;
   }
-  for (int c = nvec * 8 + threadIdx.x; c < V; c += blockDim.x) se += __expf(bf2f(row[c]) - mx);
+  for (int c = nvec * 8 + threadIdx.x; c < V; c += blockDim.x) {
+    const float f = bf2f(row[c]);
+    const float mn = fmaxf(mx, f);
+    se = se * __expf(mx - mn) + __expf(f - mn);
+    mx = mn;
+  }
+  const float bmx = block_max(mx, scratch);
+  se = (mx == -INFINITY) ? 0.f : se * __expf(mx - bmx);
+  mx = bmx;
   se = block_sum(se, scratch);
   const float lse = mx + __logf(se);
   const int64_t tgt = target[m];
@@ -550,7 +579,7 @@ static int norm_bwd(const float* x, const void* dy, const void* g, const float* 
   unsigned grid = 0;
   auto go = [&](auto kern, int tpr) {
     int64_t blocks = (M * tpr + kRowThreads - 1) / kRowThreads;
-    const int64_t cap = tpr == 32 ? kNormBwdMaxBlocks : kNumSMs * 2;
+    const int64_t cap = tpr <= 64 ? kNormBwdMaxBlocks : kNumSMs * 2;
     grid = (unsigned)(blocks < cap ? blocks : cap);  // partial buffer: grid * 3 * D floats
     kern<<<grid, kRowThreads, 0, st>>>(x, (const __nv_bfloat16*)dy, (const __nv_bfloat16*)g, mean, rstd, dx,
                                        (__nv_bfloat16*)dx_bf16, work, M, dxsum != nullptr);
@@ -561,7 +590,7 @@ static int norm_bwd(const float* x, const void* dy, const void* g, const float* 
     case 128: rc = go(norm_bwd_kernel<128, 32, RMS>, 32); break;
     case 256: rc = go(norm_bwd_kernel<256, 32, RMS>, 32); break;
     case 512: rc = go(norm_bwd_kernel<512, 32, RMS>, 32); break;
-    case 768: rc = go(norm_bwd_kernel<768, 32, RMS>, 32); break;
+    case 768: rc = go(norm_bwd_kernel<768, 64, RMS>, 64); break;
     case 1024: rc = go(norm_bwd_kernel<1024, 32, RMS>, 32); break;
     case 2048: rc = go(norm_bwd_kernel<2048, 256, RMS>, 256); break;
     case 4096: rc = go(norm_bwd_kernel<4096, 256, RMS>, 256); break;
@@ -570,12 +599,9 @@ static int norm_bwd(const float* x, const void* dy, const void* g, const float* 
       return B2S_EUNSUPPORTED;
   }
   if (rc) return rc;
-  const unsigned g2 = (D + 31) / 32;
-  int n = 0;
-  if (dg) { reduce_parts_kernel<<<g2, 256, 0, st>>>(work, grid, D, 0, dg); ++n; }
-  if (!RMS && db) { reduce_parts_kernel<<<g2, 256, 0, st>>>(work, grid, D, 1, db); ++n; }
-  if (dxsum) { reduce_parts_kernel<<<g2, 256, 0, st>>>(work, grid, D, 2, dxsum); ++n; }
-  return check_launch("norm_bwd_reduce", n);
+  if (!dg && !(db && !RMS) && !dxsum) return B2S_OK;
+  reduce_parts_kernel<<<dim3((D + 31) / 32, 3), 256, 0, st>>>(work, grid, D, dg, RMS ? nullptr : db, dxsum);
+  return check_launch("norm_bwd_reduce");
 }
 
 }  // namespace ew

@@ -50,7 +50,7 @@ class FusedAdamW:
         """Device scalar: global squared L2 norm of the (reduce-scattered) gradients."""
         flats = params.flat
         dev = flats[0].g.device
-        nparts = 64
+        nparts = 4 * 148
         if self._part is None:
             self._part = torch.empty(len(flats) * nparts, device=dev)
             self._gn2 = torch.empty(1, device=dev)
