@@ -15,6 +15,8 @@
 // TMA store (or TMA add-reduce when accumulating), so global writes are
 // full-line and asynchronous. Grid = #SMs, tiles strided over CTAs.
 #include <mutex>
+#include <stdio.h>
+#include <stdlib.h>
 #include "common.cuh"
 #include "sm100.cuh"
 
@@ -94,12 +96,12 @@ __device__ __forceinline__ float gelu_tanh_grad(float x) {
   return 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * k0 * (1.f + 3.f * k1 * x2);
 }
 
-template <int BN>
+template <int BN, int CG>
 struct Cfg {
-  static constexpr int kABytes = BM * BK * 2;
-  static constexpr int kBBytes = BN * BK * 2;
+  static constexpr int kABytes = BM * BK * 2;          // this CTA's 128 rows of A
+  static constexpr int kBBytes = (BN / CG) * BK * 2;   // this CTA's share of B's BN rows
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kStages = (BN == 256) ? 3 : 4;
+  static constexpr int kStages = (CG == 2) ? 5 : (BN == 256 ? 3 : 4);
   static constexpr int kTmemCols = 2 * BN;  // double-buffered accumulator
   static constexpr int kSmem = kStages * kStageBytes + kEpiSmem + 1024 /*align*/ + 256 /*barriers*/;
   static_assert(kSmem <= 227 * 1024, "smem budget");
@@ -129,13 +131,21 @@ __device__ __forceinline__ void stage_f32(uint8_t* buf, int lane, const float* v
   }
 }
 
-template <int BN, bool A_MN, bool B_MN>
+// CG = 1: one CTA computes a 128 x BN tile.
+// CG = 2: a CTA pair (cluster of 2) computes a 256 x BN tile with
+//   tcgen05.mma.cta_group::2 (M = 256): each CTA stages its 128 rows of A and
+//   BN/2 rows of B, TMA completion bytes of both land on the leader's barrier,
+//   the leader alone issues the MMAs, and commits multicast to both CTAs.
+//   Each CTA's TMEM holds its own 128 x BN half of the accumulator, which its
+//   own epilogue warps drain. Per-SM operand traffic drops by 1/3.
+template <int BN, int CG, bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmAux,
                 int M, int N, int K, int splits, Epi epi) {
-  using C_ = Cfg<BN>;
-  constexpr uint32_t kIdesc = make_idesc_bf16(BM, BN, A_MN, B_MN);
+  using C_ = Cfg<BN, CG>;
+  constexpr uint32_t kIdesc = make_idesc_bf16(BM * CG, BN, A_MN, B_MN);
+  constexpr int BNc = BN / CG;  // B rows (N) staged by this CTA
   extern __shared__ uint8_t smem_raw[];
   // align by offsetting (keeps the shared address space: STS, not generic stores)
   uint8_t* smem = smem_raw + ((1024u - (static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw)) & 1023u)) & 1023u);
@@ -148,66 +158,90 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(auxbar + kEpiWarps);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int num_m = (M + BM - 1) / BM, num_n = (N + BN - 1) / BN;
+  const uint32_t rank = (CG == 2) ? cluster_ctarank() : 0;
+  const bool leader = rank == 0;
+  const int num_m = (M + BM * CG - 1) / (BM * CG), num_n = (N + BN - 1) / BN;
   const int num_tiles = num_m * num_n * splits;  // split-K tiles add-reduce into C
   const int num_kb_all = (K + BK - 1) / BK;
   const int kb_per = (num_kb_all + splits - 1) / splits;
+  const int tile0 = blockIdx.x / CG, tstride = gridDim.x / CG;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
     tma_prefetch(&tmC);
     for (int s = 0; s < C_::kStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], kEpiWarps); }
+    for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], CG * kEpiWarps); }
     for (int w = 0; w < kEpiWarps; ++w) mbar_init(&auxbar[w], 1);
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc<C_::kTmemCols>(tmem_base_slot);
+  if (warp == 1) {
+    if constexpr (CG == 2) tmem_alloc_pair<C_::kTmemCols>(tmem_base_slot);
+    else tmem_alloc<C_::kTmemCols>(tmem_base_slot);
+  }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) cluster_sync();  // peer barriers initialised before any remote arrive
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_base_slot;
 
   if (warp == 0) {
-    // ------------------------------------------------ TMA producer
+    // ------------------------------------------------ TMA producer (both CTAs)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      for (int tile = tile0; tile < num_tiles; tile += tstride) {
         const int mn = tile % (num_m * num_n), ks = tile / (num_m * num_n);
-        const int m0 = (mn % num_m) * BM, n0 = (mn / num_m) * BN;
+        const int m0 = (mn % num_m) * BM * CG + rank * BM, n0 = (mn / num_m) * BN + rank * BNc;
         const int kb0 = ks * kb_per, kb1 = min(num_kb_all, kb0 + kb_per);
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * C_::kStageBytes;
           uint8_t* sb = sa + C_::kABytes;
           const int k0 = kb * BK;
-          if constexpr (A_MN) {
+          if constexpr (CG == 1) {
+            if constexpr (A_MN) {
 #pragma unroll
-            for (int j = 0; j < BM / 64; ++j) tma_load_2d(sa + j * (64 * BK * 2), &tmA, &full[stage], m0 + 64 * j, k0);
-          } else {
-            tma_load_2d(sa, &tmA, &full[stage], k0, m0);
-          }
-          if constexpr (B_MN) {
+              for (int j = 0; j < BM / 64; ++j) tma_load_2d(sa + j * (64 * BK * 2), &tmA, &full[stage], m0 + 64 * j, k0);
+            } else {
+              tma_load_2d(sa, &tmA, &full[stage], k0, m0);
+            }
+            if constexpr (B_MN) {
 #pragma unroll
-            for (int j = 0; j < BN / 64; ++j) tma_load_2d(sb + j * (64 * BK * 2), &tmB, &full[stage], n0 + 64 * j, k0);
+              for (int j = 0; j < BNc / 64; ++j) tma_load_2d(sb + j * (64 * BK * 2), &tmB, &full[stage], n0 + 64 * j, k0);
+            } else {
+              tma_load_2d(sb, &tmB, &full[stage], k0, n0);
+            }
+            mbar_arrive_expect_tx(&full[stage], C_::kStageBytes);
           } else {
-            tma_load_2d(sb, &tmB, &full[stage], k0, n0);
+            const uint32_t bar = mapa_shared(smem_u32(&full[stage]), 0);  // the leader's barrier
+            if (leader) mbar_arrive_expect_tx(&full[stage], 2 * C_::kStageBytes);
+            if constexpr (A_MN) {
+#pragma unroll
+              for (int j = 0; j < BM / 64; ++j) tma_load_2d_pair(sa + j * (64 * BK * 2), &tmA, bar, m0 + 64 * j, k0);
+            } else {
+              tma_load_2d_pair(sa, &tmA, bar, k0, m0);
+            }
+            if constexpr (B_MN) {
+#pragma unroll
+              for (int j = 0; j < BNc / 64; ++j) tma_load_2d_pair(sb + j * (64 * BK * 2), &tmB, bar, n0 + 64 * j, k0);
+            } else {
+              tma_load_2d_pair(sb, &tmB, bar, k0, n0);
+            }
           }
-          mbar_arrive_expect_tx(&full[stage], C_::kStageBytes);
           if (++stage == C_::kStages) { stage = 0; phase ^= 1; }
         }
       }
     }
     __syncwarp();
   } else if (warp == 1) {
-    // ------------------------------------------------ MMA issuer
-    if (lane == 0) {
+    // ------------------------------------------------ MMA issuer (leader CTA)
+    if (lane == 0 && leader) {
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      for (int tile = tile0; tile < num_tiles; tile += tstride) {
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
@@ -225,12 +259,17 @@ __global__ void __launch_bounds__(kThreads, 1)
             else ad = make_sdesc(sa + kk * (UMMA_K * 2), 16, 1024);
             if constexpr (B_MN) bd = make_sdesc(sb + kk * (UMMA_K * 128), 64 * BK * 2, 1024);
             else bd = make_sdesc(sb + kk * (UMMA_K * 2), 16, 1024);
-            mma_bf16_ss(d_tmem, ad, bd, kIdesc, (kb > kb0 || kk) ? 1u : 0u);
+            if constexpr (CG == 2) mma_bf16_ss_pair(d_tmem, ad, bd, kIdesc, (kb > kb0 || kk) ? 1u : 0u);
+            else mma_bf16_ss(d_tmem, ad, bd, kIdesc, (kb > kb0 || kk) ? 1u : 0u);
           }
-          mma_commit(&empty[stage]);  // frees the smem slot once these MMAs retire
+          // frees the smem slot (in both CTAs) once these MMAs retire
+          if constexpr (CG == 2) mma_commit_pair(&empty[stage], 0x3);
+          else mma_commit(&empty[stage]);
           if (++stage == C_::kStages) { stage = 0; phase ^= 1; }
         }
-        mma_commit(&tfull[acc]);  // accumulator ready for the epilogue
+        // accumulator ready for the epilogue(s)
+        if constexpr (CG == 2) mma_commit_pair(&tfull[acc], 0x3);
+        else mma_commit(&tfull[acc]);
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
     }
@@ -253,9 +292,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       slot ^= 1;
       return b;
     };
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+    for (int tile = tile0; tile < num_tiles; tile += tstride) {
       const int mn = tile % (num_m * num_n);
-      const int m0 = (mn % num_m) * BM, n0 = (mn / num_m) * BN;
+      const int m0 = (mn % num_m) * BM * CG + rank * BM, n0 = (mn / num_m) * BN;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const int rbase = m0 + q * 32;
@@ -277,7 +316,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (c + 2 >= BN / 32) {  // this warp's last chunk read: release the accumulator
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&tempty[acc]);
+          if (lane == 0) {
+            if constexpr (CG == 2) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));
+            else mbar_arrive(&tempty[acc]);
+          }
         }
         if (!live) continue;
         float v[32];
@@ -332,48 +374,89 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) cluster_sync();  // no CTA leaves while its peer may still signal it
+  else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc<C_::kTmemCols>(tmem_base);
+    if constexpr (CG == 2) tmem_dealloc_pair<C_::kTmemCols>(tmem_base);
+    else tmem_dealloc<C_::kTmemCols>(tmem_base);
   }
 }
 
-template <int BN, bool A_MN, bool B_MN>
+template <int BN, int CG, bool A_MN, bool B_MN>
 static int launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc,
                   const CUtensorMap& tx, int M, int N, int K, int splits, const Epi& e, cudaStream_t st) {
-  using C_ = Cfg<BN>;
-  auto kern = gemm_kernel<BN, A_MN, B_MN>;
+  using C_ = Cfg<BN, CG>;
+  auto kern = gemm_kernel<BN, CG, A_MN, B_MN>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::kSmem);
+    if (CG == 2) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
     attr_set = true;
   }
-  const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN) * splits;
-  const int grid = tiles < kNumSMs ? tiles : kNumSMs;
-  kern<<<grid, kThreads, C_::kSmem, st>>>(ta, tb, tc, tx, M, N, K, splits, e);
+  const int tiles = ((M + BM * CG - 1) / (BM * CG)) * ((N + BN - 1) / BN) * splits;
+  const int slots = kNumSMs / CG;
+  const int grid = (tiles < slots ? tiles : slots) * CG;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = C_::kSmem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, tx, M, N, K, splits, e);
   return check_launch("gemm");
 }
 
-template <int BN>
+template <int BN, int CG>
 static int dispatch(bool amn, bool bmn, const CUtensorMap& ta, const CUtensorMap& tb,
                     const CUtensorMap& tc, const CUtensorMap& tx, int M, int N, int K,
                     int splits, const Epi& e, cudaStream_t st) {
-  if (!amn && !bmn) return launch<BN, false, false>(ta, tb, tc, tx, M, N, K, splits, e, st);
-  if (!amn && bmn) return launch<BN, false, true>(ta, tb, tc, tx, M, N, K, splits, e, st);
-  if (amn && !bmn) return launch<BN, true, false>(ta, tb, tc, tx, M, N, K, splits, e, st);
-  return launch<BN, true, true>(ta, tb, tc, tx, M, N, K, splits, e, st);
+  if (!amn && !bmn) return launch<BN, CG, false, false>(ta, tb, tc, tx, M, N, K, splits, e, st);
+  if (!amn && bmn) return launch<BN, CG, false, true>(ta, tb, tc, tx, M, N, K, splits, e, st);
+  if (amn && !bmn) return launch<BN, CG, true, false>(ta, tb, tc, tx, M, N, K, splits, e, st);
+  return launch<BN, CG, true, true>(ta, tb, tc, tx, M, N, K, splits, e, st);
 }
 
-// Pick the N tile: 256 unless 128 fills the 148 SMs' last wave much better.
-static int pick_bn(int M, int N) {
-  auto eff = [&](int bn) {
-    long t = (long)((M + BM - 1) / BM) * ((N + bn - 1) / bn);
-    long waves = (t + kNumSMs - 1) / kNumSMs;
-    double pad = (double)N / (double)(((N + bn - 1) / bn) * bn);
-    return pad * (double)t / (double)(waves * kNumSMs);
-  };
-  return eff(128) > eff(256) * 1.08 ? 128 : 256;
+// Tile choice: (BN, CTA group, split-K) maximising filled SM slots in the last
+// wave, weighted by the measured per-tile speed of each configuration.
+struct Choice {
+  int bn, cg, splits;
+};
+static Choice choose(int M, int N, int K, bool can_split) {
+  const int nkb = (K + BK - 1) / BK;
+  if (const char* f = getenv("B2S_GEMM_FORCE")) {  // "bn,cg,splits" (tests / tuning)
+    Choice c{256, 1, 1};
+    if (sscanf(f, "%d,%d,%d", &c.bn, &c.cg, &c.splits) == 3 && (c.bn == 128 || c.bn == 256) &&
+        (c.cg == 1 || (c.cg == 2 && c.bn == 256)) && c.splits >= 1) {
+      if (!can_split) c.splits = 1;
+      return c;
+    }
+  }
+  const Choice cands[3] = {{256, 2, 1}, {256, 1, 1}, {128, 1, 1}};
+  const double speed[3] = {1.2, 1.05, 1.0};
+  Choice best = cands[2];
+  double best_score = -1.0;
+  for (int i = 0; i < 3; ++i) {
+    for (int sp = 1; sp <= (can_split ? 16 : 1); sp *= 2) {
+      if (sp > 1 && nkb / sp < 8) break;
+      const Choice c{cands[i].bn, cands[i].cg, sp};
+      const long mt = (M + BM * c.cg - 1) / (BM * c.cg), nt = (N + c.bn - 1) / c.bn;
+      const long tiles = mt * nt * sp, slots = kNumSMs / c.cg;
+      const long waves = (tiles + slots - 1) / slots;
+      const double fill = (double)tiles / (double)(waves * slots);
+      const double pad = ((double)M / (mt * BM * c.cg)) * ((double)N / (nt * c.bn));
+      const double split_cost = 1.0 - 0.02 * (sp - 1);  // extra fp32 add-reduce traffic
+      const double score = fill * pad * speed[i] * split_cost;
+      if (score > best_score * 1.001) { best_score = score; best = c; }
+    }
+  }
+  return best;
 }
 
 }  // namespace gemm
@@ -396,14 +479,15 @@ extern "C" int b2s_gemm(const void* d_A, int a_mn_major, int64_t lda, const void
                            ((uintptr_t)d_aux % 16) == 0),
               B2S_EINVAL, "gemm: activation epilogue needs an aligned bf16 aux buffer and bf16 output");
   B2S_REQUIRE(!(accumulate && act == 1), B2S_EINVAL, "gemm: accumulate with GELU is not supported");
-  const int bn = gemm::pick_bn(M, N);
+  const gemm::Choice ch = gemm::choose(M, N, K, accumulate && !d_bias && act == 0);
+  const int bn = ch.bn, bnc = ch.bn / ch.cg;
   CUtensorMap ta, tb, tc, tx;
   int rc;
   if (a_mn_major) rc = encode_tma_2d(&ta, d_A, 2, (uint64_t)M, (uint64_t)K, (uint64_t)lda * 2, 64, gemm::BK, 128);
   else rc = encode_tma_2d(&ta, d_A, 2, (uint64_t)K, (uint64_t)M, (uint64_t)lda * 2, gemm::BK, gemm::BM, 128);
   if (rc) return rc;
   if (b_mn_major) rc = encode_tma_2d(&tb, d_B, 2, (uint64_t)N, (uint64_t)K, (uint64_t)ldb * 2, 64, gemm::BK, 128);
-  else rc = encode_tma_2d(&tb, d_B, 2, (uint64_t)K, (uint64_t)N, (uint64_t)ldb * 2, gemm::BK, (uint32_t)bn, 128);
+  else rc = encode_tma_2d(&tb, d_B, 2, (uint64_t)K, (uint64_t)N, (uint64_t)ldb * 2, gemm::BK, (uint32_t)bnc, 128);
   if (rc) return rc;
   if (c_f32) rc = encode_tma_2d(&tc, d_C, 4, (uint64_t)N, (uint64_t)M, (uint64_t)ldc * 4, 32, 32, 128);
   else rc = encode_tma_2d(&tc, d_C, 2, (uint64_t)N, (uint64_t)M, (uint64_t)ldc * 2, 32, 32, 64);
@@ -413,14 +497,8 @@ extern "C" int b2s_gemm(const void* d_A, int a_mn_major, int64_t lda, const void
   if (rc) return rc;
   gemm::Epi e{c_f32, accumulate, (const __nv_bfloat16*)d_bias, act, (const __nv_bfloat16*)d_aux, ld_aux};
   cudaStream_t st = (cudaStream_t)stream;
-  // Split K when the output has too few tiles to fill the GPU; only legal when
-  // accumulating (the partial sums add-reduce into C through TMA).
-  int splits = 1;
-  if (accumulate && !d_bias && act == 0) {
-    const long tiles = (long)((M + gemm::BM - 1) / gemm::BM) * ((N + bn - 1) / bn);
-    const int nkb = (K + gemm::BK - 1) / gemm::BK;
-    while (tiles * splits * 2 <= 2L * kNumSMs && nkb / (splits * 2) >= 8) splits *= 2;
-  }
-  if (bn == 256) return gemm::dispatch<256>(a_mn_major, b_mn_major, ta, tb, tc, tx, M, N, K, splits, e, st);
-  return gemm::dispatch<128>(a_mn_major, b_mn_major, ta, tb, tc, tx, M, N, K, splits, e, st);
+  const int splits = ch.splits;
+  if (ch.cg == 2) return gemm::dispatch<256, 2>(a_mn_major, b_mn_major, ta, tb, tc, tx, M, N, K, splits, e, st);
+  if (bn == 256) return gemm::dispatch<256, 1>(a_mn_major, b_mn_major, ta, tb, tc, tx, M, N, K, splits, e, st);
+  return gemm::dispatch<128, 1>(a_mn_major, b_mn_major, ta, tb, tc, tx, M, N, K, splits, e, st);
 }

@@ -16,10 +16,22 @@ SHAPES = [(128, 128, 64), (256, 512, 128), (200, 136, 72), (1000, 776, 264), (38
           (130, 256, 4096), (64, 64, 8)]
 
 
+FORCES = ["", "256,1,1", "128,1,1", "256,2,1"]
+
+
+@pytest.fixture(params=FORCES)
+def force(request, monkeypatch):
+    if request.param:
+        monkeypatch.setenv("B2S_GEMM_FORCE", request.param)
+    else:
+        monkeypatch.delenv("B2S_GEMM_FORCE", raising=False)
+    return request.param
+
+
 @pytest.mark.parametrize("a_mn", [False, True])
 @pytest.mark.parametrize("b_mn", [False, True])
 @pytest.mark.parametrize("shape", SHAPES)
-def test_gemm_layouts(cuda, a_mn, b_mn, shape):
+def test_gemm_layouts(cuda, a_mn, b_mn, shape, force):
     from paper_2602_08387_b200 import ops
 
     M, N, K = shape
@@ -35,7 +47,7 @@ def test_gemm_layouts(cuda, a_mn, b_mn, shape):
     torch.testing.assert_close(c16.float(), ref, rtol=1e-2, atol=1e-2 * K ** 0.5)
 
 
-def test_gemm_epilogues(cuda):
+def test_gemm_epilogues(cuda, force):
     from paper_2602_08387_b200 import ops
 
     M, N, K = 300, 520, 192
@@ -66,3 +78,17 @@ def test_gemm_epilogues(cuda):
     out = res.clone()
     ops.linear(x, w, out=out, accumulate=True)
     torch.testing.assert_close(out.float(), res.float() + x.float() @ w.float().t(), rtol=1e-2, atol=3e-2)
+
+
+@pytest.mark.parametrize("force_split", ["256,1,4", "256,2,4", "128,1,8"])
+def test_gemm_split_k(cuda, monkeypatch, force_split):
+    from paper_2602_08387_b200 import ops
+
+    monkeypatch.setenv("B2S_GEMM_FORCE", force_split)
+    M, N, K = 768, 2304, 4096  # wgrad-like: few output tiles, long K
+    a = torch.randn(K, M, device=cuda).bfloat16()
+    b = torch.randn(K, N, device=cuda).bfloat16()
+    c = torch.randn(M, N, device=cuda)
+    ref = c + a.float().t() @ b.float()
+    ops.gemm(a, b, a_mn=True, b_mn=True, M=M, N=N, K=K, out=c, accumulate=True)
+    torch.testing.assert_close(c, ref, rtol=1e-4, atol=5e-2)
