@@ -62,6 +62,8 @@ class PackedDataLoader:
         self.rank, self.world, self.device = rank, world, torch.device(device)
         n = self.dataset.sample_count(self.seq_len)
         self._order = self.sampler.order(n)
+        if self.device.type != "cuda":  # host-side use (sample_ids only), e.g. gloo tests
+            return self
         B, L = self.batch_size, self.seq_len
         self._in = torch.empty(B, L, dtype=torch.int64, device=self.device)
         self._tg = torch.empty(B, L, dtype=torch.int64, device=self.device)

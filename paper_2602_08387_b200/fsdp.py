@@ -175,10 +175,13 @@ class Engine:
         self.group = group
         self.world = world
         self.prefetch = prefetch
-        self.comm = torch.cuda.Stream() if world > 1 else None
+        # CUDA: collectives on a side stream fenced by events. CPU (gloo, host-side
+        # tests of the sharding logic): plain synchronous collectives.
+        self.cuda = params.flat[0].full.is_cuda
+        self.comm = torch.cuda.Stream() if (world > 1 and self.cuda) else None
         n = len(params.flat)
-        self.ag_done = [torch.cuda.Event() for _ in range(n)]
-        self.rs_done = [torch.cuda.Event() for _ in range(n)]
+        self.ag_done = [torch.cuda.Event() for _ in range(n)] if self.cuda else [None] * n
+        self.rs_done = [torch.cuda.Event() for _ in range(n)] if self.cuda else [None] * n
         self._issued = 0
         self.bytes_ag = sum(f.padded * 2 for f in params.flat)
         self.bytes_rs = sum(f.padded * 4 for f in params.flat)
@@ -189,18 +192,22 @@ class Engine:
             f.gfull.zero_()
         self._issued = 0
         if self.world > 1:
-            ready = torch.cuda.Event()
-            ready.record()  # after the previous optimizer step wrote p16
-            self.comm.wait_event(ready)
+            if self.cuda:
+                ready = torch.cuda.Event()
+                ready.record()  # after the previous optimizer step wrote p16
+                self.comm.wait_event(ready)
             self._issue_until(min(len(self.P.flat), self.prefetch))
 
     def _issue_until(self, k: int) -> None:
-        with torch.cuda.stream(self.comm):
-            while self._issued < k:
-                f = self.P.flat[self._issued]
+        while self._issued < k:
+            f = self.P.flat[self._issued]
+            if self.cuda:
+                with torch.cuda.stream(self.comm):
+                    dist.all_gather_into_tensor(f.full, f.p16, group=self.group)
+                    self.ag_done[self._issued].record(self.comm)
+            else:
                 dist.all_gather_into_tensor(f.full, f.p16, group=self.group)
-                self.ag_done[self._issued].record(self.comm)
-                self._issued += 1
+            self._issued += 1
 
     def before_forward(self, model_unit: int) -> None:
         if self.world == 1:
@@ -209,7 +216,8 @@ class Engine:
         if self.P.first_model_unit[fi] != model_unit:
             return
         self._issue_until(min(len(self.P.flat), fi + 1 + self.prefetch))
-        torch.cuda.current_stream().wait_event(self.ag_done[fi])
+        if self.cuda:
+            torch.cuda.current_stream().wait_event(self.ag_done[fi])
 
     def after_backward(self, model_unit: int) -> None:
         if self.world == 1:
@@ -217,16 +225,21 @@ class Engine:
         fi = self.P.owner[model_unit]
         if self.P.first_model_unit[fi] != model_unit:
             return  # the unit's gradients are complete once its first model unit is done
+        f = self.P.flat[fi]
+        if not self.cuda:
+            # gloo has no AVG reduce-scatter: SUM then scale (host-side tests only)
+            dist.reduce_scatter_tensor(f.g, f.gfull, op=dist.ReduceOp.SUM, group=self.group)
+            f.g.div_(self.world)
+            return
         done = torch.cuda.Event()
         done.record()
         self.comm.wait_event(done)
-        f = self.P.flat[fi]
         with torch.cuda.stream(self.comm):
             dist.reduce_scatter_tensor(f.g, f.gfull, op=dist.ReduceOp.AVG, group=self.group)
             self.rs_done[fi].record(self.comm)
 
     def end_backward(self) -> None:
-        if self.world == 1:
+        if self.world == 1 or not self.cuda:
             return
         cur = torch.cuda.current_stream()
         for e in self.rs_done:
