@@ -78,6 +78,32 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
+// P = 2^(s*sl2 - m) for 64 columns of one row -> bf16 -> swizzled smem; returns
+// the row sum. The causal mask is a template branch so off-diagonal blocks run
+// the mask-free instruction stream.
+template <bool DIAG>
+__device__ __forceinline__ float exp_pack(const uint32_t* v, int col0, int r, float sl2, float m,
+                                          uint8_t* dst) {
+  float rs = 0.f;
+#pragma unroll
+  for (int k8 = 0; k8 < 8; ++k8) {
+    float e[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float x = ex2(fmaf(__uint_as_float(v[k8 * 8 + i]), sl2, -m));
+      e[i] = (DIAG && col0 + k8 * 8 + i > r) ? 0.f : x;
+      rs += e[i];
+    }
+    uint4 w;
+    w.x = pack_bf16x2(e[0], e[1]);
+    w.y = pack_bf16x2(e[2], e[3]);
+    w.z = pack_bf16x2(e[4], e[5]);
+    w.w = pack_bf16x2(e[6], e[7]);
+    *reinterpret_cast<uint4*>(dst + swz(r, k8)) = w;
+  }
+  return rs;
+}
+
 __global__ void __launch_bounds__(320, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_o,
                     Params p) {
@@ -93,8 +119,9 @@ __global__ void __launch_bounds__(320, 1)
   uint64_t* kv_empty = v_full + kStages;      // [kStages]
   uint64_t* s_full = kv_empty + kStages;      // [2] per tile
   uint64_t* s_empty = s_full + 2;             // [2]
-  uint64_t* p_full = s_empty + 2;             // [2]
-  uint64_t* p_empty = p_full + 2;             // [tile][buf]
+  uint64_t* p_full = s_empty + 2;             // [tile][buf]: per buffer, so a group running a block
+                                              // ahead of the MMA warp cannot alias a barrier phase
+  uint64_t* p_empty = p_full + 4;             // [tile][buf]
   uint64_t* o_done = p_empty + 4;             // [2] last PV of the tile retired
   uint64_t* pv_done = o_done + 2;             // [2] each PV retired (rescale fence)
   uint32_t* tslot = reinterpret_cast<uint32_t*>(pv_done + 2);
@@ -116,7 +143,8 @@ __global__ void __launch_bounds__(320, 1)
     mbar_init(q_full, 1);
     for (int s = 0; s < kStages; ++s) { mbar_init(&k_full[s], 1); mbar_init(&v_full[s], 1); mbar_init(&kv_empty[s], 1); }
     for (int t = 0; t < 2; ++t) {
-      mbar_init(&s_full[t], 1); mbar_init(&s_empty[t], 4); mbar_init(&p_full[t], 4);
+      mbar_init(&s_full[t], 1); mbar_init(&s_empty[t], 4);
+      mbar_init(&p_full[2 * t], 4); mbar_init(&p_full[2 * t + 1], 4);
       mbar_init(&o_done[t], 1); mbar_init(&pv_done[t], 1);
       mbar_init(&p_empty[2 * t], 1); mbar_init(&p_empty[2 * t + 1], 1);
     }
@@ -164,7 +192,7 @@ __global__ void __launch_bounds__(320, 1)
       auto issue_PV = [&](int t, int j, bool last) {
         const int s = j % kStages;
         mbar_wait(&v_full[s], (j / kStages) & 1);
-        mbar_wait(&p_full[t], j & 1);
+        mbar_wait(&p_full[2 * t + (j & 1)], (j >> 1) & 1);
         tc_fence_after();
         const uint32_t pbase = aP + (2 * t + (j & 1)) * 2 * kTile;
 #pragma unroll
@@ -179,10 +207,12 @@ __global__ void __launch_bounds__(320, 1)
       issue_S(0, 0);
       if (nB > 0) issue_S(1, 0);
       for (int j = 0; j < nkv; ++j) {
-        if (j < nA) issue_PV(0, j, j + 1 == nA);
+        // QK^T of block j+1 goes in as soon as each softmax group holds S(j) in
+        // registers, so it is ready when the group finishes block j
         if (j + 1 < nA) issue_S(0, j + 1);
-        if (j < nB) issue_PV(1, j, j + 1 == nB);
         if (j + 1 < nB) issue_S(1, j + 1);
+        if (j < nA) issue_PV(0, j, j + 1 == nA);
+        if (j < nB) issue_PV(1, j, j + 1 == nB);
         mma_commit(&kv_empty[j % kStages]);  // K_j / V_j no longer read once these retire
       }
     }
@@ -203,23 +233,22 @@ __global__ void __launch_bounds__(320, 1)
       mbar_wait(&s_full[t], j & 1);
       tc_fence_after();
       const bool diag = (j == qt);
-      // 10 warps/CTA puts 3 warps on some SMSPs: 168 registers per thread, so
-      // S is read from TMEM in two 64-column halves (max pass, then exp pass)
+      // the whole 128-column S row in registers: one TMEM round trip per block
+      uint32_t v[BKV];
+#pragma unroll
+      for (int c = 0; c < BKV / 32; ++c) tmem_ld32(tS + c * 32, v + c * 32);
+      tmem_wait_ld();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s_empty[t]);  // S(j) is in registers: QK^T(j+1) may overwrite it
       float mx = -INFINITY;
+      if (diag) {
 #pragma unroll
-      for (int hf = 0; hf < 2; ++hf) {
-        uint32_t v[64];
-        tmem_ld32(tS + hf * 64, v);
-        tmem_ld32(tS + hf * 64 + 32, v + 32);
-        tmem_wait_ld();
-        if (diag) {
+        for (int i = 0; i < BKV; ++i)
+          if (i <= r) mx = fmaxf(mx, __uint_as_float(v[i]));
+      } else {
 #pragma unroll
-          for (int i = 0; i < 64; ++i)
-            if (hf * 64 + i <= r) mx = fmaxf(mx, __uint_as_float(v[i]));
-        } else {
-#pragma unroll
-          for (int i = 0; i < 64; ++i) mx = fmaxf(mx, __uint_as_float(v[i]));
-        }
+        for (int i = 0; i < BKV; ++i) mx = fmaxf(mx, __uint_as_float(v[i]));
       }
       const float m_cand = mx * sl2;
       // lazy rescale: keep the old max unless the new one exceeds it by > 2^8
@@ -247,40 +276,19 @@ __global__ void __launch_bounds__(320, 1)
       if (j >= 2) mbar_wait(&p_empty[2 * t + pb], ((j >> 1) - 1) & 1);
       uint8_t* myP = sP + (2 * t + pb) * 2 * kTile;
       float rs = 0.f;
-#pragma unroll
-      for (int hf = 0; hf < 2; ++hf) {
-        uint32_t v[64];
-        tmem_ld32(tS + hf * 64, v);
-        tmem_ld32(tS + hf * 64 + 32, v + 32);
-        tmem_wait_ld();
-        if (hf == 1) {  // S fully consumed: the next QK^T may overwrite it
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&s_empty[t]);
-        }
-#pragma unroll
-        for (int k8 = 0; k8 < 8; ++k8) {
-          float e[8];
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const int col = hf * 64 + k8 * 8 + i;
-            e[i] = (diag && col > r) ? 0.f : ex2(fmaf(__uint_as_float(v[k8 * 8 + i]), sl2, -m_use));
-            rs += e[i];
-          }
-          uint4 w;
-          w.x = pack_bf16x2(e[0], e[1]);
-          w.y = pack_bf16x2(e[2], e[3]);
-          w.z = pack_bf16x2(e[4], e[5]);
-          w.w = pack_bf16x2(e[6], e[7]);
-          *reinterpret_cast<uint4*>(myP + hf * kTile + swz(r, k8)) = w;
-        }
+      if (diag) {
+        rs += exp_pack<true>(v, 0, r, sl2, m_use, myP);
+        rs += exp_pack<true>(v + 64, 64, r, sl2, m_use, myP + kTile);
+      } else {
+        rs += exp_pack<false>(v, 0, r, sl2, m_use, myP);
+        rs += exp_pack<false>(v + 64, 64, r, sl2, m_use, myP + kTile);
       }
       l = l * alpha + rs;
       m = m_use;
       tc_fence_before();
       fence_proxy_async_smem();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full[t]);
+      if (lane == 0) mbar_arrive(&p_full[2 * t + pb]);
     }
     if (nj > 0) {
       // epilogue: O (TMEM) / l -> bf16 -> this tile's Q buffer (all MMAs retired) -> TMA store
@@ -380,6 +388,21 @@ __global__ void attn_bwd_dq_kernel(const float* __restrict__ dq_acc, __nv_bfloat
 // double-buffered in TMEM: the compute warps drain dQ(t-1) (TMA add-reduce
 // into the fp32 accumulator) after publishing P/dS(t).
 constexpr int kBwdThreads = 320;
+
+// P^T = 2^(s*sl2 - lse2[q]) and dS^T = P^T (dP^T - D[q]) for 32 query columns of
+// one key row, in place in sv / dv (bit patterns of fp32). Mask = template branch.
+template <bool DIAG>
+__device__ __forceinline__ void p_ds(uint32_t* sv, uint32_t* dv, int q0, int r, float sl2, const float* lse2,
+                                     const float* dd) {
+#pragma unroll
+  for (int e = 0; e < 32; ++e) {
+    const int q = q0 + e;
+    float pv = ex2(fmaf(__uint_as_float(sv[e]), sl2, -lse2[q]));
+    if (DIAG && q < r) pv = 0.f;  // query index below key index: masked
+    sv[e] = __float_as_uint(pv);
+    dv[e] = __float_as_uint(pv * (__uint_as_float(dv[e]) - dd[q]));
+  }
+}
 constexpr int kBwdSmem = 1024 + 2 * kTile /*K,V*/ + 4 * kTile /*Q,dO x2*/ + 2 * kTile /*P^T*/ + 2 * kTile /*dS^T*/ +
                          2 * kTile /*dQ fp32 staging*/ + 4 * BQ * 4 /*lse2, D x2*/ + 256;
 
@@ -566,14 +589,8 @@ __global__ void __launch_bounds__(320, 1)
           __syncwarp();
           if (lane == 0) mbar_arrive(st_empty);  // the next step's S^T / dP^T may overwrite TMEM
         }
-#pragma unroll
-        for (int e = 0; e < 32; ++e) {
-          const int q = half * 64 + qq * 32 + e;
-          float pv = ex2(fmaf(__uint_as_float(sv[e]), p.scale_log2, -lse2[q]));
-          if (diag && q < r) pv = 0.f;  // query index below key index: masked
-          sv[e] = __float_as_uint(pv);
-          dv[e] = __float_as_uint(pv * (__uint_as_float(dv[e]) - dd[q]));
-        }
+        if (diag) p_ds<true>(sv, dv, half * 64 + qq * 32, r, p.scale_log2, lse2, dd);
+        else p_ds<false>(sv, dv, half * 64 + qq * 32, r, p.scale_log2, lse2, dd);
         if (qq == 0 && t > 0) mbar_wait(pds_empty, (t - 1) & 1);  // step t-1's MMAs released sP / sdS
 #pragma unroll
         for (int k8 = 0; k8 < 4; ++k8) {
