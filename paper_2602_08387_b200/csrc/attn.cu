@@ -43,6 +43,13 @@ __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
   const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(p));
   return p + ((1024u - (a & 1023u)) & 1023u);
 }
+// 1-D bulk copy global -> shared, completion counted on `bar` (no tensor map).
+__device__ __forceinline__ void bulk_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
 __device__ __forceinline__ void named_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
@@ -397,14 +404,14 @@ __device__ __forceinline__ void p_ds(uint32_t* sv, uint32_t* dv, int q0, int r, 
 #pragma unroll
   for (int e = 0; e < 32; ++e) {
     const int q = q0 + e;
-    float pv = ex2(fmaf(__uint_as_float(sv[e]), sl2, -lse2[q]));
+    float pv = ex2(fmaf(__uint_as_float(sv[e]), sl2, -lse2[q] * kLog2e));
     if (DIAG && q < r) pv = 0.f;  // query index below key index: masked
     sv[e] = __float_as_uint(pv);
     dv[e] = __float_as_uint(pv * (__uint_as_float(dv[e]) - dd[q]));
   }
 }
 constexpr int kBwdSmem = 1024 + 2 * kTile /*K,V*/ + 4 * kTile /*Q,dO x2*/ + 2 * kTile /*P^T*/ + 2 * kTile /*dS^T*/ +
-                         2 * kTile /*dQ fp32 staging*/ + 4 * BQ * 4 /*lse2, D x2*/ + 256;
+                         2 * kTile /*dQ fp32 staging: 8 warps x 4 KB*/ + 4 * BQ * 4 /*LSE, D x2*/ + 256;
 
 __global__ void __launch_bounds__(320, 1)
     attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
@@ -417,8 +424,8 @@ __global__ void __launch_bounds__(320, 1)
   uint8_t* sP = sdO + 2 * kTile;     // P^T  [128 keys][128 q] as two 64-column atoms
   uint8_t* sdS = sP + 2 * kTile;     // dS^T
   uint8_t* sdQ = sdS + 2 * kTile;    // fp32 128 x 64 as two 32-column boxes (16 KB each)
-  float* sLse = reinterpret_cast<float*>(sdQ + 2 * kTile);  // [2][128] (log2 domain)
-  float* sD = sLse + 2 * BQ;                                 // [2][128]
+  float* sLse = reinterpret_cast<float*>(sdQ + 2 * kTile);  // [2][128] natural-log LSE (TMA bulk)
+  float* sD = sLse + 2 * BQ;                                 // [2][128] rowsum(dO*O)
   uint64_t* bars = reinterpret_cast<uint64_t*>(sD + 2 * BQ);
   uint64_t* kv_full = bars;
   uint64_t* qd_full = bars + 1;   // [2]
@@ -430,7 +437,9 @@ __global__ void __launch_bounds__(320, 1)
   uint64_t* dq_full = bars + 9;   // [2]
   uint64_t* dq_empty = bars + 11; // [2]
   uint64_t* done = bars + 13;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 14);
+  uint64_t* st_ld_full = bars + 14;   // [2] lse / D of a step landed
+  uint64_t* st_ld_empty = bars + 16;  // [2] all compute warps done with them
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 18);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nbk = p.B * p.Hkv;
@@ -454,6 +463,7 @@ __global__ void __launch_bounds__(320, 1)
     mbar_init(pds_full, 8);
     mbar_init(pds_empty, 1);
     mbar_init(done, 1);
+    for (int s = 0; s < 2; ++s) { mbar_init(&st_ld_full[s], 1); mbar_init(&st_ld_empty[s], 8); }
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<512>(tslot);
@@ -471,6 +481,11 @@ __global__ void __launch_bounds__(320, 1)
       for (int t = 0; t < nsteps; ++t) {
         const int h = kvh * G + t / nq, i = kt + t % nq;
         const int s = t & 1;
+        mbar_wait(&st_ld_empty[s], ((t >> 1) & 1) ^ 1);
+        const size_t off = ((size_t)b * p.Hq + h) * p.T + (size_t)i * BQ;
+        mbar_arrive_expect_tx(&st_ld_full[s], 2 * BQ * 4);
+        bulk_load_1d(sLse + s * BQ, p.lse + off, BQ * 4, &st_ld_full[s]);
+        bulk_load_1d(sD + s * BQ, p.dsum + off, BQ * 4, &st_ld_full[s]);
         mbar_wait(&qd_empty[s], ((t >> 1) & 1) ^ 1);
         mbar_arrive_expect_tx(&qd_full[s], 2 * kTile);
         tma_load_2d(sQ + s * kTile, &tm_qkv, &qd_full[s], h * DH, b * p.T + i * BQ);
@@ -534,7 +549,10 @@ __global__ void __launch_bounds__(320, 1)
     const int half = (warp - 2) >> 2;
     const int r = q4 * 32 + lane;  // key row (S^T / dP^T / dV / dK lanes) and query row (dQ lanes)
     const uint32_t lrow = (uint32_t)(q4 * 32) << 16;
-    auto drain_dq = [&](int t) {  // dQ(t) (TMEM buffer t&1) -> fp32 smem -> TMA add-reduce
+    // dQ(t) (TMEM buffer t&1): each warp drains its own 32 query rows x 32 columns
+    // through a private 4 KB staging tile and its own TMA add-reduce (no CTA-wide sync)
+    uint8_t* mystage = sdQ + (warp - 2) * 4096;
+    auto drain_dq = [&](int t) {
       const int h = kvh * G + t / nq, i = kt + t % nq;
       mbar_wait(&dq_full[t & 1], (t >> 1) & 1);
       tc_fence_after();
@@ -543,38 +561,29 @@ __global__ void __launch_bounds__(320, 1)
       tmem_wait_ld();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&dq_empty[t & 1]);
-      if (ct == 0) bulk_wait_read<0>();  // the previous add-reduce has finished reading sdQ
-      named_sync(2, 256);
-      uint8_t* box = sdQ + half * kTile;
+      if (lane == 0) {
+        mbar_arrive(&dq_empty[t & 1]);
+        bulk_wait_read<0>();  // this warp's previous add-reduce has read its staging tile
+      }
+      __syncwarp();
 #pragma unroll
       for (int c = 0; c < 8; ++c)
-        *reinterpret_cast<float4*>(box + swz(r, c)) =
+        *reinterpret_cast<float4*>(mystage + swz(lane, c)) =
             make_float4(__uint_as_float(qv[4 * c]) * p.scale, __uint_as_float(qv[4 * c + 1]) * p.scale,
                         __uint_as_float(qv[4 * c + 2]) * p.scale, __uint_as_float(qv[4 * c + 3]) * p.scale);
       fence_proxy_async_smem();
-      named_sync(3, 256);
-      if (ct == 0) {
-        tma_reduce_add_2d(&tm_dq, sdQ, h * DH, b * p.T + i * BQ);
-        tma_reduce_add_2d(&tm_dq, sdQ + kTile, h * DH + 32, b * p.T + i * BQ);
+      __syncwarp();
+      if (lane == 0) {
+        tma_reduce_add_2d(&tm_dq, mystage, h * DH + half * 32, b * p.T + i * BQ + q4 * 32);
         bulk_commit();
       }
     };
-    // lse / D of step t live in buffer t&1; step t+1's are loaded during step t
-    auto load_stats = [&](int t) {
-      const int h = kvh * G + t / nq, i = kt + t % nq;
-      const size_t off = ((size_t)b * p.Hq + h) * p.T + (size_t)i * BQ + (ct & 127);
-      if (ct < 128) sLse[(t & 1) * BQ + ct] = p.lse[off] * kLog2e;
-      else sD[(t & 1) * BQ + ct - 128] = p.dsum[off];
-    };
-    if (nsteps > 0) load_stats(0);
     for (int t = 0; t < nsteps; ++t) {
       const int i = kt + t % nq;
       const bool diag = (i == kt);
-      float* lse2 = sLse + (t & 1) * BQ;
-      float* dd = sD + (t & 1) * BQ;
-      named_sync(1, 256);  // stats of step t visible; everyone is done with step t-1's buffer
-      if (t + 1 < nsteps) load_stats(t + 1);
+      mbar_wait(&st_ld_full[t & 1], (t >> 1) & 1);
+      const float* lse2 = sLse + (t & 1) * BQ;  // natural log; p_ds folds in log2(e)
+      const float* dd = sD + (t & 1) * BQ;
       mbar_wait(st_full, t & 1);
       tc_fence_after();
       // 168 registers per thread (3 warps on some SMSPs): two 32-column passes
@@ -610,10 +619,15 @@ __global__ void __launch_bounds__(320, 1)
       }
       fence_proxy_async_smem();
       __syncwarp();
-      if (lane == 0) mbar_arrive(pds_full);
+      if (lane == 0) {
+        mbar_arrive(pds_full);
+        mbar_arrive(&st_ld_empty[t & 1]);
+      }
       if (t > 0) drain_dq(t - 1);
     }
     if (nsteps > 0) drain_dq(nsteps - 1);
+    if (lane == 0) bulk_wait<0>();  // this warp's add-reduces are complete before smem is reused / freed
+    __syncwarp();
     // dK (scaled) and dV -> bf16 -> smem (Q stages are free) -> TMA store into dqkv
     mbar_wait(done, 0);
     tc_fence_after();
@@ -704,7 +718,7 @@ extern "C" int b2s_attn_bwd(const void* d_qkv, const void* d_o, const void* d_do
   if (rc) return rc;
   rc = encode_tma_2d(&tdo, d_do, 2, (uint64_t)Hq * dh, (uint64_t)M, (uint64_t)Hq * dh * 2, 64, 128, 128);
   if (rc) return rc;
-  rc = encode_tma_2d(&tdq, dq_acc, 4, (uint64_t)Hq * dh, (uint64_t)M, (uint64_t)Hq * dh * 4, 32, 128, 128);
+  rc = encode_tma_2d(&tdq, dq_acc, 4, (uint64_t)Hq * dh, (uint64_t)M, (uint64_t)Hq * dh * 4, 32, 32, 128);
   if (rc) return rc;
   rc = encode_tma_2d(&tdkv, d_dqkv, 2, (uint64_t)ldq, (uint64_t)M, (uint64_t)ldq * 2, 64, 128, 128);
   if (rc) return rc;

@@ -335,19 +335,34 @@ __global__ void embed_bwd_pos_kernel(const float* __restrict__ dx, float* __rest
 __global__ void rope_kernel(__nv_bfloat16* __restrict__ qkv, int64_t M, int T, int64_t ld, int nheads,
                             int dh, const float* __restrict__ cos_t, const float* __restrict__ sin_t,
                             int inverse) {
+  // one thread = 8 consecutive rotation pairs of one head of one row (16-byte vectors)
   const int half = dh / 2;
-  const int64_t per_row = (int64_t)nheads * half;
+  const int vph = half / 8;  // vectors per head
+  const int64_t per_row = (int64_t)nheads * vph;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < M * per_row;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t m = i / per_row;
     const int r = (int)(i - m * per_row);
-    const int h = r / half, j = r - h * half;
+    const int h = r / vph, j0 = (r - h * vph) * 8;
     const int t = (int)(m % T);
-    const float c = cos_t[t * half + j], s = inverse ? -sin_t[t * half + j] : sin_t[t * half + j];
-    __nv_bfloat16* p = qkv + m * ld + (int64_t)h * dh;
-    const float a = bf2f(p[j]), b = bf2f(p[j + half]);
-    p[j] = f2bf(a * c - b * s);
-    p[j + half] = f2bf(b * c + a * s);
+    __nv_bfloat16* p = qkv + m * ld + (int64_t)h * dh + j0;
+    float a[8], b[8], c[8], sn[8];
+    unpack8(*reinterpret_cast<const bf16x8*>(p), a);
+    unpack8(*reinterpret_cast<const bf16x8*>(p + half), b);
+    const float4* cp = reinterpret_cast<const float4*>(cos_t + (int64_t)t * half + j0);
+    const float4* sp = reinterpret_cast<const float4*>(sin_t + (int64_t)t * half + j0);
+    float4 c0 = cp[0], c1 = cp[1], s0 = sp[0], s1 = sp[1];
+    c[0] = c0.x; c[1] = c0.y; c[2] = c0.z; c[3] = c0.w; c[4] = c1.x; c[5] = c1.y; c[6] = c1.z; c[7] = c1.w;
+    sn[0] = s0.x; sn[1] = s0.y; sn[2] = s0.z; sn[3] = s0.w; sn[4] = s1.x; sn[5] = s1.y; sn[6] = s1.z; sn[7] = s1.w;
+    float oa[8], ob[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const float s_ = inverse ? -sn[k] : sn[k];
+      oa[k] = a[k] * c[k] - b[k] * s_;
+      ob[k] = b[k] * c[k] + a[k] * s_;
+    }
+    *reinterpret_cast<bf16x8*>(p) = pack8(oa);
+    *reinterpret_cast<bf16x8*>(p + half) = pack8(ob);
   }
 }
 
@@ -670,7 +685,9 @@ int b2s_embedding_bwd(const int64_t* d_tok, const float* d_dx, float* d_dwte, fl
 
 int b2s_rope(void* d_qkv, int64_t M, int T, int64_t ld, int nheads, int dh, const float* d_cos,
              const float* d_sin, int inverse, b2s_stream_t stream) {
-  ew::rope_kernel<<<ew::flat_grid(M * nheads * dh / 2, 1), 256, 0, (cudaStream_t)stream>>>(
+  B2S_REQUIRE(dh % 16 == 0 && ld % 8 == 0 && ((uintptr_t)d_qkv % 16) == 0, B2S_EUNSUPPORTED,
+              "rope: head dim must be a multiple of 16 and rows 16-byte aligned");
+  ew::rope_kernel<<<ew::flat_grid(M * nheads * dh / 16, 1), 256, 0, (cudaStream_t)stream>>>(
       (__nv_bfloat16*)d_qkv, M, T, ld, nheads, dh, d_cos, d_sin, inverse);
   return check_launch("rope");
 }

@@ -9,7 +9,8 @@ import sys
 
 rep = sys.argv[1]
 ntop = int(sys.argv[2]) if len(sys.argv) > 2 else 25
-raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+kfilter = ["-k", "regex:" + sys.argv[3]] if len(sys.argv) > 3 else []
+raw = subprocess.run(["ncu", "-i", rep, *kfilter, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(raw[raw.index('"ID"'):])))
 h, units, vals = rows[0], rows[1], rows[2]
 want = ["Kernel Name", "gpu__time_duration.sum", "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
@@ -23,14 +24,14 @@ for k in want:
     for i, x in enumerate(h):
         if x == k:
             print(f"{k:75s} {vals[i]:>20s} {units[i]}")
-src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"], capture_output=True,
-                     text=True).stdout
+src = subprocess.run(["ncu", "-i", rep, *kfilter, "--page", "source", "--csv", "--print-source", "sass"],
+                     capture_output=True, text=True).stdout
 lines = src.splitlines()
 start = next(i for i, l in enumerate(lines) if l.startswith('"Address"'))
 srows = list(csv.reader(io.StringIO("\n".join(lines[start:]))))
 hh = srows[0]
 iS, iSrc = hh.index("Warp Stall Sampling (All Samples)"), hh.index("Source")
-data = srows[1:]
+data = [r for r in srows[1:] if len(r) > iS and r[iS] and r[iS][0].isdigit()]
 tot = sum(float(r[iS] or 0) for r in data) or 1
 print(f"--- top {ntop} SASS lines by stall samples")
 for r in sorted(data, key=lambda r: -float(r[iS] or 0))[:ntop]:
