@@ -13,7 +13,7 @@ import re
 from ctypes import POINTER, c_char_p, c_int, c_int32, c_int64, c_uint64, c_void_p, c_float
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libb2s.so")
+LIB_PATH = os.environ.get("B2S_LIB") or os.path.join(_HERE, "libb2s.so")  # B2S_LIB: experiment builds
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "b2s.h")
 
 B2S_OK = 0

@@ -181,7 +181,7 @@ __global__ void __launch_bounds__(320, 1)
     }
     __syncwarp();
   } else if (warp == 1) {
-    if (lane == 0) {
+    {  // whole warp, converged; one lane elected per tcgen05 instruction
       constexpr uint32_t idS = make_idesc_bf16(BQ, BKV, false, false);
       constexpr uint32_t idO = make_idesc_bf16(BQ, DH, false, true);
       const uint32_t aQ = smem_u32(sQ), aK = smem_u32(sK), aV = smem_u32(sV), aP = smem_u32(sP);
@@ -192,9 +192,9 @@ __global__ void __launch_bounds__(320, 1)
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < DH / 16; ++kk)
-          mma_bf16_ss(tbase + t * BKV, make_sdesc(aQ + t * kTile + kk * 32, 16, 1024),
+          mma_bf16_ss_w(tbase + t * BKV, make_sdesc(aQ + t * kTile + kk * 32, 16, 1024),
                       make_sdesc(aK + s * kTile + kk * 32, 16, 1024), idS, kk > 0);
-        mma_commit(&s_full[t]);
+        mma_commit_w(&s_full[t]);
       };
       auto issue_PV = [&](int t, int j, bool last) {
         const int s = j % kStages;
@@ -204,11 +204,11 @@ __global__ void __launch_bounds__(320, 1)
         const uint32_t pbase = aP + (2 * t + (j & 1)) * 2 * kTile;
 #pragma unroll
         for (int kk = 0; kk < BKV / 16; ++kk)
-          mma_bf16_ss(tbase + 256 + t * DH, make_sdesc(pbase + (kk >> 2) * kTile + (kk & 3) * 32, 16, 1024),
+          mma_bf16_ss_w(tbase + 256 + t * DH, make_sdesc(pbase + (kk >> 2) * kTile + (kk & 3) * 32, 16, 1024),
                       make_sdesc(aV + s * kTile + kk * 2048, kTile, 1024), idO, (j > 0 || kk > 0) ? 1u : 0u);
-        mma_commit(&p_empty[2 * t + (j & 1)]);
-        mma_commit(&pv_done[t]);
-        if (last) mma_commit(&o_done[t]);
+        mma_commit_w(&p_empty[2 * t + (j & 1)]);
+        mma_commit_w(&pv_done[t]);
+        if (last) mma_commit_w(&o_done[t]);
       };
       mbar_wait(q_full, 0);
       issue_S(0, 0);
@@ -220,7 +220,7 @@ __global__ void __launch_bounds__(320, 1)
         if (j + 1 < nB) issue_S(1, j + 1);
         if (j < nA) issue_PV(0, j, j + 1 == nA);
         if (j < nB) issue_PV(1, j, j + 1 == nB);
-        mma_commit(&kv_empty[j % kStages]);  // K_j / V_j no longer read once these retire
+        mma_commit_w(&kv_empty[j % kStages]);  // K_j / V_j no longer read once these retire
       }
     }
     __syncwarp();
@@ -404,7 +404,11 @@ __device__ __forceinline__ void p_ds(uint32_t* sv, uint32_t* dv, int q0, int r, 
 #pragma unroll
   for (int e = 0; e < 32; ++e) {
     const int q = q0 + e;
+#ifdef B2S_EXP_NOEXP
+    float pv = __uint_as_float(sv[e]);
+#else
     float pv = ex2(fmaf(__uint_as_float(sv[e]), sl2, -lse2[q] * kLog2e));
+#endif
     if (DIAG && q < r) pv = 0.f;  // query index below key index: masked
     sv[e] = __float_as_uint(pv);
     dv[e] = __float_as_uint(pv * (__uint_as_float(dv[e]) - dd[q]));
@@ -494,7 +498,7 @@ __global__ void __launch_bounds__(320, 1)
     }
     __syncwarp();
   } else if (warp == 1) {
-    if (lane == 0) {
+    {  // whole warp, converged; one lane elected per tcgen05 instruction
       constexpr uint32_t idSS = make_idesc_bf16(128, 128, false, false);  // S^T, dP^T
       constexpr uint32_t idKM = make_idesc_bf16(128, DH, false, true);    // dV, dK
       constexpr uint32_t idMM = make_idesc_bf16(128, DH, true, true);     // dQ
@@ -508,11 +512,11 @@ __global__ void __launch_bounds__(320, 1)
         const uint32_t q_ = aQ + s * kTile, do_ = adO + s * kTile;
 #pragma unroll
         for (int kk = 0; kk < DH / 16; ++kk)
-          mma_bf16_ss(tS, make_sdesc(aK + kk * 32, 16, 1024), make_sdesc(q_ + kk * 32, 16, 1024), idSS, kk > 0);
+          mma_bf16_ss_w(tS, make_sdesc(aK + kk * 32, 16, 1024), make_sdesc(q_ + kk * 32, 16, 1024), idSS, kk > 0);
 #pragma unroll
         for (int kk = 0; kk < DH / 16; ++kk)
-          mma_bf16_ss(tdP, make_sdesc(aV + kk * 32, 16, 1024), make_sdesc(do_ + kk * 32, 16, 1024), idSS, kk > 0);
-        mma_commit(st_full);
+          mma_bf16_ss_w(tdP, make_sdesc(aV + kk * 32, 16, 1024), make_sdesc(do_ + kk * 32, 16, 1024), idSS, kk > 0);
+        mma_commit_w(st_full);
       };
       mbar_wait(kv_full, 0);
       issue_S(0);
@@ -526,20 +530,20 @@ __global__ void __launch_bounds__(320, 1)
         for (int kk = 0; kk < BQ / 16; ++kk) {
           const uint64_t a_p = make_sdesc(aP + (kk >> 2) * kTile + (kk & 3) * 32, 16, 1024);
           const uint64_t a_ds = make_sdesc(adS + (kk >> 2) * kTile + (kk & 3) * 32, 16, 1024);
-          mma_bf16_ss(tdV, a_p, make_sdesc(do_ + kk * 2048, kTile, 1024), idKM, (t > 0 || kk > 0));
-          mma_bf16_ss(tdK, a_ds, make_sdesc(q_ + kk * 2048, kTile, 1024), idKM, (t > 0 || kk > 0));
+          mma_bf16_ss_w(tdV, a_p, make_sdesc(do_ + kk * 2048, kTile, 1024), idKM, (t > 0 || kk > 0));
+          mma_bf16_ss_w(tdK, a_ds, make_sdesc(q_ + kk * 2048, kTile, 1024), idKM, (t > 0 || kk > 0));
         }
         mbar_wait(&dq_empty[s], ((t >> 1) & 1) ^ 1);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < BKV / 16; ++kk)
-          mma_bf16_ss(tdQ + s * DH, make_sdesc(adS + kk * 2048, kTile, 1024), make_sdesc(aK + kk * 2048, kTile, 1024),
+          mma_bf16_ss_w(tdQ + s * DH, make_sdesc(adS + kk * 2048, kTile, 1024), make_sdesc(aK + kk * 2048, kTile, 1024),
                       idMM, kk > 0);
-        mma_commit(&qd_empty[s]);
-        mma_commit(pds_empty);
-        mma_commit(&dq_full[s]);
+        mma_commit_w(&qd_empty[s]);
+        mma_commit_w(pds_empty);
+        mma_commit_w(&dq_full[s]);
       }
-      mma_commit(done);
+      mma_commit_w(done);
     }
     __syncwarp();
   } else {
@@ -623,9 +627,17 @@ __global__ void __launch_bounds__(320, 1)
         mbar_arrive(pds_full);
         mbar_arrive(&st_ld_empty[t & 1]);
       }
+#ifndef B2S_EXP_NODQ
       if (t > 0) drain_dq(t - 1);
+#else
+      if (t > 0) { mbar_wait(&dq_full[(t - 1) & 1], ((t - 1) >> 1) & 1); tc_fence_after(); __syncwarp(); if (lane == 0) mbar_arrive(&dq_empty[(t - 1) & 1]); }
+#endif
     }
+#ifndef B2S_EXP_NODQ
     if (nsteps > 0) drain_dq(nsteps - 1);
+#else
+    if (nsteps > 0) { mbar_wait(&dq_full[(nsteps - 1) & 1], ((nsteps - 1) >> 1) & 1); if (lane == 0) mbar_arrive(&dq_empty[(nsteps - 1) & 1]); }
+#endif
     if (lane == 0) bulk_wait<0>();  // this warp's add-reduces are complete before smem is reused / freed
     __syncwarp();
     // dK (scaled) and dV -> bf16 -> smem (Q stages are free) -> TMA store into dqkv
