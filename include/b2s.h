@@ -185,6 +185,48 @@ int b2s_attn_bwd(const void* d_qkv, const void* d_o, const void* d_do, const flo
                  float* d_work, int B, int T, int Hq, int Hkv, int dh, b2s_stream_t stream);
 int64_t b2s_attn_bwd_work_floats(int B, int T, int Hq, int dh);
 
+/* ------------------------------------------------------------------ */
+/* fp32 mode (north star: per-step losses/gradients within 1e-4 of the  */
+/* CPU fp32 reference). Same contracts as the bf16 entry points above   */
+/* with every activation / weight operand fp32; GEMM and attention run  */
+/* true-fp32 FFMA on the CUDA cores (not TF32).   */
+/* ------------------------------------------------------------------ */
+/* C[M,N] (fp32) = epi(sum_k A(m,k) B(n,k)); layouts, bias, act, aux and
+ * accumulate as b2s_gemm (aux fp32). Any M, N, K >= 0. */
+int b2s_gemm_f32(const float* d_A, int a_mn_major, int64_t lda, const float* d_B, int b_mn_major, int64_t ldb,
+                 float* d_C, int64_t ldc, int M, int N, int K, int accumulate, const float* d_bias, int act,
+                 float* d_aux, int64_t ld_aux, b2s_stream_t stream);
+int b2s_layernorm_fwd_f32(const float* d_x, const float* d_g, const float* d_b, float* d_y, float* d_mean,
+                          float* d_rstd, float* d_x_copy, int64_t M, int D, float eps, b2s_stream_t stream);
+int b2s_rmsnorm_fwd_f32(const float* d_x, const float* d_g, float* d_y, float* d_rstd, float* d_x_copy,
+                        int64_t M, int D, float eps, b2s_stream_t stream);
+/* d_dx_copy: optional second copy of the updated dx (usually null in fp32 mode). */
+int b2s_layernorm_bwd_f32(const float* d_x, const float* d_dy, const float* d_g, const float* d_mean,
+                          const float* d_rstd, float* d_dx, float* d_dx_copy, float* d_dg, float* d_db,
+                          float* d_dxsum, float* d_work, int64_t M, int D, b2s_stream_t stream);
+int b2s_rmsnorm_bwd_f32(const float* d_x, const float* d_dy, const float* d_g, const float* d_rstd, float* d_dx,
+                        float* d_dx_copy, float* d_dg, float* d_dxsum, float* d_work, int64_t M, int D,
+                        b2s_stream_t stream);
+int b2s_embedding_fwd_f32(const int64_t* d_tok, const float* d_wte, const float* d_wpe, float* d_x, int64_t M,
+                          int T, int D, b2s_stream_t stream);
+int b2s_rope_f32(float* d_qkv, int64_t M, int T, int64_t ld, int nheads, int dh, const float* d_cos,
+                 const float* d_sin, int inverse, b2s_stream_t stream);
+int b2s_swiglu_fwd_f32(const float* d_gu, float* d_h, int64_t M, int F, b2s_stream_t stream);
+int b2s_swiglu_bwd_f32(const float* d_gu, const float* d_dh, float* d_dgu, int64_t M, int F, b2s_stream_t stream);
+int b2s_cross_entropy_f32(float* d_logits, int64_t ld, int V, const int64_t* d_target, float* d_loss_rows,
+                          float grad_scale, int64_t M, int write_grad, b2s_stream_t stream);
+/* d_p_copy: optional fp32 copy of the updated p (null when p is itself the
+ * all-gather source / compute buffer). */
+int b2s_adamw_f32(float* d_p, float* d_m, float* d_v, const float* d_g, float* d_p_copy, const uint8_t* d_wd_mask,
+                  int64_t n, const float* d_gn2, float max_norm, float lr, float beta1, float beta2, float eps,
+                  float wd, int step, b2s_stream_t stream);
+/* Causal attention, fp32 [B*T, (Hq+2Hkv)*dh] fused projection, head dims
+ * 32 / 64 / 128, any T >= 1. d_work: b2s_attn_bwd_work_floats() floats. */
+int b2s_attn_fwd_f32(const float* d_qkv, float* d_o, float* d_lse, int B, int T, int Hq, int Hkv, int dh,
+                     b2s_stream_t stream);
+int b2s_attn_bwd_f32(const float* d_qkv, const float* d_o, const float* d_do, const float* d_lse, float* d_dqkv,
+                     float* d_work, int B, int T, int Hq, int Hkv, int dh, b2s_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

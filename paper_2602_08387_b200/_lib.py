@@ -67,6 +67,20 @@ _SIGS = {
     "b2s_scale_f32": "plfp",
     "b2s_attn_fwd": "pppiiiiip",
     "b2s_attn_bwd": "ppppppiiiiip",
+    # fp32 mode (same argument order as the bf16 entry points)
+    "b2s_gemm_f32": "pilpilpliiiipiplp",
+    "b2s_layernorm_fwd_f32": "ppppppplifp",
+    "b2s_rmsnorm_fwd_f32": "ppppplifp",
+    "b2s_layernorm_bwd_f32": "ppppppppppplip",
+    "b2s_rmsnorm_bwd_f32": "ppppppppplip",
+    "b2s_embedding_fwd_f32": "ppppliip",
+    "b2s_rope_f32": "pliliippip",
+    "b2s_swiglu_fwd_f32": "pplip",
+    "b2s_swiglu_bwd_f32": "ppplip",
+    "b2s_cross_entropy_f32": "plippflip",
+    "b2s_adamw_f32": "pppppplpffffffip",
+    "b2s_attn_fwd_f32": "pppiiiiip",
+    "b2s_attn_bwd_f32": "ppppppiiiiip",
 }
 # functions returning int64 sizes (not statuses): name -> argument signature
 _SIZE_FNS = {"b2s_launch_count": "", "b2s_norm_work_floats": "i", "b2s_colsum_work_floats": "i", "b2s_attn_bwd_work_floats": "iiii"}

@@ -25,6 +25,25 @@ __device__ __forceinline__ void st_bf4(__nv_bfloat16* p, const float* f) {
   u.y = pack_bf16x2(f[2], f[3]);
   *reinterpret_cast<uint2*>(p) = u;
 }
+// Activation-type generic 4- and 8-element vectors: T = __nv_bfloat16 (the
+// training precision) or float (fp32 mode, the 1e-4 parity configuration).
+__device__ __forceinline__ void ld_v4(const __nv_bfloat16* p, float* f) { ld_bf4(p, f); }
+__device__ __forceinline__ void ld_v4(const float* p, float* f) {
+  const float4 v = ld4(p);
+  f[0] = v.x; f[1] = v.y; f[2] = v.z; f[3] = v.w;
+}
+__device__ __forceinline__ void st_v4(__nv_bfloat16* p, const float* f) { st_bf4(p, f); }
+__device__ __forceinline__ void st_v4(float* p, const float* f) { st4(p, make_float4(f[0], f[1], f[2], f[3])); }
+__device__ __forceinline__ void ld_v8(const __nv_bfloat16* p, float* f) {
+  unpack8(*reinterpret_cast<const bf16x8*>(p), f);
+}
+__device__ __forceinline__ void ld_v8(const float* p, float* f) { ld_v4(p, f); ld_v4(p + 4, f + 4); }
+__device__ __forceinline__ void st_v8(__nv_bfloat16* p, const float* f) { *reinterpret_cast<bf16x8*>(p) = pack8(f); }
+__device__ __forceinline__ void st_v8(float* p, const float* f) { st_v4(p, f); st_v4(p + 4, f + 4); }
+__device__ __forceinline__ float to_f(__nv_bfloat16 v) { return bf2f(v); }
+__device__ __forceinline__ float to_f(float v) { return v; }
+__device__ __forceinline__ void from_f(__nv_bfloat16& d, float v) { d = f2bf(v); }
+__device__ __forceinline__ void from_f(float& d, float v) { d = v; }
 
 
 // ------------------------------------------------------------------ norms
@@ -52,10 +71,10 @@ __device__ __forceinline__ float row_sum(float v, float* scratch, int& toggle) {
   }
 }
 
-template <int D, int TPR, bool RMS>
+template <int D, int TPR, bool RMS, typename T = __nv_bfloat16>
 __global__ void __launch_bounds__(kRowThreads) norm_fwd_kernel(
-    const float* __restrict__ x, const __nv_bfloat16* __restrict__ g, const __nv_bfloat16* __restrict__ b,
-    __nv_bfloat16* __restrict__ y, float* __restrict__ mean_out, float* __restrict__ rstd_out,
+    const float* __restrict__ x, const T* __restrict__ g, const T* __restrict__ b,
+    T* __restrict__ y, float* __restrict__ mean_out, float* __restrict__ rstd_out,
     float* __restrict__ x_copy, int64_t M, float eps) {
   constexpr int V = D / (TPR * 4);  // float4 vectors per thread
   static_assert(V * TPR * 4 == D, "hidden size must tile the row threads");
@@ -67,8 +86,8 @@ __global__ void __launch_bounds__(kRowThreads) norm_fwd_kernel(
   float gv[V][4], bv[V][4];
 #pragma unroll
   for (int j = 0; j < V; ++j) {
-    ld_bf4(g + t * 4 + j * TPR * 4, gv[j]);
-    if (!RMS) ld_bf4(b + t * 4 + j * TPR * 4, bv[j]);
+    ld_v4(g + t * 4 + j * TPR * 4, gv[j]);
+    if (!RMS) ld_v4(b + t * 4 + j * TPR * 4, bv[j]);
   }
   for (int64_t row = r0; row < M; row += nr) {
     const float* xr = x + row * D;
@@ -97,7 +116,7 @@ __global__ void __launch_bounds__(kRowThreads) norm_fwd_kernel(
                     (xv[j].w - mean) * rstd};
 #pragma unroll
       for (int u = 0; u < 4; ++u) o[u] = RMS ? o[u] * gv[j][u] : o[u] * gv[j][u] + bv[j][u];
-      st_bf4(y + row * D + t * 4 + j * TPR * 4, o);
+      st_v4(y + row * D + t * 4 + j * TPR * 4, o);
     }
     if (t == 0) {
       if (!RMS) mean_out[row] = mean;
@@ -109,11 +128,11 @@ __global__ void __launch_bounds__(kRowThreads) norm_fwd_kernel(
 // Backward. dy bf16 [M,D]; dx fp32 accumulated in place (dx += ...), with a
 // bf16 copy of the updated dx (the next GEMM operand) when dx_bf16 != null.
 // dg/db partial sums per block into part[blockIdx][2][D] (db only for LN).
-template <int D, int TPR, bool RMS>
+template <int D, int TPR, bool RMS, typename T = __nv_bfloat16>
 __global__ void __launch_bounds__(kRowThreads) norm_bwd_kernel(
-    const float* __restrict__ x, const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ g,
+    const float* __restrict__ x, const T* __restrict__ dy, const T* __restrict__ g,
     const float* __restrict__ mean_in, const float* __restrict__ rstd_in, float* __restrict__ dx,
-    __nv_bfloat16* __restrict__ dx_bf16, float* __restrict__ part, int64_t M, int want_dxsum) {
+    T* __restrict__ dx_bf16, float* __restrict__ part, int64_t M, int want_dxsum) {
   constexpr int V = D / (TPR * 4);
   constexpr int kGroups = kRowThreads / TPR;  // rows processed concurrently by the block
   constexpr int kChunk = 1024;                // columns reduced per smem pass
@@ -126,7 +145,7 @@ __global__ void __launch_bounds__(kRowThreads) norm_bwd_kernel(
   float gv[V][4], dg[V][4], db[V][4], ds[V][4];
 #pragma unroll
   for (int j = 0; j < V; ++j) {
-    ld_bf4(g + t * 4 + j * TPR * 4, gv[j]);
+    ld_v4(g + t * 4 + j * TPR * 4, gv[j]);
 #pragma unroll
     for (int u = 0; u < 4; ++u) { dg[j][u] = 0.f; db[j][u] = 0.f; ds[j][u] = 0.f; }
   }
@@ -142,7 +161,7 @@ __global__ void __launch_bounds__(kRowThreads) norm_bwd_kernel(
     for (int j = 0; j < V; ++j) {
       const float4 xv = ld4(x + row * D + t * 4 + j * TPR * 4);
       float d4[4];
-      ld_bf4(dy + row * D + t * 4 + j * TPR * 4, d4);
+      ld_v4(dy + row * D + t * 4 + j * TPR * 4, d4);
       const float xs[4] = {xv.x, xv.y, xv.z, xv.w};
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
@@ -160,7 +179,7 @@ __global__ void __launch_bounds__(kRowThreads) norm_bwd_kernel(
       const float4 xv = ld4(x + off);
       float4 o = ld4(dx + off);
       float d4[4];
-      ld_bf4(dy + off, d4);
+      ld_v4(dy + off, d4);
       const float xs[4] = {xv.x, xv.y, xv.z, xv.w};
       float os[4] = {o.x, o.y, o.z, o.w};
 #pragma unroll
@@ -172,7 +191,7 @@ __global__ void __launch_bounds__(kRowThreads) norm_bwd_kernel(
         ds[j][u] += os[u];
       }
       st4(dx + off, make_float4(os[0], os[1], os[2], os[3]));
-      if (dx_bf16) st_bf4(dx_bf16 + off, os);
+      if (dx_bf16) st_v4(dx_bf16 + off, os);
     }
   }
   // block-level reduction of dg, db, sum(dx) over the row groups -> part[block][pass]
@@ -285,8 +304,9 @@ __global__ void __launch_bounds__(256) colsum_final_kernel(const float* __restri
 
 // ------------------------------------------------------------------ embedding
 // x[m, :] = wte[tok[m], :] (+ wpe[m % T, :]), fp32 out.
-__global__ void embed_fwd_kernel(const int64_t* __restrict__ tok, const __nv_bfloat16* __restrict__ wte,
-                                 const __nv_bfloat16* __restrict__ wpe, float* __restrict__ x, int64_t M,
+template <typename E>
+__global__ void embed_fwd_kernel(const int64_t* __restrict__ tok, const E* __restrict__ wte,
+                                 const E* __restrict__ wpe, float* __restrict__ x, int64_t M,
                                  int T, int D) {
   const int vec = D / 4;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < M * vec;
@@ -294,10 +314,10 @@ __global__ void embed_fwd_kernel(const int64_t* __restrict__ tok, const __nv_bfl
     const int64_t m = i / vec;
     const int c = (int)(i - m * vec) * 4;
     float f[4];
-    ld_bf4(wte + tok[m] * D + c, f);
+    ld_v4(wte + tok[m] * D + c, f);
     if (wpe) {
       float p[4];
-      ld_bf4(wpe + (int64_t)(m % T) * D + c, p);
+      ld_v4(wpe + (int64_t)(m % T) * D + c, p);
       f[0] += p[0]; f[1] += p[1]; f[2] += p[2]; f[3] += p[3];
     }
     st4(x + m * D + c, make_float4(f[0], f[1], f[2], f[3]));
@@ -332,7 +352,8 @@ __global__ void embed_bwd_pos_kernel(const float* __restrict__ dx, float* __rest
 // In place on the q and k heads of a [M, ld] bf16 buffer, rotate-half pairing
 // (i, i + dh/2) as in Llama: (a, b) -> (a cos - b sin, b cos + a sin).
 // inverse=1 applies the transpose rotation (backward).
-__global__ void rope_kernel(__nv_bfloat16* __restrict__ qkv, int64_t M, int T, int64_t ld, int nheads,
+template <typename E>
+__global__ void rope_kernel(E* __restrict__ qkv, int64_t M, int T, int64_t ld, int nheads,
                             int dh, const float* __restrict__ cos_t, const float* __restrict__ sin_t,
                             int inverse) {
   // one thread = 8 consecutive rotation pairs of one head of one row (16-byte vectors)
@@ -345,10 +366,10 @@ __global__ void rope_kernel(__nv_bfloat16* __restrict__ qkv, int64_t M, int T, i
     const int r = (int)(i - m * per_row);
     const int h = r / vph, j0 = (r - h * vph) * 8;
     const int t = (int)(m % T);
-    __nv_bfloat16* p = qkv + m * ld + (int64_t)h * dh + j0;
+    E* p = qkv + m * ld + (int64_t)h * dh + j0;
     float a[8], b[8], c[8], sn[8];
-    unpack8(*reinterpret_cast<const bf16x8*>(p), a);
-    unpack8(*reinterpret_cast<const bf16x8*>(p + half), b);
+    ld_v8(p, a);
+    ld_v8(p + half, b);
     const float4* cp = reinterpret_cast<const float4*>(cos_t + (int64_t)t * half + j0);
     const float4* sp = reinterpret_cast<const float4*>(sin_t + (int64_t)t * half + j0);
     float4 c0 = cp[0], c1 = cp[1], s0 = sp[0], s1 = sp[1];
@@ -361,14 +382,15 @@ __global__ void rope_kernel(__nv_bfloat16* __restrict__ qkv, int64_t M, int T, i
       oa[k] = a[k] * c[k] - b[k] * s_;
       ob[k] = b[k] * c[k] + a[k] * s_;
     }
-    *reinterpret_cast<bf16x8*>(p) = pack8(oa);
-    *reinterpret_cast<bf16x8*>(p + half) = pack8(ob);
+    st_v8(p, oa);
+    st_v8(p + half, ob);
   }
 }
 
 // ------------------------------------------------------------------ SwiGLU
 // gu [M, 2F] (gate | up), h [M, F] = silu(gate) * up
-__global__ void swiglu_fwd_kernel(const __nv_bfloat16* __restrict__ gu, __nv_bfloat16* __restrict__ h,
+template <typename T>
+__global__ void swiglu_fwd_kernel(const T* __restrict__ gu, T* __restrict__ h,
                                   int64_t M, int F) {
   const int vec = F / 8;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < M * vec;
@@ -376,34 +398,35 @@ __global__ void swiglu_fwd_kernel(const __nv_bfloat16* __restrict__ gu, __nv_bfl
     const int64_t m = i / vec;
     const int c = (int)(i - m * vec) * 8;
     float g[8], u[8], o[8];
-    unpack8(*reinterpret_cast<const bf16x8*>(gu + m * 2 * F + c), g);
-    unpack8(*reinterpret_cast<const bf16x8*>(gu + m * 2 * F + F + c), u);
+    ld_v8(gu + m * 2 * F + c, g);
+    ld_v8(gu + m * 2 * F + F + c, u);
 #pragma unroll
-    for (int t = 0; t < 8; ++t) o[t] = g[t] / (1.f + __expf(-g[t])) * u[t];
-    *reinterpret_cast<bf16x8*>(h + m * F + c) = pack8(o);
+    for (int t = 0; t < 8; ++t) o[t] = g[t] / (1.f + expf(-g[t])) * u[t];
+    st_v8(h + m * F + c, o);
   }
 }
 // dgu = [dgate | dup] from dh and the saved gu
-__global__ void swiglu_bwd_kernel(const __nv_bfloat16* __restrict__ gu, const __nv_bfloat16* __restrict__ dh,
-                                  __nv_bfloat16* __restrict__ dgu, int64_t M, int F) {
+template <typename T>
+__global__ void swiglu_bwd_kernel(const T* __restrict__ gu, const T* __restrict__ dh,
+                                  T* __restrict__ dgu, int64_t M, int F) {
   const int vec = F / 8;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < M * vec;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t m = i / vec;
     const int c = (int)(i - m * vec) * 8;
     float g[8], u[8], d[8], dg[8], du[8];
-    unpack8(*reinterpret_cast<const bf16x8*>(gu + m * 2 * F + c), g);
-    unpack8(*reinterpret_cast<const bf16x8*>(gu + m * 2 * F + F + c), u);
-    unpack8(*reinterpret_cast<const bf16x8*>(dh + m * F + c), d);
+    ld_v8(gu + m * 2 * F + c, g);
+    ld_v8(gu + m * 2 * F + F + c, u);
+    ld_v8(dh + m * F + c, d);
 #pragma unroll
     for (int t = 0; t < 8; ++t) {
-      const float sg = 1.f / (1.f + __expf(-g[t]));
+      const float sg = 1.f / (1.f + expf(-g[t]));
       const float silu = g[t] * sg;
       du[t] = d[t] * silu;
       dg[t] = d[t] * u[t] * sg * (1.f + g[t] * (1.f - sg));
     }
-    *reinterpret_cast<bf16x8*>(dgu + m * 2 * F + c) = pack8(dg);
-    *reinterpret_cast<bf16x8*>(dgu + m * 2 * F + F + c) = pack8(du);
+    st_v8(dgu + m * 2 * F + c, dg);
+    st_v8(dgu + m * 2 * F + F + c, du);
   }
 }
 
@@ -411,18 +434,19 @@ __global__ void swiglu_bwd_kernel(const __nv_bfloat16* __restrict__ gu, const __
 // One block per row of bf16 logits [M, ld] (first V columns valid). Writes
 // loss[m] = logsumexp - logit[target] (fp32) and, in place over the logits,
 // dlogits = (softmax - onehot) * gscale (columns >= V zeroed).
-__global__ void __launch_bounds__(512) xent_kernel(__nv_bfloat16* __restrict__ logits, int64_t ld, int V,
+template <typename T>
+__global__ void __launch_bounds__(512) xent_kernel(T* __restrict__ logits, int64_t ld, int V,
                                                    const int64_t* __restrict__ target, float* __restrict__ loss,
                                                    float gscale, int64_t M, int write_grad) {
   __shared__ float scratch[32];
   const int64_t m = blockIdx.x;
-  __nv_bfloat16* row = logits + m * ld;
+  T* row = logits + m * ld;
   const int nvec = V / 8;  // full 8-wide vectors
   // one pass: per-thread online (max, sum of exp), then a block-wide merge
   float mx = -INFINITY, se = 0.f;
   for (int i = threadIdx.x; i < nvec; i += blockDim.x) {
     float f[8];
-    unpack8(*reinterpret_cast<const bf16x8*>(row + i * 8), f);
+    ld_v8(row + i * 8, f);
     float lm = f[0];
 #pragma unroll
     for (int t = 1; t < 8; ++t) lm = fmaxf(lm, f[t]);
@@ -434,7 +458,7 @@ __global__ void __launch_bounds__(512) xent_kernel(__nv_bfloat16* __restrict__ l
     mx = mn;
   }
   for (int c = nvec * 8 + threadIdx.x; c < V; c += blockDim.x) {
-    const float f = bf2f(row[c]);
+    const float f = to_f(row[c]);
     const float mn = fmaxf(mx, f);
     se = se * __expf(mx - mn) + __expf(f - mn);
     mx = mn;
@@ -445,25 +469,25 @@ __global__ void __launch_bounds__(512) xent_kernel(__nv_bfloat16* __restrict__ l
   se = block_sum(se, scratch);
   const float lse = mx + __logf(se);
   const int64_t tgt = target[m];
-  const float xt = bf2f(row[tgt]);
+  const float xt = to_f(row[tgt]);
   __syncthreads();
   if (threadIdx.x == 0) loss[m] = lse - xt;
   if (!write_grad) return;
   const float inv = 1.f / se;
   for (int i = threadIdx.x; i < nvec; i += blockDim.x) {
     float f[8];
-    unpack8(*reinterpret_cast<const bf16x8*>(row + i * 8), f);
+    ld_v8(row + i * 8, f);
 #pragma unroll
     for (int t = 0; t < 8; ++t) {
       const int c = i * 8 + t;
       f[t] = (__expf(f[t] - mx) * inv - (c == tgt ? 1.f : 0.f)) * gscale;
     }
-    *reinterpret_cast<bf16x8*>(row + i * 8) = pack8(f);
+    st_v8(row + i * 8, f);
   }
   for (int c = nvec * 8 + threadIdx.x; c < ld; c += blockDim.x) {
     float g = 0.f;
-    if (c < V) g = (__expf(bf2f(row[c]) - mx) * inv - (c == tgt ? 1.f : 0.f)) * gscale;
-    row[c] = f2bf(g);
+    if (c < V) g = (__expf(to_f(row[c]) - mx) * inv - (c == tgt ? 1.f : 0.f)) * gscale;
+    from_f(row[c], g);
   }
 }
 
@@ -499,9 +523,10 @@ __global__ void __launch_bounds__(256) sumsq_part_kernel(const float* __restrict
 // computed on the device from the all-reduced grad-norm^2 (no host sync):
 //   clip = min(1, max_norm / (sqrt(gn2) + 1e-6)).
 // Weight decay is applied where wd_mask (per-element u8, or null = all) is set.
+template <typename T>
 __global__ void __launch_bounds__(256) adamw_kernel(
     float* __restrict__ p, float* __restrict__ m, float* __restrict__ v, const float* __restrict__ g,
-    __nv_bfloat16* __restrict__ p_bf16, const uint8_t* __restrict__ wd_mask, int64_t n,
+    T* __restrict__ p_bf16, const uint8_t* __restrict__ wd_mask, int64_t n,
     const float* __restrict__ gn2, float max_norm, float lr, float beta1, float beta2, float eps,
     float wd, float bc1, float bc2) {
   float clip = 1.f;
@@ -524,7 +549,7 @@ __global__ void __launch_bounds__(256) adamw_kernel(
     st4(p + 4 * i, make_float4(P[0], P[1], P[2], P[3]));
     st4(m + 4 * i, make_float4(Mv[0], Mv[1], Mv[2], Mv[3]));
     st4(v + 4 * i, make_float4(Vv[0], Vv[1], Vv[2], Vv[3]));
-    st_bf4(p_bf16 + 4 * i, P);
+    if (p_bf16) st_v4(p_bf16 + 4 * i, P);
   }
   for (int64_t i = nv * 4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const float gt = g[i] * clip;
@@ -535,7 +560,7 @@ __global__ void __launch_bounds__(256) adamw_kernel(
     pi = pi - lr * dec * pi;
     pi = pi - lr * (mi / bc1) / (sqrtf(vi / bc2) + eps);
     p[i] = pi; m[i] = mi; v[i] = vi;
-    p_bf16[i] = f2bf(pi);
+    if (p_bf16) from_f(p_bf16[i], pi);
   }
 }
 
@@ -562,24 +587,24 @@ static unsigned flat_grid(int64_t n, int per_thread = 4) {
   return (unsigned)(blocks < cap ? blocks : cap);
 }
 
-template <bool RMS>
+template <bool RMS, typename T = __nv_bfloat16>
 static int norm_fwd(const float* x, const void* g, const void* b, void* y, float* mean, float* rstd,
                     float* x_copy, int64_t M, int D, float eps, cudaStream_t st) {
   auto go = [&](auto kern, int tpr) {
     int64_t blocks = (M * tpr + kRowThreads - 1) / kRowThreads;
     const int64_t cap = (int64_t)kNumSMs * 8;
     kern<<<(unsigned)(blocks < cap ? blocks : cap), kRowThreads, 0, st>>>(
-        x, (const __nv_bfloat16*)g, (const __nv_bfloat16*)b, (__nv_bfloat16*)y, mean, rstd, x_copy, M, eps);
+        x, (const T*)g, (const T*)b, (T*)y, mean, rstd, x_copy, M, eps);
     return check_launch("norm_fwd");
   };
   switch (D) {
-    case 128: return go(norm_fwd_kernel<128, 32, RMS>, 32);
-    case 256: return go(norm_fwd_kernel<256, 32, RMS>, 32);
-    case 512: return go(norm_fwd_kernel<512, 32, RMS>, 32);
-    case 768: return go(norm_fwd_kernel<768, 32, RMS>, 32);
-    case 1024: return go(norm_fwd_kernel<1024, 32, RMS>, 32);
-    case 2048: return go(norm_fwd_kernel<2048, 256, RMS>, 256);
-    case 4096: return go(norm_fwd_kernel<4096, 256, RMS>, 256);
+    case 128: return go(norm_fwd_kernel<128, 32, RMS, T>, 32);
+    case 256: return go(norm_fwd_kernel<256, 32, RMS, T>, 32);
+    case 512: return go(norm_fwd_kernel<512, 32, RMS, T>, 32);
+    case 768: return go(norm_fwd_kernel<768, 32, RMS, T>, 32);
+    case 1024: return go(norm_fwd_kernel<1024, 32, RMS, T>, 32);
+    case 2048: return go(norm_fwd_kernel<2048, 256, RMS, T>, 256);
+    case 4096: return go(norm_fwd_kernel<4096, 256, RMS, T>, 256);
   }
   set_error("norm: unsupported hidden size %d", D);
   return B2S_EUNSUPPORTED;
@@ -587,7 +612,7 @@ static int norm_fwd(const float* x, const void* g, const void* b, void* y, float
 
 constexpr int kNormBwdMaxBlocks = kNumSMs * 4;
 
-template <bool RMS>
+template <bool RMS, typename T = __nv_bfloat16>
 static int norm_bwd(const float* x, const void* dy, const void* g, const float* mean, const float* rstd,
                     float* dx, void* dx_bf16, float* dg, float* db, float* dxsum, float* work, int64_t M, int D,
                     cudaStream_t st) {
@@ -596,19 +621,19 @@ static int norm_bwd(const float* x, const void* dy, const void* g, const float* 
     int64_t blocks = (M * tpr + kRowThreads - 1) / kRowThreads;
     const int64_t cap = tpr <= 64 ? kNormBwdMaxBlocks : kNumSMs * 2;
     grid = (unsigned)(blocks < cap ? blocks : cap);  // partial buffer: grid * 3 * D floats
-    kern<<<grid, kRowThreads, 0, st>>>(x, (const __nv_bfloat16*)dy, (const __nv_bfloat16*)g, mean, rstd, dx,
-                                       (__nv_bfloat16*)dx_bf16, work, M, dxsum != nullptr);
+    kern<<<grid, kRowThreads, 0, st>>>(x, (const T*)dy, (const T*)g, mean, rstd, dx, (T*)dx_bf16, work, M,
+                                       dxsum != nullptr);
     return check_launch("norm_bwd");
   };
   int rc;
   switch (D) {
-    case 128: rc = go(norm_bwd_kernel<128, 32, RMS>, 32); break;
-    case 256: rc = go(norm_bwd_kernel<256, 32, RMS>, 32); break;
-    case 512: rc = go(norm_bwd_kernel<512, 32, RMS>, 32); break;
-    case 768: rc = go(norm_bwd_kernel<768, 64, RMS>, 64); break;
-    case 1024: rc = go(norm_bwd_kernel<1024, 32, RMS>, 32); break;
-    case 2048: rc = go(norm_bwd_kernel<2048, 256, RMS>, 256); break;
-    case 4096: rc = go(norm_bwd_kernel<4096, 256, RMS>, 256); break;
+    case 128: rc = go(norm_bwd_kernel<128, 32, RMS, T>, 32); break;
+    case 256: rc = go(norm_bwd_kernel<256, 32, RMS, T>, 32); break;
+    case 512: rc = go(norm_bwd_kernel<512, 32, RMS, T>, 32); break;
+    case 768: rc = go(norm_bwd_kernel<768, 64, RMS, T>, 64); break;
+    case 1024: rc = go(norm_bwd_kernel<1024, 32, RMS, T>, 32); break;
+    case 2048: rc = go(norm_bwd_kernel<2048, 256, RMS, T>, 256); break;
+    case 4096: rc = go(norm_bwd_kernel<4096, 256, RMS, T>, 256); break;
     default:
       set_error("norm_bwd: unsupported hidden size %d", D);
       return B2S_EUNSUPPORTED;
@@ -624,27 +649,103 @@ static int norm_bwd(const float* x, const void* dy, const void* g, const float* 
 
 using namespace b2s;
 
+namespace {
+// Host launchers shared by the bf16 and fp32 entry points (T = activation type).
+template <typename T>
+int embedding_fwd(const int64_t* d_tok, const void* d_wte, const void* d_wpe, float* d_x, int64_t M, int T_,
+                  int D, cudaStream_t st) {
+  B2S_REQUIRE(D % 4 == 0, B2S_EUNSUPPORTED, "embedding: D %% 4 != 0");
+  ew::embed_fwd_kernel<T><<<ew::flat_grid(M * D), 256, 0, st>>>(d_tok, (const T*)d_wte, (const T*)d_wpe, d_x, M,
+                                                                 T_, D);
+  return check_launch("embedding_fwd");
+}
+template <typename T>
+int rope(void* d_qkv, int64_t M, int T_, int64_t ld, int nheads, int dh, const float* d_cos, const float* d_sin,
+         int inverse, cudaStream_t st) {
+  B2S_REQUIRE(dh % 16 == 0 && ld % 8 == 0 && ((uintptr_t)d_qkv % 16) == 0, B2S_EUNSUPPORTED,
+              "rope: head dim must be a multiple of 16 and rows 16-byte aligned");
+  ew::rope_kernel<T><<<ew::flat_grid(M * nheads * dh / 16, 1), 256, 0, st>>>((T*)d_qkv, M, T_, ld, nheads, dh,
+                                                                           d_cos, d_sin, inverse);
+  return check_launch("rope");
+}
+template <typename T>
+int swiglu_fwd(const void* d_gu, void* d_h, int64_t M, int F, cudaStream_t st) {
+  B2S_REQUIRE(F % 8 == 0, B2S_EUNSUPPORTED, "swiglu: F %% 8 != 0");
+  ew::swiglu_fwd_kernel<T><<<ew::flat_grid(M * F, 8), 256, 0, st>>>((const T*)d_gu, (T*)d_h, M, F);
+  return check_launch("swiglu_fwd");
+}
+template <typename T>
+int swiglu_bwd(const void* d_gu, const void* d_dh, void* d_dgu, int64_t M, int F, cudaStream_t st) {
+  B2S_REQUIRE(F % 8 == 0, B2S_EUNSUPPORTED, "swiglu: F %% 8 != 0");
+  ew::swiglu_bwd_kernel<T><<<ew::flat_grid(M * F, 8), 256, 0, st>>>((const T*)d_gu, (const T*)d_dh, (T*)d_dgu, M,
+                                                                    F);
+  return check_launch("swiglu_bwd");
+}
+template <typename T>
+int cross_entropy(void* d_logits, int64_t ld, int V, const int64_t* d_target, float* d_loss_rows,
+                  float grad_scale, int64_t M, int write_grad, cudaStream_t st) {
+  B2S_REQUIRE(ld % 8 == 0 && V <= ld, B2S_EUNSUPPORTED, "cross_entropy: ld must be a multiple of 8 >= V");
+  ew::xent_kernel<T><<<(unsigned)M, 512, 0, st>>>((T*)d_logits, ld, V, d_target, d_loss_rows, grad_scale, M,
+                                                  write_grad);
+  return check_launch("cross_entropy");
+}
+template <typename T>
+int adamw(float* d_p, float* d_m, float* d_v, const float* d_g, void* d_p_out, const uint8_t* d_wd_mask, int64_t n,
+          const float* d_gn2, float max_norm, float lr, float beta1, float beta2, float eps, float wd, int step,
+          cudaStream_t st) {
+  B2S_REQUIRE(((uintptr_t)d_p | (uintptr_t)d_m | (uintptr_t)d_v | (uintptr_t)d_g) % 16 == 0 &&
+                  ((uintptr_t)d_p_out % (4 * sizeof(T))) == 0 && (!d_wd_mask || ((uintptr_t)d_wd_mask % 4) == 0),
+              B2S_EUNSUPPORTED, "adamw: misaligned shard");
+  const float bc1 = 1.f - powf(beta1, (float)step), bc2 = 1.f - powf(beta2, (float)step);
+  ew::adamw_kernel<T><<<ew::flat_grid(n), 256, 0, st>>>(d_p, d_m, d_v, d_g, (T*)d_p_out, d_wd_mask, n, d_gn2,
+                                                        max_norm, lr, beta1, beta2, eps, wd, bc1, bc2);
+  return check_launch("adamw");
+}
+}  // namespace
+
+#define B2S_ST(s) ((cudaStream_t)(s))
+
 extern "C" {
 
 int b2s_layernorm_fwd(const float* d_x, const void* d_g, const void* d_b, void* d_y, float* d_mean,
                       float* d_rstd, float* d_x_copy, int64_t M, int D, float eps, b2s_stream_t stream) {
-  return ew::norm_fwd<false>(d_x, d_g, d_b, d_y, d_mean, d_rstd, d_x_copy, M, D, eps, (cudaStream_t)stream);
+  return ew::norm_fwd<false>(d_x, d_g, d_b, d_y, d_mean, d_rstd, d_x_copy, M, D, eps, B2S_ST(stream));
 }
 int b2s_rmsnorm_fwd(const float* d_x, const void* d_g, void* d_y, float* d_rstd, float* d_x_copy,
                     int64_t M, int D, float eps, b2s_stream_t stream) {
-  return ew::norm_fwd<true>(d_x, d_g, nullptr, d_y, nullptr, d_rstd, d_x_copy, M, D, eps, (cudaStream_t)stream);
+  return ew::norm_fwd<true>(d_x, d_g, nullptr, d_y, nullptr, d_rstd, d_x_copy, M, D, eps, B2S_ST(stream));
 }
 int b2s_layernorm_bwd(const float* d_x, const void* d_dy, const void* d_g, const float* d_mean,
                       const float* d_rstd, float* d_dx, void* d_dx_bf16, float* d_dg, float* d_db,
                       float* d_dxsum, float* d_work, int64_t M, int D, b2s_stream_t stream) {
   return ew::norm_bwd<false>(d_x, d_dy, d_g, d_mean, d_rstd, d_dx, d_dx_bf16, d_dg, d_db, d_dxsum, d_work, M, D,
-                             (cudaStream_t)stream);
+                             B2S_ST(stream));
 }
 int b2s_rmsnorm_bwd(const float* d_x, const void* d_dy, const void* d_g, const float* d_rstd, float* d_dx,
                     void* d_dx_bf16, float* d_dg, float* d_dxsum, float* d_work, int64_t M, int D,
                     b2s_stream_t stream) {
   return ew::norm_bwd<true>(d_x, d_dy, d_g, nullptr, d_rstd, d_dx, d_dx_bf16, d_dg, nullptr, d_dxsum, d_work, M,
-                            D, (cudaStream_t)stream);
+                            D, B2S_ST(stream));
+}
+int b2s_layernorm_fwd_f32(const float* d_x, const float* d_g, const float* d_b, float* d_y, float* d_mean,
+                          float* d_rstd, float* d_x_copy, int64_t M, int D, float eps, b2s_stream_t stream) {
+  return ew::norm_fwd<false, float>(d_x, d_g, d_b, d_y, d_mean, d_rstd, d_x_copy, M, D, eps, B2S_ST(stream));
+}
+int b2s_rmsnorm_fwd_f32(const float* d_x, const float* d_g, float* d_y, float* d_rstd, float* d_x_copy,
+                        int64_t M, int D, float eps, b2s_stream_t stream) {
+  return ew::norm_fwd<true, float>(d_x, d_g, nullptr, d_y, nullptr, d_rstd, d_x_copy, M, D, eps, B2S_ST(stream));
+}
+int b2s_layernorm_bwd_f32(const float* d_x, const float* d_dy, const float* d_g, const float* d_mean,
+                          const float* d_rstd, float* d_dx, float* d_dx_copy, float* d_dg, float* d_db,
+                          float* d_dxsum, float* d_work, int64_t M, int D, b2s_stream_t stream) {
+  return ew::norm_bwd<false, float>(d_x, d_dy, d_g, d_mean, d_rstd, d_dx, d_dx_copy, d_dg, d_db, d_dxsum, d_work,
+                                    M, D, B2S_ST(stream));
+}
+int b2s_rmsnorm_bwd_f32(const float* d_x, const float* d_dy, const float* d_g, const float* d_rstd, float* d_dx,
+                        float* d_dx_copy, float* d_dg, float* d_dxsum, float* d_work, int64_t M, int D,
+                        b2s_stream_t stream) {
+  return ew::norm_bwd<true, float>(d_x, d_dy, d_g, nullptr, d_rstd, d_dx, d_dx_copy, d_dg, nullptr, d_dxsum,
+                                   d_work, M, D, B2S_ST(stream));
 }
 int64_t b2s_norm_work_floats(int D) { return (int64_t)ew::kNormBwdMaxBlocks * 3 * D; }
 
@@ -669,10 +770,11 @@ int64_t b2s_colsum_work_floats(int N) { return 256LL * N; }
 
 int b2s_embedding_fwd(const int64_t* d_tok, const void* d_wte, const void* d_wpe, float* d_x, int64_t M,
                       int T, int D, b2s_stream_t stream) {
-  B2S_REQUIRE(D % 4 == 0, B2S_EUNSUPPORTED, "embedding: D %% 4 != 0");
-  ew::embed_fwd_kernel<<<ew::flat_grid(M * D), 256, 0, (cudaStream_t)stream>>>(
-      d_tok, (const __nv_bfloat16*)d_wte, (const __nv_bfloat16*)d_wpe, d_x, M, T, D);
-  return check_launch("embedding_fwd");
+  return embedding_fwd<__nv_bfloat16>(d_tok, d_wte, d_wpe, d_x, M, T, D, B2S_ST(stream));
+}
+int b2s_embedding_fwd_f32(const int64_t* d_tok, const float* d_wte, const float* d_wpe, float* d_x, int64_t M,
+                          int T, int D, b2s_stream_t stream) {
+  return embedding_fwd<float>(d_tok, d_wte, d_wpe, d_x, M, T, D, B2S_ST(stream));
 }
 int b2s_embedding_bwd(const int64_t* d_tok, const float* d_dx, float* d_dwte, float* d_dwpe, int B, int T,
                       int D, b2s_stream_t stream) {
@@ -685,32 +787,34 @@ int b2s_embedding_bwd(const int64_t* d_tok, const float* d_dx, float* d_dwte, fl
 
 int b2s_rope(void* d_qkv, int64_t M, int T, int64_t ld, int nheads, int dh, const float* d_cos,
              const float* d_sin, int inverse, b2s_stream_t stream) {
-  B2S_REQUIRE(dh % 16 == 0 && ld % 8 == 0 && ((uintptr_t)d_qkv % 16) == 0, B2S_EUNSUPPORTED,
-              "rope: head dim must be a multiple of 16 and rows 16-byte aligned");
-  ew::rope_kernel<<<ew::flat_grid(M * nheads * dh / 16, 1), 256, 0, (cudaStream_t)stream>>>(
-      (__nv_bfloat16*)d_qkv, M, T, ld, nheads, dh, d_cos, d_sin, inverse);
-  return check_launch("rope");
+  return rope<__nv_bfloat16>(d_qkv, M, T, ld, nheads, dh, d_cos, d_sin, inverse, B2S_ST(stream));
+}
+int b2s_rope_f32(float* d_qkv, int64_t M, int T, int64_t ld, int nheads, int dh, const float* d_cos,
+                 const float* d_sin, int inverse, b2s_stream_t stream) {
+  return rope<float>(d_qkv, M, T, ld, nheads, dh, d_cos, d_sin, inverse, B2S_ST(stream));
 }
 
 int b2s_swiglu_fwd(const void* d_gu, void* d_h, int64_t M, int F, b2s_stream_t stream) {
-  B2S_REQUIRE(F % 8 == 0, B2S_EUNSUPPORTED, "swiglu: F %% 8 != 0");
-  ew::swiglu_fwd_kernel<<<ew::flat_grid(M * F, 8), 256, 0, (cudaStream_t)stream>>>(
-      (const __nv_bfloat16*)d_gu, (__nv_bfloat16*)d_h, M, F);
-  return check_launch("swiglu_fwd");
+  return swiglu_fwd<__nv_bfloat16>(d_gu, d_h, M, F, B2S_ST(stream));
 }
 int b2s_swiglu_bwd(const void* d_gu, const void* d_dh, void* d_dgu, int64_t M, int F, b2s_stream_t stream) {
-  B2S_REQUIRE(F % 8 == 0, B2S_EUNSUPPORTED, "swiglu: F %% 8 != 0");
-  ew::swiglu_bwd_kernel<<<ew::flat_grid(M * F, 8), 256, 0, (cudaStream_t)stream>>>(
-      (const __nv_bfloat16*)d_gu, (const __nv_bfloat16*)d_dh, (__nv_bfloat16*)d_dgu, M, F);
-  return check_launch("swiglu_bwd");
+  return swiglu_bwd<__nv_bfloat16>(d_gu, d_dh, d_dgu, M, F, B2S_ST(stream));
+}
+int b2s_swiglu_fwd_f32(const float* d_gu, float* d_h, int64_t M, int F, b2s_stream_t stream) {
+  return swiglu_fwd<float>(d_gu, d_h, M, F, B2S_ST(stream));
+}
+int b2s_swiglu_bwd_f32(const float* d_gu, const float* d_dh, float* d_dgu, int64_t M, int F, b2s_stream_t stream) {
+  return swiglu_bwd<float>(d_gu, d_dh, d_dgu, M, F, B2S_ST(stream));
 }
 
 int b2s_cross_entropy(void* d_logits, int64_t ld, int V, const int64_t* d_target, float* d_loss_rows,
                       float grad_scale, int64_t M, int write_grad, b2s_stream_t stream) {
-  B2S_REQUIRE(ld % 8 == 0 && V <= ld, B2S_EUNSUPPORTED, "cross_entropy: ld must be a multiple of 8 >= V");
-  ew::xent_kernel<<<(unsigned)M, 512, 0, (cudaStream_t)stream>>>((__nv_bfloat16*)d_logits, ld, V, d_target,
-                                                                 d_loss_rows, grad_scale, M, write_grad);
-  return check_launch("cross_entropy");
+  return cross_entropy<__nv_bfloat16>(d_logits, ld, V, d_target, d_loss_rows, grad_scale, M, write_grad,
+                                      B2S_ST(stream));
+}
+int b2s_cross_entropy_f32(float* d_logits, int64_t ld, int V, const int64_t* d_target, float* d_loss_rows,
+                          float grad_scale, int64_t M, int write_grad, b2s_stream_t stream) {
+  return cross_entropy<float>(d_logits, ld, V, d_target, d_loss_rows, grad_scale, M, write_grad, B2S_ST(stream));
 }
 
 int b2s_sum(const float* d_x, int64_t n, int squares, float* d_out, float scale, b2s_stream_t stream) {
@@ -725,14 +829,14 @@ int b2s_sumsq_partial(const float* d_x, int64_t n, float* d_part, int nparts, b2
 int b2s_adamw(float* d_p, float* d_m, float* d_v, const float* d_g, void* d_p_bf16, const uint8_t* d_wd_mask,
               int64_t n, const float* d_gn2, float max_norm, float lr, float beta1, float beta2, float eps,
               float wd, int step, b2s_stream_t stream) {
-  B2S_REQUIRE(((uintptr_t)d_p | (uintptr_t)d_m | (uintptr_t)d_v | (uintptr_t)d_g) % 16 == 0 &&
-                  ((uintptr_t)d_p_bf16 % 8) == 0 && (!d_wd_mask || ((uintptr_t)d_wd_mask % 4) == 0),
-              B2S_EUNSUPPORTED, "adamw: misaligned shard");
-  const float bc1 = 1.f - powf(beta1, (float)step), bc2 = 1.f - powf(beta2, (float)step);
-  ew::adamw_kernel<<<ew::flat_grid(n), 256, 0, (cudaStream_t)stream>>>(
-      d_p, d_m, d_v, d_g, (__nv_bfloat16*)d_p_bf16, d_wd_mask, n, d_gn2, max_norm, lr, beta1, beta2, eps, wd,
-      bc1, bc2);
-  return check_launch("adamw");
+  return adamw<__nv_bfloat16>(d_p, d_m, d_v, d_g, d_p_bf16, d_wd_mask, n, d_gn2, max_norm, lr, beta1, beta2, eps,
+                              wd, step, B2S_ST(stream));
+}
+int b2s_adamw_f32(float* d_p, float* d_m, float* d_v, const float* d_g, float* d_p_copy, const uint8_t* d_wd_mask,
+                  int64_t n, const float* d_gn2, float max_norm, float lr, float beta1, float beta2, float eps,
+                  float wd, int step, b2s_stream_t stream) {
+  return adamw<float>(d_p, d_m, d_v, d_g, d_p_copy, d_wd_mask, n, d_gn2, max_norm, lr, beta1, beta2, eps, wd, step,
+                      B2S_ST(stream));
 }
 
 int b2s_f32_to_bf16(const float* d_x, void* d_y, int64_t n, float scale, b2s_stream_t stream) {

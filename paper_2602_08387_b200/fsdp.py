@@ -16,6 +16,9 @@ backward): per step each unit does one NCCL all-gather (before its forward,
 prefetched on a side stream) and one reduce-scatter (as soon as its backward
 is done, on the same side stream), overlapping the compute of other units.
 At W = 1 the shard IS the full buffer and no collective is issued.
+In fp32 mode (compute dtype fp32) the compute weights are the master
+parameters themselves: p16 aliases master (the all-gather source) and, at
+W = 1, master aliases full -- AdamW updates the compute buffer in place.
 `comm_planner.plan_unit_size` picks how many blocks form a unit.
 """
 
@@ -28,7 +31,7 @@ from .model import ALIGN, UnitSpec
 
 
 class FlatUnit:
-    def __init__(self, specs: list, rank: int, world: int, device):
+    def __init__(self, specs: list, rank: int, world: int, device, dtype=torch.bfloat16):
         self.specs = specs  # one or more model UnitSpecs grouped into this FSDP unit
         self.rank, self.world = rank, world
         self.offsets = {}
@@ -41,17 +44,20 @@ class FlatUnit:
         per = -(-off // world)
         self.shard = -(-per // ALIGN) * ALIGN
         self.padded = self.shard * world
-        bf, f32 = torch.bfloat16, torch.float32
+        bf, f32 = dtype, torch.float32
         self.full = torch.zeros(self.padded, device=device, dtype=bf)
         self.gfull = torch.zeros(self.padded, device=device, dtype=f32)
         lo = rank * self.shard
         if world == 1:
-            self.p16 = self.full
             self.g = self.gfull
         else:
-            self.p16 = torch.zeros(self.shard, device=device, dtype=bf)
             self.g = torch.zeros(self.shard, device=device, dtype=f32)
-        self.master = torch.zeros(self.shard, device=device, dtype=f32)
+        if bf == f32:  # fp32 mode: compute copy == master (no separate low-precision shard)
+            self.master = self.full if world == 1 else torch.zeros(self.shard, device=device, dtype=f32)
+            self.p16 = self.master
+        else:
+            self.master = torch.zeros(self.shard, device=device, dtype=f32)
+            self.p16 = self.full if world == 1 else torch.zeros(self.shard, device=device, dtype=bf)
         self.m = torch.zeros(self.shard, device=device, dtype=f32)
         self.v = torch.zeros(self.shard, device=device, dtype=f32)
         mask = torch.zeros(self.padded, dtype=torch.uint8)
@@ -69,8 +75,10 @@ class FlatUnit:
             full[o:o + t.numel()] = t.reshape(-1).to(full.device, torch.float32)
         lo = self.rank * self.shard
         self.master.copy_(full[lo:lo + self.shard])
-        self.p16.copy_(self.master)
-        self.full.copy_(full)  # initial gather done locally (every rank has the same init)
+        if self.p16 is not self.master:
+            self.p16.copy_(self.master)
+        if self.full is not self.master:
+            self.full.copy_(full)  # initial gather done locally (every rank has the same init)
 
     def view(self, buf, unit: str, name: str):
         o, shape, _ = self.offsets[(unit, name)]
@@ -93,7 +101,8 @@ class UnitView:
 class FlatParams:
     """All FSDP units of a model; ``unit(i)`` addresses the i-th *model* unit."""
 
-    def __init__(self, unit_specs: list, rank: int, world: int, device, blocks_per_unit: int = 1):
+    def __init__(self, unit_specs: list, rank: int, world: int, device, blocks_per_unit: int = 1,
+                 dtype=torch.bfloat16):
         self.model_units = unit_specs
         groups, cur = [], []
         # embedding and head are units of their own; blocks are grouped g at a time
@@ -110,7 +119,7 @@ class FlatParams:
                 groups.append([s])
         if cur:
             groups.append(cur)
-        self.flat = [FlatUnit(g, rank, world, device) for g in groups]
+        self.flat = [FlatUnit(g, rank, world, device, dtype) for g in groups]
         self.owner = {}
         self.first_model_unit = {}
         self.last_model_unit = {}
@@ -183,7 +192,7 @@ class Engine:
         self.ag_done = [torch.cuda.Event() for _ in range(n)] if self.cuda else [None] * n
         self.rs_done = [torch.cuda.Event() for _ in range(n)] if self.cuda else [None] * n
         self._issued = 0
-        self.bytes_ag = sum(f.padded * 2 for f in params.flat)
+        self.bytes_ag = sum(f.padded * f.full.element_size() for f in params.flat)
         self.bytes_rs = sum(f.padded * 4 for f in params.flat)
 
     # ------------------------------------------------------------------ step

@@ -9,9 +9,15 @@ allocated once per (batch, seq) shape, which keeps the step CUDA-graph
 capturable and lets the backward write weight gradients straight into the
 FSDP flat gradient buffers (see fsdp.py).
 
-Numerics: bf16 weights/activations into tcgen05 GEMMs and attention with
-fp32 accumulation; the residual stream, its gradient, norm statistics, the
-loss and all parameter gradients are fp32.
+Numerics (``precision``):
+  "bf16"  bf16 weights/activations into tcgen05 GEMMs and attention with fp32
+          accumulation; the residual stream, its gradient, norm statistics,
+          the loss and all parameter gradients are fp32 (the training mode).
+  "fp32"  every tensor fp32; GEMMs and attention on the true-fp32 SIMT kernels
+          (f32.cu), the bandwidth kernels in their fp32 instantiation -- the
+          north star's "fp32 mode" (per-step losses and gradients within 1e-4
+          relative of the CPU fp32 reference). Same call sequence, same
+          buffers, only the element type changes.
 """
 
 from __future__ import annotations
@@ -24,6 +30,7 @@ import torch
 from . import ops
 
 ALIGN = 64  # parameter offsets inside a flat unit, in elements (128 B of bf16)
+PRECISIONS = {"bf16": torch.bfloat16, "fp32": torch.float32}
 
 
 @dataclass(frozen=True)
@@ -217,9 +224,9 @@ def rope_tables(cfg: ModelConfig, T: int, device):
 class _Acts:
     """Activation buffers for one (B, T): saved forward tensors + backward scratch."""
 
-    def __init__(self, cfg: ModelConfig, B: int, T: int, device):
+    def __init__(self, cfg: ModelConfig, B: int, T: int, device, act_dtype=torch.bfloat16):
         M, d, f, L = B * T, cfg.d_model, cfg.d_ff, cfg.n_layer
-        bf, f32 = torch.bfloat16, torch.float32
+        bf, f32 = act_dtype, torch.float32
         e = lambda *s, dt=bf: torch.empty(*s, device=device, dtype=dt)  # noqa: E731
         self.B, self.T, self.M = B, T, M
         # residual stream: xs[2i] enters block i's attention, xs[2i+1] its MLP, xs[2L] the head
@@ -241,7 +248,8 @@ class _Acts:
         self.loss = e(1, dt=f32)
         # backward scratch (reused across layers)
         self.dx = e(M, d, dt=f32)
-        self.dxb = e(M, d)
+        # low-precision copy of dx for the GEMMs; in fp32 mode dx itself
+        self.dxb = self.dx if bf == f32 else e(M, d)
         self.dln = e(M, d)
         self.do = e(M, cfg.n_head * cfg.head_dim)
         self.dqkv = e(M, cfg.qkv_dim)
@@ -254,9 +262,16 @@ class _Acts:
 class DecoderLM(torch.nn.Module):
     """Decoder-only LM whose parameters live in FSDP flat units (see fsdp.FlatParams)."""
 
-    def __init__(self, cfg: ModelConfig):
+    def __init__(self, cfg: ModelConfig, precision: str = "bf16"):
         super().__init__()
+        if precision not in PRECISIONS:
+            raise ValueError(f"precision must be one of {sorted(PRECISIONS)}, got {precision!r}")
+        if precision == "bf16" and cfg.head_dim != 64:
+            raise ValueError(f"bf16 attention kernel implements head dim 64 (got {cfg.head_dim}); "
+                             "use precision='fp32' for other head dims")
         self.cfg = cfg
+        self.precision = precision
+        self.dtype = PRECISIONS[precision]
         self.units = unit_specs(cfg)
         self._acts = {}
         self._rope = {}
@@ -269,7 +284,7 @@ class DecoderLM(torch.nn.Module):
         key = (B, T)
         if key not in self._acts:
             self._acts.clear()
-            self._acts[key] = _Acts(self.cfg, B, T, device)
+            self._acts[key] = _Acts(self.cfg, B, T, device, self.dtype)
         return self._acts[key]
 
     def rope(self, T, device):

@@ -101,6 +101,9 @@ def gemm(a, b, *, a_mn: bool, b_mn: bool, M: int, N: int, K: int, out=None, out_
     whose rows are contiguous.
     """
     _dev(a, b, out, bias, aux)
+    if a.dtype == torch.float32:
+        return _gemm_f32(a, b, a_mn=a_mn, b_mn=b_mn, M=M, N=N, K=K, out=out, accumulate=accumulate, bias=bias,
+                         act=act, aux=aux)
     assert a.dtype == torch.bfloat16 and b.dtype == torch.bfloat16
     if out is None:
         out = torch.empty(M, N, device=a.device, dtype=torch.float32 if out_f32 else torch.bfloat16)
@@ -113,6 +116,24 @@ def gemm(a, b, *, a_mn: bool, b_mn: bool, M: int, N: int, K: int, out=None, out_
         detail=(M, N, K, "MN" if a_mn else "K", "MN" if b_mn else "K", "f32" if out.dtype == torch.float32 else "bf16",
                 "acc" if accumulate else "", "bias" if bias is not None else "", act))
     return out
+
+
+def _gemm_f32(a, b, *, a_mn, b_mn, M, N, K, out=None, accumulate=False, bias=None, act=0, aux=None):
+    """fp32 mode: the same contract on the true-fp32 SIMT kernel (fp32 operands and output)."""
+    assert b.dtype == torch.float32 and (bias is None or bias.dtype == torch.float32)
+    if out is None:
+        out = torch.empty(M, N, device=a.device, dtype=torch.float32)
+    assert out.dtype == torch.float32 and out.stride(-1) == 1 and a.stride(-1) == 1 and b.stride(-1) == 1
+    ld_aux = aux.stride(0) if aux is not None else 0
+    _timed("gemm", 2.0 * M * N * K, lambda: _call(
+        "b2s_gemm_f32", a.data_ptr(), int(a_mn), a.stride(0), b.data_ptr(), int(b_mn), b.stride(0), out.data_ptr(),
+        out.stride(0), M, N, K, int(accumulate), _ptr(bias), act, _ptr(aux), ld_aux, _sp()))
+    return out
+
+
+def _sfx(t):
+    """C-ABI entry-point suffix for the element type of an activation tensor."""
+    return "_f32" if t.dtype == torch.float32 else ""
 
 
 def linear(x, w, bias=None, out=None, act=0, aux=None, accumulate=False):
@@ -165,7 +186,7 @@ def layernorm_fwd(x, g, b, eps=1e-5, y=None, mean=None, rstd=None, x_copy=None):
     y = torch.empty(M, D, device=x.device, dtype=torch.bfloat16) if y is None else y
     mean = torch.empty(M, device=x.device) if mean is None else mean
     rstd = torch.empty(M, device=x.device) if rstd is None else rstd
-    _call("b2s_layernorm_fwd", x.data_ptr(), g.data_ptr(), b.data_ptr(), y.data_ptr(), mean.data_ptr(),
+    _call("b2s_layernorm_fwd" + _sfx(y), x.data_ptr(), g.data_ptr(), b.data_ptr(), y.data_ptr(), mean.data_ptr(),
           rstd.data_ptr(), _ptr(x_copy), M, D, eps, _sp())
     return y, mean, rstd
 
@@ -175,7 +196,7 @@ def rmsnorm_fwd(x, g, eps=1e-5, y=None, rstd=None, x_copy=None):
     M, D = x.shape
     y = torch.empty(M, D, device=x.device, dtype=torch.bfloat16) if y is None else y
     rstd = torch.empty(M, device=x.device) if rstd is None else rstd
-    _call("b2s_rmsnorm_fwd", x.data_ptr(), g.data_ptr(), y.data_ptr(), rstd.data_ptr(), _ptr(x_copy), M, D,
+    _call("b2s_rmsnorm_fwd" + _sfx(y), x.data_ptr(), g.data_ptr(), y.data_ptr(), rstd.data_ptr(), _ptr(x_copy), M, D,
           eps, _sp())
     return y, rstd
 
@@ -184,14 +205,18 @@ def layernorm_bwd(x, dy, g, mean, rstd, dx, dx_bf16=None, dg=None, db=None, dxsu
     """dx += LN backward; dg/db (fp32) accumulated; dxsum += colsum(updated dx)."""
     M, D = x.shape
     work = _work(_lib.load().b2s_norm_work_floats(D), x.device)
-    _call("b2s_layernorm_bwd", x.data_ptr(), dy.data_ptr(), g.data_ptr(), mean.data_ptr(), rstd.data_ptr(),
+    if dx_bf16 is dx:  # fp32 mode: the GEMM operand is dx itself
+        dx_bf16 = None
+    _call("b2s_layernorm_bwd" + _sfx(dy), x.data_ptr(), dy.data_ptr(), g.data_ptr(), mean.data_ptr(), rstd.data_ptr(),
           dx.data_ptr(), _ptr(dx_bf16), _ptr(dg), _ptr(db), _ptr(dxsum), work.data_ptr(), M, D, _sp())
 
 
 def rmsnorm_bwd(x, dy, g, rstd, dx, dx_bf16=None, dg=None, dxsum=None):
     M, D = x.shape
     work = _work(_lib.load().b2s_norm_work_floats(D), x.device)
-    _call("b2s_rmsnorm_bwd", x.data_ptr(), dy.data_ptr(), g.data_ptr(), rstd.data_ptr(), dx.data_ptr(),
+    if dx_bf16 is dx:
+        dx_bf16 = None
+    _call("b2s_rmsnorm_bwd" + _sfx(dy), x.data_ptr(), dy.data_ptr(), g.data_ptr(), rstd.data_ptr(), dx.data_ptr(),
           _ptr(dx_bf16), _ptr(dg), _ptr(dxsum), work.data_ptr(), M, D, _sp())
 
 
@@ -210,7 +235,7 @@ def embedding_fwd(tok, wte, wpe, T, out=None):
     M = tok.numel()
     D = wte.shape[1]
     out = torch.empty(M, D, device=tok.device) if out is None else out
-    _call("b2s_embedding_fwd", tok.data_ptr(), wte.data_ptr(), _ptr(wpe), out.data_ptr(), M, T, D, _sp())
+    _call("b2s_embedding_fwd" + _sfx(wte), tok.data_ptr(), wte.data_ptr(), _ptr(wpe), out.data_ptr(), M, T, D, _sp())
     return out
 
 
@@ -221,28 +246,28 @@ def embedding_bwd(tok, dx, dwte, dwpe, B, T):
 
 def rope(qkv, T, nheads, dh, cos, sin, inverse=False):
     M = qkv.shape[0]
-    _call("b2s_rope", qkv.data_ptr(), M, T, qkv.stride(0), nheads, dh, cos.data_ptr(), sin.data_ptr(),
+    _call("b2s_rope" + _sfx(qkv), qkv.data_ptr(), M, T, qkv.stride(0), nheads, dh, cos.data_ptr(), sin.data_ptr(),
           int(inverse), _sp())
 
 
 def swiglu_fwd(gu, h=None):
     M, F2 = gu.shape
-    h = torch.empty(M, F2 // 2, device=gu.device, dtype=torch.bfloat16) if h is None else h
-    _call("b2s_swiglu_fwd", gu.data_ptr(), h.data_ptr(), M, F2 // 2, _sp())
+    h = torch.empty(M, F2 // 2, device=gu.device, dtype=gu.dtype) if h is None else h
+    _call("b2s_swiglu_fwd" + _sfx(gu), gu.data_ptr(), h.data_ptr(), M, F2 // 2, _sp())
     return h
 
 
 def swiglu_bwd(gu, dh, dgu=None):
     M, F2 = gu.shape
     dgu = torch.empty_like(gu) if dgu is None else dgu
-    _call("b2s_swiglu_bwd", gu.data_ptr(), dh.data_ptr(), dgu.data_ptr(), M, F2 // 2, _sp())
+    _call("b2s_swiglu_bwd" + _sfx(gu), gu.data_ptr(), dh.data_ptr(), dgu.data_ptr(), M, F2 // 2, _sp())
     return dgu
 
 
 def cross_entropy(logits, V, target, loss_rows=None, grad_scale=1.0, write_grad=True):
     M = logits.shape[0]
     loss_rows = torch.empty(M, device=logits.device) if loss_rows is None else loss_rows
-    _call("b2s_cross_entropy", logits.data_ptr(), logits.stride(0), V, target.data_ptr(), loss_rows.data_ptr(),
+    _call("b2s_cross_entropy" + _sfx(logits), logits.data_ptr(), logits.stride(0), V, target.data_ptr(), loss_rows.data_ptr(),
           grad_scale, M, int(write_grad), _sp())
     return loss_rows
 
@@ -257,7 +282,11 @@ def sumsq_partial(x, part):
 
 
 def adamw(p, m, v, g, p_bf16, step, lr, beta1, beta2, eps, wd, gn2=None, max_norm=0.0, wd_mask=None):
-    _call("b2s_adamw", p.data_ptr(), m.data_ptr(), v.data_ptr(), g.data_ptr(), p_bf16.data_ptr(), _ptr(wd_mask),
+    """p_bf16: the compute copy written after the update (bf16 or fp32), or None / p itself (fp32 mode)."""
+    if p_bf16 is p:
+        p_bf16 = None
+    name = "b2s_adamw_f32" if p_bf16 is None or p_bf16.dtype == torch.float32 else "b2s_adamw"
+    _call(name, p.data_ptr(), m.data_ptr(), v.data_ptr(), g.data_ptr(), _ptr(p_bf16), _ptr(wd_mask),
           p.numel(), _ptr(gn2), max_norm, lr, beta1, beta2, eps, wd, step, _sp())
 
 
@@ -276,10 +305,10 @@ def scale_f32(x, scale):
 def attn_fwd(qkv, B, T, Hq, Hkv, dh, o=None, lse=None):
     """Causal attention over the fused [B*T, (Hq+2Hkv)*dh] projection output."""
     _dev(qkv)
-    o = torch.empty(B * T, Hq * dh, device=qkv.device, dtype=torch.bfloat16) if o is None else o
+    o = torch.empty(B * T, Hq * dh, device=qkv.device, dtype=qkv.dtype) if o is None else o
     lse = torch.empty(B, Hq, T, device=qkv.device, dtype=torch.float32) if lse is None else lse
     flops = 4.0 * B * Hq * dh * T * T / 2  # algorithmic causal FLOPs: QK^T and PV, lower triangle
-    _timed("attn_fwd", flops, lambda: _call("b2s_attn_fwd", qkv.data_ptr(), o.data_ptr(), lse.data_ptr(), B, T,
+    _timed("attn_fwd", flops, lambda: _call("b2s_attn_fwd" + _sfx(qkv), qkv.data_ptr(), o.data_ptr(), lse.data_ptr(), B, T,
                                             Hq, Hkv, dh, _sp()))
     return o, lse
 
@@ -290,7 +319,7 @@ def attn_bwd(qkv, o, do, lse, B, T, Hq, Hkv, dh, dqkv=None, work=None):
     n = _lib.load().b2s_attn_bwd_work_floats(B, T, Hq, dh)
     work = _work(n, qkv.device) if work is None else work
     flops = 10.0 * B * Hq * dh * T * T / 2  # S, dP, dV, dK, dQ over the lower triangle
-    _timed("attn_bwd", flops, lambda: _call("b2s_attn_bwd", qkv.data_ptr(), o.data_ptr(), do.data_ptr(),
+    _timed("attn_bwd", flops, lambda: _call("b2s_attn_bwd" + _sfx(qkv), qkv.data_ptr(), o.data_ptr(), do.data_ptr(),
                                             lse.data_ptr(), dqkv.data_ptr(), work.data_ptr(), B, T, Hq, Hkv, dh,
                                             _sp()))
     return dqkv

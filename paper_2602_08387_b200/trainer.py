@@ -61,7 +61,8 @@ class SPMDTrainer:
         self.rank, self.world, self.local_rank, self.device = init_distributed()
         self.group = dist.group.WORLD if self.world > 1 else None
         cfg = self.model.cfg
-        self.params = FlatParams(self.model.units, self.rank, self.world, self.device, self.blocks_per_unit)
+        self.params = FlatParams(self.model.units, self.rank, self.world, self.device, self.blocks_per_unit,
+                                 dtype=self.model.dtype)
         init_dev = "cpu" if self.init_device == "cpu" else self.device
         self.params.load(param_initializer(cfg, self.seed, init_dev))
         self.model.attach(self.params)
