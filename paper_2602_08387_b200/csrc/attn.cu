@@ -1,9 +1,10 @@
-// Causal multi-head / grouped-query attention on tcgen05 (K7), head dim 64.
+// Causal multi-head / grouped-query attention on tcgen05 (K7), head dims 64 and 128.
 //
 // Layout: q/k/v are read straight out of the fused QKV projection output
 // [B*T, (Hq + 2*Hkv) * dh] (bf16, head h of q at column h*dh, kv head j of k
 // at (Hq + j)*dh and of v at (Hq + Hkv + j)*dh) by 2-D TMA boxes of
-// 64 (dh) x 128 (tokens) -- no transpose/copy kernel. Output o is
+// 64 (dh) x 128 (tokens) -- no transpose/copy kernel (two boxes per tile at
+// dh = 128: a tile is then two 128B-swizzle atoms, 16 KB apart). Output o is
 // [B*T, Hq*dh] bf16 (the O-projection GEMM's A operand) and the per-row
 // log-sum-exp lse[B, Hq, T] (fp32, natural log) is kept for the backward.
 //
@@ -27,9 +28,10 @@ namespace b2s {
 using namespace sm100;
 namespace attn {
 
-constexpr int BQ = 128, BKV = 128, DH = 64;
+constexpr int BQ = 128, BKV = 128;
 
-constexpr int kTile = BQ * DH * 2;  // 16 KB bf16 128x64 tile
+constexpr int kTile = BQ * 64 * 2;  // 16 KB: one 128-row x 64-column bf16 swizzle atom
+constexpr int kPBuf = BQ * BKV * 2; // 32 KB: a 128 x 128 bf16 P tile (two atoms)
 constexpr int kStages = 2;
 constexpr float kLog2e = 1.4426950408889634f;
 
@@ -75,8 +77,17 @@ struct Params {
 // <= 256 -- so the softmax loop never waits for the PV MMA it just enabled.
 // P is double-buffered in smem per tile so P(j+1) can be written while
 // PV(j) still reads P(j).
-constexpr int kFwdThreads = 320;
-constexpr int kFwdSmem = 1024 + 2 * kTile /*Q_A,Q_B*/ + 2 * kStages * kTile /*K,V*/ + 8 * kTile /*P: 2 tiles x 2 bufs*/ + 256;
+// dh = 128 runs one query tile per CTA (TILES = 1, warps 6-9 absent): the
+// 32 KB Q / K / V tiles leave room for 2 K/V stages and a double-buffered P
+// only for one tile in 227 KB of shared memory.
+template <int DH>
+struct Fwd {
+  static constexpr int TILES = DH == 64 ? 2 : 1;
+  static constexpr int kThreads = 64 + 128 * TILES;
+  static constexpr int kTileQ = BQ * DH * 2;  // Q / K / V tile bytes (DH/64 atoms)
+  static constexpr int kSmem = 1024 + TILES * kTileQ + 2 * kStages * kTileQ + TILES * 2 * kPBuf + 256;
+  static_assert(kSmem <= 232448, "forward tiles exceed shared memory");
+};
 constexpr float kRescaleThresh = 8.0f;  // log2 units
 
 __device__ __forceinline__ float ex2(float x) {
@@ -111,15 +122,18 @@ __device__ __forceinline__ float exp_pack(const uint32_t* v, int col0, int r, fl
   return rs;
 }
 
-__global__ void __launch_bounds__(320, 1)
+template <int DH>
+__global__ void __launch_bounds__(Fwd<DH>::kThreads, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_o,
                     Params p) {
+  using C = Fwd<DH>;
+  constexpr int TILES = C::TILES, kTQ = C::kTileQ, NA = DH / 64;  // NA: 64-column atoms per tile
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* sQ = align1024(smem_raw);          // [2] tiles A, B
-  uint8_t* sK = sQ + 2 * kTile;               // [kStages]
-  uint8_t* sV = sK + kStages * kTile;         // [kStages]
-  uint8_t* sP = sV + kStages * kTile;         // [tile][buf] x 32 KB (two 64-key atoms each)
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + 8 * kTile);
+  uint8_t* sQ = align1024(smem_raw);          // [TILES] tiles A, B
+  uint8_t* sK = sQ + TILES * kTQ;             // [kStages]
+  uint8_t* sV = sK + kStages * kTQ;           // [kStages]
+  uint8_t* sP = sV + kStages * kTQ;           // [tile][buf] x 32 KB (two 64-key atoms each)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + TILES * 2 * kPBuf);
   uint64_t* q_full = bars;                    // 1
   uint64_t* k_full = bars + 1;                // [kStages]
   uint64_t* v_full = k_full + kStages;        // [kStages]
@@ -134,14 +148,14 @@ __global__ void __launch_bounds__(320, 1)
   uint32_t* tslot = reinterpret_cast<uint32_t*>(pv_done + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int npair = (p.nqt + 1) / 2;
+  const int npair = (p.nqt + TILES - 1) / TILES;
   const int nbh = p.B * p.Hq;
   const int pr = npair - 1 - (int)(blockIdx.x / nbh);  // heaviest pairs first
   const int bh = blockIdx.x % nbh;
   const int b = bh / p.Hq, h = bh % p.Hq;
   const int kvh = h / (p.Hq / p.Hkv);
-  const int qtA = 2 * pr, qtB = 2 * pr + 1;
-  const bool hasB = qtB < p.nqt;
+  const int qtA = TILES * pr, qtB = TILES * pr + 1;
+  const bool hasB = TILES == 2 && qtB < p.nqt;
   const int nA = qtA + 1, nB = hasB ? qtB + 1 : 0;
   const int nkv = hasB ? nB : nA;
 
@@ -162,21 +176,25 @@ __global__ void __launch_bounds__(320, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tslot;
-  // TMEM: S_A [0,128) S_B [128,256) O_A [256,320) O_B [320,384)
+  // TMEM: S_A [0,128) S_B [128,256) O_A [256,256+DH) O_B [256+DH,256+2DH)
 
   if (warp == 0) {
     if (lane == 0) {
-      mbar_arrive_expect_tx(q_full, hasB ? 2 * kTile : kTile);
-      tma_load_2d(sQ, &tm_qkv, q_full, h * DH, b * p.T + qtA * BQ);
-      if (hasB) tma_load_2d(sQ + kTile, &tm_qkv, q_full, h * DH, b * p.T + qtB * BQ);
+      mbar_arrive_expect_tx(q_full, hasB ? 2 * kTQ : kTQ);
+      for (int a = 0; a < NA; ++a) {
+        tma_load_2d(sQ + a * kTile, &tm_qkv, q_full, h * DH + a * 64, b * p.T + qtA * BQ);
+        if (hasB) tma_load_2d(sQ + kTQ + a * kTile, &tm_qkv, q_full, h * DH + a * 64, b * p.T + qtB * BQ);
+      }
       for (int j = 0; j < nkv; ++j) {
         const int s = j % kStages;
         mbar_wait(&kv_empty[s], ((j / kStages) & 1) ^ 1);
         const int r = b * p.T + j * BKV;
-        mbar_arrive_expect_tx(&k_full[s], kTile);
-        tma_load_2d(sK + s * kTile, &tm_qkv, &k_full[s], (p.Hq + kvh) * DH, r);
-        mbar_arrive_expect_tx(&v_full[s], kTile);
-        tma_load_2d(sV + s * kTile, &tm_qkv, &v_full[s], (p.Hq + p.Hkv + kvh) * DH, r);
+        mbar_arrive_expect_tx(&k_full[s], kTQ);
+        for (int a = 0; a < NA; ++a)
+          tma_load_2d(sK + s * kTQ + a * kTile, &tm_qkv, &k_full[s], (p.Hq + kvh) * DH + a * 64, r);
+        mbar_arrive_expect_tx(&v_full[s], kTQ);
+        for (int a = 0; a < NA; ++a)
+          tma_load_2d(sV + s * kTQ + a * kTile, &tm_qkv, &v_full[s], (p.Hq + p.Hkv + kvh) * DH + a * 64, r);
       }
     }
     __syncwarp();
@@ -191,9 +209,11 @@ __global__ void __launch_bounds__(320, 1)
         mbar_wait(&s_empty[t], (j & 1) ^ 1);
         tc_fence_after();
 #pragma unroll
-        for (int kk = 0; kk < DH / 16; ++kk)
-          mma_bf16_ss_w(tbase + t * BKV, make_sdesc(aQ + t * kTile + kk * 32, 16, 1024),
-                      make_sdesc(aK + s * kTile + kk * 32, 16, 1024), idS, kk > 0);
+        for (int kk = 0; kk < DH / 16; ++kk) {
+          const uint32_t ko = (kk >> 2) * kTile + (kk & 3) * 32;  // atom, then 16-element K step
+          mma_bf16_ss_w(tbase + t * BKV, make_sdesc(aQ + t * kTQ + ko, 16, 1024),
+                        make_sdesc(aK + s * kTQ + ko, 16, 1024), idS, kk > 0);
+        }
         mma_commit_w(&s_full[t]);
       };
       auto issue_PV = [&](int t, int j, bool last) {
@@ -201,11 +221,12 @@ __global__ void __launch_bounds__(320, 1)
         mbar_wait(&v_full[s], (j / kStages) & 1);
         mbar_wait(&p_full[2 * t + (j & 1)], (j >> 1) & 1);
         tc_fence_after();
-        const uint32_t pbase = aP + (2 * t + (j & 1)) * 2 * kTile;
+        const uint32_t pbase = aP + (2 * t + (j & 1)) * kPBuf;
+        // V as an MN-major operand: 16 keys per K step (2 KB of 128-B rows), dh atoms LBO = 16 KB apart
 #pragma unroll
         for (int kk = 0; kk < BKV / 16; ++kk)
           mma_bf16_ss_w(tbase + 256 + t * DH, make_sdesc(pbase + (kk >> 2) * kTile + (kk & 3) * 32, 16, 1024),
-                      make_sdesc(aV + s * kTile + kk * 2048, kTile, 1024), idO, (j > 0 || kk > 0) ? 1u : 0u);
+                        make_sdesc(aV + s * kTQ + kk * 2048, kTile, 1024), idO, (j > 0 || kk > 0) ? 1u : 0u);
         mma_commit_w(&p_empty[2 * t + (j & 1)]);
         mma_commit_w(&pv_done[t]);
         if (last) mma_commit_w(&o_done[t]);
@@ -281,7 +302,7 @@ __global__ void __launch_bounds__(320, 1)
       // P = 2^(s*sl2 - m_use) -> bf16 -> smem buffer (j & 1); row sum
       const int pb = j & 1;
       if (j >= 2) mbar_wait(&p_empty[2 * t + pb], ((j >> 1) - 1) & 1);
-      uint8_t* myP = sP + (2 * t + pb) * 2 * kTile;
+      uint8_t* myP = sP + (2 * t + pb) * kPBuf;
       float rs = 0.f;
       if (diag) {
         rs += exp_pack<true>(v, 0, r, sl2, m_use, myP);
@@ -301,7 +322,7 @@ __global__ void __launch_bounds__(320, 1)
       // epilogue: O (TMEM) / l -> bf16 -> this tile's Q buffer (all MMAs retired) -> TMA store
       mbar_wait(&o_done[t], 0);
       tc_fence_after();
-      uint8_t* sO = sQ + t * kTile;
+      uint8_t* sO = sQ + t * kTQ;
       const float inv = 1.f / l;
 #pragma unroll
       for (int c = 0; c < DH / 32; ++c) {
@@ -315,14 +336,14 @@ __global__ void __launch_bounds__(320, 1)
           w.y = pack_bf16x2(__uint_as_float(o[8 * k8 + 2]) * inv, __uint_as_float(o[8 * k8 + 3]) * inv);
           w.z = pack_bf16x2(__uint_as_float(o[8 * k8 + 4]) * inv, __uint_as_float(o[8 * k8 + 5]) * inv);
           w.w = pack_bf16x2(__uint_as_float(o[8 * k8 + 6]) * inv, __uint_as_float(o[8 * k8 + 7]) * inv);
-          *reinterpret_cast<uint4*>(sO + swz(r, c * 4 + k8)) = w;
+          *reinterpret_cast<uint4*>(sO + (c >> 1) * kTile + swz(r, (c & 1) * 4 + k8)) = w;
         }
       }
       p.lse[((size_t)b * p.Hq + h) * p.T + qt * BQ + r] = (m + log2f(l)) * (1.f / kLog2e);
       fence_proxy_async_smem();
       named_sync(1 + t, 128);
       if (q4 == 0 && lane == 0) {
-        tma_store_2d(&tm_o, sO, h * DH, b * p.T + qt * BQ);
+        for (int a = 0; a < NA; ++a) tma_store_2d(&tm_o, sO + a * kTile, h * DH + a * 64, b * p.T + qt * BQ);
         bulk_commit();
         bulk_wait<0>();
       }
@@ -340,14 +361,16 @@ __global__ void __launch_bounds__(320, 1)
 // =====================================================================================
 // backward
 // =====================================================================================
-// D[b, h, q] = sum_d dO * O (row-wise), and zero the fp32 dQ accumulator.
+// D[b, h, q] = sum_d dO * O (row-wise), and zero the fp32 dQ accumulator (if any).
+template <int DH>
 __global__ void attn_bwd_prep_kernel(const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ dout,
                                      float* __restrict__ dsum, float* __restrict__ dq_acc, int B, int T, int Hq) {
-  // 8 lanes per (row, head): each lane a 16-byte vector of o and dO
-  const int sub = threadIdx.x & 7;
+  // DH/8 lanes per (row, head): each lane a 16-byte vector of o and dO
+  constexpr int LPR = DH / 8;
+  const int sub = threadIdx.x & (LPR - 1);
   const int64_t nrows = (int64_t)B * T * Hq;
-  for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 3; w < nrows;
-       w += ((int64_t)gridDim.x * blockDim.x) >> 3) {
+  for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / LPR; w < nrows;
+       w += ((int64_t)gridDim.x * blockDim.x) / LPR) {
     const int64_t row = w / Hq;
     const int h = (int)(w - row * Hq);
     const int64_t off = row * Hq * DH + h * DH + sub * 8;
@@ -357,11 +380,12 @@ __global__ void attn_bwd_prep_kernel(const __nv_bfloat16* __restrict__ o, const 
     float acc = 0.f;
 #pragma unroll
     for (int i = 0; i < 8; ++i) acc += a[i] * g[i];
-    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-    acc += __shfl_xor_sync(0xffffffffu, acc, 4);
-    *reinterpret_cast<float4*>(dq_acc + off) = make_float4(0.f, 0.f, 0.f, 0.f);
-    *reinterpret_cast<float4*>(dq_acc + off + 4) = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int x = 1; x < LPR; x <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, x);
+    if (dq_acc) {
+      *reinterpret_cast<float4*>(dq_acc + off) = make_float4(0.f, 0.f, 0.f, 0.f);
+      *reinterpret_cast<float4*>(dq_acc + off + 4) = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
     if (sub == 0) {
       const int64_t b = row / T, t = row - b * T;
       dsum[(b * Hq + h) * T + t] = acc;
@@ -369,9 +393,10 @@ __global__ void attn_bwd_prep_kernel(const __nv_bfloat16* __restrict__ o, const 
   }
 }
 
-// dqkv[:, q heads] = bf16(dq_acc)
+// dqkv[:, q heads] = bf16(dq_acc)  (dh = 64 path)
 __global__ void attn_bwd_dq_kernel(const float* __restrict__ dq_acc, __nv_bfloat16* __restrict__ dqkv, int64_t M,
                                    int Hq, int64_t ldq) {
+  constexpr int DH = 64;
   const int width = Hq * DH;
   const int64_t nvec = M * width / 4;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nvec; i += (int64_t)gridDim.x * blockDim.x) {
@@ -414,21 +439,37 @@ __device__ __forceinline__ void p_ds(uint32_t* sv, uint32_t* dv, int q0, int r, 
     dv[e] = __float_as_uint(pv * (__uint_as_float(dv[e]) - dd[q]));
   }
 }
-constexpr int kBwdSmem = 1024 + 2 * kTile /*K,V*/ + 4 * kTile /*Q,dO x2*/ + 2 * kTile /*P^T*/ + 2 * kTile /*dS^T*/ +
-                         2 * kTile /*dQ fp32 staging: 8 warps x 4 KB*/ + 4 * BQ * 4 /*LSE, D x2*/ + 256;
+// dh = 64: dQ fused (TMEM S^T 128 + dP^T 128 + dV 64 + dK 64 + dQ 2x64 = 512
+// columns) and Q / dO double-buffered. dh = 128: dV + dK take 256 columns, so
+// this kernel computes dK / dV only (single-buffered Q / dO to fit 227 KB of
+// smem) and attn_bwd_q_kernel produces dQ per query tile.
+template <int DH>
+struct Bwd {
+  static constexpr bool DQ = DH == 64;        // dQ fused into the key-tile kernel
+  static constexpr int QS = DH == 64 ? 2 : 1; // Q / dO stages
+  static constexpr int kTileQ = BQ * DH * 2;
+  static constexpr int kSmem = 1024 + 2 * kTileQ /*K,V*/ + 2 * QS * kTileQ /*Q,dO*/ + 2 * kPBuf /*P^T,dS^T*/ +
+                               (DQ ? 2 * kTile : 0) /*dQ fp32 staging: 8 warps x 4 KB*/ + 4 * BQ * 4 /*LSE, D x2*/ +
+                               256;
+  static_assert(kSmem <= 232448, "backward tiles exceed shared memory");
+};
 
+template <int DH>
 __global__ void __launch_bounds__(320, 1)
     attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
                     const __grid_constant__ CUtensorMap tm_dq, const __grid_constant__ CUtensorMap tm_dkv, Params p) {
+  using C = Bwd<DH>;
+  constexpr int kTQ = C::kTileQ, QS = C::QS, NA = DH / 64;
+  constexpr bool DQ = C::DQ;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sK = align1024(smem_raw);
-  uint8_t* sV = sK + kTile;
-  uint8_t* sQ = sV + kTile;          // [2]
-  uint8_t* sdO = sQ + 2 * kTile;     // [2]
-  uint8_t* sP = sdO + 2 * kTile;     // P^T  [128 keys][128 q] as two 64-column atoms
-  uint8_t* sdS = sP + 2 * kTile;     // dS^T
-  uint8_t* sdQ = sdS + 2 * kTile;    // fp32 128 x 64 as two 32-column boxes (16 KB each)
-  float* sLse = reinterpret_cast<float*>(sdQ + 2 * kTile);  // [2][128] natural-log LSE (TMA bulk)
+  uint8_t* sV = sK + kTQ;
+  uint8_t* sQ = sV + kTQ;            // [QS]
+  uint8_t* sdO = sQ + QS * kTQ;      // [QS]
+  uint8_t* sP = sdO + QS * kTQ;      // P^T  [128 keys][128 q] as two 64-column atoms
+  uint8_t* sdS = sP + kPBuf;         // dS^T
+  uint8_t* sdQ = sdS + kPBuf;        // fp32 128 x 64 as two 32-column boxes (16 KB each), dh 64 only
+  float* sLse = reinterpret_cast<float*>(sdQ + (DQ ? 2 * kTile : 0));  // [2][128] natural-log LSE (TMA bulk)
   float* sD = sLse + 2 * BQ;                                 // [2][128] rowsum(dO*O)
   uint64_t* bars = reinterpret_cast<uint64_t*>(sD + 2 * BQ);
   uint64_t* kv_full = bars;
@@ -475,13 +516,16 @@ __global__ void __launch_bounds__(320, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tslot;
-  const uint32_t tS = tbase, tdP = tbase + 128, tdV = tbase + 256, tdK = tbase + 320, tdQ = tbase + 384;  // dQ: [2] x 64
+  // dQ: [2] x 64 (dh 64 only)
+  const uint32_t tS = tbase, tdP = tbase + 128, tdV = tbase + 256, tdK = tbase + 256 + DH, tdQ = tbase + 384;
 
   if (warp == 0) {
     if (lane == 0) {
-      mbar_arrive_expect_tx(kv_full, 2 * kTile);
-      tma_load_2d(sK, &tm_qkv, kv_full, (p.Hq + kvh) * DH, krow0);
-      tma_load_2d(sV, &tm_qkv, kv_full, (p.Hq + p.Hkv + kvh) * DH, krow0);
+      mbar_arrive_expect_tx(kv_full, 2 * kTQ);
+      for (int a = 0; a < NA; ++a) {
+        tma_load_2d(sK + a * kTile, &tm_qkv, kv_full, (p.Hq + kvh) * DH + a * 64, krow0);
+        tma_load_2d(sV + a * kTile, &tm_qkv, kv_full, (p.Hq + p.Hkv + kvh) * DH + a * 64, krow0);
+      }
       for (int t = 0; t < nsteps; ++t) {
         const int h = kvh * G + t / nq, i = kt + t % nq;
         const int s = t & 1;
@@ -490,10 +534,13 @@ __global__ void __launch_bounds__(320, 1)
         mbar_arrive_expect_tx(&st_ld_full[s], 2 * BQ * 4);
         bulk_load_1d(sLse + s * BQ, p.lse + off, BQ * 4, &st_ld_full[s]);
         bulk_load_1d(sD + s * BQ, p.dsum + off, BQ * 4, &st_ld_full[s]);
-        mbar_wait(&qd_empty[s], ((t >> 1) & 1) ^ 1);
-        mbar_arrive_expect_tx(&qd_full[s], 2 * kTile);
-        tma_load_2d(sQ + s * kTile, &tm_qkv, &qd_full[s], h * DH, b * p.T + i * BQ);
-        tma_load_2d(sdO + s * kTile, &tm_do, &qd_full[s], h * DH, b * p.T + i * BQ);
+        const int qs = t % QS;
+        mbar_wait(&qd_empty[qs], ((t / QS) & 1) ^ 1);
+        mbar_arrive_expect_tx(&qd_full[qs], 2 * kTQ);
+        for (int a = 0; a < NA; ++a) {
+          tma_load_2d(sQ + qs * kTQ + a * kTile, &tm_qkv, &qd_full[qs], h * DH + a * 64, b * p.T + i * BQ);
+          tma_load_2d(sdO + qs * kTQ + a * kTile, &tm_do, &qd_full[qs], h * DH + a * 64, b * p.T + i * BQ);
+        }
       }
     }
     __syncwarp();
@@ -505,25 +552,30 @@ __global__ void __launch_bounds__(320, 1)
       const uint32_t aK = smem_u32(sK), aV = smem_u32(sV), aQ = smem_u32(sQ), adO = smem_u32(sdO);
       const uint32_t aP = smem_u32(sP), adS = smem_u32(sdS);
       auto issue_S = [&](int t) {
-        const int s = t & 1;
-        mbar_wait(&qd_full[s], (t >> 1) & 1);
+        const int qs = t % QS;
+        mbar_wait(&qd_full[qs], (t / QS) & 1);
         if (t > 0) mbar_wait(st_empty, (t - 1) & 1);
         tc_fence_after();
-        const uint32_t q_ = aQ + s * kTile, do_ = adO + s * kTile;
+        const uint32_t q_ = aQ + qs * kTQ, do_ = adO + qs * kTQ;
 #pragma unroll
-        for (int kk = 0; kk < DH / 16; ++kk)
-          mma_bf16_ss_w(tS, make_sdesc(aK + kk * 32, 16, 1024), make_sdesc(q_ + kk * 32, 16, 1024), idSS, kk > 0);
+        for (int kk = 0; kk < DH / 16; ++kk) {
+          const uint32_t ko = (kk >> 2) * kTile + (kk & 3) * 32;
+          mma_bf16_ss_w(tS, make_sdesc(aK + ko, 16, 1024), make_sdesc(q_ + ko, 16, 1024), idSS, kk > 0);
+        }
 #pragma unroll
-        for (int kk = 0; kk < DH / 16; ++kk)
-          mma_bf16_ss_w(tdP, make_sdesc(aV + kk * 32, 16, 1024), make_sdesc(do_ + kk * 32, 16, 1024), idSS, kk > 0);
+        for (int kk = 0; kk < DH / 16; ++kk) {
+          const uint32_t ko = (kk >> 2) * kTile + (kk & 3) * 32;
+          mma_bf16_ss_w(tdP, make_sdesc(aV + ko, 16, 1024), make_sdesc(do_ + ko, 16, 1024), idSS, kk > 0);
+        }
         mma_commit_w(st_full);
       };
       mbar_wait(kv_full, 0);
       issue_S(0);
       for (int t = 0; t < nsteps; ++t) {
-        const int s = t & 1;
-        const uint32_t q_ = aQ + s * kTile, do_ = adO + s * kTile;
-        if (t + 1 < nsteps) issue_S(t + 1);
+        const int s = t & 1, qs = t % QS;
+        const uint32_t q_ = aQ + qs * kTQ, do_ = adO + qs * kTQ;
+        // with a single Q / dO stage, S(t+1) needs this step's dV / dK MMAs to have read Q(t) / dO(t)
+        if (QS == 2 && t + 1 < nsteps) issue_S(t + 1);
         mbar_wait(pds_full, t & 1);
         tc_fence_after();
 #pragma unroll
@@ -533,15 +585,18 @@ __global__ void __launch_bounds__(320, 1)
           mma_bf16_ss_w(tdV, a_p, make_sdesc(do_ + kk * 2048, kTile, 1024), idKM, (t > 0 || kk > 0));
           mma_bf16_ss_w(tdK, a_ds, make_sdesc(q_ + kk * 2048, kTile, 1024), idKM, (t > 0 || kk > 0));
         }
-        mbar_wait(&dq_empty[s], ((t >> 1) & 1) ^ 1);
-        tc_fence_after();
+        if constexpr (DQ) {
+          mbar_wait(&dq_empty[s], ((t >> 1) & 1) ^ 1);
+          tc_fence_after();
 #pragma unroll
-        for (int kk = 0; kk < BKV / 16; ++kk)
-          mma_bf16_ss_w(tdQ + s * DH, make_sdesc(adS + kk * 2048, kTile, 1024), make_sdesc(aK + kk * 2048, kTile, 1024),
-                      idMM, kk > 0);
-        mma_commit_w(&qd_empty[s]);
+          for (int kk = 0; kk < BKV / 16; ++kk)
+            mma_bf16_ss_w(tdQ + s * DH, make_sdesc(adS + kk * 2048, kTile, 1024),
+                          make_sdesc(aK + kk * 2048, kTile, 1024), idMM, kk > 0);
+        }
+        mma_commit_w(&qd_empty[qs]);
         mma_commit_w(pds_empty);
-        mma_commit_w(&dq_full[s]);
+        if constexpr (DQ) mma_commit_w(&dq_full[s]);
+        if (QS == 1 && t + 1 < nsteps) issue_S(t + 1);
       }
       mma_commit_w(done);
     }
@@ -557,6 +612,7 @@ __global__ void __launch_bounds__(320, 1)
     // through a private 4 KB staging tile and its own TMA add-reduce (no CTA-wide sync)
     uint8_t* mystage = sdQ + (warp - 2) * 4096;
     auto drain_dq = [&](int t) {
+      if constexpr (!DQ) return;
       const int h = kvh * G + t / nq, i = kt + t % nq;
       mbar_wait(&dq_full[t & 1], (t >> 1) & 1);
       tc_fence_after();
@@ -638,34 +694,253 @@ __global__ void __launch_bounds__(320, 1)
 #else
     if (nsteps > 0) { mbar_wait(&dq_full[(nsteps - 1) & 1], ((nsteps - 1) >> 1) & 1); if (lane == 0) mbar_arrive(&dq_empty[(nsteps - 1) & 1]); }
 #endif
-    if (lane == 0) bulk_wait<0>();  // this warp's add-reduces are complete before smem is reused / freed
+    if (DQ && lane == 0) bulk_wait<0>();  // this warp's add-reduces are complete before smem is reused / freed
     __syncwarp();
-    // dK (scaled) and dV -> bf16 -> smem (Q stages are free) -> TMA store into dqkv
+    // dK (scaled) and dV -> bf16 -> smem (Q / dO stages are free) -> TMA store into dqkv
     mbar_wait(done, 0);
     tc_fence_after();
-    uint32_t kv[32], vv[32];
-    tmem_ld32(tdK + lrow + half * 32, kv);
-    tmem_ld32(tdV + lrow + half * 32, vv);
-    tmem_wait_ld();
+    uint8_t* sdK_out = sQ;
+    uint8_t* sdV_out = DQ ? sQ + kTile : sdO;
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      uint4 w, z;
-      w.x = pack_bf16x2(__uint_as_float(kv[8 * c + 0]) * p.scale, __uint_as_float(kv[8 * c + 1]) * p.scale);
-      w.y = pack_bf16x2(__uint_as_float(kv[8 * c + 2]) * p.scale, __uint_as_float(kv[8 * c + 3]) * p.scale);
-      w.z = pack_bf16x2(__uint_as_float(kv[8 * c + 4]) * p.scale, __uint_as_float(kv[8 * c + 5]) * p.scale);
-      w.w = pack_bf16x2(__uint_as_float(kv[8 * c + 6]) * p.scale, __uint_as_float(kv[8 * c + 7]) * p.scale);
-      z.x = pack_bf16x2(__uint_as_float(vv[8 * c + 0]), __uint_as_float(vv[8 * c + 1]));
-      z.y = pack_bf16x2(__uint_as_float(vv[8 * c + 2]), __uint_as_float(vv[8 * c + 3]));
-      z.z = pack_bf16x2(__uint_as_float(vv[8 * c + 4]), __uint_as_float(vv[8 * c + 5]));
-      z.w = pack_bf16x2(__uint_as_float(vv[8 * c + 6]), __uint_as_float(vv[8 * c + 7]));
-      *reinterpret_cast<uint4*>(sQ + swz(r, half * 4 + c)) = w;
-      *reinterpret_cast<uint4*>(sQ + kTile + swz(r, half * 4 + c)) = z;
+    for (int cc = 0; cc < DH / 64; ++cc) {  // this warp's half of the DH columns, 32 at a time
+      const int col0 = half * (DH / 2) + cc * 32;
+      uint32_t kv[32], vv[32];
+      tmem_ld32(tdK + lrow + col0, kv);
+      tmem_ld32(tdV + lrow + col0, vv);
+      tmem_wait_ld();
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint4 w, z;
+        w.x = pack_bf16x2(__uint_as_float(kv[8 * c + 0]) * p.scale, __uint_as_float(kv[8 * c + 1]) * p.scale);
+        w.y = pack_bf16x2(__uint_as_float(kv[8 * c + 2]) * p.scale, __uint_as_float(kv[8 * c + 3]) * p.scale);
+        w.z = pack_bf16x2(__uint_as_float(kv[8 * c + 4]) * p.scale, __uint_as_float(kv[8 * c + 5]) * p.scale);
+        w.w = pack_bf16x2(__uint_as_float(kv[8 * c + 6]) * p.scale, __uint_as_float(kv[8 * c + 7]) * p.scale);
+        z.x = pack_bf16x2(__uint_as_float(vv[8 * c + 0]), __uint_as_float(vv[8 * c + 1]));
+        z.y = pack_bf16x2(__uint_as_float(vv[8 * c + 2]), __uint_as_float(vv[8 * c + 3]));
+        z.z = pack_bf16x2(__uint_as_float(vv[8 * c + 4]), __uint_as_float(vv[8 * c + 5]));
+        z.w = pack_bf16x2(__uint_as_float(vv[8 * c + 6]), __uint_as_float(vv[8 * c + 7]));
+        const int chunk = col0 / 8 + c;  // 16-byte chunk of the row: atom chunk / 8, position chunk % 8
+        *reinterpret_cast<uint4*>(sdK_out + (chunk >> 3) * kTile + swz(r, chunk & 7)) = w;
+        *reinterpret_cast<uint4*>(sdV_out + (chunk >> 3) * kTile + swz(r, chunk & 7)) = z;
+      }
     }
     fence_proxy_async_smem();
     named_sync(1, 256);
     if (ct == 0) {
-      tma_store_2d(&tm_dkv, sQ, (p.Hq + kvh) * DH, krow0);
-      tma_store_2d(&tm_dkv, sQ + kTile, (p.Hq + p.Hkv + kvh) * DH, krow0);
+      for (int a = 0; a < NA; ++a) {
+        tma_store_2d(&tm_dkv, sdK_out + a * kTile, (p.Hq + kvh) * DH + a * 64, krow0);
+        tma_store_2d(&tm_dkv, sdV_out + a * kTile, (p.Hq + p.Hkv + kvh) * DH + a * 64, krow0);
+      }
+      bulk_commit();
+      bulk_wait<0>();
+    }
+    __syncwarp();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<512>(tbase);
+  }
+}
+
+// -------------------------------------------------------------------------------------
+// dQ for dh = 128: CTA = (batch, q head, 128-query tile), looping over the causal key
+// tiles j <= i. S = Q K_j^T and dP = dO V_j^T into TMEM, thread = query row:
+// dS = P (dP - D) -> bf16 -> smem, dQ += dS K_j (TMEM accumulator across the loop,
+// K_j as an MN-major operand) -> x scale -> bf16 -> TMA store into dqkv.
+// smem 224 KB: Q, dO (32 KB each), K / V 2 stages (128 KB), dS (32 KB).
+template <int DH>
+struct BwdQ {
+  static constexpr int kTileQ = BQ * DH * 2;
+  static constexpr int kSmem = 1024 + 2 * kTileQ + 2 * kStages * kTileQ + kPBuf + 256;
+  static_assert(kSmem <= 232448, "dQ tiles exceed shared memory");
+};
+
+template <int DH>
+__global__ void __launch_bounds__(320, 1)
+    attn_bwd_q_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
+                      const __grid_constant__ CUtensorMap tm_dqkv, Params p) {
+  constexpr int kTQ = BwdQ<DH>::kTileQ, NA = DH / 64;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sQ = align1024(smem_raw);
+  uint8_t* sdO = sQ + kTQ;
+  uint8_t* sK = sdO + kTQ;              // [kStages]
+  uint8_t* sV = sK + kStages * kTQ;     // [kStages]
+  uint8_t* sdS = sV + kStages * kTQ;    // dS [128 q][128 keys], two 64-key atoms
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sdS + kPBuf);
+  uint64_t* qd_full = bars;
+  uint64_t* k_full = bars + 1;          // [kStages]
+  uint64_t* v_full = k_full + kStages;  // [kStages]
+  uint64_t* kv_empty = v_full + kStages;
+  uint64_t* st_full = kv_empty + kStages;
+  uint64_t* st_empty = st_full + 1;
+  uint64_t* pds_full = st_empty + 1;
+  uint64_t* pds_empty = pds_full + 1;
+  uint64_t* done = pds_empty + 1;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(done + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nbh = p.B * p.Hq;
+  const int i = p.nqt - 1 - (int)(blockIdx.x / nbh);  // heaviest query tiles first
+  const int bh = blockIdx.x % nbh;
+  const int b = bh / p.Hq, h = bh % p.Hq;
+  const int kvh = h / (p.Hq / p.Hkv);
+  const int nkv = i + 1;
+  const int qrow0 = b * p.T + i * BQ;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tm_qkv);
+    tma_prefetch(&tm_do);
+    mbar_init(qd_full, 1);
+    for (int s = 0; s < kStages; ++s) { mbar_init(&k_full[s], 1); mbar_init(&v_full[s], 1); mbar_init(&kv_empty[s], 1); }
+    mbar_init(st_full, 1);
+    mbar_init(st_empty, 8);
+    mbar_init(pds_full, 8);
+    mbar_init(pds_empty, 1);
+    mbar_init(done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tslot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tslot;
+  const uint32_t tS = tbase, tdP = tbase + 128, tdQ = tbase + 256;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(qd_full, 2 * kTQ);
+      for (int a = 0; a < NA; ++a) {
+        tma_load_2d(sQ + a * kTile, &tm_qkv, qd_full, h * DH + a * 64, qrow0);
+        tma_load_2d(sdO + a * kTile, &tm_do, qd_full, h * DH + a * 64, qrow0);
+      }
+      for (int j = 0; j < nkv; ++j) {
+        const int s = j % kStages;
+        mbar_wait(&kv_empty[s], ((j / kStages) & 1) ^ 1);
+        const int r = b * p.T + j * BKV;
+        mbar_arrive_expect_tx(&k_full[s], kTQ);
+        for (int a = 0; a < NA; ++a)
+          tma_load_2d(sK + s * kTQ + a * kTile, &tm_qkv, &k_full[s], (p.Hq + kvh) * DH + a * 64, r);
+        mbar_arrive_expect_tx(&v_full[s], kTQ);
+        for (int a = 0; a < NA; ++a)
+          tma_load_2d(sV + s * kTQ + a * kTile, &tm_qkv, &v_full[s], (p.Hq + p.Hkv + kvh) * DH + a * 64, r);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    {
+      constexpr uint32_t idSS = make_idesc_bf16(BQ, BKV, false, false);  // S, dP
+      constexpr uint32_t idQ = make_idesc_bf16(BQ, DH, false, true);     // dQ += dS K (K MN-major)
+      const uint32_t aQ = smem_u32(sQ), adO = smem_u32(sdO), aK = smem_u32(sK), aV = smem_u32(sV);
+      const uint32_t adS = smem_u32(sdS);
+      auto issue_S = [&](int j) {
+        const int s = j % kStages;
+        mbar_wait(&k_full[s], (j / kStages) & 1);
+        mbar_wait(&v_full[s], (j / kStages) & 1);
+        if (j > 0) mbar_wait(st_empty, (j - 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < DH / 16; ++kk) {
+          const uint32_t ko = (kk >> 2) * kTile + (kk & 3) * 32;
+          mma_bf16_ss_w(tS, make_sdesc(aQ + ko, 16, 1024), make_sdesc(aK + s * kTQ + ko, 16, 1024), idSS, kk > 0);
+        }
+#pragma unroll
+        for (int kk = 0; kk < DH / 16; ++kk) {
+          const uint32_t ko = (kk >> 2) * kTile + (kk & 3) * 32;
+          mma_bf16_ss_w(tdP, make_sdesc(adO + ko, 16, 1024), make_sdesc(aV + s * kTQ + ko, 16, 1024), idSS,
+                        kk > 0);
+        }
+        mma_commit_w(st_full);
+      };
+      mbar_wait(qd_full, 0);
+      issue_S(0);
+      for (int j = 0; j < nkv; ++j) {
+        const int s = j % kStages;
+        if (j + 1 < nkv) issue_S(j + 1);
+        mbar_wait(pds_full, j & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < BKV / 16; ++kk)
+          mma_bf16_ss_w(tdQ, make_sdesc(adS + (kk >> 2) * kTile + (kk & 3) * 32, 16, 1024),
+                        make_sdesc(aK + s * kTQ + kk * 2048, kTile, 1024), idQ, (j > 0 || kk > 0) ? 1u : 0u);
+        mma_commit_w(pds_empty);
+        mma_commit_w(&kv_empty[s]);
+      }
+      mma_commit_w(done);
+    }
+    __syncwarp();
+  } else {
+    const int ct = threadIdx.x - 64;
+    const int q4 = warp & 3;
+    const int half = (warp - 2) >> 2;  // key columns half*64 .. +63
+    const int r = q4 * 32 + lane;      // query row
+    const uint32_t lrow = (uint32_t)(q4 * 32) << 16;
+    const size_t roff = ((size_t)b * p.Hq + h) * p.T + (size_t)i * BQ + r;
+    const float lse2 = p.lse[roff] * kLog2e;
+    const float dd = p.dsum[roff];
+    const float sl2 = p.scale_log2;
+    for (int j = 0; j < nkv; ++j) {
+      const bool diag = (j == i);
+      mbar_wait(st_full, j & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int qq = 0; qq < 2; ++qq) {
+        uint32_t sv[32], dv[32];
+        tmem_ld32(tS + lrow + half * 64 + qq * 32, sv);
+        tmem_ld32(tdP + lrow + half * 64 + qq * 32, dv);
+        tmem_wait_ld();
+        if (qq == 1) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(st_empty);
+        }
+        const int k0 = half * 64 + qq * 32;
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          float pv = ex2(fmaf(__uint_as_float(sv[e]), sl2, -lse2));
+          if (diag && k0 + e > r) pv = 0.f;  // key after query: masked
+          dv[e] = __float_as_uint(pv * (__uint_as_float(dv[e]) - dd));
+        }
+        if (qq == 0 && j > 0) mbar_wait(pds_empty, (j - 1) & 1);
+#pragma unroll
+        for (int k8 = 0; k8 < 4; ++k8) {
+          uint4 z;
+          z.x = pack_bf16x2(__uint_as_float(dv[8 * k8 + 0]), __uint_as_float(dv[8 * k8 + 1]));
+          z.y = pack_bf16x2(__uint_as_float(dv[8 * k8 + 2]), __uint_as_float(dv[8 * k8 + 3]));
+          z.z = pack_bf16x2(__uint_as_float(dv[8 * k8 + 4]), __uint_as_float(dv[8 * k8 + 5]));
+          z.w = pack_bf16x2(__uint_as_float(dv[8 * k8 + 6]), __uint_as_float(dv[8 * k8 + 7]));
+          *reinterpret_cast<uint4*>(sdS + half * kTile + swz(r, qq * 4 + k8)) = z;
+        }
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(pds_full);
+    }
+    // dQ (TMEM) * scale -> bf16 -> smem (Q / dO are free once every MMA retired) -> TMA store
+    mbar_wait(done, 0);
+    tc_fence_after();
+#pragma unroll
+    for (int cc = 0; cc < DH / 64; ++cc) {
+      const int col0 = half * (DH / 2) + cc * 32;
+      uint32_t qv[32];
+      tmem_ld32(tdQ + lrow + col0, qv);
+      tmem_wait_ld();
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint4 w;
+        w.x = pack_bf16x2(__uint_as_float(qv[8 * c + 0]) * p.scale, __uint_as_float(qv[8 * c + 1]) * p.scale);
+        w.y = pack_bf16x2(__uint_as_float(qv[8 * c + 2]) * p.scale, __uint_as_float(qv[8 * c + 3]) * p.scale);
+        w.z = pack_bf16x2(__uint_as_float(qv[8 * c + 4]) * p.scale, __uint_as_float(qv[8 * c + 5]) * p.scale);
+        w.w = pack_bf16x2(__uint_as_float(qv[8 * c + 6]) * p.scale, __uint_as_float(qv[8 * c + 7]) * p.scale);
+        const int chunk = col0 / 8 + c;
+        *reinterpret_cast<uint4*>(sQ + (chunk >> 3) * kTile + swz(r, chunk & 7)) = w;
+      }
+    }
+    fence_proxy_async_smem();
+    named_sync(1, 256);
+    if (ct == 0) {
+      for (int a = 0; a < NA; ++a) tma_store_2d(&tm_dqkv, sQ + a * kTile, h * DH + a * 64, qrow0);
       bulk_commit();
       bulk_wait<0>();
     }
@@ -684,27 +959,82 @@ __global__ void __launch_bounds__(320, 1)
 
 using namespace b2s;
 
-extern "C" int b2s_attn_fwd(const void* d_qkv, void* d_o, float* d_lse, int B, int T, int Hq, int Hkv, int dh,
-                            b2s_stream_t stream) {
-  B2S_REQUIRE(dh == attn::DH, B2S_EUNSUPPORTED, "attention: head dim %d not implemented (64 only)", dh);
-  B2S_REQUIRE(T % attn::BQ == 0 && T > 0, B2S_EUNSUPPORTED, "attention: T must be a multiple of 128");
-  B2S_REQUIRE(Hkv > 0 && Hq % Hkv == 0, B2S_EINVAL, "attention: Hq must be a multiple of Hkv");
-  const int ldq = (Hq + 2 * Hkv) * dh;
+namespace {
+template <int DH>
+int attn_fwd_dh(const void* d_qkv, void* d_o, float* d_lse, int B, int T, int Hq, int Hkv, cudaStream_t st) {
+  using C = attn::Fwd<DH>;
+  const int ldq = (Hq + 2 * Hkv) * DH;
   CUtensorMap tq, to;
   int rc = encode_tma_2d(&tq, d_qkv, 2, (uint64_t)ldq, (uint64_t)B * T, (uint64_t)ldq * 2, 64, 128, 128);
   if (rc) return rc;
-  rc = encode_tma_2d(&to, d_o, 2, (uint64_t)Hq * dh, (uint64_t)B * T, (uint64_t)Hq * dh * 2, 64, 128, 128);
+  rc = encode_tma_2d(&to, d_o, 2, (uint64_t)Hq * DH, (uint64_t)B * T, (uint64_t)Hq * DH * 2, 64, 128, 128);
   if (rc) return rc;
-  attn::Params p{B, T, Hq, Hkv, T / attn::BQ, attn::kLog2e / sqrtf((float)dh), 1.f / sqrtf((float)dh), d_lse,
+  attn::Params p{B, T, Hq, Hkv, T / attn::BQ, attn::kLog2e / sqrtf((float)DH), 1.f / sqrtf((float)DH), d_lse,
                  nullptr};
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(attn::attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, attn::kFwdSmem);
+    cudaFuncSetAttribute(attn::attn_fwd_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
     attr = true;
   }
-  const unsigned grid = (unsigned)(B * Hq * ((T / attn::BQ + 1) / 2));
-  attn::attn_fwd_kernel<<<grid, attn::kFwdThreads, attn::kFwdSmem, (cudaStream_t)stream>>>(tq, to, p);
+  const unsigned grid = (unsigned)(B * Hq * ((T / attn::BQ + C::TILES - 1) / C::TILES));
+  attn::attn_fwd_kernel<DH><<<grid, C::kThreads, C::kSmem, st>>>(tq, to, p);
   return check_launch("attn_fwd");
+}
+
+template <int DH>
+int attn_bwd_dh(const void* d_qkv, const void* d_o, const void* d_do, const float* d_lse, void* d_dqkv,
+                float* d_work, int B, int T, int Hq, int Hkv, cudaStream_t st) {
+  using C = attn::Bwd<DH>;
+  const int ldq = (Hq + 2 * Hkv) * DH;
+  const int64_t M = (int64_t)B * T;
+  float* dq_acc = C::DQ ? d_work : nullptr;
+  float* dsum = d_work + M * Hq * DH;
+  attn::attn_bwd_prep_kernel<DH><<<kNumSMs * 8, 256, 0, st>>>((const __nv_bfloat16*)d_o,
+                                                              (const __nv_bfloat16*)d_do, dsum, dq_acc, B, T, Hq);
+  int rc = check_launch("attn_bwd_prep");
+  if (rc) return rc;
+  CUtensorMap tq, tdo, tdq, tdkv;
+  rc = encode_tma_2d(&tq, d_qkv, 2, (uint64_t)ldq, (uint64_t)M, (uint64_t)ldq * 2, 64, 128, 128);
+  if (rc) return rc;
+  rc = encode_tma_2d(&tdo, d_do, 2, (uint64_t)Hq * DH, (uint64_t)M, (uint64_t)Hq * DH * 2, 64, 128, 128);
+  if (rc) return rc;
+  rc = encode_tma_2d(&tdq, d_work, 4, (uint64_t)Hq * DH, (uint64_t)M, (uint64_t)Hq * DH * 4, 32, 32, 128);
+  if (rc) return rc;
+  rc = encode_tma_2d(&tdkv, d_dqkv, 2, (uint64_t)ldq, (uint64_t)M, (uint64_t)ldq * 2, 64, 128, 128);
+  if (rc) return rc;
+  attn::Params p{B, T, Hq, Hkv, T / attn::BQ, attn::kLog2e / sqrtf((float)DH), 1.f / sqrtf((float)DH),
+                 const_cast<float*>(d_lse), dsum};
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(attn::attn_bwd_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+    if constexpr (!C::DQ)
+      cudaFuncSetAttribute(attn::attn_bwd_q_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           attn::BwdQ<DH>::kSmem);
+    attr = true;
+  }
+  const unsigned grid = (unsigned)(B * Hkv * (T / attn::BQ));
+  attn::attn_bwd_kernel<DH><<<grid, attn::kBwdThreads, C::kSmem, st>>>(tq, tdo, tdq, tdkv, p);
+  rc = check_launch("attn_bwd");
+  if (rc) return rc;
+  if constexpr (C::DQ) {
+    attn::attn_bwd_dq_kernel<<<kNumSMs * 8, 256, 0, st>>>(dq_acc, (__nv_bfloat16*)d_dqkv, M, Hq, ldq);
+    return check_launch("attn_bwd_dq");
+  } else {
+    attn::attn_bwd_q_kernel<DH><<<(unsigned)(B * Hq * (T / attn::BQ)), 320, attn::BwdQ<DH>::kSmem, st>>>(tq, tdo,
+                                                                                                       tdkv, p);
+    return check_launch("attn_bwd_q");
+  }
+}
+}  // namespace
+
+extern "C" int b2s_attn_fwd(const void* d_qkv, void* d_o, float* d_lse, int B, int T, int Hq, int Hkv, int dh,
+                            b2s_stream_t stream) {
+  B2S_REQUIRE(dh == 64 || dh == 128, B2S_EUNSUPPORTED, "attention: head dim %d not implemented (64, 128)", dh);
+  B2S_REQUIRE(T % attn::BQ == 0 && T > 0, B2S_EUNSUPPORTED, "attention: T must be a multiple of 128");
+  B2S_REQUIRE(Hkv > 0 && Hq % Hkv == 0, B2S_EINVAL, "attention: Hq must be a multiple of Hkv");
+  cudaStream_t st = (cudaStream_t)stream;
+  return dh == 64 ? attn_fwd_dh<64>(d_qkv, d_o, d_lse, B, T, Hq, Hkv, st)
+                  : attn_fwd_dh<128>(d_qkv, d_o, d_lse, B, T, Hq, Hkv, st);
 }
 
 extern "C" int64_t b2s_attn_bwd_work_floats(int B, int T, int Hq, int dh) {
@@ -713,38 +1043,10 @@ extern "C" int64_t b2s_attn_bwd_work_floats(int B, int T, int Hq, int dh) {
 
 extern "C" int b2s_attn_bwd(const void* d_qkv, const void* d_o, const void* d_do, const float* d_lse, void* d_dqkv,
                             float* d_work, int B, int T, int Hq, int Hkv, int dh, b2s_stream_t stream) {
-  B2S_REQUIRE(dh == attn::DH, B2S_EUNSUPPORTED, "attention: head dim %d not implemented (64 only)", dh);
+  B2S_REQUIRE(dh == 64 || dh == 128, B2S_EUNSUPPORTED, "attention: head dim %d not implemented (64, 128)", dh);
   B2S_REQUIRE(T % attn::BQ == 0 && T > 0, B2S_EUNSUPPORTED, "attention: T must be a multiple of 128");
   B2S_REQUIRE(Hkv > 0 && Hq % Hkv == 0, B2S_EINVAL, "attention: Hq must be a multiple of Hkv");
   cudaStream_t st = (cudaStream_t)stream;
-  const int ldq = (Hq + 2 * Hkv) * dh;
-  const int64_t M = (int64_t)B * T;
-  float* dq_acc = d_work;
-  float* dsum = d_work + M * Hq * dh;
-  attn::attn_bwd_prep_kernel<<<kNumSMs * 8, 256, 0, st>>>((const __nv_bfloat16*)d_o, (const __nv_bfloat16*)d_do,
-                                                          dsum, dq_acc, B, T, Hq);
-  int rc = check_launch("attn_bwd_prep");
-  if (rc) return rc;
-  CUtensorMap tq, tdo, tdq, tdkv;
-  rc = encode_tma_2d(&tq, d_qkv, 2, (uint64_t)ldq, (uint64_t)M, (uint64_t)ldq * 2, 64, 128, 128);
-  if (rc) return rc;
-  rc = encode_tma_2d(&tdo, d_do, 2, (uint64_t)Hq * dh, (uint64_t)M, (uint64_t)Hq * dh * 2, 64, 128, 128);
-  if (rc) return rc;
-  rc = encode_tma_2d(&tdq, dq_acc, 4, (uint64_t)Hq * dh, (uint64_t)M, (uint64_t)Hq * dh * 4, 32, 32, 128);
-  if (rc) return rc;
-  rc = encode_tma_2d(&tdkv, d_dqkv, 2, (uint64_t)ldq, (uint64_t)M, (uint64_t)ldq * 2, 64, 128, 128);
-  if (rc) return rc;
-  attn::Params p{B, T, Hq, Hkv, T / attn::BQ, attn::kLog2e / sqrtf((float)dh), 1.f / sqrtf((float)dh),
-                 const_cast<float*>(d_lse), dsum};
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(attn::attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, attn::kBwdSmem);
-    attr = true;
-  }
-  const unsigned grid = (unsigned)(B * Hkv * (T / attn::BQ));
-  attn::attn_bwd_kernel<<<grid, attn::kBwdThreads, attn::kBwdSmem, st>>>(tq, tdo, tdq, tdkv, p);
-  rc = check_launch("attn_bwd");
-  if (rc) return rc;
-  attn::attn_bwd_dq_kernel<<<kNumSMs * 8, 256, 0, st>>>(dq_acc, (__nv_bfloat16*)d_dqkv, M, Hq, ldq);
-  return check_launch("attn_bwd_dq");
+  return dh == 64 ? attn_bwd_dh<64>(d_qkv, d_o, d_do, d_lse, d_dqkv, d_work, B, T, Hq, Hkv, st)
+                  : attn_bwd_dh<128>(d_qkv, d_o, d_do, d_lse, d_dqkv, d_work, B, T, Hq, Hkv, st);
 }

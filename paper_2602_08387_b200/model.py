@@ -91,6 +91,7 @@ PRESETS = {
     # GPU parity configs (head dim 64, the attention kernel's tile): tiny GPT-2 / tiny Llama
     "tiny-gpt2-dh64": ModelConfig("gpt2", 2, 256, 4, 4, 1024, 4096, 256),
     "tiny-llama": ModelConfig("llama", 2, 256, 4, 2, 512, 4096, 256),
+    "tiny-llama-dh128": ModelConfig("llama", 2, 256, 2, 1, 512, 4096, 256),  # the 8B's head dim / GQA path
     # configs[1]
     "gpt2-124m": ModelConfig("gpt2", 12, 768, 12, 12, 3072, 50257, 2048),
     # configs[2]: Llama-3.2-1B-like (tied head, GQA 32/8, dh 64)
@@ -266,8 +267,8 @@ class DecoderLM(torch.nn.Module):
         super().__init__()
         if precision not in PRECISIONS:
             raise ValueError(f"precision must be one of {sorted(PRECISIONS)}, got {precision!r}")
-        if precision == "bf16" and cfg.head_dim != 64:
-            raise ValueError(f"bf16 attention kernel implements head dim 64 (got {cfg.head_dim}); "
+        if precision == "bf16" and cfg.head_dim not in (64, 128):
+            raise ValueError(f"bf16 attention kernels implement head dims 64 and 128 (got {cfg.head_dim}); "
                              "use precision='fp32' for other head dims")
         self.cfg = cfg
         self.precision = precision

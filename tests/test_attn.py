@@ -1,4 +1,4 @@
-"""tcgen05 causal attention vs a plain PyTorch fp32 reference (same bf16 inputs)."""
+"""tcgen05 causal attention (head dims 64 and 128) vs a plain PyTorch fp32 reference (same bf16 inputs)."""
 
 import math
 
@@ -21,11 +21,14 @@ def _ref(qkv, B, T, Hq, Hkv, dh):
     return o.transpose(1, 2).reshape(B * T, Hq * dh), lse
 
 
-@pytest.mark.parametrize("B,T,Hq,Hkv", [(1, 128, 1, 1), (2, 256, 4, 2), (1, 512, 3, 3), (2, 384, 8, 2)])
-def test_attn_fwd(cuda, B, T, Hq, Hkv):
+CASES = [(1, 128, 1, 1), (2, 256, 4, 2), (1, 512, 3, 3), (2, 384, 8, 2)]
+
+
+@pytest.mark.parametrize("dh", [64, 128])
+@pytest.mark.parametrize("B,T,Hq,Hkv", CASES)
+def test_attn_fwd(cuda, B, T, Hq, Hkv, dh):
     from paper_2602_08387_b200 import ops
 
-    dh = 64
     torch.manual_seed(B * T + Hq)
     qkv = torch.randn(B * T, (Hq + 2 * Hkv) * dh, device=cuda).bfloat16()
     o, lse = ops.attn_fwd(qkv, B, T, Hq, Hkv, dh)
@@ -34,11 +37,11 @@ def test_attn_fwd(cuda, B, T, Hq, Hkv):
     torch.testing.assert_close(o.float(), ro, rtol=2e-2, atol=2e-2)
 
 
-@pytest.mark.parametrize("B,T,Hq,Hkv", [(1, 128, 1, 1), (2, 256, 4, 2), (1, 512, 3, 3), (2, 384, 8, 2)])
-def test_attn_bwd(cuda, B, T, Hq, Hkv):
+@pytest.mark.parametrize("dh", [64, 128])
+@pytest.mark.parametrize("B,T,Hq,Hkv", CASES)
+def test_attn_bwd(cuda, B, T, Hq, Hkv, dh):
     from paper_2602_08387_b200 import ops
 
-    dh = 64
     torch.manual_seed(B * T + Hq + 1)
     qkv = torch.randn(B * T, (Hq + 2 * Hkv) * dh, device=cuda).bfloat16()
     o, lse = ops.attn_fwd(qkv, B, T, Hq, Hkv, dh)

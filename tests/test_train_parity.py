@@ -35,7 +35,7 @@ def _oracle_batch(path, ids, T):
     return torch.from_numpy(x), torch.from_numpy(y)
 
 
-@pytest.mark.parametrize("preset", ["tiny-gpt2-dh64", "tiny-llama"])
+@pytest.mark.parametrize("preset", ["tiny-gpt2-dh64", "tiny-llama", "tiny-llama-dh128"])
 def test_first_step_grads_match_oracle(cuda, tmp_path, preset):
     from paper_2602_08387_b200.model import init_params
 
@@ -60,7 +60,7 @@ def test_first_step_grads_match_oracle(cuda, tmp_path, preset):
         assert cos > 0.995 and rel < 0.08, (k, float(cos), float(rel))
 
 
-@pytest.mark.parametrize("preset", ["tiny-gpt2-dh64", "tiny-llama"])
+@pytest.mark.parametrize("preset", ["tiny-gpt2-dh64", "tiny-llama", "tiny-llama-dh128"])
 def test_loss_curve_matches_oracle(cuda, tmp_path, preset):
     """North star: the bf16 loss curve stays within 2% of the fp32 reference over the first 200 steps."""
     from paper_2602_08387_b200.model import init_params

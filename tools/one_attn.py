@@ -1,6 +1,6 @@
 """Run causal attention fwd(+bwd) once at a model shape (for ncu captures).
 
-    python tools/one_attn.py B T Hq Hkv [bwd]
+    [DH=128] python tools/one_attn.py B T Hq Hkv [bwd]
 """
 import os
 import sys
@@ -12,7 +12,7 @@ from paper_2602_08387_b200 import ops  # noqa: E402
 
 B, T, Hq, Hkv = (int(x) for x in sys.argv[1:5])
 bwd = len(sys.argv) > 5
-dh = 64
+dh = int(os.environ.get("DH", "64"))
 qkv = torch.randn(B * T, (Hq + 2 * Hkv) * dh, device="cuda").bfloat16()
 for _ in range(2):
     o, lse = ops.attn_fwd(qkv, B, T, Hq, Hkv, dh)
