@@ -137,7 +137,7 @@ def run_ours(args):
     path = None
     if rank == 0:
         path = _data_path(cfg, n_tokens)
-    tr = SPMDTrainer(DecoderLM(cfg), AdamWConfig(), None, steps=0, seed=0,
+    tr = SPMDTrainer(DecoderLM(cfg, activation_checkpointing=args.ac), AdamWConfig(), None, steps=0, seed=0,
                      blocks_per_unit=args.blocks_per_unit, init_device="cuda")
     # distributed init happens in setup(); make sure the data file exists first
     from paper_2602_08387_b200.trainer import init_distributed
@@ -229,6 +229,7 @@ def run_ours(args):
         "config": {"workload": f"{args.config} FSDP training step (fwd+bwd+AdamW), seq {T}, "
                                f"{B} seqs/GPU", "model": args.config, "global_batch": world * B, "seq_len": T,
                    "parallelism": f"fsdp{world}", "blocks_per_unit": args.blocks_per_unit,
+                   "activation_checkpointing": args.ac,
                    "l2": "working set (weights + activations) >> 126 MB L2; no explicit flush"},
         "tokens_per_sec_per_gpu": round(per_gpu, 1),
         "mfu": round(mfu, 4),
@@ -317,6 +318,7 @@ def main():
     ap.add_argument("--seq", type=int, default=2048)
     ap.add_argument("--blocks-per-unit", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    ap.add_argument("--ac", action="store_true", help="per-block activation checkpointing (the 8B config)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3

@@ -69,7 +69,7 @@ def _dataloader(dataset, batch_size, seq_len, sampler=None, feed="resident"):
 def _model(arch):
     def build(preset=None, n_layer=None, d_model=None, n_head=None, n_kv_head=None, d_ff=None, vocab_size=None,
               max_seq_len=None, tie_embeddings=None, norm_eps=None, rope_theta=None, init_std=None,
-              precision="bf16"):
+              precision="bf16", activation_checkpointing=False):
         from dataclasses import replace
 
         from .model import PRESETS, DecoderLM, ModelConfig
@@ -87,7 +87,7 @@ def _model(arch):
             if arch == "gpt2":
                 explicit.setdefault("n_kv_head", explicit.get("n_head"))
             cfg = ModelConfig(arch=arch, **explicit)
-        return DecoderLM(cfg, precision)
+        return DecoderLM(cfg, precision, activation_checkpointing)
 
     return build
 
@@ -98,7 +98,8 @@ _MODEL_PARAMS = (P("preset", "string", required=False), P("n_layer", "int", requ
                  P("vocab_size", "int", required=False), P("max_seq_len", "int", required=False),
                  P("tie_embeddings", "bool", required=False), P("norm_eps", "float", required=False),
                  P("rope_theta", "float", required=False), P("init_std", "float", required=False),
-                 P("precision", "string", required=False, default="bf16"))
+                 P("precision", "string", required=False, default="bf16"),
+                 P("activation_checkpointing", "bool", required=False, default=False))
 
 
 def _optimizer(lr=3e-4, beta1=0.9, beta2=0.95, eps=1e-8, weight_decay=0.1, grad_clip=1.0, warmup_steps=10):

@@ -222,28 +222,61 @@ def rope_tables(cfg: ModelConfig, T: int, device):
     return ang.cos().float().contiguous().to(device), ang.sin().float().contiguous().to(device)
 
 
-class _Acts:
-    """Activation buffers for one (B, T): saved forward tensors + backward scratch."""
+class _Slot:
+    """The forward buffers of one transformer block (see _Acts)."""
 
-    def __init__(self, cfg: ModelConfig, B: int, T: int, device, act_dtype=torch.bfloat16):
+    __slots__ = ("xa", "xb", "xn", "ln_a", "mean_a", "rstd_a", "ln_b", "mean_b", "rstd_b", "qkv", "o", "lse",
+                 "hpre", "gu", "h")
+
+
+class _Acts:
+    """Activation buffers for one (B, T): saved forward tensors + backward scratch.
+
+    Residual stream (fp32): block i reads xa, forwards it (in the norm kernel)
+    into xb to which the attention output is added, then forwards xb into xn
+    (= the next block's xa) to which the MLP output is added.
+
+    Without checkpointing every block owns its slot (all saved). With
+    ``checkpoint`` only the block inputs xa (L + 1 fp32 [M, d] buffers) are
+    kept; every other per-block buffer is one shared slot that the backward
+    refills by recomputing the block's forward.
+    """
+
+    def __init__(self, cfg: ModelConfig, B: int, T: int, device, act_dtype=torch.bfloat16, checkpoint=False):
         M, d, f, L = B * T, cfg.d_model, cfg.d_ff, cfg.n_layer
         bf, f32 = act_dtype, torch.float32
         e = lambda *s, dt=bf: torch.empty(*s, device=device, dtype=dt)  # noqa: E731
         self.B, self.T, self.M = B, T, M
-        # residual stream: xs[2i] enters block i's attention, xs[2i+1] its MLP, xs[2L] the head
-        self.xs = [e(M, d, dt=f32) for _ in range(2 * L + 1)]
-        self.ln = [e(M, d) for _ in range(2 * L + 1)]
-        self.mean = [e(M, dt=f32) for _ in range(2 * L + 1)]
-        self.rstd = [e(M, dt=f32) for _ in range(2 * L + 1)]
-        self.qkv = [e(M, cfg.qkv_dim) for _ in range(L)]
-        self.o = [e(M, cfg.n_head * cfg.head_dim) for _ in range(L)]
-        self.lse = [e(B, cfg.n_head, T, dt=f32) for _ in range(L)]
-        if cfg.arch == "gpt2":
-            self.hpre = [e(M, f) for _ in range(L)]
-            self.h = [e(M, f) for _ in range(L)]
+        self.checkpoint = checkpoint
+        self.xin = [e(M, d, dt=f32) for _ in range(L + 1)]  # block inputs; xin[L] enters the head
+
+        def slot(i, xb=None):
+            sl = _Slot()
+            sl.xa, sl.xn = self.xin[i], self.xin[i + 1]
+            sl.xb = e(M, d, dt=f32) if xb is None else xb
+            sl.ln_a, sl.ln_b = e(M, d), e(M, d)
+            sl.mean_a, sl.rstd_a, sl.mean_b, sl.rstd_b = (e(M, dt=f32) for _ in range(4))
+            sl.qkv = e(M, cfg.qkv_dim)
+            sl.o = e(M, cfg.n_head * cfg.head_dim)
+            sl.lse = e(B, cfg.n_head, T, dt=f32)
+            sl.hpre = e(M, f) if cfg.arch == "gpt2" else None
+            sl.gu = e(M, 2 * f) if cfg.arch == "llama" else None
+            sl.h = e(M, f)
+            return sl
+
+        if checkpoint:
+            shared = slot(0)
+            self.slots = []
+            for i in range(L):
+                sl = _Slot()
+                for k in _Slot.__slots__:
+                    setattr(sl, k, getattr(shared, k))
+                sl.xa, sl.xn = self.xin[i], self.xin[i + 1]
+                self.slots.append(sl)
         else:
-            self.gu = [e(M, 2 * f) for _ in range(L)]
-            self.h = [e(M, f) for _ in range(L)]
+            self.slots = [slot(i) for i in range(L)]
+        self.ln_f = e(M, d)
+        self.mean_f, self.rstd_f = e(M, dt=f32), e(M, dt=f32)
         self.logits = e(M, cfg.padded_vocab)
         self.loss_rows = e(M, dt=f32)
         self.loss = e(1, dt=f32)
@@ -263,7 +296,7 @@ class _Acts:
 class DecoderLM(torch.nn.Module):
     """Decoder-only LM whose parameters live in FSDP flat units (see fsdp.FlatParams)."""
 
-    def __init__(self, cfg: ModelConfig, precision: str = "bf16"):
+    def __init__(self, cfg: ModelConfig, precision: str = "bf16", activation_checkpointing: bool = False):
         super().__init__()
         if precision not in PRECISIONS:
             raise ValueError(f"precision must be one of {sorted(PRECISIONS)}, got {precision!r}")
@@ -273,6 +306,7 @@ class DecoderLM(torch.nn.Module):
         self.cfg = cfg
         self.precision = precision
         self.dtype = PRECISIONS[precision]
+        self.activation_checkpointing = bool(activation_checkpointing)
         self.units = unit_specs(cfg)
         self._acts = {}
         self._rope = {}
@@ -285,7 +319,7 @@ class DecoderLM(torch.nn.Module):
         key = (B, T)
         if key not in self._acts:
             self._acts.clear()
-            self._acts[key] = _Acts(self.cfg, B, T, device, self.dtype)
+            self._acts[key] = _Acts(self.cfg, B, T, device, self.dtype, self.activation_checkpointing)
         return self._acts[key]
 
     def rope(self, T, device):
@@ -294,13 +328,48 @@ class DecoderLM(torch.nn.Module):
         return self._rope[T]
 
     # ------------------------------------------------------------------ step
+    def _block_forward(self, i, S, T, rope, with_output=True):
+        """Block i's forward over slot S; with_output=False skips the MLP output GEMM
+        (the checkpoint recompute needs every saved input, not the block output)."""
+        cfg, U = self.cfg, self.params.unit(i + 1)
+        M, d = S.xa.shape
+        B = M // T
+        H, Hkv, dh, eps = cfg.n_head, cfg.n_kv_head, cfg.head_dim, cfg.norm_eps
+        if cfg.arch == "gpt2":
+            ops.layernorm_fwd(S.xa, U.p("ln1_g"), U.p("ln1_b"), eps, S.ln_a, S.mean_a, S.rstd_a, x_copy=S.xb)
+            ops.linear(S.ln_a, U.p("qkv_w"), bias=U.p("qkv_b"), out=S.qkv)
+        else:
+            ops.rmsnorm_fwd(S.xa, U.p("attn_norm"), eps, S.ln_a, S.rstd_a, x_copy=S.xb)
+            ops.linear(S.ln_a, U.p("wqkv"), out=S.qkv)
+            ops.rope(S.qkv, T, H + Hkv, dh, *rope)
+        ops.attn_fwd(S.qkv, B, T, H, Hkv, dh, o=S.o, lse=S.lse)
+        # residual: xb (= copy of xa) += o @ Wo^T (+ bias)  (fp32 TMA add-reduce)
+        gpt2 = cfg.arch == "gpt2"
+        ops.gemm(S.o, U.p("proj_w" if gpt2 else "wo"), a_mn=False, b_mn=False, M=M, N=d, K=H * dh, out=S.xb,
+                 accumulate=True, bias=U.p("proj_b") if gpt2 else None)
+        xn = S.xn if with_output else None
+        if gpt2:
+            ops.layernorm_fwd(S.xb, U.p("ln2_g"), U.p("ln2_b"), eps, S.ln_b, S.mean_b, S.rstd_b, x_copy=xn)
+            ops.linear(S.ln_b, U.p("fc_w"), bias=U.p("fc_b"), out=S.h, act=1, aux=S.hpre)
+            if with_output:
+                ops.gemm(S.h, U.p("fc2_w"), a_mn=False, b_mn=False, M=M, N=d, K=cfg.d_ff, out=S.xn,
+                         accumulate=True, bias=U.p("fc2_b"))
+        else:
+            ops.rmsnorm_fwd(S.xb, U.p("mlp_norm"), eps, S.ln_b, S.rstd_b, x_copy=xn)
+            ops.linear(S.ln_b, U.p("w13"), out=S.gu)
+            ops.swiglu_fwd(S.gu, S.h)
+            if with_output:
+                ops.gemm(S.h, U.p("w2"), a_mn=False, b_mn=False, M=M, N=d, K=cfg.d_ff, out=S.xn, accumulate=True)
+
     def forward_backward(self, tokens, targets, hooks=None, compute_grad: bool = True):
         """One training forward + backward over int64 tokens/targets [B, T].
 
         Writes fp32 parameter gradients into the flat grad buffers (accumulated;
         the caller zeroes them) and returns the device scalar mean loss.
         ``hooks`` (fsdp.Engine) is told when each unit's parameters are needed
-        and when each unit's gradients are complete.
+        and when each unit's gradients are complete. With activation
+        checkpointing each block's forward is re-run (into the shared slot)
+        right before its backward.
         """
         cfg, P = self.cfg, self.params
         B, T = tokens.shape
@@ -315,50 +384,24 @@ class DecoderLM(torch.nn.Module):
         pre = (lambda u: hk.before_forward(u)) if hk else (lambda u: None)
         post = (lambda u: hk.after_backward(u)) if hk else (lambda u: None)
         eps = cfg.norm_eps
-        if not gpt2:
-            cos, sin = self.rope(T, dev)
+        rope = None if gpt2 else self.rope(T, dev)
 
         # ---------------- forward
         pre(0)
         E = P.unit(0)
-        ops.embedding_fwd(tok, E.p("wte"), E.p("wpe") if gpt2 else None, T, out=A.xs[0])
+        ops.embedding_fwd(tok, E.p("wte"), E.p("wpe") if gpt2 else None, T, out=A.xin[0])
         for i in range(L):
             pre(i + 1)
-            U = P.unit(i + 1)
-            a, b = 2 * i, 2 * i + 1
-            if gpt2:
-                ops.layernorm_fwd(A.xs[a], U.p("ln1_g"), U.p("ln1_b"), eps, A.ln[a], A.mean[a], A.rstd[a], x_copy=A.xs[b])
-                ops.linear(A.ln[a], U.p("qkv_w"), bias=U.p("qkv_b"), out=A.qkv[i])
-            else:
-                ops.rmsnorm_fwd(A.xs[a], U.p("attn_norm"), eps, A.ln[a], A.rstd[a], x_copy=A.xs[b])
-                ops.linear(A.ln[a], U.p("wqkv"), out=A.qkv[i])
-                ops.rope(A.qkv[i], T, H + Hkv, dh, cos, sin)
-            ops.attn_fwd(A.qkv[i], B, T, H, Hkv, dh, o=A.o[i], lse=A.lse[i])
-            # residual: xs[b] (= copy of xs[a]) += o @ Wo^T (+ bias)  (fp32 TMA add-reduce)
-            ops.gemm(A.o[i], U.p("proj_w" if gpt2 else "wo"), a_mn=False, b_mn=False, M=M, N=d, K=H * dh,
-                     out=A.xs[b], accumulate=True, bias=U.p("proj_b") if gpt2 else None)
-            nxt = b + 1
-            if gpt2:
-                ops.layernorm_fwd(A.xs[b], U.p("ln2_g"), U.p("ln2_b"), eps, A.ln[b], A.mean[b], A.rstd[b],
-                                  x_copy=A.xs[nxt])
-                ops.linear(A.ln[b], U.p("fc_w"), bias=U.p("fc_b"), out=A.h[i], act=1, aux=A.hpre[i])
-                ops.gemm(A.h[i], U.p("fc2_w"), a_mn=False, b_mn=False, M=M, N=d, K=cfg.d_ff, out=A.xs[nxt],
-                         accumulate=True, bias=U.p("fc2_b"))
-            else:
-                ops.rmsnorm_fwd(A.xs[b], U.p("mlp_norm"), eps, A.ln[b], A.rstd[b], x_copy=A.xs[nxt])
-                ops.linear(A.ln[b], U.p("w13"), out=A.gu[i])
-                ops.swiglu_fwd(A.gu[i], A.h[i])
-                ops.gemm(A.h[i], U.p("w2"), a_mn=False, b_mn=False, M=M, N=d, K=cfg.d_ff, out=A.xs[nxt],
-                         accumulate=True)
+            self._block_forward(i, A.slots[i], T, rope)
         pre(L + 1)
         Hd = P.unit(L + 1)
-        f_ = 2 * L
+        xf = A.xin[L]
         if gpt2:
-            ops.layernorm_fwd(A.xs[f_], Hd.p("lnf_g"), Hd.p("lnf_b"), eps, A.ln[f_], A.mean[f_], A.rstd[f_])
+            ops.layernorm_fwd(xf, Hd.p("lnf_g"), Hd.p("lnf_b"), eps, A.ln_f, A.mean_f, A.rstd_f)
         else:
-            ops.rmsnorm_fwd(A.xs[f_], Hd.p("lnf_g"), eps, A.ln[f_], A.rstd[f_])
+            ops.rmsnorm_fwd(xf, Hd.p("lnf_g"), eps, A.ln_f, A.rstd_f)
         w_head = E.p("wte") if cfg.tie_embeddings else Hd.p("lm_head")
-        ops.linear(A.ln[f_], w_head, out=A.logits)
+        ops.linear(A.ln_f, w_head, out=A.logits)
         ops.cross_entropy(A.logits, cfg.vocab_size, tgt, A.loss_rows, grad_scale=1.0 / M, write_grad=compute_grad)
         ops.sum_(A.loss_rows, A.loss, scale=1.0 / M)
         if not compute_grad:
@@ -367,53 +410,55 @@ class DecoderLM(torch.nn.Module):
         # ---------------- backward
         # head: dlogits (in A.logits) -> d ln_f, dW_head
         g_head = E.g("wte") if cfg.tie_embeddings else Hd.g("lm_head")
-        ops.linear_wgrad(A.logits, A.ln[f_], out=g_head, accumulate=True)
+        ops.linear_wgrad(A.logits, A.ln_f, out=g_head, accumulate=True)
         ops.linear_dgrad(A.logits, w_head, out=A.dln)
         A.dx.zero_()
         if gpt2:
             # the updated dx is the output gradient of the last block's fc2 -> its bias grad
-            ops.layernorm_bwd(A.xs[f_], A.dln, Hd.p("lnf_g"), A.mean[f_], A.rstd[f_], A.dx, A.dxb,
+            ops.layernorm_bwd(xf, A.dln, Hd.p("lnf_g"), A.mean_f, A.rstd_f, A.dx, A.dxb,
                               Hd.g("lnf_g"), Hd.g("lnf_b"), dxsum=P.unit(L).g("fc2_b"))
         else:
-            ops.rmsnorm_bwd(A.xs[f_], A.dln, Hd.p("lnf_g"), A.rstd[f_], A.dx, A.dxb, Hd.g("lnf_g"))
+            ops.rmsnorm_bwd(xf, A.dln, Hd.p("lnf_g"), A.rstd_f, A.dx, A.dxb, Hd.g("lnf_g"))
         post(L + 1)
         for i in reversed(range(L)):
             U = P.unit(i + 1)
-            a, b = 2 * i, 2 * i + 1
+            S = A.slots[i]
+            if A.checkpoint:
+                self._block_forward(i, S, T, rope, with_output=False)
             # --- MLP (its output gradient is the residual gradient dx, bf16 copy in dxb)
             if gpt2:  # fc2_b's grad was summed by the norm backward that produced dx
-                ops.linear_wgrad(A.dxb, A.h[i], out=U.g("fc2_w"), accumulate=True)
-                ops.linear_dgrad(A.dxb, U.p("fc2_w"), out=A.dh, act=2, aux=A.hpre[i])
+                ops.linear_wgrad(A.dxb, S.h, out=U.g("fc2_w"), accumulate=True)
+                ops.linear_dgrad(A.dxb, U.p("fc2_w"), out=A.dh, act=2, aux=S.hpre)
                 ops.colsum_accumulate(A.dh, U.g("fc_b"))
-                ops.linear_wgrad(A.dh, A.ln[b], out=U.g("fc_w"), accumulate=True)
+                ops.linear_wgrad(A.dh, S.ln_b, out=U.g("fc_w"), accumulate=True)
                 ops.linear_dgrad(A.dh, U.p("fc_w"), out=A.dln)
-                ops.layernorm_bwd(A.xs[b], A.dln, U.p("ln2_g"), A.mean[b], A.rstd[b], A.dx, A.dxb,
+                ops.layernorm_bwd(S.xb, A.dln, U.p("ln2_g"), S.mean_b, S.rstd_b, A.dx, A.dxb,
                                   U.g("ln2_g"), U.g("ln2_b"), dxsum=U.g("proj_b"))
             else:
-                ops.linear_wgrad(A.dxb, A.h[i], out=U.g("w2"), accumulate=True)
+                ops.linear_wgrad(A.dxb, S.h, out=U.g("w2"), accumulate=True)
                 ops.linear_dgrad(A.dxb, U.p("w2"), out=A.dh)
-                ops.swiglu_bwd(A.gu[i], A.dh, A.dgu)
-                ops.linear_wgrad(A.dgu, A.ln[b], out=U.g("w13"), accumulate=True)
+                ops.swiglu_bwd(S.gu, A.dh, A.dgu)
+                ops.linear_wgrad(A.dgu, S.ln_b, out=U.g("w13"), accumulate=True)
                 ops.linear_dgrad(A.dgu, U.p("w13"), out=A.dln)
-                ops.rmsnorm_bwd(A.xs[b], A.dln, U.p("mlp_norm"), A.rstd[b], A.dx, A.dxb, U.g("mlp_norm"))
+                ops.rmsnorm_bwd(S.xb, A.dln, U.p("mlp_norm"), S.rstd_b, A.dx, A.dxb, U.g("mlp_norm"))
             # --- attention
             wo = "proj_w" if gpt2 else "wo"
-            ops.linear_wgrad(A.dxb, A.o[i], out=U.g(wo), accumulate=True)
+            ops.linear_wgrad(A.dxb, S.o, out=U.g(wo), accumulate=True)
             ops.linear_dgrad(A.dxb, U.p(wo), out=A.do)
-            ops.attn_bwd(A.qkv[i], A.o[i], A.do, A.lse[i], B, T, H, Hkv, dh, dqkv=A.dqkv, work=A.attn_work)
+            ops.attn_bwd(S.qkv, S.o, A.do, S.lse, B, T, H, Hkv, dh, dqkv=A.dqkv, work=A.attn_work)
             if not gpt2:
-                ops.rope(A.dqkv, T, H + Hkv, dh, cos, sin, inverse=True)
+                ops.rope(A.dqkv, T, H + Hkv, dh, *rope, inverse=True)
             wq = "qkv_w" if gpt2 else "wqkv"
             if gpt2:
                 ops.colsum_accumulate(A.dqkv, U.g("qkv_b"))
-            ops.linear_wgrad(A.dqkv, A.ln[a], out=U.g(wq), accumulate=True)
+            ops.linear_wgrad(A.dqkv, S.ln_a, out=U.g(wq), accumulate=True)
             ops.linear_dgrad(A.dqkv, U.p(wq), out=A.dln)
             if gpt2:
                 prev_fc2_b = P.unit(i).g("fc2_b") if i > 0 else None
-                ops.layernorm_bwd(A.xs[a], A.dln, U.p("ln1_g"), A.mean[a], A.rstd[a], A.dx, A.dxb,
+                ops.layernorm_bwd(S.xa, A.dln, U.p("ln1_g"), S.mean_a, S.rstd_a, A.dx, A.dxb,
                                   U.g("ln1_g"), U.g("ln1_b"), dxsum=prev_fc2_b)
             else:
-                ops.rmsnorm_bwd(A.xs[a], A.dln, U.p("attn_norm"), A.rstd[a], A.dx, A.dxb, U.g("attn_norm"))
+                ops.rmsnorm_bwd(S.xa, A.dln, U.p("attn_norm"), S.rstd_a, A.dx, A.dxb, U.g("attn_norm"))
             post(i + 1)
         ops.embedding_bwd(tok, A.dx, E.g("wte"), E.g("wpe") if gpt2 else None, B, T)
         post(0)

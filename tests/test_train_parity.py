@@ -76,3 +76,32 @@ def test_loss_curve_matches_oracle(cuda, tmp_path, preset):
     rel = [abs(a - b) / b for a, b in zip(gpu, ref)]
     assert max(rel) < 0.02, list(zip(gpu, ref))
     assert gpu[-1] < gpu[0] - 0.3  # it learns the Markov stream
+
+
+@pytest.mark.parametrize("preset", ["tiny-gpt2-dh64", "tiny-llama"])
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_activation_checkpointing_same_grads(cuda, tmp_path, preset, precision):
+    """Per-block activation checkpointing (recompute in the backward) gives the same step."""
+    from paper_2602_08387_b200.data import PackedDataLoader, Sampler, make_synthetic_packed
+    from paper_2602_08387_b200.model import PRESETS, DecoderLM
+    from paper_2602_08387_b200.optim import AdamWConfig
+    from paper_2602_08387_b200.packed import open_packed
+    from paper_2602_08387_b200.trainer import SPMDTrainer
+
+    cfg = PRESETS[preset]
+    path = str(tmp_path / "data.cfpk")
+    make_synthetic_packed(path, 1 << 18, cfg.vocab_size, kind="markov", seed=2)
+    out = []
+    for ac in (False, True):
+        dl = PackedDataLoader(open_packed(path), 4, 256, Sampler(shuffle=True, seed=1))
+        tr = SPMDTrainer(DecoderLM(cfg, precision, activation_checkpointing=ac), AdamWConfig(), dl).setup()
+        x, y = tr.dataloader.batch(0)
+        tr.engine.begin_step()
+        loss = float(tr.model.forward_backward(x, y, hooks=tr.engine).item())
+        out.append((loss, tr.params.grads_full_fp32()))
+    (l0, g0), (l1, g1) = out
+    assert l0 == l1
+    tol = 1e-6 if precision == "fp32" else 2e-3
+    for k in g0:
+        rel = float((g0[k] - g1[k]).norm() / (g0[k].norm() + 1e-30))
+        assert rel <= tol, (k, rel)
