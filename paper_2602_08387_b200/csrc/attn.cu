@@ -102,7 +102,9 @@ __device__ __forceinline__ float ex2(float x) {
 template <bool DIAG>
 __device__ __forceinline__ float exp_pack(const uint32_t* v, int col0, int r, float sl2, float m,
                                           uint8_t* dst) {
-  float rs = 0.f;
+  // row sum as 4 independent partial sums combined by a tree: a single serial
+  // FADD chain over 64 elements would be longer than the MUFU work it follows
+  float rs4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
   for (int k8 = 0; k8 < 8; ++k8) {
     float e[8];
@@ -110,8 +112,8 @@ __device__ __forceinline__ float exp_pack(const uint32_t* v, int col0, int r, fl
     for (int i = 0; i < 8; ++i) {
       const float x = ex2(fmaf(__uint_as_float(v[k8 * 8 + i]), sl2, -m));
       e[i] = (DIAG && col0 + k8 * 8 + i > r) ? 0.f : x;
-      rs += e[i];
     }
+    rs4[k8 & 3] += ((e[0] + e[1]) + (e[2] + e[3])) + ((e[4] + e[5]) + (e[6] + e[7]));
     uint4 w;
     w.x = pack_bf16x2(e[0], e[1]);
     w.y = pack_bf16x2(e[2], e[3]);
@@ -119,7 +121,7 @@ __device__ __forceinline__ float exp_pack(const uint32_t* v, int col0, int r, fl
     w.w = pack_bf16x2(e[6], e[7]);
     *reinterpret_cast<uint4*>(dst + swz(r, k8)) = w;
   }
-  return rs;
+  return (rs4[0] + rs4[1]) + (rs4[2] + rs4[3]);
 }
 
 template <int DH>
@@ -269,15 +271,20 @@ __global__ void __launch_bounds__(Fwd<DH>::kThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&s_empty[t]);  // S(j) is in registers: QK^T(j+1) may overwrite it
-      float mx = -INFINITY;
+      // row max over 8 independent partial maxima (short dependency chains)
+      float mx8[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) mx8[u] = -INFINITY;
       if (diag) {
 #pragma unroll
         for (int i = 0; i < BKV; ++i)
-          if (i <= r) mx = fmaxf(mx, __uint_as_float(v[i]));
+          if (i <= r) mx8[i & 7] = fmaxf(mx8[i & 7], __uint_as_float(v[i]));
       } else {
 #pragma unroll
-        for (int i = 0; i < BKV; ++i) mx = fmaxf(mx, __uint_as_float(v[i]));
+        for (int i = 0; i < BKV; ++i) mx8[i & 7] = fmaxf(mx8[i & 7], __uint_as_float(v[i]));
       }
+      const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                             fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
       const float m_cand = mx * sl2;
       // lazy rescale: keep the old max unless the new one exceeds it by > 2^8
       float m_use = m;

@@ -219,24 +219,27 @@ __global__ void __launch_bounds__(kRowThreads) norm_bwd_kernel(
 }
 
 // out[c] += sum_b part[b][which][c]  (deterministic second stage): block =
-// 32 columns x 8 row groups, fixed summation order.
-__global__ void __launch_bounds__(256) reduce_parts_kernel(const float* __restrict__ part, int nblocks, int D,
-                                                           float* __restrict__ out0, float* __restrict__ out1,
-                                                           float* __restrict__ out2) {
-  __shared__ float red[8][33];
+// 32 columns x 32 row groups (enough independent loads in flight to hide L2
+// latency), fixed summation order.
+__global__ void __launch_bounds__(1024) reduce_parts_kernel(const float* __restrict__ part, int nblocks, int D,
+                                                            float* __restrict__ out0, float* __restrict__ out1,
+                                                            float* __restrict__ out2) {
+  __shared__ float red[32][33];
   const int which = blockIdx.y;
   float* out = which == 0 ? out0 : which == 1 ? out1 : out2;
   if (out == nullptr) return;
   const int c = blockIdx.x * 32 + (threadIdx.x & 31), rg = threadIdx.x >> 5;
   float acc = 0.f;
-  if (c < D)
-    for (int b = rg; b < nblocks; b += 8) acc += part[((int64_t)b * 3 + which) * D + c];
+  if (c < D) {
+#pragma unroll 4
+    for (int b = rg; b < nblocks; b += 32) acc += part[((int64_t)b * 3 + which) * D + c];
+  }
   red[rg][threadIdx.x & 31] = acc;
   __syncthreads();
   if (rg == 0 && c < D) {
     float s = 0.f;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) s += red[k][threadIdx.x & 31];
+    for (int k = 0; k < 32; ++k) s += red[k][threadIdx.x & 31];
     out[c] += s;
   }
 }
@@ -284,20 +287,22 @@ __global__ void __launch_bounds__(256) colsum_kernel(const T* __restrict__ x, in
     }
   }
 }
-// out[c] += sum_p part[p][c]: 32 columns x 8 part-groups per block, fixed order.
-__global__ void __launch_bounds__(256) colsum_final_kernel(const float* __restrict__ part, int nparts, int N,
-                                                           float* __restrict__ out) {
-  __shared__ float red[8][33];
+// out[c] += sum_p part[p][c]: 32 columns x 32 part-groups per block, fixed order.
+__global__ void __launch_bounds__(1024) colsum_final_kernel(const float* __restrict__ part, int nparts, int N,
+                                                            float* __restrict__ out) {
+  __shared__ float red[32][33];
   const int c = blockIdx.x * 32 + (threadIdx.x & 31), rg = threadIdx.x >> 5;
   float acc = 0.f;
-  if (c < N)
-    for (int p = rg; p < nparts; p += 8) acc += part[(int64_t)p * N + c];
+  if (c < N) {
+#pragma unroll 4
+    for (int p = rg; p < nparts; p += 32) acc += part[(int64_t)p * N + c];
+  }
   red[rg][threadIdx.x & 31] = acc;
   __syncthreads();
   if (rg == 0 && c < N) {
     float s = 0.f;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) s += red[k][threadIdx.x & 31];
+    for (int k = 0; k < 32; ++k) s += red[k][threadIdx.x & 31];
     out[c] += s;
   }
 }
@@ -640,7 +645,7 @@ static int norm_bwd(const float* x, const void* dy, const void* g, const float* 
   }
   if (rc) return rc;
   if (!dg && !(db && !RMS) && !dxsum) return B2S_OK;
-  reduce_parts_kernel<<<dim3((D + 31) / 32, 3), 256, 0, st>>>(work, grid, D, dg, RMS ? nullptr : db, dxsum);
+  reduce_parts_kernel<<<dim3((D + 31) / 32, 3), 1024, 0, st>>>(work, grid, D, dg, RMS ? nullptr : db, dxsum);
   return check_launch("norm_bwd_reduce");
 }
 
@@ -763,7 +768,7 @@ int b2s_colsum_accumulate(const void* d_x, int x_f32, int64_t M, int N, int64_t 
   dim3 grid(nblk, nparts);
   if (x_f32) ew::colsum_kernel<float><<<grid, 256, 0, st>>>((const float*)d_x, M, N, ld, rows_per, d_work);
   else ew::colsum_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>((const __nv_bfloat16*)d_x, M, N, ld, rows_per, d_work);
-  ew::colsum_final_kernel<<<(N + 31) / 32, 256, 0, st>>>(d_work, nparts, N, d_out);
+  ew::colsum_final_kernel<<<(N + 31) / 32, 1024, 0, st>>>(d_work, nparts, N, d_out);
   return check_launch("colsum", 2);
 }
 int64_t b2s_colsum_work_floats(int N) { return 256LL * N; }

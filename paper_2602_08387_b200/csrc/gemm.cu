@@ -154,8 +154,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* empty = full + C_::kStages;
   uint64_t* tfull = empty + C_::kStages;
   uint64_t* tempty = tfull + 2;
-  uint64_t* auxbar = tempty + 2;  // [kEpiWarps]: aux-tile TMA loads (dGELU epilogue)
-  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(auxbar + kEpiWarps);
+  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = (CG == 2) ? cluster_ctarank() : 0;
@@ -172,7 +171,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch(&tmC);
     for (int s = 0; s < C_::kStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], CG * kEpiWarps); }
-    for (int w = 0; w < kEpiWarps; ++w) mbar_init(&auxbar[w], 1);
     fence_barrier_init();
   }
   if (warp == 1) {
@@ -282,7 +280,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     int slot = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
-    uint32_t aux_phase = 0;
     // Hand the next staging slot to this warp: the bulk store issued from it
     // two jobs ago must have finished reading smem.
     auto next_slot = [&]() -> uint8_t* {
@@ -292,6 +289,22 @@ __global__ void __launch_bounds__(kThreads, 1)
       slot ^= 1;
       return b;
     };
+    // dGELU epilogue: this lane's 32 pre-activation values of the chunk, loaded
+    // into registers one chunk ahead (the next chunk's loads are in flight while
+    // the current one is processed), so the aux read latency is off the path.
+    uint4 aux[4];
+    auto load_aux = [&](int tile, int c) {
+      if (epi.act != 2 || tile >= num_tiles) return;
+      const int mn_ = tile % (num_m * num_n);
+      const int row = (mn_ % num_m) * BM * CG + rank * BM + q * 32 + lane;
+      const int col = (mn_ / num_m) * BN + c * 32;
+      if (row >= M) return;
+      const __nv_bfloat16* p = epi.aux_in + (int64_t)row * epi.ld_aux + col;
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (col + 8 * k < N) aux[k] = __ldg(reinterpret_cast<const uint4*>(p + 8 * k));
+    };
+    load_aux(tile0, half);
     for (int tile = tile0; tile < num_tiles; tile += tstride) {
       const int mn = tile % (num_m * num_n);
       const int m0 = (mn % num_m) * BM * CG + rank * BM, n0 = (mn / num_m) * BN;
@@ -302,14 +315,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int c = half; c < BN / 32; c += 2) {
         const int col0 = n0 + c * 32;
         const bool live = rbase < M && col0 < N;  // warp-uniform
-        uint8_t* slot_b = nullptr;
-        if (epi.act == 2 && live) {  // dGELU: TMA the 32x32 pre-activation tile into the slot's upper half
-          slot_b = next_slot();
-          if (lane == 0) {
-            mbar_arrive_expect_tx(&auxbar[warp - 2], 2048);
-            tma_load_2d(slot_b + 2048, &tmAux, &auxbar[warp - 2], col0, rbase);
-          }
-        }
         uint32_t r[32];
         tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, r);
         tmem_wait_ld();
@@ -321,7 +326,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             else mbar_arrive(&tempty[acc]);
           }
         }
-        if (!live) continue;
+        if (!live) {
+          if (epi.act == 2) {  // keep the aux prefetch chain going
+            if (c + 2 < BN / 32) load_aux(tile, c + 2);
+            else load_aux(tile + tstride, half);
+          }
+          continue;
+        }
         float v[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
@@ -345,18 +356,18 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] = gelu_tanh(__bfloat162float(__float2bfloat16_rn(v[i])));
         } else if (epi.act == 2) {
-          mbar_wait(&auxbar[warp - 2], aux_phase);
-          aux_phase ^= 1;
-          const uint8_t* ap = slot_b + 2048;
 #pragma unroll
           for (int c8 = 0; c8 < 4; ++c8) {
             float h[8];
-            unpack8(*reinterpret_cast<const bf16x8*>(ap + lane * 64 + ((c8 ^ ((lane >> 1) & 3)) << 4)), h);
+            unpack8(*reinterpret_cast<const bf16x8*>(&aux[c8]), h);
 #pragma unroll
             for (int j = 0; j < 8; ++j) v[c8 * 8 + j] *= gelu_tanh_grad(h[j]);
           }
+          // prefetch the next chunk of this warp (or the first of its next tile)
+          if (c + 2 < BN / 32) load_aux(tile, c + 2);
+          else load_aux(tile + tstride, half);
         }
-        uint8_t* b = slot_b ? slot_b : next_slot();
+        uint8_t* b = next_slot();
         if (epi.out_f32) stage_f32(b, lane, v);
         else stage_bf16(b, lane, v);
         fence_proxy_async_smem();

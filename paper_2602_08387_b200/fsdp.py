@@ -192,6 +192,7 @@ class Engine:
         self.ag_done = [torch.cuda.Event() for _ in range(n)] if self.cuda else [None] * n
         self.rs_done = [torch.cuda.Event() for _ in range(n)] if self.cuda else [None] * n
         self._issued = 0
+        self._prefetched = 0  # units whose next-step all-gather was issued after their optimizer update
         self.bytes_ag = sum(f.padded * f.full.element_size() for f in params.flat)
         self.bytes_rs = sum(f.padded * 4 for f in params.flat)
 
@@ -199,13 +200,34 @@ class Engine:
     def begin_step(self) -> None:
         for f in self.P.flat:
             f.gfull.zero_()
+        if self.world > 1 and self._prefetched == len(self.P.flat):
+            # every unit's all-gather was queued right after its optimizer update
+            self._issued = len(self.P.flat)
+            self._prefetched = 0
+            return
         self._issued = 0
+        self._prefetched = 0
         if self.world > 1:
             if self.cuda:
                 ready = torch.cuda.Event()
                 ready.record()  # after the previous optimizer step wrote p16
                 self.comm.wait_event(ready)
             self._issue_until(min(len(self.P.flat), self.prefetch))
+
+    def after_update(self, fi: int) -> None:
+        """FSDP unit fi's shard was just updated by the optimizer (compute stream):
+        queue its all-gather for the next step now, so it overlaps the remaining
+        optimizer kernels and the next step's first forward kernels."""
+        if self.world == 1 or not self.cuda or fi != self._prefetched:
+            return
+        f = self.P.flat[fi]
+        ready = torch.cuda.Event()
+        ready.record()
+        self.comm.wait_event(ready)
+        with torch.cuda.stream(self.comm):
+            dist.all_gather_into_tensor(f.full, f.p16, group=self.group)
+            self.ag_done[fi].record(self.comm)
+        self._prefetched += 1
 
     def _issue_until(self, k: int) -> None:
         while self._issued < k:

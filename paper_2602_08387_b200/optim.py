@@ -46,27 +46,45 @@ class FusedAdamW:
         self._gn2 = None
         self._part = None
 
-    def grad_norm_sq(self, params, group=None, world=1):
-        """Device scalar: global squared L2 norm of the (reduce-scattered) gradients."""
+    def grad_norm_sq(self, params, group=None, world=1, loss=None):
+        """Device scalar: global squared L2 norm of the (reduce-scattered) gradients.
+
+        With ``loss`` (a device scalar, W > 1) the rank-mean loss rides in the
+        same all-reduce (one 2-float collective per step instead of two)."""
         flats = params.flat
         dev = flats[0].g.device
         nparts = 4 * 148
         if self._part is None:
             self._part = torch.empty(len(flats) * nparts, device=dev)
-            self._gn2 = torch.empty(1, device=dev)
+            self._red = torch.zeros(2, device=dev)
+            self._gn2 = self._red[0:1]
         for i, f in enumerate(flats):
             ops.sumsq_partial(f.g, self._part[i * nparts:(i + 1) * nparts])
         ops.sum_(self._part, self._gn2)
         if world > 1:
-            dist.all_reduce(self._gn2, op=dist.ReduceOp.SUM, group=group)
+            if loss is not None:
+                self._red[1:2].copy_(loss)
+                dist.all_reduce(self._red, op=dist.ReduceOp.SUM, group=group)
+                loss.copy_(self._red[1:2])
+                ops.scale_f32(loss, 1.0 / world)
+            else:
+                dist.all_reduce(self._gn2, op=dist.ReduceOp.SUM, group=group)
         return self._gn2
 
-    def step(self, params, group=None, world=1):
+    def step(self, params, group=None, world=1, loss=None, engine=None):
+        """AdamW over every FSDP unit; ``engine.after_update(i)`` lets the FSDP engine
+        start unit i's next-step all-gather while later units are still updating."""
         self.step_count += 1
         c = self.cfg
-        gn2 = self.grad_norm_sq(params, group, world) if c.grad_clip > 0 else None
+        if c.grad_clip > 0 or loss is not None:
+            gn2 = self.grad_norm_sq(params, group, world, loss)
+        else:
+            gn2 = None
         lr = c.lr_at(self.step_count)
-        for f in params.flat:
+        for i, f in enumerate(params.flat):
             ops.adamw(f.master, f.m, f.v, f.g, f.p16, self.step_count, lr, c.beta1, c.beta2, c.eps,
-                      c.weight_decay, gn2=gn2, max_norm=c.grad_clip, wd_mask=f.wd_mask)
+                      c.weight_decay, gn2=gn2 if c.grad_clip > 0 else None, max_norm=c.grad_clip,
+                      wd_mask=f.wd_mask)
+            if engine is not None:
+                engine.after_update(i)
         return gn2

@@ -9,8 +9,9 @@ collectives. A step is:
   model.forward_backward(...)       tcgen05 GEMMs / attention + bandwidth kernels;
                                     reduce-scatters queued per unit during backward
   engine.end_backward()             compute waits for the reduce-scatters
-  optimizer.step(...)               grad-norm all-reduce + fused sharded AdamW
-  all_reduce(loss, AVG)             for logging (D2H only when the caller asks)
+  optimizer.step(...)               one all-reduce of (grad-norm^2, loss), fused sharded AdamW;
+                                    each unit's next-step all-gather queued after its update
+
 """
 
 from __future__ import annotations
@@ -84,10 +85,11 @@ class SPMDTrainer:
         self.engine.begin_step()
         loss = self.model.forward_backward(inputs, targets, hooks=self.engine)
         self.engine.end_backward()
-        self.optimizer.step(self.params, self.group, self.world)
         self._loss.copy_(loss)
-        if self.world > 1:
-            dist.all_reduce(self._loss, op=dist.ReduceOp.AVG, group=self.group)
+        # the rank-mean loss shares the grad-norm all-reduce; the optimizer then
+        # queues each unit's next-step all-gather as soon as that unit is updated
+        self.optimizer.step(self.params, self.group, self.world, loss=self._loss if self.world > 1 else None,
+                            engine=self.engine)
         return self._loss
 
     def run(self) -> list:

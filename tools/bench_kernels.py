@@ -70,6 +70,42 @@ def bench_gemm():
     return rows
 
 
+def bench_epilogues():
+    """The GPT-2 step's GEMMs with their fused epilogues (bias / GELU / dGELU / fp32 residual add)."""
+    rows = []
+    M, d, f = 16384, 768, 3072
+    g = torch.Generator(device="cuda").manual_seed(0)
+    x = torch.randn(M, d, device="cuda", generator=g).bfloat16()
+    w_fc = torch.randn(f, d, device="cuda", generator=g).bfloat16()
+    b_fc = torch.randn(f, device="cuda", generator=g).bfloat16()
+    h = torch.empty(M, f, device="cuda", dtype=torch.bfloat16)
+    hpre = torch.empty_like(h)
+    dy = torch.randn(M, d, device="cuda", generator=g).bfloat16()
+    w_fc2 = torch.randn(d, f, device="cuda", generator=g).bfloat16()
+    b_d = torch.randn(d, device="cuda", generator=g).bfloat16()
+    resid = torch.zeros(M, d, device="cuda")
+    dh = torch.empty(M, f, device="cuda", dtype=torch.bfloat16)
+    o = torch.randn(M, d, device="cuda", generator=g).bfloat16()
+    w_o = torch.randn(d, d, device="cuda", generator=g).bfloat16()
+    cases = [
+        ("fc.fwd+bias+gelu", M, f, d, lambda: ops.linear(x, w_fc, bias=b_fc, out=h, act=1, aux=hpre)),
+        ("fc.fwd plain", M, f, d, lambda: ops.linear(x, w_fc, out=h)),
+        ("fc2.dgrad+dgelu", M, f, d, lambda: ops.linear_dgrad(dy, w_fc2, out=dh, act=2, aux=hpre)),
+        ("fc2.dgrad plain", M, f, d, lambda: ops.linear_dgrad(dy, w_fc2, out=dh)),
+        ("fc2.fwd+bias+f32 resid add", M, d, f, lambda: ops.gemm(h, w_fc2, a_mn=False, b_mn=False, M=M, N=d, K=f,
+                                                                  out=resid, accumulate=True, bias=b_d)),
+        ("proj.fwd+bias+f32 resid add", M, d, d, lambda: ops.gemm(o, w_o, a_mn=False, b_mn=False, M=M, N=d, K=d,
+                                                                   out=resid, accumulate=True, bias=b_d)),
+        ("proj.fwd plain bf16", M, d, d, lambda: ops.linear(o, w_o)),
+    ]
+    for name, m, n, k, fn in cases:
+        ms = time_it(fn)
+        rows.append({"name": name, "M": m, "N": n, "K": k, "us": round(ms * 1e3, 1),
+                     "tflops": round(2.0 * m * n * k / ms / 1e9, 1)})
+        print(json.dumps(rows[-1]), flush=True)
+    return rows
+
+
 if __name__ == "__main__":
     what = sys.argv[1] if len(sys.argv) > 1 else "gemm"
-    {"gemm": bench_gemm}[what]()
+    {"gemm": bench_gemm, "epi": bench_epilogues}[what]()
