@@ -13,7 +13,12 @@
 // overlaps the MMAs of tile i+1. The epilogue moves 32x32 sub-tiles
 // TMEM -> registers (bias / GELU / dGELU applied there) -> swizzled smem ->
 // TMA store (or TMA add-reduce when accumulating), so global writes are
-// full-line and asynchronous. Grid = #SMs, tiles strided over CTAs.
+// full-line and asynchronous. Grid = #SMs; tiles are handed out dynamically
+// from a global atomic counter (the producer warp of the CTA / CTA-pair
+// leader fetches the next tile index and publishes it through an smem ring to
+// the MMA and epilogue warps -- and to the peer CTA of a pair), so CTAs that
+// start late (SMs busy with NCCL kernels on the comm stream) take fewer tiles
+// instead of stretching the kernel.
 #include <mutex>
 #include <stdio.h>
 #include <stdlib.h>
@@ -68,6 +73,7 @@ constexpr int kEpiWarps = 8;  // two per TMEM lane quarter, splitting the tile's
 constexpr int kThreads = 64 + 32 * kEpiWarps;
 constexpr int kStageSlot = 4096;  // one 32x32 fp32 (or bf16) staging sub-tile
 constexpr int kEpiSmem = kEpiWarps * 2 * kStageSlot;
+constexpr int kRing = 8;  // tile-index ring depth (producer runs ahead of MMA + 2 epilogue buffers)
 
 struct Epi {
   int out_f32;                // 1: fp32 output, 0: bf16
@@ -103,7 +109,7 @@ struct Cfg {
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kStages = (CG == 2) ? 5 : (BN == 256 ? 3 : 4);
   static constexpr int kTmemCols = 2 * BN;  // double-buffered accumulator
-  static constexpr int kSmem = kStages * kStageBytes + kEpiSmem + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int kSmem = kStages * kStageBytes + kEpiSmem + 1024 /*align*/ + 512 /*barriers, tile ring*/;
   static_assert(kSmem <= 227 * 1024, "smem budget");
 };
 
@@ -142,7 +148,7 @@ template <int BN, int CG, bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmAux,
-                int M, int N, int K, int splits, Epi epi) {
+                int M, int N, int K, int splits, Epi epi, int* __restrict__ sched) {
   using C_ = Cfg<BN, CG>;
   constexpr uint32_t kIdesc = make_idesc_bf16(BM * CG, BN, A_MN, B_MN);
   constexpr int BNc = BN / CG;  // B rows (N) staged by this CTA
@@ -154,7 +160,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* empty = full + C_::kStages;
   uint64_t* tfull = empty + C_::kStages;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* rfull = tempty + 2;       // [kRing] tile index published
+  uint64_t* rempty = rfull + kRing;   // [kRing] every reader done with the slot (leader CTA's count)
+  int* ring = reinterpret_cast<int*>(rempty + kRing);
+  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(ring + kRing);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = (CG == 2) ? cluster_ctarank() : 0;
@@ -163,7 +172,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int num_tiles = num_m * num_n * splits;  // split-K tiles add-reduce into C
   const int num_kb_all = (K + BK - 1) / BK;
   const int kb_per = (num_kb_all + splits - 1) / splits;
-  const int tile0 = blockIdx.x / CG, tstride = gridDim.x / CG;
+  // readers of a ring slot: MMA warp + 8 epilogue warps (+ the peer's producer and 8 epilogue warps)
+  constexpr uint32_t kRingReaders = (CG == 2) ? 2 + 2 * kEpiWarps : 1 + kEpiWarps;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
@@ -171,6 +181,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch(&tmC);
     for (int s = 0; s < C_::kStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], CG * kEpiWarps); }
+    for (int i = 0; i < kRing; ++i) { mbar_init(&rfull[i], 1); mbar_init(&rempty[i], kRingReaders); }
     fence_barrier_init();
   }
   if (warp == 1) {
@@ -183,12 +194,47 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_base_slot;
 
+  // tile-index ring: get the i-th tile of this CTA (blocking), then release the slot
+  auto ring_get = [&](int i) -> int {
+    if (CG == 2 && !leader) mbar_wait_cluster(&rfull[i % kRing], (i / kRing) & 1);  // published by the leader
+    else mbar_wait(&rfull[i % kRing], (i / kRing) & 1);
+    return *reinterpret_cast<volatile int*>(&ring[i % kRing]);
+  };
+  auto ring_release = [&](int i) {
+    if constexpr (CG == 2) {
+      if (!leader) { mbar_arrive_cluster(mapa_shared(smem_u32(&rempty[i % kRing]), 0)); return; }
+    }
+    mbar_arrive(&rempty[i % kRing]);
+  };
+
   if (warp == 0) {
     // ------------------------------------------------ TMA producer (both CTAs)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = tile0; tile < num_tiles; tile += tstride) {
+      // first tile static (blockIdx), later ones from the counter; the atomic for
+      // tile i+1 is issued when tile i starts loading, so its latency is hidden
+      const int tstride = gridDim.x / CG;
+      int next = blockIdx.x / CG;
+      for (int it = 0;; ++it) {
+        int tile;
+        if (leader) {  // publish the next tile (to the peer CTA too)
+          const int slot = it % kRing;
+          mbar_wait(&rempty[slot], ((it / kRing) & 1) ^ 1);
+          tile = next < num_tiles ? next : num_tiles;  // num_tiles = sentinel: no more work
+          ring[slot] = tile;
+          mbar_arrive(&rfull[slot]);
+          if constexpr (CG == 2) {
+            const uint32_t peer_slot = mapa_shared(smem_u32(&ring[slot]), 1);
+            asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(peer_slot), "r"(tile) : "memory");
+            mbar_arrive_cluster(mapa_shared(smem_u32(&rfull[slot]), 1));
+          }
+        } else {
+          tile = ring_get(it);
+          ring_release(it);
+        }
+        if (tile >= num_tiles) break;
+        if (leader) next = sched ? tstride + atomicAdd(sched, 1) : tile + tstride;
         const int mn = tile % (num_m * num_n), ks = tile / (num_m * num_n);
         const int m0 = (mn % num_m) * BM * CG + rank * BM, n0 = (mn / num_m) * BN + rank * BNc;
         const int kb0 = ks * kb_per, kb1 = min(num_kb_all, kb0 + kb_per);
@@ -239,7 +285,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int tile = tile0; tile < num_tiles; tile += tstride) {
+      for (int it = 0;; ++it) {
+        const int tile = ring_get(it);
+        ring_release(it);
+        if (tile >= num_tiles) break;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
@@ -294,7 +343,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // the current one is processed), so the aux read latency is off the path.
     uint4 aux[4];
     auto load_aux = [&](int tile, int c) {
-      if (epi.act != 2 || tile >= num_tiles) return;
+      if (epi.act != 2) return;
       const int mn_ = tile % (num_m * num_n);
       const int row = (mn_ % num_m) * BM * CG + rank * BM + q * 32 + lane;
       const int col = (mn_ / num_m) * BN + c * 32;
@@ -304,8 +353,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int k = 0; k < 4; ++k)
         if (col + 8 * k < N) aux[k] = __ldg(reinterpret_cast<const uint4*>(p + 8 * k));
     };
-    load_aux(tile0, half);
-    for (int tile = tile0; tile < num_tiles; tile += tstride) {
+    for (int it = 0;; ++it) {
+      const int tile = ring_get(it);
+      __syncwarp();
+      if (lane == 0) ring_release(it);
+      if (tile >= num_tiles) break;
+      load_aux(tile, half);  // first chunk's pre-activations: in flight while the MMAs finish
       const int mn = tile % (num_m * num_n);
       const int m0 = (mn % num_m) * BM * CG + rank * BM, n0 = (mn / num_m) * BN;
       mbar_wait(&tfull[acc], acc_phase);
@@ -327,10 +380,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         if (!live) {
-          if (epi.act == 2) {  // keep the aux prefetch chain going
-            if (c + 2 < BN / 32) load_aux(tile, c + 2);
-            else load_aux(tile + tstride, half);
-          }
+          if (epi.act == 2 && c + 2 < BN / 32) load_aux(tile, c + 2);  // keep the prefetch chain going
           continue;
         }
         float v[32];
@@ -363,9 +413,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int j = 0; j < 8; ++j) v[c8 * 8 + j] *= gelu_tanh_grad(h[j]);
           }
-          // prefetch the next chunk of this warp (or the first of its next tile)
+          // prefetch the next chunk of this warp (the next tile's first chunk is loaded on arrival)
           if (c + 2 < BN / 32) load_aux(tile, c + 2);
-          else load_aux(tile + tstride, half);
         }
         uint8_t* b = next_slot();
         if (epi.out_f32) stage_f32(b, lane, v);
@@ -392,6 +441,35 @@ __global__ void __launch_bounds__(kThreads, 1)
     if constexpr (CG == 2) tmem_dealloc_pair<C_::kTmemCols>(tmem_base);
     else tmem_dealloc<C_::kTmemCols>(tmem_base);
   }
+  // every CTA has fetched its sentinel: the last one out re-arms the counter for the next launch
+  if (sched && threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(sched + 1, 1) == (int)gridDim.x - 1) {
+      sched[0] = 0;
+      sched[1] = 0;
+      __threadfence();
+    }
+  }
+}
+
+// Per-device pool of zeroed scheduler counters {next_tile, ctas_done}; launches
+// rotate through the pool so GEMMs in flight on different streams never share one.
+constexpr int kSchedSlots = 64;
+static int* sched_slot() {
+  static int* pool[64] = {};
+  static int next[64] = {};
+  static std::mutex mu;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  if (!pool[dev]) {
+    if (cudaMalloc(&pool[dev], kSchedSlots * 2 * sizeof(int)) != cudaSuccess) return nullptr;
+    cudaMemset(pool[dev], 0, kSchedSlots * 2 * sizeof(int));
+    cudaDeviceSynchronize();
+  }
+  int* p = pool[dev] + 2 * next[dev];
+  next[dev] = (next[dev] + 1) % kSchedSlots;
+  return p;
 }
 
 template <int BN, int CG, bool A_MN, bool B_MN>
@@ -420,7 +498,11 @@ static int launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMa
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, tx, M, N, K, splits, e);
+  // B2S_GEMM_STATIC=1: static strided tile schedule (A/B comparisons)
+  static const bool static_sched = getenv("B2S_GEMM_STATIC") && atoi(getenv("B2S_GEMM_STATIC")) != 0;
+  int* sched = static_sched ? nullptr : sched_slot();
+  if (!static_sched && !sched) { set_error("gemm: scheduler counter allocation failed"); return B2S_ECUDA; }
+  cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, tx, M, N, K, splits, e, sched);
   return check_launch("gemm");
 }
 
