@@ -162,7 +162,7 @@ def run_ours(args):
         tr.train_step(step)
         step += 1
     barrier_sync()
-    launches0 = _lib.load().b2s_launch_count()
+    launches0 = _lib.launch_count()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         start.record()
@@ -171,7 +171,7 @@ def run_ours(args):
             step += 1
         end.record()
         barrier_sync()
-    launches = _lib.load().b2s_launch_count() - launches0
+    launches = _lib.launch_count() - launches0
     ms = start.elapsed_time(end) / args.steps
     t = torch.tensor([ms], device=device)
     if world > 1:
@@ -180,12 +180,16 @@ def run_ours(args):
     loss_dev = float(tr._loss.item())
     # per-kernel roofline: the same steps again with CUDA events around every
     # GEMM / attention launch on the compute stream (kept out of `value`)
+    if world > 1:
+        tr.engine.timing = []  # CUDA events around every all-gather / reduce-scatter (same pass)
     with ops.KernelTimer() as kt:
         for _ in range(args.steps):
             tr.train_step(step)
             step += 1
         barrier_sync()
     kern = kt.summary()
+    coll = tr.engine.collective_summary() if world > 1 else None
+    tr.engine.timing = None
 
     # ---- end to end through the public API with host buffers (staged windows, loss D2H each step)
     e2e_dl = PackedDataLoader(reader, B, T, Sampler(shuffle=True, seed=0), feed="staged")
@@ -244,6 +248,10 @@ def run_ours(args):
                                      f"{args.steps} instrumented steps",
                      "launches_per_step": g["launches"] // max(1, args.steps)},
         "kernels": per_kernel,
+        # FSDP collectives (NCCL over NVLink 5 / NVSwitch), nccl-tests busbw vs 900 GB/s per direction,
+        # timed on the comm stream while they overlap compute (so below the isolated sweep's numbers)
+        "collectives": ({k: {kk: vv for kk, vv in v.items() if kk != "bytes"} | {"bytes_per_step": v["bytes"] // args.steps}
+                         for k, v in coll.items()} if coll else None),
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
         "e2e": {"value": round(tokens_step / (e2e_ms / 1000), 1), "unit": UNIT,

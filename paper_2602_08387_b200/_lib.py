@@ -121,6 +121,21 @@ def call(name: str, *args) -> None:
         raise B2SError(name, rc, lib.b2s_last_error().decode(errors="replace"))
 
 
+_replayed = 0
+
+
+def count_replayed_launches(n: int) -> None:
+    """Kernels launched by replaying a captured CUDA graph (the library's own
+    counter only sees host-side launches)."""
+    global _replayed
+    _replayed += n
+
+
+def launch_count() -> int:
+    """Library kernels launched so far: direct launches + CUDA-graph replays."""
+    return int(load().b2s_launch_count()) + _replayed
+
+
 def last_error() -> str:
     return load().b2s_last_error().decode(errors="replace")
 

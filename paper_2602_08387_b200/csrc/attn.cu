@@ -96,6 +96,22 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
+// 2^x on the FMA / ALU pipes (no MUFU): x = n + f, n = rint(x) by the 1.5*2^23
+// magic add, f in [-0.5, 0.5], 2^f by a degree-3 minimax polynomial (max
+// relative error 1.0e-4, well below the bf16 rounding P is stored with), the
+// exponent added as integer n << 23. x is clamped to >= -127 (2^-127 ~ 0).
+// Offloads part of the softmax exponentials from the 16/clk/SM MUFU unit.
+__device__ __forceinline__ float ex2_poly(float x) {
+  x = fmaxf(x, -127.f);
+  const float j = x + 12582912.f;
+  const float f = x - (j - 12582912.f);
+  float p = fmaf(fmaf(fmaf(0.05500891f, f, 0.242211f), f, 0.69328293f), f, 1.0f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(j) << 23));
+}
+#ifndef B2S_EXP_POLY_MASK
+#define B2S_EXP_POLY_MASK 0x00  // 8-column groups (bitmask) using ex2_poly; 0: measured fastest (the softmax is latency-, not MUFU-bound)
+#endif
+
 // P = 2^(s*sl2 - m) for 64 columns of one row -> bf16 -> swizzled smem; returns
 // the row sum. The causal mask is a template branch so off-diagonal blocks run
 // the mask-free instruction stream.
@@ -110,7 +126,8 @@ __device__ __forceinline__ float exp_pack(const uint32_t* v, int col0, int r, fl
     float e[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      const float x = ex2(fmaf(__uint_as_float(v[k8 * 8 + i]), sl2, -m));
+      const float a = fmaf(__uint_as_float(v[k8 * 8 + i]), sl2, -m);
+      const float x = ((B2S_EXP_POLY_MASK >> k8) & 1) ? ex2_poly(a) : ex2(a);
       e[i] = (DIAG && col0 + k8 * 8 + i > r) ? 0.f : x;
     }
     rs4[k8 & 3] += ((e[0] + e[1]) + (e[2] + e[3])) + ((e[4] + e[5]) + (e[6] + e[7]));

@@ -67,15 +67,36 @@ class PackedDataLoader:
         B, L = self.batch_size, self.seq_len
         self._in = torch.empty(B, L, dtype=torch.int64, device=self.device)
         self._tg = torch.empty(B, L, dtype=torch.int64, device=self.device)
+        # Pinned host staging is a ring: the host may run several steps ahead of
+        # the GPU (CUDA-graph replay makes a step a handful of launches), so a
+        # buffer is rewritten only after the H2D copy that last read it has run.
+        self._ring = [None] * self.RING
+        self._slot = 0
         if self.feed == "resident":
             self._dev = DevicePackedStream(self.dataset, self.device)
-            self._ids_host = torch.empty(B, dtype=torch.int64, pin_memory=True)
+            self._ids_host = [torch.empty(B, dtype=torch.int64, pin_memory=True) for _ in range(self.RING)]
             self._ids_dev = torch.empty(B, dtype=torch.int64, device=self.device)
         else:
             w = self.dataset.token_width
-            self._stage_host = torch.empty(B * (L + 1) * w, dtype=torch.uint8, pin_memory=True)
+            self._stage_host = [torch.empty(B * (L + 1) * w, dtype=torch.uint8, pin_memory=True)
+                                for _ in range(self.RING)]
             self._stage_dev = torch.empty(B * (L + 1) * w + 16, dtype=torch.uint8, device=self.device)
         return self
+
+    RING = 4
+
+    def _host_slot(self) -> int:
+        """Next pinned staging buffer, waiting for the copy that last read it."""
+        i = self._slot
+        self._slot = (i + 1) % self.RING
+        if self._ring[i] is not None:
+            self._ring[i].synchronize()
+        return i
+
+    def _copied(self, i: int) -> None:
+        ev = torch.cuda.Event()
+        ev.record()
+        self._ring[i] = ev
 
     @property
     def steps_available(self) -> int:
@@ -98,20 +119,23 @@ class PackedDataLoader:
         ids = self.sample_ids(step)
         B, L = self.batch_size, self.seq_len
         stream = _lib.stream_ptr()
+        i = self._host_slot()
         if self.feed == "resident":
-            self._ids_host.numpy()[:] = ids.view(np.int64)
-            self._ids_dev.copy_(self._ids_host, non_blocking=True)
+            self._ids_host[i].numpy()[:] = ids.view(np.int64)
+            self._ids_dev.copy_(self._ids_host[i], non_blocking=True)
+            self._copied(i)
             _lib.call("b2s_gather_samples", self._dev.payload.data_ptr(), self._dev.token_width,
                       self._dev.token_count, self._ids_dev.data_ptr(), B, L, self._in.data_ptr(),
                       self._tg.data_ptr(), self._dev.status.data_ptr(), stream)
         else:
             w = self.dataset.token_width
             pay = self.dataset.payload
-            host = self._stage_host.numpy().view(pay.dtype).reshape(B, L + 1)
+            host = self._stage_host[i].numpy().view(pay.dtype).reshape(B, L + 1)
             for b, s in enumerate(ids):
                 lo = int(s) * L
                 host[b] = pay[lo:lo + L + 1]
-            self._stage_dev[: B * (L + 1) * w].copy_(self._stage_host, non_blocking=True)
+            self._stage_dev[: B * (L + 1) * w].copy_(self._stage_host[i], non_blocking=True)
+            self._copied(i)
             _lib.call("b2s_unpack_windows", self._stage_dev.data_ptr(), w, B, L, self._in.data_ptr(),
                       self._tg.data_ptr(), stream)
         return self._in, self._tg

@@ -193,6 +193,7 @@ class Engine:
         self.rs_done = [torch.cuda.Event() for _ in range(n)] if self.cuda else [None] * n
         self._issued = 0
         self._prefetched = 0  # units whose next-step all-gather was issued after their optimizer update
+        self.timing = None  # list of (kind, bytes, start_event, end_event) while collective timing is on
         self.bytes_ag = sum(f.padded * f.full.element_size() for f in params.flat)
         self.bytes_rs = sum(f.padded * 4 for f in params.flat)
 
@@ -225,16 +226,44 @@ class Engine:
         ready.record()
         self.comm.wait_event(ready)
         with torch.cuda.stream(self.comm):
-            dist.all_gather_into_tensor(f.full, f.p16, group=self.group)
+            self._timed_collective("all_gather", f.full, lambda: dist.all_gather_into_tensor(
+                f.full, f.p16, group=self.group))
             self.ag_done[fi].record(self.comm)
         self._prefetched += 1
+
+    def _timed_collective(self, kind, full_tensor, fn):
+        if self.timing is None:
+            return fn()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record(self.comm)
+        fn()
+        e.record(self.comm)
+        self.timing.append((kind, full_tensor.numel() * full_tensor.element_size(), s, e))
+
+    def collective_summary(self):
+        """nccl-tests bus bandwidth of the timed collectives: busbw = (bytes / t) * (W - 1) / W,
+        bytes = the full (gathered / pre-reduction) buffer."""
+        torch.cuda.synchronize()
+        out = {}
+        for kind, nbytes, s, e in self.timing or []:
+            d = out.setdefault(kind, {"calls": 0, "bytes": 0, "ms": 0.0})
+            d["calls"] += 1
+            d["bytes"] += nbytes
+            d["ms"] += s.elapsed_time(e)
+        for d in out.values():
+            alg = d["bytes"] / (d["ms"] / 1e3) if d["ms"] > 0 else 0.0
+            d["busbw_GBps"] = round(alg * (self.world - 1) / self.world / 1e9, 1)
+            d["frac_of_900GBps"] = round(d["busbw_GBps"] / 900.0, 3)
+            d["ms"] = round(d["ms"], 3)
+        return out
 
     def _issue_until(self, k: int) -> None:
         while self._issued < k:
             f = self.P.flat[self._issued]
             if self.cuda:
                 with torch.cuda.stream(self.comm):
-                    dist.all_gather_into_tensor(f.full, f.p16, group=self.group)
+                    self._timed_collective("all_gather", f.full, lambda: dist.all_gather_into_tensor(
+                        f.full, f.p16, group=self.group))
                     self.ag_done[self._issued].record(self.comm)
             else:
                 dist.all_gather_into_tensor(f.full, f.p16, group=self.group)
@@ -266,7 +295,8 @@ class Engine:
         done.record()
         self.comm.wait_event(done)
         with torch.cuda.stream(self.comm):
-            dist.reduce_scatter_tensor(f.g, f.gfull, op=dist.ReduceOp.AVG, group=self.group)
+            self._timed_collective("reduce_scatter", f.gfull, lambda: dist.reduce_scatter_tensor(
+                f.g, f.gfull, op=dist.ReduceOp.AVG, group=self.group))
             self.rs_done[fi].record(self.comm)
 
     def end_backward(self) -> None:

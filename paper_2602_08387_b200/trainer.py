@@ -45,7 +45,8 @@ def init_distributed():
 
 class SPMDTrainer:
     def __init__(self, model: DecoderLM, optimizer, dataloader: PackedDataLoader, steps: int = 20,
-                 seed: int = 0, blocks_per_unit: int = 1, init_device: str = "cpu", log_every: int = 0):
+                 seed: int = 0, blocks_per_unit: int = 1, init_device: str = "cpu", log_every: int = 0,
+                 cuda_graph: bool = True):
         self.model = model
         self.opt_cfg = optimizer if isinstance(optimizer, AdamWConfig) else optimizer.cfg
         self.dataloader = dataloader
@@ -54,6 +55,12 @@ class SPMDTrainer:
         self.blocks_per_unit = blocks_per_unit
         self.init_device = init_device
         self.log_every = log_every
+        # single GPU: after two eager steps the forward+backward (~350 launches) is
+        # captured once as a CUDA graph and replayed (optimizer stays eager: its
+        # learning rate / bias corrections are per-step host scalars)
+        self.cuda_graph = cuda_graph
+        self._graph = None
+        self._eager_steps = 0
         self._ready = False
 
     def setup(self) -> "SPMDTrainer":
@@ -81,9 +88,40 @@ class SPMDTrainer:
         inputs, targets = self.dataloader.batch(step)
         return self.step_on(inputs, targets)
 
+    def _graph_forward_backward(self, inputs, targets):
+        from . import _lib
+
+        if self._graph is None:
+            self._gx, self._gy = inputs.clone(), targets.clone()
+            n0 = _lib.load().b2s_launch_count()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self.engine.begin_step()
+                self._gloss = self.model.forward_backward(self._gx, self._gy, hooks=self.engine)
+            self._graph_launches = int(_lib.load().b2s_launch_count() - n0)
+            _lib.count_replayed_launches(-self._graph_launches)  # capture launched nothing
+            self._graph = g
+        self._gx.copy_(inputs)
+        self._gy.copy_(targets)
+        self._graph.replay()
+        _lib.count_replayed_launches(self._graph_launches)
+        return self._gloss
+
     def step_on(self, inputs, targets):
-        self.engine.begin_step()
-        loss = self.model.forward_backward(inputs, targets, hooks=self.engine)
+        from . import ops
+
+        shape = tuple(inputs.shape)
+        if self._graph is not None and shape != self._gshape:
+            self._graph, self._eager_steps = None, 0  # new activation buffers: re-warm, re-capture
+        use_graph = (self.cuda_graph and self.world == 1 and ops.KernelTimer.active is None
+                     and self._eager_steps >= 2)
+        if use_graph:
+            self._gshape = shape
+            loss = self._graph_forward_backward(inputs, targets)
+        else:
+            self._eager_steps += 1
+            self.engine.begin_step()
+            loss = self.model.forward_backward(inputs, targets, hooks=self.engine)
         self.engine.end_backward()
         self._loss.copy_(loss)
         # the rank-mean loss shares the grad-norm all-reduce; the optimizer then

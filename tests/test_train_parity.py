@@ -105,3 +105,22 @@ def test_activation_checkpointing_same_grads(cuda, tmp_path, preset, precision):
     for k in g0:
         rel = float((g0[k] - g1[k]).norm() / (g0[k].norm() + 1e-30))
         assert rel <= tol, (k, rel)
+
+
+def test_host_running_ahead_sees_every_batch(cuda, tmp_path):
+    """The host enqueues many steps before the GPU runs them (CUDA-graph replay makes a step a few
+    launches): every step must still train on its own batch (pinned staging ring, no overwrite)."""
+    cfg, tr_sync, reader, path = _setup(tmp_path, "tiny-llama", steps=24)
+    synced = tr_sync.run()  # .item() each step: host never ahead
+    for feed in ("resident", "staged"):
+        from paper_2602_08387_b200.data import PackedDataLoader, Sampler
+        from paper_2602_08387_b200.model import DecoderLM
+        from paper_2602_08387_b200.optim import AdamWConfig
+        from paper_2602_08387_b200.trainer import SPMDTrainer
+
+        dl = PackedDataLoader(reader, 8, 256, Sampler(shuffle=True, seed=5), feed=feed)
+        tr = SPMDTrainer(DecoderLM(cfg), AdamWConfig(lr=1e-3, warmup_steps=5), dl, steps=24).setup()
+        losses = [tr.train_step(s).clone() for s in range(24)]  # no host sync in the loop
+        got = [float(x.item()) for x in losses]
+        rel = max(abs(a - b) / b for a, b in zip(got, synced))
+        assert rel < 1e-3, (feed, list(zip(got, synced)))
