@@ -22,6 +22,7 @@
 #include <mutex>
 #include <stdio.h>
 #include <stdlib.h>
+#include <cuda_fp16.h>
 #include "common.cuh"
 #include "sm100.cuh"
 
@@ -69,10 +70,12 @@ namespace gemm {
 constexpr int BM = 128;
 constexpr int BK = 64;  // 64 bf16 = 128 B = one swizzle row
 constexpr int UMMA_K = 16;
-constexpr int kEpiWarps = 8;  // two per TMEM lane quarter, splitting the tile's columns
-constexpr int kThreads = 64 + 32 * kEpiWarps;
+// Epilogue warps per CTA (EW, a multiple of 4: one group per TMEM lane quarter,
+// splitting the tile's 32-column chunks): 12 for CTA-pair GEMMs with an
+// activation epilogue (GELU / dGELU: epilogue-latency bound at K = 768), which
+// costs one smem pipeline stage; 8 otherwise.
 constexpr int kStageSlot = 4096;  // one 32x32 fp32 (or bf16) staging sub-tile
-constexpr int kEpiSmem = kEpiWarps * 2 * kStageSlot;
+
 constexpr int kRing = 8;  // tile-index ring depth (producer runs ahead of MMA + 2 epilogue buffers)
 
 struct Epi {
@@ -94,6 +97,37 @@ __device__ __forceinline__ float gelu_tanh(float x) {
   float u = k0 * (x + k1 * x * x * x);
   return 0.5f * x * (1.f + tanh_fast(u));
 }
+// Packed half2 forms for the epilogue (two elements per instruction; the
+// epilogue of the K = 768 GPT-2 GEMMs is instruction-issue bound). fp16 keeps
+// 11 mantissa bits (error ~1e-3 relative on the activation / its derivative,
+// below the bf16 rounding of the stored result) and the range of |x| < 64 the
+// tanh argument needs; tanh.approx.f16x2 runs two elements per MUFU op.
+__device__ __forceinline__ __half2 tanh_h2(__half2 x) {
+  uint32_t y, xi = *reinterpret_cast<uint32_t*>(&x);
+  asm("tanh.approx.f16x2 %0, %1;" : "=r"(y) : "r"(xi));
+  return *reinterpret_cast<__half2*>(&y);
+}
+// gelu(x) for the pair (a, b) -> float2
+__device__ __forceinline__ float2 gelu_tanh2(float a, float b) {
+  const __half2 x = __floats2half2_rn(a, b);
+  const __half2 x2 = __hmul2(x, x);
+  const __half2 u = __hmul2(x, __hfma2(x2, __float2half2_rn(0.7978845608f * 0.044715f), __float2half2_rn(0.7978845608f)));
+  const __half2 hx = __hmul2(x, __float2half2_rn(0.5f));
+  const __half2 g = __hfma2(hx, tanh_h2(u), hx);  // 0.5 x (1 + tanh u)
+  return __half22float2(g);
+}
+// gelu'(x) for the pair (a, b) -> float2
+__device__ __forceinline__ float2 gelu_tanh_grad2(float a, float b) {
+  const float k0 = 0.7978845608f, k1 = 0.044715f;
+  const __half2 x = __floats2half2_rn(a, b);
+  const __half2 x2 = __hmul2(x, x);
+  const __half2 t = tanh_h2(__hmul2(x, __hfma2(x2, __float2half2_rn(k0 * k1), __float2half2_rn(k0))));
+  const __half2 half_ = __float2half2_rn(0.5f);
+  const __half2 a_ = __hfma2(half_, t, half_);                        // 0.5 (1 + t)
+  const __half2 b_ = __hfma2(__hneg2(t), t, __float2half2_rn(1.f));    // 1 - t^2
+  const __half2 c_ = __hmul2(x, __hfma2(x2, __float2half2_rn(1.5f * k0 * k1), __float2half2_rn(0.5f * k0)));
+  return __half22float2(__hfma2(c_, b_, a_));
+}
 __device__ __forceinline__ float gelu_tanh_grad(float x) {
   const float k0 = 0.7978845608028654f, k1 = 0.044715f;
   float x2 = x * x;
@@ -102,12 +136,15 @@ __device__ __forceinline__ float gelu_tanh_grad(float x) {
   return 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * k0 * (1.f + 3.f * k1 * x2);
 }
 
-template <int BN, int CG>
+template <int BN, int CG, int EW = 8>
 struct Cfg {
+  static constexpr int kEpiWarps = EW;
+  static constexpr int kThreads = 64 + 32 * EW;
+  static constexpr int kEpiSmem = kEpiWarps * 2 * kStageSlot;
   static constexpr int kABytes = BM * BK * 2;          // this CTA's 128 rows of A
   static constexpr int kBBytes = (BN / CG) * BK * 2;   // this CTA's share of B's BN rows
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kStages = (CG == 2) ? 5 : (BN == 256 ? 3 : 4);
+  static constexpr int kStages = (CG == 2) ? (EW == 8 ? 5 : 4) : (BN == 256 ? 3 : 4);
   static constexpr int kTmemCols = 2 * BN;  // double-buffered accumulator
   static constexpr int kSmem = kStages * kStageBytes + kEpiSmem + 1024 /*align*/ + 512 /*barriers, tile ring*/;
   static_assert(kSmem <= 227 * 1024, "smem budget");
@@ -144,12 +181,14 @@ __device__ __forceinline__ void stage_f32(uint8_t* buf, int lane, const float* v
 //   the leader alone issues the MMAs, and commits multicast to both CTAs.
 //   Each CTA's TMEM holds its own 128 x BN half of the accumulator, which its
 //   own epilogue warps drain. Per-SM operand traffic drops by 1/3.
-template <int BN, int CG, bool A_MN, bool B_MN>
-__global__ void __launch_bounds__(kThreads, 1)
+template <int BN, int CG, bool A_MN, bool B_MN, int EW>
+__global__ void __launch_bounds__(Cfg<BN, CG, EW>::kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmAux,
                 int M, int N, int K, int splits, Epi epi, int* __restrict__ sched) {
-  using C_ = Cfg<BN, CG>;
+  using C_ = Cfg<BN, CG, EW>;
+  constexpr int kEpiWarps = C_::kEpiWarps, kEpiSmem = C_::kEpiSmem;
+  constexpr int kEG = kEpiWarps / 4;  // epilogue warps per TMEM lane quarter
   constexpr uint32_t kIdesc = make_idesc_bf16(BM * CG, BN, A_MN, B_MN);
   constexpr int BNc = BN / CG;  // B rows (N) staged by this CTA
   extern __shared__ uint8_t smem_raw[];
@@ -324,7 +363,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else {
     // ------------------------------------------------ epilogue warps 2..9
     const int q = warp & 3;  // TMEM lane quarter this warp may access
-    const int half = (warp - 2) >> 2;  // which alternate 32-column chunks this warp owns
+    const int half = (warp - 2) >> 2;  // this warp owns chunks half, half + kEG, ... of each tile
     uint8_t* ring = epi_smem + (warp - 2) * 2 * kStageSlot;
     int slot = 0;
     int acc = 0;
@@ -365,13 +404,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       const int rbase = m0 + q * 32;
 #pragma unroll 1
-      for (int c = half; c < BN / 32; c += 2) {
+      for (int c = half; c < BN / 32; c += kEG) {
         const int col0 = n0 + c * 32;
         const bool live = rbase < M && col0 < N;  // warp-uniform
         uint32_t r[32];
         tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, r);
         tmem_wait_ld();
-        if (c + 2 >= BN / 32) {  // this warp's last chunk read: release the accumulator
+        if (c + kEG >= BN / 32) {  // this warp's last chunk read: release the accumulator
           tc_fence_before();
           __syncwarp();
           if (lane == 0) {
@@ -380,7 +419,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         if (!live) {
-          if (epi.act == 2 && c + 2 < BN / 32) load_aux(tile, c + 2);  // keep the prefetch chain going
+          if (epi.act == 2 && c + kEG < BN / 32) load_aux(tile, c + kEG);  // keep the prefetch chain going
           continue;
         }
         float v[32];
@@ -404,17 +443,26 @@ __global__ void __launch_bounds__(kThreads, 1)
           __syncwarp();
           if (lane == 0) { tma_store_2d(&tmAux, b, col0, rbase); bulk_commit(); }
 #pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = gelu_tanh(__bfloat162float(__float2bfloat16_rn(v[i])));
+          for (int i = 0; i < 32; i += 2) {  // GELU of the bf16-rounded pre-activation (what the backward sees)
+            const float2 g = gelu_tanh2(__bfloat162float(__float2bfloat16_rn(v[i])),
+                                        __bfloat162float(__float2bfloat16_rn(v[i + 1])));
+            v[i] = g.x;
+            v[i + 1] = g.y;
+          }
         } else if (epi.act == 2) {
 #pragma unroll
           for (int c8 = 0; c8 < 4; ++c8) {
             float h[8];
             unpack8(*reinterpret_cast<const bf16x8*>(&aux[c8]), h);
 #pragma unroll
-            for (int j = 0; j < 8; ++j) v[c8 * 8 + j] *= gelu_tanh_grad(h[j]);
+            for (int j = 0; j < 8; j += 2) {
+              const float2 g = gelu_tanh_grad2(h[j], h[j + 1]);
+              v[c8 * 8 + j] *= g.x;
+              v[c8 * 8 + j + 1] *= g.y;
+            }
           }
           // prefetch the next chunk of this warp (the next tile's first chunk is loaded on arrival)
-          if (c + 2 < BN / 32) load_aux(tile, c + 2);
+          if (c + kEG < BN / 32) load_aux(tile, c + kEG);
         }
         uint8_t* b = next_slot();
         if (epi.out_f32) stage_f32(b, lane, v);
@@ -472,11 +520,11 @@ static int* sched_slot() {
   return p;
 }
 
-template <int BN, int CG, bool A_MN, bool B_MN>
+template <int BN, int CG, bool A_MN, bool B_MN, int EW>
 static int launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc,
                   const CUtensorMap& tx, int M, int N, int K, int splits, const Epi& e, cudaStream_t st) {
-  using C_ = Cfg<BN, CG>;
-  auto kern = gemm_kernel<BN, CG, A_MN, B_MN>;
+  using C_ = Cfg<BN, CG, EW>;
+  auto kern = gemm_kernel<BN, CG, A_MN, B_MN, EW>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::kSmem);
@@ -488,7 +536,7 @@ static int launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMa
   const int grid = (tiles < slots ? tiles : slots) * CG;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kThreads);
+  cfg.blockDim = dim3(C_::kThreads);
   cfg.dynamicSmemBytes = C_::kSmem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -506,14 +554,14 @@ static int launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMa
   return check_launch("gemm");
 }
 
-template <int BN, int CG>
+template <int BN, int CG, int EW = 8>
 static int dispatch(bool amn, bool bmn, const CUtensorMap& ta, const CUtensorMap& tb,
                     const CUtensorMap& tc, const CUtensorMap& tx, int M, int N, int K,
                     int splits, const Epi& e, cudaStream_t st) {
-  if (!amn && !bmn) return launch<BN, CG, false, false>(ta, tb, tc, tx, M, N, K, splits, e, st);
-  if (!amn && bmn) return launch<BN, CG, false, true>(ta, tb, tc, tx, M, N, K, splits, e, st);
-  if (amn && !bmn) return launch<BN, CG, true, false>(ta, tb, tc, tx, M, N, K, splits, e, st);
-  return launch<BN, CG, true, true>(ta, tb, tc, tx, M, N, K, splits, e, st);
+  if (!amn && !bmn) return launch<BN, CG, false, false, EW>(ta, tb, tc, tx, M, N, K, splits, e, st);
+  if (!amn && bmn) return launch<BN, CG, false, true, EW>(ta, tb, tc, tx, M, N, K, splits, e, st);
+  if (amn && !bmn) return launch<BN, CG, true, false, EW>(ta, tb, tc, tx, M, N, K, splits, e, st);
+  return launch<BN, CG, true, true, EW>(ta, tb, tc, tx, M, N, K, splits, e, st);
 }
 
 // Tile choice: (BN, CTA group, split-K) maximising filled SM slots in the last
@@ -591,6 +639,8 @@ extern "C" int b2s_gemm(const void* d_A, int a_mn_major, int64_t lda, const void
   gemm::Epi e{c_f32, accumulate, (const __nv_bfloat16*)d_bias, act, (const __nv_bfloat16*)d_aux, ld_aux};
   cudaStream_t st = (cudaStream_t)stream;
   const int splits = ch.splits;
+  if (ch.cg == 2 && act != 0)  // activation epilogue: 12 epilogue warps (see EW above)
+    return gemm::dispatch<256, 2, 12>(a_mn_major, b_mn_major, ta, tb, tc, tx, M, N, K, splits, e, st);
   if (ch.cg == 2) return gemm::dispatch<256, 2>(a_mn_major, b_mn_major, ta, tb, tc, tx, M, N, K, splits, e, st);
   if (bn == 256) return gemm::dispatch<256, 1>(a_mn_major, b_mn_major, ta, tb, tc, tx, M, N, K, splits, e, st);
   return gemm::dispatch<128, 1>(a_mn_major, b_mn_major, ta, tb, tc, tx, M, N, K, splits, e, st);
