@@ -450,17 +450,27 @@ constexpr int kBwdThreads = 320;
 template <bool DIAG>
 __device__ __forceinline__ void p_ds(uint32_t* sv, uint32_t* dv, int q0, int r, float sl2, const float* lse2,
                                      const float* dd) {
+  // the 32 columns' LSE / D values are the same for every thread: 16-byte
+  // broadcast loads (8 + 8 LDS.128 instead of 64 scalar LDS)
+  float ls[32], ds[32];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const float4 l4 = *reinterpret_cast<const float4*>(lse2 + q0 + 4 * k);
+    const float4 d4 = *reinterpret_cast<const float4*>(dd + q0 + 4 * k);
+    ls[4 * k] = l4.x; ls[4 * k + 1] = l4.y; ls[4 * k + 2] = l4.z; ls[4 * k + 3] = l4.w;
+    ds[4 * k] = d4.x; ds[4 * k + 1] = d4.y; ds[4 * k + 2] = d4.z; ds[4 * k + 3] = d4.w;
+  }
 #pragma unroll
   for (int e = 0; e < 32; ++e) {
     const int q = q0 + e;
 #ifdef B2S_EXP_NOEXP
     float pv = __uint_as_float(sv[e]);
 #else
-    float pv = ex2(fmaf(__uint_as_float(sv[e]), sl2, -lse2[q] * kLog2e));
+    float pv = ex2(fmaf(__uint_as_float(sv[e]), sl2, -ls[e] * kLog2e));
 #endif
     if (DIAG && q < r) pv = 0.f;  // query index below key index: masked
     sv[e] = __float_as_uint(pv);
-    dv[e] = __float_as_uint(pv * (__uint_as_float(dv[e]) - dd[q]));
+    dv[e] = __float_as_uint(pv * (__uint_as_float(dv[e]) - ds[e]));
   }
 }
 // dh = 64: dQ fused (TMEM S^T 128 + dP^T 128 + dV 64 + dK 64 + dQ 2x64 = 512

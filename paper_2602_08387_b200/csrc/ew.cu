@@ -52,20 +52,25 @@ __device__ __forceinline__ void from_f(float& d, float v) { d = v; }
 // residual into the next stream buffer while it is in registers).
 // TPR threads cooperate on a row (32 = one warp for D <= 1024, 256 = the whole
 // block for D >= 2048) so the row stays in registers at every hidden size.
-// Sum over the TPR threads sharing a row. TPR=64: two warps exchange through
-// double-buffered smem slots and a per-pair named barrier (ids 1..4).
+// Sum over the TPR threads sharing a row. TPR = 64 / 128: the row's 2 / 4 warps
+// exchange through double-buffered smem slots and a named barrier per row group
+// (ids 1..4), so row groups of one block never wait on each other.
 template <int TPR>
 __device__ __forceinline__ float row_sum(float v, float* scratch, int& toggle) {
   if constexpr (TPR == 32) {
     return warp_sum(v);
-  } else if constexpr (TPR == 64) {
+  } else if constexpr (TPR == 64 || TPR == 128) {
+    constexpr int NW = TPR / 32;
     v = warp_sum(v);
     const int wid = threadIdx.x >> 5;
     float* sl = scratch + toggle * 8;
     if ((threadIdx.x & 31) == 0) sl[wid] = v;
-    asm volatile("bar.sync %0, 64;" ::"r"(1 + (wid >> 1)) : "memory");
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + wid / NW), "n"(TPR) : "memory");
     toggle ^= 1;
-    return sl[wid & ~1] + sl[wid | 1];
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < NW; ++k) s += sl[(wid / NW) * NW + k];
+    return s;
   } else {
     return block_sum(v, scratch);
   }
@@ -393,6 +398,13 @@ __global__ void rope_kernel(E* __restrict__ qkv, int64_t M, int T, int64_t ld, i
 }
 
 // ------------------------------------------------------------------ SwiGLU
+// sigmoid: fast MUFU exp / reciprocal for bf16 activations (the kernel is then
+// HBM-bound instead of bound by IEEE expf + division), exact libm forms in fp32 mode.
+template <typename T>
+__device__ __forceinline__ float sigmoid(float x) {
+  if constexpr (sizeof(T) == 4) return 1.f / (1.f + expf(-x));
+  else return __frcp_rn(1.f + __expf(-x));
+}
 // gu [M, 2F] (gate | up), h [M, F] = silu(gate) * up
 template <typename T>
 __global__ void swiglu_fwd_kernel(const T* __restrict__ gu, T* __restrict__ h,
@@ -406,7 +418,7 @@ __global__ void swiglu_fwd_kernel(const T* __restrict__ gu, T* __restrict__ h,
     ld_v8(gu + m * 2 * F + c, g);
     ld_v8(gu + m * 2 * F + F + c, u);
 #pragma unroll
-    for (int t = 0; t < 8; ++t) o[t] = g[t] / (1.f + expf(-g[t])) * u[t];
+    for (int t = 0; t < 8; ++t) o[t] = g[t] * sigmoid<T>(g[t]) * u[t];
     st_v8(h + m * F + c, o);
   }
 }
@@ -425,7 +437,7 @@ __global__ void swiglu_bwd_kernel(const T* __restrict__ gu, const T* __restrict_
     ld_v8(dh + m * F + c, d);
 #pragma unroll
     for (int t = 0; t < 8; ++t) {
-      const float sg = 1.f / (1.f + expf(-g[t]));
+      const float sg = sigmoid<T>(g[t]);
       const float silu = g[t] * sg;
       du[t] = d[t] * silu;
       dg[t] = d[t] * u[t] * sg * (1.f + g[t] * (1.f - sg));
@@ -624,7 +636,7 @@ static int norm_bwd(const float* x, const void* dy, const void* g, const float* 
   unsigned grid = 0;
   auto go = [&](auto kern, int tpr) {
     int64_t blocks = (M * tpr + kRowThreads - 1) / kRowThreads;
-    const int64_t cap = tpr <= 64 ? kNormBwdMaxBlocks : kNumSMs * 2;
+    const int64_t cap = tpr <= 128 ? kNormBwdMaxBlocks : kNumSMs * 2;
     grid = (unsigned)(blocks < cap ? blocks : cap);  // partial buffer: grid * 3 * D floats
     kern<<<grid, kRowThreads, 0, st>>>(x, (const T*)dy, (const T*)g, mean, rstd, dx, (T*)dx_bf16, work, M,
                                        dxsum != nullptr);
@@ -637,7 +649,7 @@ static int norm_bwd(const float* x, const void* dy, const void* g, const float* 
     case 512: rc = go(norm_bwd_kernel<512, 32, RMS, T>, 32); break;
     case 768: rc = go(norm_bwd_kernel<768, 64, RMS, T>, 64); break;
     case 1024: rc = go(norm_bwd_kernel<1024, 32, RMS, T>, 32); break;
-    case 2048: rc = go(norm_bwd_kernel<2048, 256, RMS, T>, 256); break;
+    case 2048: rc = go(norm_bwd_kernel<2048, 128, RMS, T>, 128); break;  // 2 rows in flight per block
     case 4096: rc = go(norm_bwd_kernel<4096, 256, RMS, T>, 256); break;
     default:
       set_error("norm_bwd: unsupported hidden size %d", D);
