@@ -14,6 +14,7 @@
  *   packed_data.py:226-238 splitmix64                 -> b2s_splitmix64
  *   packed_data.py:257-282 make_permutation           -> b2s_make_permutation
  *   packed_data.py:322-333 chunk                      -> b2s_chunk_bounds
+ *   packed_data.py:336-344 materialize_chunk          -> b2s_gather_documents (device copy)
  * The model/optimizer/FSDP kernels below have no reference implementation
  * (SPEC.md:12 puts the training step out of the reference's scope); their
  * callers are the registered `model`, `optimizer` and `trainer` components
@@ -77,6 +78,14 @@ int b2s_gather_samples(const void* d_payload, int width, uint64_t token_count,
                        const uint64_t* d_sample_ids, int batch, int64_t seq_len,
                        int64_t* d_inputs, int64_t* d_targets, int32_t* d_status,
                        b2s_stream_t stream);
+
+/* packed_data.py:336-344 (materialize_chunk), on the device: for i < n_docs,
+ * copy source tokens [d_src_start[i], d_src_start[i] + d_len[i]) of the
+ * `width`-byte payload to token offset d_dst_start[i] of d_out. The caller
+ * validates document ordinals (OutOfRangeError) and lays out the output
+ * spans (exclusive prefix sum of the lengths). */
+int b2s_gather_documents(const void* d_payload, int width, const uint64_t* d_src_start, const uint64_t* d_len,
+                         const uint64_t* d_dst_start, int64_t n_docs, void* d_out, b2s_stream_t stream);
 
 /* Same widening split for `batch` host-staged windows of seq_len+1 tokens
  * stored back to back in d_windows (window b starts at token b*(seq_len+1)):

@@ -110,3 +110,27 @@ def chunk_sizes(n: int, k: int) -> list[int]:
         raise ValueError(k)
     q, r = divmod(n, k)
     return [q + 1 if c < r else q for c in range(k)]
+
+
+def materialize_bytes(buf: bytes, docs) -> bytes:
+    """ORACLE: the CFPKD001 file materialize_chunk (packed_data.py:336-344) writes for
+    the documents ``docs`` of the packed file ``buf``: header, the documents' tokens
+    in order, the rebuilt contiguous span index (packed_data.py:62-131 writer layout)."""
+    width, count, ndoc, index_off = parse_header(buf, len(buf))
+    dt = {1: "<u1", 2: "<u2", 4: "<u4"}[width]
+    payload = np.frombuffer(buf, dt, count, 40)
+    spans = np.frombuffer(buf, "<u8", 2 * ndoc, index_off).reshape(ndoc, 2)
+    parts, lens = [], []
+    for d in docs:
+        s, n = int(spans[int(d), 0]), int(spans[int(d), 1])
+        parts.append(payload[s:s + n])
+        lens.append(n)
+    body = np.concatenate(parts).astype(dt).tobytes() if parts else b""
+    lens = np.asarray(lens, dtype="<u8")
+    out_spans = np.zeros((len(lens), 2), dtype="<u8")
+    out_spans[:, 1] = lens
+    if len(lens) > 1:
+        out_spans[1:, 0] = np.cumsum(lens[:-1])
+    total = int(lens.sum()) if len(lens) else 0
+    hdr = struct.pack("<8sIIQQQ", b"CFPKD001", 1, width, total, len(lens), 40 + total * width)
+    return hdr + body + out_spans.tobytes()

@@ -9,6 +9,7 @@
 #include <string.h>
 #include <atomic>
 #include <thread>
+#include <type_traits>
 #include "common.cuh"
 
 namespace b2s {
@@ -71,6 +72,34 @@ __global__ void __launch_bounds__(256) gather_samples_kernel(
       if (ok[0]) { inputs[idx0] = in2[0]; targets[idx0] = tg2[0]; }
       if (ok[1] && idx0 + 1 < total) { inputs[idx0 + 1] = in2[1]; targets[idx0 + 1] = tg2[1]; }
     }
+  }
+}
+
+
+// Document-level segmented copy (materialize_chunk on the device, reference
+// packed_data.py:336-344): document i of the output is source tokens
+// [src_start[i], src_start[i] + len[i]) written at token dst_start[i]. One warp
+// per document (grid-stride), lanes on consecutive tokens: loads and stores are
+// coalesced within a document and no per-token search is needed.
+template <int W>
+__global__ void __launch_bounds__(256) gather_documents_kernel(const uint8_t* __restrict__ payload,
+                                                               const uint64_t* __restrict__ src_start,
+                                                               const uint64_t* __restrict__ len,
+                                                               const uint64_t* __restrict__ dst_start, int64_t n,
+                                                               uint8_t* __restrict__ out) {
+  using Tok = typename std::conditional<W == 1, uint8_t, typename std::conditional<W == 2, uint16_t, uint32_t>::type>::type;
+  const Tok* src = reinterpret_cast<const Tok*>(payload);
+  Tok* dst = reinterpret_cast<Tok*>(out);
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t d = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; d < n; d += warps) {
+    const uint64_t s0 = __ldg(src_start + d), l = __ldg(len + d), o0 = __ldg(dst_start + d);
+    uint64_t t = lane;
+    for (; t + 96 < l; t += 128) {  // four independent loads in flight per lane
+      const Tok a0 = src[s0 + t], a1 = src[s0 + t + 32], a2 = src[s0 + t + 64], a3 = src[s0 + t + 96];
+      dst[o0 + t] = a0; dst[o0 + t + 32] = a1; dst[o0 + t + 64] = a2; dst[o0 + t + 96] = a3;
+    }
+    for (; t < l; t += 32) dst[o0 + t] = src[s0 + t];
   }
 }
 
@@ -197,6 +226,25 @@ int b2s_unpack_windows(const void* d_windows, int width, int batch, int64_t seq_
     default: b2s::gather_samples_kernel<4><<<grid, 256, 0, st>>>(p, batch, nullptr, batch, seq_len, seq_len + 1, d_inputs, d_targets, nullptr); break;
   }
   return b2s::check_launch("unpack_windows");
+}
+
+int b2s_gather_documents(const void* d_payload, int width, const uint64_t* d_src_start, const uint64_t* d_len,
+                         const uint64_t* d_dst_start, int64_t n_docs, void* d_out, b2s_stream_t stream) {
+  B2S_REQUIRE(width == 1 || width == 2 || width == 4, B2S_EINVAL, "token width must be 1, 2 or 4, got %d", width);
+  B2S_REQUIRE(n_docs >= 0, B2S_EINVAL, "n_docs must be >= 0");
+  if (n_docs == 0) return B2S_OK;
+  B2S_REQUIRE(d_payload && d_src_start && d_len && d_dst_start && d_out, B2S_EINVAL, "null device pointer");
+  int64_t blocks = (n_docs * 32 + 255) / 256;
+  if (blocks > b2s::kNumSMs * 16) blocks = b2s::kNumSMs * 16;
+  cudaStream_t st = (cudaStream_t)stream;
+  const uint8_t* p = (const uint8_t*)d_payload;
+  uint8_t* o = (uint8_t*)d_out;
+  switch (width) {
+    case 1: b2s::gather_documents_kernel<1><<<(unsigned)blocks, 256, 0, st>>>(p, d_src_start, d_len, d_dst_start, n_docs, o); break;
+    case 2: b2s::gather_documents_kernel<2><<<(unsigned)blocks, 256, 0, st>>>(p, d_src_start, d_len, d_dst_start, n_docs, o); break;
+    default: b2s::gather_documents_kernel<4><<<(unsigned)blocks, 256, 0, st>>>(p, d_src_start, d_len, d_dst_start, n_docs, o); break;
+  }
+  return b2s::check_launch("gather_documents");
 }
 
 }  // extern "C"

@@ -284,6 +284,48 @@ def materialize_chunk(reader: PackedReader, docs, out_path) -> None:
             w.write_document(reader.get_document_tokens(int(d)))
 
 
+def materialize_chunk_gpu(reader: PackedReader, docs, out_path, device="cuda", stream=None) -> None:
+    """``materialize_chunk`` with the token copy on the GPU.
+
+    Same output bytes as the host path (reference packed_data.py:336-344): the
+    documents ``docs`` (ordinals into ``reader``), in order, as a standalone
+    CFPKD001 file with a rebuilt contiguous span index. ``stream`` may be a
+    ``DevicePackedStream`` of ``reader`` whose payload is already resident in HBM
+    (the training-time case); otherwise the payload is copied to ``device``.
+    """
+    import torch
+
+    docs = np.asarray(docs, dtype=np.int64).reshape(-1)
+    n = reader.doc_count
+    bad = docs[(docs < 0) | (docs >= n)]
+    if bad.size:
+        raise OutOfRangeError(f"document {int(bad[0])} out of range [0, {n})")
+    ds = stream if stream is not None else DevicePackedStream(reader, device)
+    spans = np.asarray(reader.spans, dtype=np.uint64)
+    src = spans[docs, 0] if docs.size else np.zeros(0, np.uint64)
+    lens = spans[docs, 1] if docs.size else np.zeros(0, np.uint64)
+    dst = np.zeros(docs.size, dtype=np.uint64)
+    if docs.size > 1:
+        np.cumsum(lens[:-1], out=dst[1:])
+    total = int(lens.sum()) if docs.size else 0
+    w = reader.token_width
+    dev = ds.payload.device
+    out = torch.empty(max(16, total * w), dtype=torch.uint8, device=dev)
+    if docs.size:
+        t = lambda a: torch.from_numpy(np.ascontiguousarray(a).view(np.int64)).to(dev)  # noqa: E731
+        d_src, d_len, d_dst = t(src), t(lens), t(dst)
+        _lib.call("b2s_gather_documents", ds.payload.data_ptr(), w, d_src.data_ptr(), d_len.data_ptr(),
+                  d_dst.data_ptr(), int(docs.size), out.data_ptr(), _lib.stream_ptr())
+    payload = out[: total * w].cpu().numpy()
+    out_spans = np.empty((docs.size, 2), dtype="<u8")
+    out_spans[:, 0] = dst
+    out_spans[:, 1] = lens
+    with open(out_path, "wb") as f:
+        f.write(_HDR.pack(PACKED_MAGIC, PACKED_VERSION, w, total, int(docs.size), HEADER_SIZE + total * w))
+        f.write(payload.tobytes())
+        f.write(out_spans.tobytes())
+
+
 # --- GPU side ---------------------------------------------------------------------
 
 

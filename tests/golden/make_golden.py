@@ -7,6 +7,8 @@ Writes:
                        sample_count answers computed by corpusforge.packed_data
   ref_w{1,2,4}.cfpk    small packed files written by the reference PackedWriter
   ref_w{1,2,4}.npz     get_sample(s, L) for a grid of (s, L), from the reference reader
+  (json) materialize   sha256 of materialize_chunk outputs for seeded permutation chunks
+  (json) perm_sidecar  sha256 of write_permutation .perm files
 The GPU box never runs this script (the reference does not travel).
 """
 
@@ -82,6 +84,30 @@ def main() -> None:
     g["nine"] = {"sample_count_4": rd.sample_count(4), "s0": rd.get_sample(0, 4).tolist(),
                  "s1": rd.get_sample(1, 4).tolist(), "file_len": os.path.getsize(path)}
     rd.close()
+
+    # materialize_chunk (packed_data.py:336-344) of each chunk of a seeded document
+    # permutation, and the .perm sidecar bytes (write_permutation, :285-290)
+    mat = {}
+    for w in (1, 2, 4):
+        rd = ref.open_packed(os.path.join(HERE, f"ref_w{w}.cfpk"))
+        for seed, k in ((0, 1), (3, 3), (11, 4)):
+            perm = ref.make_permutation(rd.doc_count, seed) if seed else ref.Permutation(
+                seed=0, order=np.arange(rd.doc_count, dtype="<u8"))
+            for c, docs in enumerate(ref.chunk(perm, k).assignments):
+                out = os.path.join(HERE, f"_mat_tmp_{w}.cfpk")
+                ref.materialize_chunk(rd, docs, out)
+                mat[f"w{w}_seed{seed}_k{k}_c{c}"] = {"docs": [int(d) for d in docs],
+                                                     "sha256": hashlib.sha256(open(out, "rb").read()).hexdigest()}
+                os.remove(out)
+        rd.close()
+    g["materialize"] = mat
+    side = {}
+    for n, seed in ((0, 0), (10, 0), (1000, 2026), (5, (1 << 64) - 1)):
+        out = os.path.join(HERE, "_perm_tmp.perm")
+        ref.write_permutation(ref.make_permutation(n, seed), out)
+        side[f"{n}_{seed}"] = hashlib.sha256(open(out, "rb").read()).hexdigest()
+        os.remove(out)
+    g["perm_sidecar_sha256"] = side
 
     with open(os.path.join(HERE, "packed_golden.json"), "w") as f:
         json.dump(g, f, indent=1)

@@ -231,3 +231,83 @@ def test_gather_full_size_tiling_property(cuda, tmp_path):
     perm = P.make_permutation(n, 11).order
     pi, pt = ds.gather(perm, L)
     assert torch.equal(pi, gi[torch.from_numpy(perm.astype(np.int64)).cuda()])
+
+
+# ---------------------------------------------------------------------------- materialize / sidecar
+
+
+def _sha(b: bytes) -> str:
+    import hashlib
+
+    return hashlib.sha256(b).hexdigest()
+
+
+def test_materialize_oracle_pinned_to_reference(golden):
+    """The oracle's materialize_chunk bytes equal the reference's (sha256 goldens)."""
+    for key, g in golden["materialize"].items():
+        w = key.split("_")[0][1:]
+        buf = open(os.path.join(GOLDEN, f"ref_w{w}.cfpk"), "rb").read()
+        assert _sha(orc.materialize_bytes(buf, g["docs"])) == g["sha256"], key
+
+
+def test_materialize_host_path_matches_reference(golden, tmp_path):
+    for key, g in golden["materialize"].items():
+        w = key.split("_")[0][1:]
+        r = P.open_packed(os.path.join(GOLDEN, f"ref_w{w}.cfpk"))
+        out = tmp_path / f"{key}.cfpk"
+        P.materialize_chunk(r, np.asarray(g["docs"], dtype=np.uint64), out)
+        assert _sha(out.read_bytes()) == g["sha256"], key
+
+
+def test_perm_sidecar_bytes_match_reference(golden, tmp_path):
+    for key, sha in golden["perm_sidecar_sha256"].items():
+        n, seed = (int(x) for x in key.split("_"))
+        path = tmp_path / f"{key}.perm"
+        P.write_permutation(P.make_permutation(n, seed), path)
+        assert _sha(path.read_bytes()) == sha, key
+        assert P.load_permutation(path) == P.make_permutation(n, seed)
+
+
+@pytest.mark.gpu
+def test_materialize_gpu_matches_reference(cuda, golden, tmp_path):
+    """b2s_gather_documents: the GPU materialize_chunk writes the reference's bytes."""
+    for key, g in golden["materialize"].items():
+        w = key.split("_")[0][1:]
+        r = P.open_packed(os.path.join(GOLDEN, f"ref_w{w}.cfpk"))
+        out = tmp_path / f"{key}.cfpk"
+        P.materialize_chunk_gpu(r, np.asarray(g["docs"], dtype=np.uint64), out)
+        assert _sha(out.read_bytes()) == g["sha256"], key
+    r = P.open_packed(os.path.join(GOLDEN, "ref_w2.cfpk"))
+    with pytest.raises(P.OutOfRangeError):
+        P.materialize_chunk_gpu(r, [0, r.doc_count], tmp_path / "bad.cfpk")
+    P.materialize_chunk_gpu(r, [], tmp_path / "empty.cfpk")  # zero documents: valid empty file
+    e = P.open_packed(tmp_path / "empty.cfpk")
+    assert e.doc_count == 0 and e.token_count == 0
+
+
+@pytest.mark.gpu
+def test_materialize_gpu_full_size(cuda, tmp_path):
+    """2^24 tokens, ragged documents (incl. empty ones), a seeded global shuffle split in 8
+    chunks: every chunk equals the oracle's bytes; re-opened chunks concatenate to the
+    permuted corpus (span contiguity); identity permutation, k=1 -> byte copy."""
+    rng = np.random.default_rng(5)
+    path = tmp_path / "corpus.cfpk"
+    lens = rng.integers(0, 4000, size=8192)
+    lens[::97] = 0
+    with P.PackedWriter(path, 4) as w:
+        for n in lens:
+            w.write_document(rng.integers(0, 128256, size=int(n)))
+    r = P.open_packed(path)
+    ds = P.DevicePackedStream(r)
+    buf = path.read_bytes()
+    perm = P.make_permutation(r.doc_count, 2026)
+    for c, docs in enumerate(P.chunk(perm, 8).assignments):
+        out = tmp_path / f"c{c}.cfpk"
+        P.materialize_chunk_gpu(r, docs, out, stream=ds)
+        assert out.read_bytes() == orc.materialize_bytes(buf, docs), c
+        cr = P.open_packed(out)
+        sp = np.asarray(cr.spans)
+        assert np.array_equal(sp[1:, 0], sp[:-1, 0] + sp[:-1, 1]) and int(sp[:, 1].sum()) == cr.token_count
+    ident = tmp_path / "ident.cfpk"
+    P.materialize_chunk_gpu(r, np.arange(r.doc_count), ident, stream=ds)
+    assert ident.read_bytes() == buf
