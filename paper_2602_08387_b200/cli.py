@@ -4,7 +4,7 @@
     python -m paper_2602_08387_b200.cli train   -c cfg.yaml --root trainer [--set ...] [--json]
     python -m paper_2602_08387_b200.cli plan    -c plan.yaml --root planner
     python -m paper_2602_08387_b200.cli table   --hidden 4096 --ffn 14336 --heads 32 --kv-heads 8 --head-dim 128 \\
-                                                --layers 32 --dp 8 64 1024 --g 1 2 4
+                                                --layers 32 --dp 8 64 1024 --g 1 2 4 [--sweep sweep.jsonl]
 
 Exit codes: 0 success, 1 runtime/IO failure, 2 configuration invalid.
 Diagnostics: one per line, "LEVEL node_id: message".
@@ -51,14 +51,17 @@ def main(argv=None) -> int:
     t.add_argument("--g", type=int, nargs="+", default=[1])
     t.add_argument("--alpha", type=float, default=1e-5)
     t.add_argument("--bandwidth", type=float, default=1e10)
+    t.add_argument("--sweep", default=None, help="fit alpha/B to this collective_sweep JSONL (all-gather, bf16)")
     args = ap.parse_args(argv)
     try:
         if args.cmd == "table":
-            from .comm_planner import CollectiveModel, ModelShape, message_size_table
+            from .comm_planner import CollectiveModel, ModelShape, calibrate, load_sweep, message_size_table
 
             shape = ModelShape(args.hidden, args.ffn, args.heads, args.kv_heads, args.head_dim, args.layers,
                                args.dtype_bytes)
-            sys.stdout.write(message_size_table(shape, args.dp, args.g, CollectiveModel(args.alpha, args.bandwidth)))
+            model = (calibrate(load_sweep(args.sweep), "all_gather", "bfloat16") if args.sweep
+                     else CollectiveModel(args.alpha, args.bandwidth))
+            sys.stdout.write(message_size_table(shape, args.dp, args.g, model))
             return 0
         if args.cmd == "resolve":
             res = _load(args, instantiate=args.instantiate)

@@ -13,6 +13,8 @@ Formulas follow the SPEC exactly:
   message_size_table       CSV dp,blocks_per_unit,shard_bytes,busbw_bytes_per_sec,
                            latency_share,step_comm_seconds               (:566-574, :594)
 
+``calibrate`` / ``calibrated_plan`` fit alpha and B from a measured NVLink 5
+sweep (tools/collective_sweep.py, committed under profiles/) and plan with them.
 ``gpt2_block_param_count`` is the GPT-2 variant this build also trains
 (2-matrix GELU MLP, biases, LayerNorm gains and biases) -- an extension, not in
 the SPEC. ``fit_alpha_beta`` re-fits (alpha, B) from a measured NVLink sweep
@@ -159,6 +161,31 @@ def fit_alpha_beta(points) -> CollectiveModel:
     slope = sxy / sxx if sxx > 0 else 0.0
     alpha = max(0.0, my - slope * mx)
     return CollectiveModel(alpha=alpha, bandwidth=1.0 / slope if slope > 0 else math.inf)
+
+
+def load_sweep(path) -> list:
+    """Rows of a tools/collective_sweep.py JSONL file (op, dtype, ranks, bytes, seconds, ...)."""
+    import json
+
+    with open(path) as f:
+        return [json.loads(line) for line in f if line.strip()]
+
+
+def calibrate(rows, op: str = "all_gather", dtype: str | None = None, min_bytes: int = 0) -> CollectiveModel:
+    """Fit the SPEC ring model t = (p-1)(alpha + m/B) to a measured NVLink
+    sweep. ``bytes`` in a sweep row is the full buffer M; the per-rank
+    ring message is m = M / p."""
+    pts = [(r["ranks"], r["bytes"] / r["ranks"], r["seconds"]) for r in rows
+           if r.get("op") == op and (dtype is None or r["dtype"] == dtype) and r["bytes"] >= min_bytes
+           and r["ranks"] >= 2]
+    if len(pts) < 2:
+        raise ValueError(f"need >= 2 sweep points for {op}/{dtype}, got {len(pts)}")
+    return fit_alpha_beta(pts)
+
+
+def calibrated_plan(shape: ModelShape, dp: int, rows, memory_cap_bytes: int = 1 << 30) -> FsdpPlan:
+    """plan_unit_size with (alpha, B) fitted to the all-gather points of a measured sweep."""
+    return plan_unit_size(shape, shape.layers, dp, calibrate(rows, "all_gather", "bfloat16"), memory_cap_bytes)
 
 
 def shape_of(cfg) -> ModelShape:

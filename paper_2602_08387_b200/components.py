@@ -15,6 +15,7 @@ the reference's registry-factory contract:
   optimizer   adamw_fused      optim.AdamWConfig (fused sharded AdamW on the GPU)
   trainer     fsdp_spmd        trainer.SPMDTrainer (the "gym")
   planner     fsdp_comm        comm_planner plan for a model shape (unit sizing)
+  planner     fsdp_comm_calibrated   the same with (alpha, B) fitted to a measured NVLink sweep
 
 ``default_registry()`` returns a registry with all of them; a user adds a new
 model architecture with ``register_component``.
@@ -123,6 +124,12 @@ def _planner(model, dp, alpha=1e-5, bandwidth=7.7e11, memory_cap_bytes=1 << 30):
     return plan_unit_size(shape, shape.layers, dp, CollectiveModel(alpha, bandwidth), memory_cap_bytes)
 
 
+def _planner_calibrated(model, dp, sweep, memory_cap_bytes=1 << 30):
+    from .comm_planner import calibrated_plan, load_sweep, shape_of
+
+    return calibrated_plan(shape_of(model.cfg), dp, load_sweep(sweep), memory_cap_bytes)
+
+
 def default_registry() -> Registry:
     r = Registry()
     r.register_component(FactoryDescriptor("dataset", "packed_memmap", (P("path", "string"),), _dataset_packed))
@@ -160,4 +167,8 @@ def default_registry() -> Registry:
         (P("model", "dependency", interface="model"), P("dp", "int"),
          P("alpha", "float", required=False, default=1e-5), P("bandwidth", "float", required=False, default=7.7e11),
          P("memory_cap_bytes", "int", required=False, default=1 << 30)), _planner))
+    r.register_component(FactoryDescriptor(
+        "planner", "fsdp_comm_calibrated",
+        (P("model", "dependency", interface="model"), P("dp", "int"), P("sweep", "string"),
+         P("memory_cap_bytes", "int", required=False, default=1 << 30)), _planner_calibrated))
     return r

@@ -106,3 +106,23 @@ def test_fit_alpha_beta():
     pts = [(p, m, cp.ring_allgather_time(true, m, p)) for p in (2, 4, 8) for m in (1e6, 1e7, 1e8, 1e9)]
     fit = cp.fit_alpha_beta(pts)
     assert fit.alpha == pytest.approx(2e-5, rel=1e-6) and fit.bandwidth == pytest.approx(7.5e11, rel=1e-6)
+
+
+def test_calibrate_from_committed_nvlink_sweeps():
+    """alpha/B fitted to the measured B200 sweeps reproduce the sweep times."""
+    import os
+
+    from conftest import ROOT
+    from paper_2602_08387_b200.comm_planner import (ModelShape, calibrate, calibrated_plan, load_sweep,
+                                                    ring_allgather_time)
+
+    for w in (2, 4):
+        rows = load_sweep(os.path.join(ROOT, "profiles", f"r1_collective_sweep_w{w}.jsonl"))
+        m = calibrate(rows, "all_gather", "bfloat16")
+        assert 0 <= m.alpha < 1e-4 and 2e11 < m.bandwidth < 2e12, (w, m)
+        big = [r for r in rows if r.get("op") == "all_gather" and r["bytes"] >= 1 << 28]
+        for r in big:  # the model predicts the large-message times within 25%
+            t = ring_allgather_time(m, r["bytes"] / r["ranks"], r["ranks"])
+            assert abs(t - r["seconds"]) / r["seconds"] < 0.25, (w, r["bytes"], t, r["seconds"])
+        plan = calibrated_plan(ModelShape(4096, 14336, 32, 8, 128, 32), w, rows, memory_cap_bytes=2 << 30)
+        assert 1 <= plan.blocks_per_unit <= 4
