@@ -15,6 +15,7 @@
  *   packed_data.py:257-282 make_permutation           -> b2s_make_permutation
  *   packed_data.py:322-333 chunk                      -> b2s_chunk_bounds
  *   packed_data.py:336-344 materialize_chunk          -> b2s_gather_documents (device copy)
+ *   corpus_index.py:68-107 build_index (newline scan) -> b2s_newline_count / b2s_newline_positions
  * The model/optimizer/FSDP kernels below have no reference implementation
  * (SPEC.md:12 puts the training step out of the reference's scope); their
  * callers are the registered `model`, `optimizer` and `trainer` components
@@ -86,6 +87,17 @@ int b2s_gather_samples(const void* d_payload, int width, uint64_t token_count,
  * spans (exclusive prefix sum of the lengths). */
 int b2s_gather_documents(const void* d_payload, int width, const uint64_t* d_src_start, const uint64_t* d_len,
                          const uint64_t* d_dst_start, int64_t n_docs, void* d_out, b2s_stream_t stream);
+
+/* corpus_index.py:68-107 (build_index), the O(bytes) part on the GPU: the
+ * newline (0x0A) byte positions of a raw buffer (16-byte aligned, n bytes)
+ * split into nblocks chunks of `chunk` bytes (multiple of 16, nblocks*chunk >= n).
+ * Pass 1: d_counts[b] = newlines in chunk b. The caller forms exclusive offsets
+ * d_offsets[b] = sum_{c<b} d_counts[c]. Pass 2: writes base + position of every
+ * newline, ascending, to d_pos[d_offsets[b] ...]. Spans follow on the host. */
+int b2s_newline_count(const void* d_buf, uint64_t n, uint64_t chunk, uint32_t* d_counts, int nblocks,
+                      b2s_stream_t stream);
+int b2s_newline_positions(const void* d_buf, uint64_t n, uint64_t chunk, const uint64_t* d_offsets, int nblocks,
+                          uint64_t base, uint64_t* d_pos, b2s_stream_t stream);
 
 /* Same widening split for `batch` host-staged windows of seq_len+1 tokens
  * stored back to back in d_windows (window b starts at token b*(seq_len+1)):

@@ -49,6 +49,8 @@ _SIGS = {
     "b2s_gather_samples": "piupilpppp",
     "b2s_unpack_windows": "piilppp",
     "b2s_gather_documents": "pippplpp",
+    "b2s_newline_count": "puupip",
+    "b2s_newline_positions": "puupiupp",
     "b2s_gemm": "pilpilpliiiiipiplp",
     "b2s_layernorm_fwd": "ppppppplifp",
     "b2s_rmsnorm_fwd": "ppppplifp",

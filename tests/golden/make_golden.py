@@ -9,6 +9,7 @@ Writes:
   ref_w{1,2,4}.npz     get_sample(s, L) for a grid of (s, L), from the reference reader
   (json) materialize   sha256 of materialize_chunk outputs for seeded permutation chunks
   (json) perm_sidecar  sha256 of write_permutation .perm files
+  idx_*.jsonl          raw fixtures; (json) corpus_index = build_index spans + .didx sha256
 The GPU box never runs this script (the reference does not travel).
 """
 
@@ -108,6 +109,34 @@ def main() -> None:
         side[f"{n}_{seed}"] = hashlib.sha256(open(out, "rb").read()).hexdigest()
         os.remove(out)
     g["perm_sidecar_sha256"] = side
+
+    # corpus_index.build_index (corpus_index.py:68-107) on small raw fixtures
+    from corpusforge import corpus_index as cidx
+
+    fixtures = {
+        "idx_mixed.jsonl": b'{"text":"a"}\n\n{"text":"bc"}\r\n\n\n{"x":1}\n{"text":"no newline at end"}',
+        "idx_trailing.jsonl": b'{"text":"one"}\n{"text":"two"}\n',
+        "idx_only_newlines.jsonl": b"\n\n\n",
+        "idx_empty.jsonl": b"",
+    }
+    rng = np.random.default_rng(11)
+    lines = []
+    for _ in range(3000):
+        k = int(rng.integers(0, 200))
+        lines.append(bytes(rng.integers(32, 127, size=k, dtype=np.uint8)) + (b"\r" if rng.random() < 0.1 else b""))
+    fixtures["idx_random.jsonl"] = b"\n".join(lines)
+    idx = {}
+    for name, data in fixtures.items():
+        path = os.path.join(HERE, name)
+        with open(path, "wb") as f:
+            f.write(data)
+        ix = cidx.build_index(path, buffer_size=7)
+        out = os.path.join(HERE, "_idx_tmp.didx")
+        cidx.write_index(ix, out)
+        idx[name] = {"source_size": ix.source_size, "spans": [[int(a), int(b)] for a, b in ix.spans],
+                     "didx_sha256": hashlib.sha256(open(out, "rb").read()).hexdigest()}
+        os.remove(out)
+    g["corpus_index"] = idx
 
     with open(os.path.join(HERE, "packed_golden.json"), "w") as f:
         json.dump(g, f, indent=1)
