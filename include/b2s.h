@@ -16,6 +16,7 @@
  *   packed_data.py:322-333 chunk                      -> b2s_chunk_bounds
  *   packed_data.py:336-344 materialize_chunk          -> b2s_gather_documents (device copy)
  *   corpus_index.py:68-107 build_index (newline scan) -> b2s_newline_count / b2s_newline_positions
+ *   pipeline.py:264-422    run_pipeline (+ tokenizers) -> b2s_tokenize_corpus (host C++ thread pool)
  * The model/optimizer/FSDP kernels below have no reference implementation
  * (SPEC.md:12 puts the training step out of the reference's scope); their
  * callers are the registered `model`, `optimizer` and `trainer` components
@@ -98,6 +99,30 @@ int b2s_newline_count(const void* d_buf, uint64_t n, uint64_t chunk, uint32_t* d
                       b2s_stream_t stream);
 int b2s_newline_positions(const void* d_buf, uint64_t n, uint64_t chunk, const uint64_t* d_offsets, int nblocks,
                           uint64_t base, uint64_t* d_pos, b2s_stream_t stream);
+
+/* tokenizers.py (ByteTokenizer / WhitespaceTokenizer / BpeTokenizer), host C++.
+ * kind: 0 byte, 1 whitespace, 2 bpe; h_pieces = n_pieces x (u32 length, UTF-8
+ * bytes) vocabulary (id = index); h_merges = n_merges x (left, right) in the same
+ * encoding (rank = index); unk / eod ids (-1: none). Returns a handle (null on error). */
+void* b2s_tokenizer_create(int kind, const void* h_pieces, int64_t n_pieces, const void* h_merges, int64_t n_merges,
+                           int64_t unk_id, int64_t eod_id);
+void b2s_tokenizer_destroy(void* tokenizer);
+/* encode one text given as UTF-8 ('surrogatepass' for lone surrogates) into at
+ * most cap ids; *h_n = number of ids (B2S_ERANGE if > cap). B2S_EINVAL when the
+ * byte / bpe tokenizer meets a lone surrogate (reference: UnicodeEncodeError). */
+int b2s_tokenizer_encode(void* tokenizer, const char* h_text, int64_t len, uint32_t* h_out, int64_t cap,
+                         int64_t* h_n);
+
+/* pipeline.py:264-422 run_pipeline, as a host C++ thread pool (SURVEY §8(f)
+ * rank 1): tokenize documents h_spans[2*i] (byte offset), h_spans[2*i+1]
+ * (length) of raw_path, in index order, with `workers` threads over batches of
+ * batch_size documents, into the CFPKD001 file out_path -- byte-identical for
+ * any `workers` (order restored by the writer). h_stats (optional, 4 x i64):
+ * documents, skipped, malformed, tokens. B2S_EINVAL on a lone surrogate under
+ * the byte / bpe tokenizers (the reference run fails there too). */
+int b2s_tokenize_corpus(const char* raw_path, const uint64_t* h_spans, int64_t n_docs, void* tokenizer,
+                        const char* text_key, int append_eod, int width, int workers, int batch_size,
+                        const char* out_path, int64_t* h_stats);
 
 /* Same widening split for `batch` host-staged windows of seq_len+1 tokens
  * stored back to back in d_windows (window b starts at token b*(seq_len+1)):

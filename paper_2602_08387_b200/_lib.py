@@ -51,6 +51,8 @@ _SIGS = {
     "b2s_gather_documents": "pippplpp",
     "b2s_newline_count": "puupip",
     "b2s_newline_positions": "puupiupp",
+    "b2s_tokenizer_encode": "pplplp",
+    "b2s_tokenize_corpus": "pplppiiiipp",
     "b2s_gemm": "pilpilpliiiiipiplp",
     "b2s_layernorm_fwd": "ppppppplifp",
     "b2s_rmsnorm_fwd": "ppppplifp",
@@ -108,6 +110,10 @@ def load():
         fn = getattr(lib, name)
         fn.restype = c_int
         fn.argtypes = [_CT[c] for c in sig]
+    lib.b2s_tokenizer_create.restype = c_void_p
+    lib.b2s_tokenizer_create.argtypes = [c_int, c_void_p, c_int64, c_void_p, c_int64, c_int64, c_int64]
+    lib.b2s_tokenizer_destroy.restype = None
+    lib.b2s_tokenizer_destroy.argtypes = [c_void_p]
     for name, sig in _SIZE_FNS.items():
         fn = getattr(lib, name)
         fn.restype = c_int64
