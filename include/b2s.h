@@ -157,6 +157,14 @@ int b2s_layernorm_fwd(const float* d_x, const void* d_g, const void* d_b, void* 
                       float* d_rstd, float* d_x_copy, int64_t M, int D, float eps, b2s_stream_t stream);
 int b2s_rmsnorm_fwd(const float* d_x, const void* d_g, void* d_y, float* d_rstd, float* d_x_copy,
                     int64_t M, int D, float eps, b2s_stream_t stream);
+/* Residual-add forms: x_out = x + res (res = the previous sublayer's output,
+ * bf16 [M, D]; x_out the new fp32 residual stream, may alias nothing else),
+ * then y = norm(x_out). Replaces an fp32 add-reduce in the producing GEMM. */
+int b2s_layernorm_fwd_res(const float* d_x, const void* d_res, const void* d_g, const void* d_b, void* d_y,
+                          float* d_mean, float* d_rstd, float* d_x_out, int64_t M, int D, float eps,
+                          b2s_stream_t stream);
+int b2s_rmsnorm_fwd_res(const float* d_x, const void* d_res, const void* d_g, void* d_y, float* d_rstd,
+                        float* d_x_out, int64_t M, int D, float eps, b2s_stream_t stream);
 /* dx (fp32) += norm backward of dy (bf16); d_dx_bf16 (optional) <- bf16(dx);
  * d_dg / d_db (fp32 [D], optional) += parameter grads; d_dxsum (optional)
  * += column sums of the updated dx (the bias gradient of the linear layer
@@ -247,6 +255,11 @@ int b2s_layernorm_fwd_f32(const float* d_x, const float* d_g, const float* d_b, 
 int b2s_rmsnorm_fwd_f32(const float* d_x, const float* d_g, float* d_y, float* d_rstd, float* d_x_copy,
                         int64_t M, int D, float eps, b2s_stream_t stream);
 /* d_dx_copy: optional second copy of the updated dx (usually null in fp32 mode). */
+int b2s_layernorm_fwd_res_f32(const float* d_x, const float* d_res, const float* d_g, const float* d_b, float* d_y,
+                              float* d_mean, float* d_rstd, float* d_x_out, int64_t M, int D, float eps,
+                              b2s_stream_t stream);
+int b2s_rmsnorm_fwd_res_f32(const float* d_x, const float* d_res, const float* d_g, float* d_y, float* d_rstd,
+                            float* d_x_out, int64_t M, int D, float eps, b2s_stream_t stream);
 int b2s_layernorm_bwd_f32(const float* d_x, const float* d_dy, const float* d_g, const float* d_mean,
                           const float* d_rstd, float* d_dx, float* d_dx_copy, float* d_dg, float* d_db,
                           float* d_dxsum, float* d_work, int64_t M, int D, b2s_stream_t stream);

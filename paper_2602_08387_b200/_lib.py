@@ -56,6 +56,10 @@ _SIGS = {
     "b2s_gemm": "pilpilpliiiiipiplp",
     "b2s_layernorm_fwd": "ppppppplifp",
     "b2s_rmsnorm_fwd": "ppppplifp",
+    "b2s_layernorm_fwd_res": "pppppppplifp",
+    "b2s_rmsnorm_fwd_res": "pppppplifp",
+    "b2s_layernorm_fwd_res_f32": "pppppppplifp",
+    "b2s_rmsnorm_fwd_res_f32": "pppppplifp",
     "b2s_layernorm_bwd": "ppppppppppplip",
     "b2s_rmsnorm_bwd": "ppppppppplip",
     "b2s_colsum_accumulate": "pililppp",

@@ -76,11 +76,14 @@ __device__ __forceinline__ float row_sum(float v, float* scratch, int& toggle) {
   }
 }
 
+// res (optional): the sublayer output y_prev [M, D] (activation type) to add to x
+// first -- the residual add of the previous GEMM; x_copy then receives x + res
+// (the new residual stream), which is what gets normalised.
 template <int D, int TPR, bool RMS, typename T = __nv_bfloat16>
 __global__ void __launch_bounds__(kRowThreads) norm_fwd_kernel(
     const float* __restrict__ x, const T* __restrict__ g, const T* __restrict__ b,
     T* __restrict__ y, float* __restrict__ mean_out, float* __restrict__ rstd_out,
-    float* __restrict__ x_copy, int64_t M, float eps) {
+    float* __restrict__ x_copy, int64_t M, float eps, const T* __restrict__ res) {
   constexpr int V = D / (TPR * 4);  // float4 vectors per thread
   static_assert(V * TPR * 4 == D, "hidden size must tile the row threads");
   __shared__ float scratch[32];
@@ -101,6 +104,11 @@ __global__ void __launch_bounds__(kRowThreads) norm_fwd_kernel(
 #pragma unroll
     for (int j = 0; j < V; ++j) {
       xv[j] = ld4(xr + t * 4 + j * TPR * 4);
+      if (res) {
+        float r4[4];
+        ld_v4(res + row * D + t * 4 + j * TPR * 4, r4);
+        xv[j].x += r4[0]; xv[j].y += r4[1]; xv[j].z += r4[2]; xv[j].w += r4[3];
+      }
       s += xv[j].x + xv[j].y + xv[j].z + xv[j].w;
     }
     if (x_copy) {
@@ -606,12 +614,12 @@ static unsigned flat_grid(int64_t n, int per_thread = 4) {
 
 template <bool RMS, typename T = __nv_bfloat16>
 static int norm_fwd(const float* x, const void* g, const void* b, void* y, float* mean, float* rstd,
-                    float* x_copy, int64_t M, int D, float eps, cudaStream_t st) {
+                    float* x_copy, int64_t M, int D, float eps, cudaStream_t st, const void* res = nullptr) {
   auto go = [&](auto kern, int tpr) {
     int64_t blocks = (M * tpr + kRowThreads - 1) / kRowThreads;
     const int64_t cap = (int64_t)kNumSMs * 8;
     kern<<<(unsigned)(blocks < cap ? blocks : cap), kRowThreads, 0, st>>>(
-        x, (const T*)g, (const T*)b, (T*)y, mean, rstd, x_copy, M, eps);
+        x, (const T*)g, (const T*)b, (T*)y, mean, rstd, x_copy, M, eps, (const T*)res);
     return check_launch("norm_fwd");
   };
   switch (D) {
@@ -763,6 +771,25 @@ int b2s_rmsnorm_bwd_f32(const float* d_x, const float* d_dy, const float* d_g, c
                         b2s_stream_t stream) {
   return ew::norm_bwd<true, float>(d_x, d_dy, d_g, nullptr, d_rstd, d_dx, d_dx_copy, d_dg, nullptr, d_dxsum,
                                    d_work, M, D, B2S_ST(stream));
+}
+int b2s_layernorm_fwd_res(const float* d_x, const void* d_res, const void* d_g, const void* d_b, void* d_y,
+                          float* d_mean, float* d_rstd, float* d_x_out, int64_t M, int D, float eps,
+                          b2s_stream_t stream) {
+  return ew::norm_fwd<false>(d_x, d_g, d_b, d_y, d_mean, d_rstd, d_x_out, M, D, eps, B2S_ST(stream), d_res);
+}
+int b2s_rmsnorm_fwd_res(const float* d_x, const void* d_res, const void* d_g, void* d_y, float* d_rstd,
+                        float* d_x_out, int64_t M, int D, float eps, b2s_stream_t stream) {
+  return ew::norm_fwd<true>(d_x, d_g, nullptr, d_y, nullptr, d_rstd, d_x_out, M, D, eps, B2S_ST(stream), d_res);
+}
+int b2s_layernorm_fwd_res_f32(const float* d_x, const float* d_res, const float* d_g, const float* d_b, float* d_y,
+                              float* d_mean, float* d_rstd, float* d_x_out, int64_t M, int D, float eps,
+                              b2s_stream_t stream) {
+  return ew::norm_fwd<false, float>(d_x, d_g, d_b, d_y, d_mean, d_rstd, d_x_out, M, D, eps, B2S_ST(stream), d_res);
+}
+int b2s_rmsnorm_fwd_res_f32(const float* d_x, const float* d_res, const float* d_g, float* d_y, float* d_rstd,
+                            float* d_x_out, int64_t M, int D, float eps, b2s_stream_t stream) {
+  return ew::norm_fwd<true, float>(d_x, d_g, nullptr, d_y, nullptr, d_rstd, d_x_out, M, D, eps, B2S_ST(stream),
+                                   d_res);
 }
 int64_t b2s_norm_work_floats(int D) { return (int64_t)ew::kNormBwdMaxBlocks * 3 * D; }
 

@@ -226,15 +226,18 @@ class _Slot:
     """The forward buffers of one transformer block (see _Acts)."""
 
     __slots__ = ("xa", "xb", "xn", "ln_a", "mean_a", "rstd_a", "ln_b", "mean_b", "rstd_b", "qkv", "o", "lse",
-                 "hpre", "gu", "h")
+                 "ya", "yb", "hpre", "gu", "h")
 
 
 class _Acts:
     """Activation buffers for one (B, T): saved forward tensors + backward scratch.
 
-    Residual stream (fp32): block i reads xa, forwards it (in the norm kernel)
-    into xb to which the attention output is added, then forwards xb into xn
-    (= the next block's xa) to which the MLP output is added.
+    Residual stream (fp32): the attention output projection writes its result y1
+    (bf16, bias included) and the next norm kernel forms xb = xa + y1 while it
+    normalises; likewise the MLP output y2 is added into xn (= the next block's
+    xa) by the next block's first norm (or the final norm). The fp32 residual
+    is therefore written once per sublayer by a norm kernel instead of being
+    read-modify-written by a TMA add-reduce in the GEMM epilogue.
 
     Without checkpointing every block owns its slot (all saved). With
     ``checkpoint`` only the block inputs xa (L + 1 fp32 [M, d] buffers) are
@@ -249,6 +252,7 @@ class _Acts:
         self.B, self.T, self.M = B, T, M
         self.checkpoint = checkpoint
         self.xin = [e(M, d, dt=f32) for _ in range(L + 1)]  # block inputs; xin[L] enters the head
+        self.ya, self.yb = e(M, d), e(M, d)  # attention / MLP sublayer outputs (bias added)
 
         def slot(i, xb=None):
             sl = _Slot()
@@ -259,6 +263,7 @@ class _Acts:
             sl.qkv = e(M, cfg.qkv_dim)
             sl.o = e(M, cfg.n_head * cfg.head_dim)
             sl.lse = e(B, cfg.n_head, T, dt=f32)
+            sl.ya, sl.yb = self.ya, self.yb  # sublayer outputs: consumed by the next norm, shared
             sl.hpre = e(M, f) if cfg.arch == "gpt2" else None
             sl.gu = e(M, 2 * f) if cfg.arch == "llama" else None
             sl.h = e(M, f)
@@ -328,38 +333,47 @@ class DecoderLM(torch.nn.Module):
         return self._rope[T]
 
     # ------------------------------------------------------------------ step
-    def _block_forward(self, i, S, T, rope, with_output=True):
-        """Block i's forward over slot S; with_output=False skips the MLP output GEMM
-        (the checkpoint recompute needs every saved input, not the block output)."""
+    def _block_forward(self, i, S, T, rope, pending=None, with_output=True):
+        """Block i's forward over slot S. ``pending`` = (x, y) of the previous sublayer: the
+        first norm forms S.xa = x + y while normalising (None: S.xa is already the input).
+        Leaves (S.xb, S.yb) pending for the next norm; with_output=False (the checkpoint
+        recompute) skips the MLP output GEMM, whose result the backward does not need."""
         cfg, U = self.cfg, self.params.unit(i + 1)
         M, d = S.xa.shape
         B = M // T
         H, Hkv, dh, eps = cfg.n_head, cfg.n_kv_head, cfg.head_dim, cfg.norm_eps
-        if cfg.arch == "gpt2":
-            ops.layernorm_fwd(S.xa, U.p("ln1_g"), U.p("ln1_b"), eps, S.ln_a, S.mean_a, S.rstd_a, x_copy=S.xb)
+        gpt2 = cfg.arch == "gpt2"
+        if gpt2:
+            if pending is None:
+                ops.layernorm_fwd(S.xa, U.p("ln1_g"), U.p("ln1_b"), eps, S.ln_a, S.mean_a, S.rstd_a)
+            else:
+                ops.layernorm_fwd_res(pending[0], pending[1], U.p("ln1_g"), U.p("ln1_b"), eps, S.ln_a, S.mean_a,
+                                      S.rstd_a, S.xa)
             ops.linear(S.ln_a, U.p("qkv_w"), bias=U.p("qkv_b"), out=S.qkv)
         else:
-            ops.rmsnorm_fwd(S.xa, U.p("attn_norm"), eps, S.ln_a, S.rstd_a, x_copy=S.xb)
+            if pending is None:
+                ops.rmsnorm_fwd(S.xa, U.p("attn_norm"), eps, S.ln_a, S.rstd_a)
+            else:
+                ops.rmsnorm_fwd_res(pending[0], pending[1], U.p("attn_norm"), eps, S.ln_a, S.rstd_a, S.xa)
             ops.linear(S.ln_a, U.p("wqkv"), out=S.qkv)
             ops.rope(S.qkv, T, H + Hkv, dh, *rope)
         ops.attn_fwd(S.qkv, B, T, H, Hkv, dh, o=S.o, lse=S.lse)
-        # residual: xb (= copy of xa) += o @ Wo^T (+ bias)  (fp32 TMA add-reduce)
-        gpt2 = cfg.arch == "gpt2"
-        ops.gemm(S.o, U.p("proj_w" if gpt2 else "wo"), a_mn=False, b_mn=False, M=M, N=d, K=H * dh, out=S.xb,
-                 accumulate=True, bias=U.p("proj_b") if gpt2 else None)
-        xn = S.xn if with_output else None
+        # y1 = o @ Wo^T (+ bias); the next norm adds it into the residual: xb = xa + y1
+        ops.gemm(S.o, U.p("proj_w" if gpt2 else "wo"), a_mn=False, b_mn=False, M=M, N=d, K=H * dh, out=S.ya,
+                 bias=U.p("proj_b") if gpt2 else None)
         if gpt2:
-            ops.layernorm_fwd(S.xb, U.p("ln2_g"), U.p("ln2_b"), eps, S.ln_b, S.mean_b, S.rstd_b, x_copy=xn)
+            ops.layernorm_fwd_res(S.xa, S.ya, U.p("ln2_g"), U.p("ln2_b"), eps, S.ln_b, S.mean_b, S.rstd_b, S.xb)
             ops.linear(S.ln_b, U.p("fc_w"), bias=U.p("fc_b"), out=S.h, act=1, aux=S.hpre)
             if with_output:
-                ops.gemm(S.h, U.p("fc2_w"), a_mn=False, b_mn=False, M=M, N=d, K=cfg.d_ff, out=S.xn,
-                         accumulate=True, bias=U.p("fc2_b"))
+                ops.gemm(S.h, U.p("fc2_w"), a_mn=False, b_mn=False, M=M, N=d, K=cfg.d_ff, out=S.yb,
+                         bias=U.p("fc2_b"))
         else:
-            ops.rmsnorm_fwd(S.xb, U.p("mlp_norm"), eps, S.ln_b, S.rstd_b, x_copy=xn)
+            ops.rmsnorm_fwd_res(S.xa, S.ya, U.p("mlp_norm"), eps, S.ln_b, S.rstd_b, S.xb)
             ops.linear(S.ln_b, U.p("w13"), out=S.gu)
             ops.swiglu_fwd(S.gu, S.h)
             if with_output:
-                ops.gemm(S.h, U.p("w2"), a_mn=False, b_mn=False, M=M, N=d, K=cfg.d_ff, out=S.xn, accumulate=True)
+                ops.gemm(S.h, U.p("w2"), a_mn=False, b_mn=False, M=M, N=d, K=cfg.d_ff, out=S.yb)
+        return (S.xb, S.yb)
 
     def forward_backward(self, tokens, targets, hooks=None, compute_grad: bool = True):
         """One training forward + backward over int64 tokens/targets [B, T].
@@ -390,16 +404,18 @@ class DecoderLM(torch.nn.Module):
         pre(0)
         E = P.unit(0)
         ops.embedding_fwd(tok, E.p("wte"), E.p("wpe") if gpt2 else None, T, out=A.xin[0])
+        pending = None
         for i in range(L):
             pre(i + 1)
-            self._block_forward(i, A.slots[i], T, rope)
+            pending = self._block_forward(i, A.slots[i], T, rope, pending)
         pre(L + 1)
         Hd = P.unit(L + 1)
-        xf = A.xin[L]
+        xf = A.xin[L]  # = the last block's xb + its MLP output, formed by the final norm
         if gpt2:
-            ops.layernorm_fwd(xf, Hd.p("lnf_g"), Hd.p("lnf_b"), eps, A.ln_f, A.mean_f, A.rstd_f)
+            ops.layernorm_fwd_res(pending[0], pending[1], Hd.p("lnf_g"), Hd.p("lnf_b"), eps, A.ln_f, A.mean_f,
+                                  A.rstd_f, xf)
         else:
-            ops.rmsnorm_fwd(xf, Hd.p("lnf_g"), eps, A.ln_f, A.rstd_f)
+            ops.rmsnorm_fwd_res(pending[0], pending[1], Hd.p("lnf_g"), eps, A.ln_f, A.rstd_f, xf)
         w_head = E.p("wte") if cfg.tie_embeddings else Hd.p("lm_head")
         ops.linear(A.ln_f, w_head, out=A.logits)
         ops.cross_entropy(A.logits, cfg.vocab_size, tgt, A.loss_rows, grad_scale=1.0 / M, write_grad=compute_grad)

@@ -201,6 +201,20 @@ def rmsnorm_fwd(x, g, eps=1e-5, y=None, rstd=None, x_copy=None):
     return y, rstd
 
 
+def layernorm_fwd_res(x, res, g, b, eps, y, mean, rstd, x_out):
+    """x_out = x + res (the residual add of the previous sublayer), y = LayerNorm(x_out)."""
+    M, D = x.shape
+    _call("b2s_layernorm_fwd_res" + _sfx(y), x.data_ptr(), res.data_ptr(), g.data_ptr(), b.data_ptr(), y.data_ptr(),
+          mean.data_ptr(), rstd.data_ptr(), x_out.data_ptr(), M, D, eps, _sp())
+
+
+def rmsnorm_fwd_res(x, res, g, eps, y, rstd, x_out):
+    """x_out = x + res, y = RMSNorm(x_out)."""
+    M, D = x.shape
+    _call("b2s_rmsnorm_fwd_res" + _sfx(y), x.data_ptr(), res.data_ptr(), g.data_ptr(), y.data_ptr(),
+          rstd.data_ptr(), x_out.data_ptr(), M, D, eps, _sp())
+
+
 def layernorm_bwd(x, dy, g, mean, rstd, dx, dx_bf16=None, dg=None, db=None, dxsum=None):
     """dx += LN backward; dg/db (fp32) accumulated; dxsum += colsum(updated dx)."""
     M, D = x.shape
