@@ -239,11 +239,12 @@ __global__ void __launch_bounds__(Cfg<BN, CG, EW>::kThreads, 1)
     else mbar_wait(&rfull[i % kRing], (i / kRing) & 1);
     return *reinterpret_cast<volatile int*>(&ring[i % kRing]);
   };
-  auto ring_release = [&](int i) {
-    if constexpr (CG == 2) {
-      if (!leader) { mbar_arrive_cluster(mapa_shared(smem_u32(&rempty[i % kRing]), 0)); return; }
-    }
-    mbar_arrive(&rempty[i % kRing]);
+  // release slot i after reading `tile` from it (relaxed, data-dependent on the read)
+  auto ring_release = [&](int i, int tile) {
+    const uint32_t rank_of_leader = 0;
+    mbar_arrive_cluster_relaxed_after(CG == 2 ? mapa_shared(smem_u32(&rempty[i % kRing]), rank_of_leader)
+                                              : smem_u32(&rempty[i % kRing]),
+                                      tile);
   };
 
   if (warp == 0) {
@@ -270,7 +271,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, EW>::kThreads, 1)
           }
         } else {
           tile = ring_get(it);
-          ring_release(it);
+          ring_release(it, tile);
         }
         if (tile >= num_tiles) break;
         if (leader) next = sched ? tstride + atomicAdd(sched, 1) : tile + tstride;
@@ -326,7 +327,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, EW>::kThreads, 1)
       uint32_t acc_phase = 0;
       for (int it = 0;; ++it) {
         const int tile = ring_get(it);
-        ring_release(it);
+        ring_release(it, tile);
         if (tile >= num_tiles) break;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
@@ -395,7 +396,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, EW>::kThreads, 1)
     for (int it = 0;; ++it) {
       const int tile = ring_get(it);
       __syncwarp();
-      if (lane == 0) ring_release(it);
+      if (lane == 0) ring_release(it, tile);
       if (tile >= num_tiles) break;
       load_aux(tile, half);  // first chunk's pre-activations: in flight while the MMAs finish
       const int mn = tile % (num_m * num_n);
@@ -407,6 +408,14 @@ __global__ void __launch_bounds__(Cfg<BN, CG, EW>::kThreads, 1)
       for (int c = half; c < BN / 32; c += kEG) {
         const int col0 = n0 + c * 32;
         const bool live = rbase < M && col0 < N;  // warp-uniform
+        // the chunk's bias (same 32 values for every lane): loads issued before the
+        // TMEM wait so their latency overlaps it
+        uint4 bias4[4];
+        if (epi.bias && live) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (col0 + 8 * k < N) bias4[k] = __ldg(reinterpret_cast<const uint4*>(epi.bias + col0 + 8 * k));
+        }
         uint32_t r[32];
         tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, r);
         tmem_wait_ld();
@@ -414,7 +423,8 @@ __global__ void __launch_bounds__(Cfg<BN, CG, EW>::kThreads, 1)
           tc_fence_before();
           __syncwarp();
           if (lane == 0) {
-            if constexpr (CG == 2) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));
+            // relaxed: the accumulator hand-off is a TMEM hazard, ordered by the tcgen05 fences
+            if constexpr (CG == 2) mbar_arrive_cluster_relaxed(mapa_shared(smem_u32(&tempty[acc]), 0));
             else mbar_arrive(&tempty[acc]);
           }
         }
@@ -427,12 +437,12 @@ __global__ void __launch_bounds__(Cfg<BN, CG, EW>::kThreads, 1)
         for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
         if (epi.bias) {
 #pragma unroll
-          for (int i = 0; i < 32; i += 8) {
-            if (col0 + i < N) {
+          for (int k = 0; k < 4; ++k) {
+            if (col0 + 8 * k < N) {
               float bb[8];
-              unpack8(*reinterpret_cast<const bf16x8*>(epi.bias + col0 + i), bb);
+              unpack8(*reinterpret_cast<const bf16x8*>(&bias4[k]), bb);
 #pragma unroll
-              for (int j = 0; j < 8; ++j) v[i + j] += bb[j];
+              for (int j = 0; j < 8; ++j) v[8 * k + j] += bb[j];
             }
           }
         }

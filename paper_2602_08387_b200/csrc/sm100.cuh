@@ -234,6 +234,19 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity
       "r"(parity)
       : "memory");
 }
+// Relaxed remote arrive: no release fence. For hand-offs whose only hazard is on
+// TMEM, which tcgen05.fence::before/after_thread_sync already orders.
+__device__ __forceinline__ void mbar_arrive_cluster_relaxed(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+// Relaxed arrive that cannot issue before `dep` (a value the thread just read from
+// the slot being released) is in a register: the read is complete, so the
+// writer that waits on this barrier can never overwrite data still being read.
+__device__ __forceinline__ void mbar_arrive_cluster_relaxed_after(uint32_t cluster_addr, int dep) {
+  asm volatile("{\n\t.reg .b32 d;\n\tmov.b32 d, %1;\n\t"
+               "mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];\n\t}" ::"r"(cluster_addr), "r"(dep)
+               : "memory");
+}
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
