@@ -170,3 +170,69 @@ def test_fp32_loss_curve_20_steps(cuda, tmp_path, preset):
     assert max(rel) < TOL, list(zip(gpu, ref, rel))
     print(f"{preset}: 20-step max loss rel {max(rel):.2e}, loss {gpu[0]:.4f} -> {gpu[-1]:.4f}")
     assert gpu[-1] < gpu[0] - 0.1
+
+
+def test_fp32_gpt2_124m_first_step_matches_oracle(cuda, tmp_path):
+    """BASELINE configs[1]'s model (GPT-2 124M, vocab 50257) in fp32 mode: the first step's loss
+    and every parameter gradient within 1e-4 of the CPU fp32 oracle (1 sequence of 1024 tokens)."""
+    from paper_2602_08387_b200.data import PackedDataLoader, Sampler, make_synthetic_packed
+    from paper_2602_08387_b200.model import PRESETS, DecoderLM, init_params
+    from paper_2602_08387_b200.optim import AdamWConfig
+    from paper_2602_08387_b200.packed import open_packed
+    from paper_2602_08387_b200.trainer import SPMDTrainer
+
+    cfg = PRESETS["gpt2-124m"]
+    path = str(tmp_path / "data.cfpk")
+    make_synthetic_packed(path, 1 << 16, cfg.vocab_size, kind="markov", seed=4)
+    dl = PackedDataLoader(open_packed(path), 1, 1024, Sampler(shuffle=True, seed=2))
+    tr = SPMDTrainer(DecoderLM(cfg, precision="fp32"), AdamWConfig(), dl).setup()
+    x, y = tr.dataloader.batch(0)
+    tr.engine.begin_step()
+    loss = float(tr.model.forward_backward(x, y, hooks=tr.engine).item())
+    gpu = tr.params.grads_full_fp32()
+    ox, oy = _oracle_batch(path, tr.dataloader.sample_ids(0), 1024)
+    ot = OracleTrainer(cfg, init_params(cfg, 0))
+    oloss = ot.model(ox, oy)
+    oloss.backward()
+    assert abs(loss - oloss.item()) / oloss.item() < TOL, (loss, oloss.item())
+    worst = 0.0
+    for k, g in ot.grads().items():
+        gg = gpu[k][: g.shape[0]] if g.dim() else gpu[k]
+        rel = float((gg.double() - g.double()).norm() / (g.double().norm() + 1e-30))
+        worst = max(worst, rel)
+        assert rel < TOL, (k, rel)
+    print(f"gpt2-124m fp32: loss rel {abs(loss - oloss.item()) / oloss.item():.2e}, worst grad rel {worst:.2e}")
+
+
+def test_fp32_llama1b_shape_first_step_matches_oracle(cuda, tmp_path):
+    """The Llama-1B block and vocabulary shapes (d 2048, GQA 32/8, FFN 8192, vocab 128256, tied)
+    with 2 layers, fp32 mode: first-step loss and gradients within 1e-4 of the CPU oracle."""
+    from dataclasses import replace
+
+    from paper_2602_08387_b200.data import PackedDataLoader, Sampler, make_synthetic_packed
+    from paper_2602_08387_b200.model import PRESETS, DecoderLM, init_params
+    from paper_2602_08387_b200.optim import AdamWConfig
+    from paper_2602_08387_b200.packed import open_packed
+    from paper_2602_08387_b200.trainer import SPMDTrainer
+
+    cfg = replace(PRESETS["llama-1b"], n_layer=2)
+    path = str(tmp_path / "data.cfpk")
+    make_synthetic_packed(path, 1 << 16, cfg.vocab_size, kind="markov", seed=6)
+    dl = PackedDataLoader(open_packed(path), 1, 512, Sampler(shuffle=True, seed=3))
+    tr = SPMDTrainer(DecoderLM(cfg, precision="fp32"), AdamWConfig(), dl).setup()
+    x, y = tr.dataloader.batch(0)
+    tr.engine.begin_step()
+    loss = float(tr.model.forward_backward(x, y, hooks=tr.engine).item())
+    gpu = tr.params.grads_full_fp32()
+    ox, oy = _oracle_batch(path, tr.dataloader.sample_ids(0), 512)
+    ot = OracleTrainer(cfg, init_params(cfg, 0))
+    oloss = ot.model(ox, oy)
+    oloss.backward()
+    assert abs(loss - oloss.item()) / oloss.item() < TOL, (loss, oloss.item())
+    worst = 0.0
+    for k, g in ot.grads().items():
+        gg = gpu[k][: g.shape[0]] if g.dim() else gpu[k]
+        rel = float((gg.double() - g.double()).norm() / (g.double().norm() + 1e-30))
+        worst = max(worst, rel)
+        assert rel < TOL, (k, rel)
+    print(f"llama-1b shape fp32: loss rel {abs(loss - oloss.item()) / oloss.item():.2e}, worst grad rel {worst:.2e}")
