@@ -16,6 +16,8 @@ the reference's registry-factory contract:
   trainer     fsdp_spmd        trainer.SPMDTrainer (the "gym")
   planner     fsdp_comm        comm_planner plan for a model shape (unit sizing)
   planner     fsdp_comm_calibrated   the same with (alpha, B) fitted to a measured NVLink sweep
+  tokenizer   byte | whitespace | bpe   tokenizers.load_tokenizer (C++ encoder)
+  pipeline    tokenize         a configured run_pipeline job (C++ thread pool)
 
 ``default_registry()`` returns a registry with all of them; a user adds a new
 model architecture with ``register_component``.
@@ -130,6 +132,40 @@ def _planner_calibrated(model, dp, sweep, memory_cap_bytes=1 << 30):
     return calibrated_plan(shape_of(model.cfg), dp, load_sweep(sweep), memory_cap_bytes)
 
 
+def _tokenizer(kind):
+    def build(vocab_path=None, merges_path=None, eod_token_id=None, unk_token_id=None):
+        from .tokenizers import TokenizerSpec, load_tokenizer
+
+        return load_tokenizer(TokenizerSpec(kind, vocab_path, merges_path, eod_token_id, unk_token_id))
+
+    return build
+
+
+class TokenizeJob:
+    """A configured tokenize run (raw JSONL + its .didx index -> CFPKD001), run() -> stats."""
+
+    def __init__(self, raw_path, out_path, tokenizer, workers, batch_size, append_eod, text_key):
+        from .pipeline import PipelineConfig
+
+        self.raw_path, self.tokenizer = raw_path, tokenizer
+        self.cfg = PipelineConfig(out_path, workers=workers, batch_size=batch_size, append_eod=append_eod,
+                                  text_key=text_key)
+
+    def run(self):
+        from . import corpus_index as CI
+        from .pipeline import run_pipeline
+
+        side = CI.index_sidecar_path(self.raw_path)
+        index = CI.load_index(side) if os.path.exists(side) else CI.build_index(self.raw_path)
+        return run_pipeline(self.raw_path, index, self.tokenizer, self.cfg)
+
+
+def _pipeline(raw_path, out_path, tokenizer, workers=0, batch_size=128, append_eod=True, text_key="text"):
+    from .pipeline import default_workers
+
+    return TokenizeJob(raw_path, out_path, tokenizer, workers or default_workers(), batch_size, append_eod, text_key)
+
+
 def default_registry() -> Registry:
     r = Registry()
     r.register_component(FactoryDescriptor("dataset", "packed_memmap", (P("path", "string"),), _dataset_packed))
@@ -167,6 +203,17 @@ def default_registry() -> Registry:
         (P("model", "dependency", interface="model"), P("dp", "int"),
          P("alpha", "float", required=False, default=1e-5), P("bandwidth", "float", required=False, default=7.7e11),
          P("memory_cap_bytes", "int", required=False, default=1 << 30)), _planner))
+    for kind in ("byte", "whitespace", "bpe"):
+        r.register_component(FactoryDescriptor(
+            "tokenizer", kind,
+            (P("vocab_path", "string", required=False), P("merges_path", "string", required=False),
+             P("eod_token_id", "int", required=False), P("unk_token_id", "int", required=False)), _tokenizer(kind)))
+    r.register_component(FactoryDescriptor(
+        "pipeline", "tokenize",
+        (P("raw_path", "string"), P("out_path", "string"), P("tokenizer", "dependency", interface="tokenizer"),
+         P("workers", "int", required=False, default=0), P("batch_size", "int", required=False, default=128),
+         P("append_eod", "bool", required=False, default=True), P("text_key", "string", required=False,
+                                                                  default="text")), _pipeline))
     r.register_component(FactoryDescriptor(
         "planner", "fsdp_comm_calibrated",
         (P("model", "dependency", interface="model"), P("dp", "int"), P("sweep", "string"),
