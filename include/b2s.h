@@ -147,6 +147,18 @@ int b2s_gemm(const void* d_A, int a_mn_major, int64_t lda, const void* d_B, int 
              int64_t ldb, void* d_C, int64_t ldc, int c_f32, int M, int N, int K, int accumulate,
              const void* d_bias, int act, void* d_aux, int64_t ld_aux, b2s_stream_t stream);
 
+/* Llama MLP with the SwiGLU fused into the GEMM epilogues (bf16).
+ * Forward: gu = x @ W13^T ([M, 2F] = gate | up, kept for the backward) and
+ * h = silu(gate) * up ([M, F]) from one GEMM -- each CTA-pair tile holds 128
+ * gate columns and the matching 128 up columns. x [M][ldx] (K contiguous),
+ * W13 [2F][ldw]; F % 128 == 0.
+ * Backward: dgu = [dgate | dup] ([M, 2F]) from dh = dy @ W2 (dy [M][ld_dy],
+ * W2 [K = d][ldw] rows of F) and the saved gu, without materialising dh. */
+int b2s_gemm_swiglu_fwd(const void* d_x, int64_t ldx, const void* d_w13, int64_t ldw, void* d_gu, int64_t ld_gu,
+                        void* d_h, int64_t ld_h, int M, int F, int K, b2s_stream_t stream);
+int b2s_gemm_swiglu_bwd(const void* d_dy, int64_t ld_dy, const void* d_w2, int64_t ldw, const void* d_gu,
+                        int64_t ld_gu, void* d_dgu, int64_t ld_dgu, int M, int F, int K, b2s_stream_t stream);
+
 /* ------------------------------------------------------------------ */
 /* Bandwidth-bound kernels (K2-K4, K8-K11); no reference counterpart    */
 /* ------------------------------------------------------------------ */

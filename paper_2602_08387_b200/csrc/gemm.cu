@@ -82,10 +82,17 @@ struct Epi {
   int out_f32;                // 1: fp32 output, 0: bf16
   int accumulate;             // C += result (TMA add-reduce)
   const __nv_bfloat16* bias;  // [N] or null
-  int act;                    // 0 none, 1 gelu-tanh (aux <- pre-activation), 2 x gelu'(aux)
-  const __nv_bfloat16* aux_in;  // act=2: [M, ld_aux]
+  int act;                    // 0 none, 1 gelu-tanh (aux <- pre-activation), 2 x gelu'(aux),
+                              // 3 SwiGLU forward, 4 SwiGLU backward (see b2s_gemm_swiglu_*)
+  const __nv_bfloat16* aux_in;  // act=2: [M, ld_aux]; act=4: gu [M, ld_aux = 2F]
   int64_t ld_aux;
+  int glu_F;                  // act 3 / 4: the gate / up split F
 };
+
+__device__ __forceinline__ float silu_sig(float g, float& sg) {
+  sg = __frcp_rn(1.f + __expf(-g));
+  return g * sg;
+}
 
 __device__ __forceinline__ float tanh_fast(float x) {
   float y;
@@ -276,7 +283,11 @@ __global__ void __launch_bounds__(Cfg<BN, CG, EW>::kThreads, 1)
         if (tile >= num_tiles) break;
         if (leader) next = sched ? tstride + atomicAdd(sched, 1) : tile + tstride;
         const int mn = tile % (num_m * num_n), ks = tile / (num_m * num_n);
-        const int m0 = (mn % num_m) * BM * CG + rank * BM, n0 = (mn / num_m) * BN + rank * BNc;
+        const int m0 = (mn % num_m) * BM * CG + rank * BM;
+        // act 3 (SwiGLU forward, CTA pairs): tile n covers gate rows [128n, 128n+128) (leader)
+        // and the matching up rows [F + 128n, ...) (peer), so each accumulator holds both
+        const int n0 = epi.act == 3 ? (rank ? epi.glu_F : 0) + (mn / num_m) * (BN / 2)
+                                    : (mn / num_m) * BN + rank * BNc;
         const int kb0 = ks * kb_per, kb1 = min(num_kb_all, kb0 + kb_per);
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
@@ -404,6 +415,109 @@ __global__ void __launch_bounds__(Cfg<BN, CG, EW>::kThreads, 1)
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const int rbase = m0 + q * 32;
+      if (epi.act == 3) {  // SwiGLU forward: gate chunk c with up chunk c + BN/64 of the same rows
+        const int F = epi.glu_F, h0 = (mn / num_m) * (BN / 2);
+#pragma unroll 1
+        for (int c = half; c < BN / 64; c += kEG) {
+          uint32_t rg[32], ru[32];
+          tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, rg);
+          tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + (c + BN / 64) * 32, ru);
+          tmem_wait_ld();
+          if (c + kEG >= BN / 64) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+              if constexpr (CG == 2) mbar_arrive_cluster_relaxed(mapa_shared(smem_u32(&tempty[acc]), 0));
+              else mbar_arrive(&tempty[acc]);
+            }
+          }
+          const int hc = h0 + c * 32;
+          if (rbase >= M || hc >= F) continue;
+          float g[32], u[32], hv[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {  // what the unfused path stores and re-reads: bf16 gate / up
+            g[i] = __bfloat162float(__float2bfloat16_rn(__uint_as_float(rg[i])));
+            u[i] = __bfloat162float(__float2bfloat16_rn(__uint_as_float(ru[i])));
+            float sg;
+            hv[i] = silu_sig(g[i], sg) * u[i];
+          }
+          const float* outs[3] = {g, u, hv};
+          const int cols[3] = {hc, F + hc, hc};
+#pragma unroll
+          for (int o = 0; o < 3; ++o) {
+            uint8_t* b = next_slot();
+            stage_bf16(b, lane, outs[o]);
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(o == 2 ? &tmAux : &tmC, b, cols[o], rbase);
+              bulk_commit();
+            }
+          }
+        }
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        continue;
+      }
+      if (epi.act == 4) {  // SwiGLU backward: dh chunk (accumulator) -> [dgate | dup] using gu
+        const int F = epi.glu_F;
+#pragma unroll 1
+        for (int c = half; c < BN / 32; c += kEG) {
+          const int col0 = n0 + c * 32;
+          const bool live = rbase < M && col0 < N;
+          uint4 gq[4], uq[4];
+          if (live) {
+            const __nv_bfloat16* p = epi.aux_in + (int64_t)(rbase + lane) * epi.ld_aux + col0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              if (rbase + lane < M && col0 + 8 * k < N) {
+                gq[k] = __ldg(reinterpret_cast<const uint4*>(p + 8 * k));
+                uq[k] = __ldg(reinterpret_cast<const uint4*>(p + F + 8 * k));
+              }
+            }
+          }
+          uint32_t r[32];
+          tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, r);
+          tmem_wait_ld();
+          if (c + kEG >= BN / 32) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+              if constexpr (CG == 2) mbar_arrive_cluster_relaxed(mapa_shared(smem_u32(&tempty[acc]), 0));
+              else mbar_arrive(&tempty[acc]);
+            }
+          }
+          if (!live) continue;
+          float dg[32], du[32];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            float g8[8], u8[8];
+            unpack8(*reinterpret_cast<const bf16x8*>(&gq[k]), g8);
+            unpack8(*reinterpret_cast<const bf16x8*>(&uq[k]), u8);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const float d = __bfloat162float(__float2bfloat16_rn(__uint_as_float(r[8 * k + j])));  // bf16 dh
+              float sg;
+              const float silu = silu_sig(g8[j], sg);
+              du[8 * k + j] = d * silu;
+              dg[8 * k + j] = d * u8[j] * sg * (1.f + g8[j] * (1.f - sg));
+            }
+          }
+          const float* outs[2] = {dg, du};
+#pragma unroll
+          for (int o = 0; o < 2; ++o) {
+            uint8_t* b = next_slot();
+            stage_bf16(b, lane, outs[o]);
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(&tmC, b, col0 + o * F, rbase);
+              bulk_commit();
+            }
+          }
+        }
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        continue;
+      }
 #pragma unroll 1
       for (int c = half; c < BN / 32; c += kEG) {
         const int col0 = n0 + c * 32;
@@ -613,10 +727,12 @@ static Choice choose(int M, int N, int K, bool can_split) {
 }  // namespace gemm
 }  // namespace b2s
 
-extern "C" int b2s_gemm(const void* d_A, int a_mn_major, int64_t lda, const void* d_B,
-                        int b_mn_major, int64_t ldb, void* d_C, int64_t ldc, int c_f32, int M,
-                        int N, int K, int accumulate, const void* d_bias, int act, void* d_aux,
-                        int64_t ld_aux, b2s_stream_t stream) {
+namespace {
+// Shared host path. glu_F / c_width: SwiGLU epilogues (act 3: N = 2F, aux = h [M, F];
+// act 4: N = F, C = dgu [M, 2F] of width c_width, aux = gu).
+int gemm_run(const void* d_A, int a_mn_major, int64_t lda, const void* d_B, int b_mn_major, int64_t ldb, void* d_C,
+             int64_t ldc, int c_f32, int M, int N, int K, int accumulate, const void* d_bias, int act, void* d_aux,
+             int64_t ld_aux, int glu_F, int64_t c_width, int64_t aux_width, cudaStream_t st) {
   using namespace b2s;
   B2S_REQUIRE(M > 0 && N > 0 && K > 0, B2S_EINVAL, "gemm: empty shape %d x %d x %d", M, N, K);
   B2S_REQUIRE(d_A && d_B && d_C, B2S_EINVAL, "gemm: null operand");
@@ -626,11 +742,14 @@ extern "C" int b2s_gemm(const void* d_A, int a_mn_major, int64_t lda, const void
               B2S_EUNSUPPORTED, "gemm: operands must be 16-byte aligned");
   B2S_REQUIRE((ldc * (c_f32 ? 4 : 2)) % 16 == 0 && N % 8 == 0, B2S_EUNSUPPORTED,
               "gemm: N and ldc must keep output rows 16B aligned");
-  B2S_REQUIRE(act == 0 || ((act == 1 || act == 2) && d_aux && !c_f32 && (ld_aux * 2) % 16 == 0 &&
+  B2S_REQUIRE(act == 0 || (act >= 1 && act <= 4 && d_aux && !c_f32 && (ld_aux * 2) % 16 == 0 &&
                            ((uintptr_t)d_aux % 16) == 0),
               B2S_EINVAL, "gemm: activation epilogue needs an aligned bf16 aux buffer and bf16 output");
-  B2S_REQUIRE(!(accumulate && act == 1), B2S_EINVAL, "gemm: accumulate with GELU is not supported");
-  const gemm::Choice ch = gemm::choose(M, N, K, accumulate && !d_bias && act == 0);
+  B2S_REQUIRE(!(accumulate && (act == 1 || act >= 3)), B2S_EINVAL,
+              "gemm: accumulate with a GELU / SwiGLU epilogue is not supported");
+  gemm::Choice ch = gemm::choose(M, N, K, accumulate && !d_bias && act == 0);
+  if (act == 3) ch = gemm::Choice{256, 2, 1};  // the gate / up interleave needs CTA-pair 256-wide tiles
+  if (act == 4) ch.splits = 1;
   const int bn = ch.bn, bnc = ch.bn / ch.cg;
   CUtensorMap ta, tb, tc, tx;
   int rc;
@@ -640,18 +759,45 @@ extern "C" int b2s_gemm(const void* d_A, int a_mn_major, int64_t lda, const void
   if (b_mn_major) rc = encode_tma_2d(&tb, d_B, 2, (uint64_t)N, (uint64_t)K, (uint64_t)ldb * 2, 64, gemm::BK, 128);
   else rc = encode_tma_2d(&tb, d_B, 2, (uint64_t)K, (uint64_t)N, (uint64_t)ldb * 2, gemm::BK, (uint32_t)bnc, 128);
   if (rc) return rc;
-  if (c_f32) rc = encode_tma_2d(&tc, d_C, 4, (uint64_t)N, (uint64_t)M, (uint64_t)ldc * 4, 32, 32, 128);
-  else rc = encode_tma_2d(&tc, d_C, 2, (uint64_t)N, (uint64_t)M, (uint64_t)ldc * 2, 32, 32, 64);
+  if (c_f32) rc = encode_tma_2d(&tc, d_C, 4, (uint64_t)c_width, (uint64_t)M, (uint64_t)ldc * 4, 32, 32, 128);
+  else rc = encode_tma_2d(&tc, d_C, 2, (uint64_t)c_width, (uint64_t)M, (uint64_t)ldc * 2, 32, 32, 64);
   if (rc) return rc;
-  if (act == 1 || act == 2) rc = encode_tma_2d(&tx, d_aux, 2, (uint64_t)N, (uint64_t)M, (uint64_t)ld_aux * 2, 32, 32, 64);
+  if (act == 1 || act == 2 || act == 3)
+    rc = encode_tma_2d(&tx, d_aux, 2, (uint64_t)aux_width, (uint64_t)M, (uint64_t)ld_aux * 2, 32, 32, 64);
   else tx = tc;
   if (rc) return rc;
-  gemm::Epi e{c_f32, accumulate, (const __nv_bfloat16*)d_bias, act, (const __nv_bfloat16*)d_aux, ld_aux};
-  cudaStream_t st = (cudaStream_t)stream;
+  gemm::Epi e{c_f32, accumulate, (const __nv_bfloat16*)d_bias, act, (const __nv_bfloat16*)d_aux, ld_aux, glu_F};
   const int splits = ch.splits;
   if (ch.cg == 2 && act != 0)  // activation epilogue: 12 epilogue warps (see EW above)
     return gemm::dispatch<256, 2, 12>(a_mn_major, b_mn_major, ta, tb, tc, tx, M, N, K, splits, e, st);
   if (ch.cg == 2) return gemm::dispatch<256, 2>(a_mn_major, b_mn_major, ta, tb, tc, tx, M, N, K, splits, e, st);
   if (bn == 256) return gemm::dispatch<256, 1>(a_mn_major, b_mn_major, ta, tb, tc, tx, M, N, K, splits, e, st);
   return gemm::dispatch<128, 1>(a_mn_major, b_mn_major, ta, tb, tc, tx, M, N, K, splits, e, st);
+}
+}  // namespace
+
+extern "C" int b2s_gemm(const void* d_A, int a_mn_major, int64_t lda, const void* d_B,
+                        int b_mn_major, int64_t ldb, void* d_C, int64_t ldc, int c_f32, int M,
+                        int N, int K, int accumulate, const void* d_bias, int act, void* d_aux,
+                        int64_t ld_aux, b2s_stream_t stream) {
+  B2S_REQUIRE(act >= 0 && act <= 2, B2S_EINVAL, "gemm: act must be 0, 1 or 2 (SwiGLU: b2s_gemm_swiglu_*)");
+  B2S_REQUIRE(!(accumulate && act == 1), B2S_EINVAL, "gemm: accumulate with GELU is not supported");
+  return gemm_run(d_A, a_mn_major, lda, d_B, b_mn_major, ldb, d_C, ldc, c_f32, M, N, K, accumulate, d_bias, act,
+                  d_aux, ld_aux, 0, N, N, (cudaStream_t)stream);
+}
+
+extern "C" int b2s_gemm_swiglu_fwd(const void* d_x, int64_t ldx, const void* d_w13, int64_t ldw, void* d_gu,
+                                   int64_t ld_gu, void* d_h, int64_t ld_h, int M, int F, int K,
+                                   b2s_stream_t stream) {
+  B2S_REQUIRE(F > 0 && F % 128 == 0, B2S_EUNSUPPORTED, "gemm_swiglu_fwd: F must be a multiple of 128, got %d", F);
+  return gemm_run(d_x, 0, ldx, d_w13, 0, ldw, d_gu, ld_gu, 0, M, 2 * F, K, 0, nullptr, 3, d_h, ld_h, F, 2 * F, F,
+                  (cudaStream_t)stream);
+}
+
+extern "C" int b2s_gemm_swiglu_bwd(const void* d_dy, int64_t ld_dy, const void* d_w2, int64_t ldw, const void* d_gu,
+                                   int64_t ld_gu, void* d_dgu, int64_t ld_dgu, int M, int F, int K,
+                                   b2s_stream_t stream) {
+  B2S_REQUIRE(F > 0 && F % 8 == 0, B2S_EUNSUPPORTED, "gemm_swiglu_bwd: F must be a multiple of 8");
+  return gemm_run(d_dy, 0, ld_dy, d_w2, 1, ldw, d_dgu, ld_dgu, 0, M, F, K, 0, nullptr, 4, const_cast<void*>(d_gu),
+                  ld_gu, F, 2 * F, 2 * F, (cudaStream_t)stream);
 }

@@ -369,8 +369,11 @@ class DecoderLM(torch.nn.Module):
                          bias=U.p("fc2_b"))
         else:
             ops.rmsnorm_fwd_res(S.xa, S.ya, U.p("mlp_norm"), eps, S.ln_b, S.rstd_b, S.xb)
-            ops.linear(S.ln_b, U.p("w13"), out=S.gu)
-            ops.swiglu_fwd(S.gu, S.h)
+            if self.dtype == torch.bfloat16:  # gate|up GEMM with the SwiGLU in its epilogue
+                ops.linear_swiglu(S.ln_b, U.p("w13"), S.gu, S.h)
+            else:
+                ops.linear(S.ln_b, U.p("w13"), out=S.gu)
+                ops.swiglu_fwd(S.gu, S.h)
             if with_output:
                 ops.gemm(S.h, U.p("w2"), a_mn=False, b_mn=False, M=M, N=d, K=cfg.d_ff, out=S.yb)
         return (S.xb, S.yb)
@@ -452,8 +455,11 @@ class DecoderLM(torch.nn.Module):
                                   U.g("ln2_g"), U.g("ln2_b"), dxsum=U.g("proj_b"))
             else:
                 ops.linear_wgrad(A.dxb, S.h, out=U.g("w2"), accumulate=True)
-                ops.linear_dgrad(A.dxb, U.p("w2"), out=A.dh)
-                ops.swiglu_bwd(S.gu, A.dh, A.dgu)
+                if self.dtype == torch.bfloat16:  # dgrad GEMM with the SwiGLU backward in its epilogue
+                    ops.linear_dgrad_swiglu(A.dxb, U.p("w2"), S.gu, A.dgu)
+                else:
+                    ops.linear_dgrad(A.dxb, U.p("w2"), out=A.dh)
+                    ops.swiglu_bwd(S.gu, A.dh, A.dgu)
                 ops.linear_wgrad(A.dgu, S.ln_b, out=U.g("w13"), accumulate=True)
                 ops.linear_dgrad(A.dgu, U.p("w13"), out=A.dln)
                 ops.rmsnorm_bwd(S.xb, A.dln, U.p("mlp_norm"), S.rstd_b, A.dx, A.dxb, U.g("mlp_norm"))

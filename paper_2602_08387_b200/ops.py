@@ -152,6 +152,28 @@ def linear_dgrad(dy, w, out=None, act=0, aux=None, accumulate=False):
                 accumulate=accumulate)
 
 
+def linear_swiglu(x, w13, gu, h):
+    """gu = x @ w13^T ([M, 2F] gate | up) and h = silu(gate) * up ([M, F]) in one GEMM."""
+    _dev(x, w13, gu, h)
+    M, K = x.shape
+    F = w13.shape[0] // 2
+    _timed("gemm", 2.0 * M * 2 * F * K, lambda: _call(
+        "b2s_gemm_swiglu_fwd", x.data_ptr(), x.stride(0), w13.data_ptr(), w13.stride(0), gu.data_ptr(), gu.stride(0),
+        h.data_ptr(), h.stride(0), M, F, K, _sp()), detail=(M, 2 * F, K, "K", "K", "bf16", "", "", "swiglu"))
+    return gu, h
+
+
+def linear_dgrad_swiglu(dy, w2, gu, dgu):
+    """dgu = SwiGLU backward of dh = dy @ w2 (dy [M, d], w2 [d, F]) without materialising dh."""
+    _dev(dy, w2, gu, dgu)
+    M, K = dy.shape
+    F = w2.shape[1]
+    _timed("gemm", 2.0 * M * F * K, lambda: _call(
+        "b2s_gemm_swiglu_bwd", dy.data_ptr(), dy.stride(0), w2.data_ptr(), w2.stride(0), gu.data_ptr(), gu.stride(0),
+        dgu.data_ptr(), dgu.stride(0), M, F, K, _sp()), detail=(M, F, K, "K", "MN", "bf16", "", "", "dswiglu"))
+    return dgu
+
+
 def linear_wgrad(dy, x, out=None, accumulate=False, out_f32=True):
     """dw = dy^T @ x: dy [M,N], x [M,K] -> [N,K] (fp32 by default)."""
     M, N = dy.shape

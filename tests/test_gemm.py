@@ -92,3 +92,28 @@ def test_gemm_split_k(cuda, monkeypatch, force_split):
     ref = c + a.float().t() @ b.float()
     ops.gemm(a, b, a_mn=True, b_mn=True, M=M, N=N, K=K, out=c, accumulate=True)
     torch.testing.assert_close(c, ref, rtol=1e-4, atol=5e-2)
+
+
+@pytest.mark.parametrize("M,F,K", [(2048, 512, 256), (1000, 384, 200), (16384, 8192, 2048)])
+def test_swiglu_fused_gemms_match_unfused(cuda, M, F, K):
+    """The SwiGLU forward / backward fused into the GEMM epilogues give the unfused chain's bits."""
+    from paper_2602_08387_b200 import ops
+
+    g = torch.Generator(device="cuda").manual_seed(M + F)
+    x = (torch.randn(M, K, device=cuda, generator=g) * 0.5).bfloat16()
+    w13 = (torch.randn(2 * F, K, device=cuda, generator=g) * K ** -0.5).bfloat16()
+    gu_ref = ops.linear(x, w13)
+    h_ref = ops.swiglu_fwd(gu_ref)
+    gu = torch.empty_like(gu_ref)
+    h = torch.empty_like(h_ref)
+    ops.linear_swiglu(x, w13, gu, h)
+    assert torch.equal(gu, gu_ref)
+    torch.testing.assert_close(h.float(), h_ref.float(), rtol=8e-3, atol=1e-6)  # <= 1 bf16 ulp
+    d = 256
+    dy = torch.randn(M, d, device=cuda, generator=g).bfloat16()
+    w2 = (torch.randn(d, F, device=cuda, generator=g) * d ** -0.5).bfloat16()
+    dh = ops.linear_dgrad(dy, w2)
+    dgu_ref = ops.swiglu_bwd(gu_ref, dh)
+    dgu = torch.empty_like(gu_ref)
+    ops.linear_dgrad_swiglu(dy, w2, gu_ref, dgu)
+    torch.testing.assert_close(dgu.float(), dgu_ref.float(), rtol=8e-3, atol=1e-5)
