@@ -382,11 +382,20 @@ __global__ void __launch_bounds__(Cfg<BN, CG, EW>::kThreads, 1)
     uint32_t acc_phase = 0;
     // Hand the next staging slot to this warp: the bulk store issued from it
     // two jobs ago must have finished reading smem.
+    // fp32 outputs: two 4 KB slots (wait until <= 1 store group still reads smem);
+    // bf16 outputs: four 2 KB slots (<= 3 pending) -- the GELU / SwiGLU epilogues
+    // issue 2-3 stores per chunk and would otherwise wait on their own stores.
     auto next_slot = [&]() -> uint8_t* {
-      if (lane == 0) bulk_wait_read<1>();
+      uint8_t* b;
+      if (epi.out_f32) {
+        if (lane == 0) bulk_wait_read<1>();
+        b = ring + (slot & 1) * kStageSlot;
+      } else {
+        if (lane == 0) bulk_wait_read<3>();
+        b = ring + (slot & 3) * (kStageSlot / 2);
+      }
       __syncwarp();
-      uint8_t* b = ring + slot * kStageSlot;
-      slot ^= 1;
+      ++slot;
       return b;
     };
     // dGELU epilogue: this lane's 32 pre-activation values of the chunk, loaded
@@ -460,21 +469,25 @@ __global__ void __launch_bounds__(Cfg<BN, CG, EW>::kThreads, 1)
       }
       if (epi.act == 4) {  // SwiGLU backward: dh chunk (accumulator) -> [dgate | dup] using gu
         const int F = epi.glu_F;
+        uint4 gq[4], uq[4], gn[4], un[4];  // this chunk's gate / up, and the next chunk's (prefetched)
+        auto load_gu = [&](int col, uint4* gg, uint4* uu) {
+          if (rbase + lane >= M) return;
+          const __nv_bfloat16* p = epi.aux_in + (int64_t)(rbase + lane) * epi.ld_aux + col;
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (col + 8 * k < N) {
+              gg[k] = __ldg(reinterpret_cast<const uint4*>(p + 8 * k));
+              uu[k] = __ldg(reinterpret_cast<const uint4*>(p + F + 8 * k));
+            }
+        };
+        if (rbase < M && n0 + half * 32 < N) load_gu(n0 + half * 32, gn, un);
 #pragma unroll 1
         for (int c = half; c < BN / 32; c += kEG) {
           const int col0 = n0 + c * 32;
           const bool live = rbase < M && col0 < N;
-          uint4 gq[4], uq[4];
-          if (live) {
-            const __nv_bfloat16* p = epi.aux_in + (int64_t)(rbase + lane) * epi.ld_aux + col0;
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              if (rbase + lane < M && col0 + 8 * k < N) {
-                gq[k] = __ldg(reinterpret_cast<const uint4*>(p + 8 * k));
-                uq[k] = __ldg(reinterpret_cast<const uint4*>(p + F + 8 * k));
-              }
-            }
-          }
+          for (int k = 0; k < 4; ++k) { gq[k] = gn[k]; uq[k] = un[k]; }
+          if (c + kEG < BN / 32 && rbase < M && col0 + kEG * 32 < N) load_gu(col0 + kEG * 32, gn, un);
           uint32_t r[32];
           tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, r);
           tmem_wait_ld();

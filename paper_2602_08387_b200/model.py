@@ -455,11 +455,10 @@ class DecoderLM(torch.nn.Module):
                                   U.g("ln2_g"), U.g("ln2_b"), dxsum=U.g("proj_b"))
             else:
                 ops.linear_wgrad(A.dxb, S.h, out=U.g("w2"), accumulate=True)
-                if self.dtype == torch.bfloat16:  # dgrad GEMM with the SwiGLU backward in its epilogue
-                    ops.linear_dgrad_swiglu(A.dxb, U.p("w2"), S.gu, A.dgu)
-                else:
-                    ops.linear_dgrad(A.dxb, U.p("w2"), out=A.dh)
-                    ops.swiglu_bwd(S.gu, A.dh, A.dgu)
+                # (b2s_gemm_swiglu_bwd fuses this pair; measured slower -- its epilogue, 8 B in and
+                # 4 B out per element, becomes the bottleneck -- so the step keeps the chain)
+                ops.linear_dgrad(A.dxb, U.p("w2"), out=A.dh)
+                ops.swiglu_bwd(S.gu, A.dh, A.dgu)
                 ops.linear_wgrad(A.dgu, S.ln_b, out=U.g("w13"), accumulate=True)
                 ops.linear_dgrad(A.dgu, U.p("w13"), out=A.dln)
                 ops.rmsnorm_bwd(S.xb, A.dln, U.p("mlp_norm"), S.rstd_b, A.dx, A.dxb, U.g("mlp_norm"))
