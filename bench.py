@@ -45,28 +45,55 @@ def _peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+    """SM clocks and clock-event (throttle) reasons sampled every 100 ms during a timed region.
 
+    In-process NVML queries (nvidia-ml-py): spawning nvidia-smi every few hundred ms
+    stalls this process's CUDA calls long enough to distort a host-synchronous timed
+    region; falls back to nvidia-smi when NVML is unavailable.
+    """
+
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown", 0x4: "sw_power_cap",
+               0x80: "hw_power_brake_slowdown"}
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index: int):
         self.index = index
-        self.rows = []
+        self.rows = []  # (sm_mhz, max_mhz, [reasons])
         self._stop = threading.Event()
         self._t = None
+        self._nvml = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self._nvml = (pynvml, pynvml.nvmlDeviceGetHandleByIndex(index))
+        except Exception:
+            self._nvml = None
+
+    def _sample(self):
+        if self._nvml is not None:
+            nv, h = self._nvml
+            sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+            mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            try:
+                bits = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+            except Exception:
+                bits = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+            return float(sm), float(mx), [n for b, n in self.REASONS.items() if bits & b]
+        out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                              "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+        v = [x.strip() for x in out.stdout.strip().split(",")]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        return float(v[0]), float(v[1]), [names[i] for i in range(4) if v[2 + i].lower() in ("active", "1")]
 
     def _run(self):
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
-                vals = [v.strip() for v in out.stdout.strip().split(",")]
-                if len(vals) == 6:
-                    self.rows.append(vals)
+                self.rows.append(self._sample())
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.1)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -79,12 +106,11 @@ class ClockSampler:
 
     def summary(self):
         if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
-        sm = sorted(float(r[0]) for r in self.rows)
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() in ("active", "1")})
-        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": float(self.rows[0][1]), "reasons": reasons,
-                "samples": len(self.rows)}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["clock query unavailable"], "samples": 0}
+        sm = sorted(r[0] for r in self.rows)
+        reasons = sorted({x for r in self.rows for x in r[2]})
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": self.rows[0][1], "reasons": reasons,
+                "samples": len(self.rows), "source": "nvml" if self._nvml else "nvidia-smi"}
 
 
 def _gemm_traffic(config):
@@ -178,19 +204,6 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
     loss_dev = float(tr._loss.item())
-    # per-kernel roofline: the same steps again with CUDA events around every
-    # GEMM / attention launch on the compute stream (kept out of `value`)
-    if world > 1:
-        tr.engine.timing = []  # CUDA events around every all-gather / reduce-scatter (same pass)
-    with ops.KernelTimer() as kt:
-        for _ in range(args.steps):
-            tr.train_step(step)
-            step += 1
-        barrier_sync()
-    kern = kt.summary()
-    coll = tr.engine.collective_summary() if world > 1 else None
-    tr.engine.timing = None
-
     # ---- end to end through the public API with host buffers (staged windows, loss D2H each step)
     e2e_dl = PackedDataLoader(reader, B, T, Sampler(shuffle=True, seed=0), feed="staged")
     e2e_dl.bind(rank, world, device)
@@ -202,27 +215,48 @@ def run_ours(args):
     # every step: its windows staged from the host memory map into pinned memory and
     # copied H2D, its loss copied D2H into pinned memory; the host reads step k's loss
     # while step k+1 runs (one step of pipelining, like a training loop that logs)
-    loss_host = [torch.empty(1, dtype=torch.float32, pin_memory=True) for _ in range(2)]
-    loss_ev = [torch.cuda.Event() for _ in range(2)]
+    lag = int(os.environ.get("B2S_E2E_LAG", "1"))  # steps between a loss's D2H and its host read
+    loss_host = [torch.empty(1, dtype=torch.float32, pin_memory=True) for _ in range(lag + 1)]
+    loss_ev = [torch.cuda.Event() for _ in range(lag + 1)]
     e2e_losses = []
+    clk_e2e = ClockSampler(local)
+    clk_e2e.__enter__()
     t0 = time.perf_counter()
     for k in range(args.steps):
         inputs, targets = e2e_dl.batch(step)
         loss = tr.step_on(inputs, targets)
-        loss_host[k & 1].copy_(loss, non_blocking=True)  # D2H of the step's result
-        loss_ev[k & 1].record()
-        if k > 0:
-            loss_ev[(k - 1) & 1].synchronize()
-            e2e_losses.append(float(loss_host[(k - 1) & 1].item()))
+        n = lag + 1
+        loss_host[k % n].copy_(loss, non_blocking=True)  # D2H of the step's result
+        loss_ev[k % n].record()
+        if k >= lag:
+            loss_ev[(k - lag) % n].synchronize()
+            e2e_losses.append(float(loss_host[(k - lag) % n].item()))
         step += 1
-    loss_ev[(args.steps - 1) & 1].synchronize()
-    e2e_losses.append(float(loss_host[(args.steps - 1) & 1].item()))
+    for j in range(max(0, args.steps - lag), args.steps):
+        loss_ev[j % (lag + 1)].synchronize()
+        e2e_losses.append(float(loss_host[j % (lag + 1)].item()))
     barrier_sync()
+    clk_e2e.__exit__(None, None, None)
     e2e_ms = (time.perf_counter() - t0) * 1000 / args.steps
     te = torch.tensor([e2e_ms], device=device)
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_ms = float(te.item())
+
+    # per-kernel roofline: the same steps again with CUDA events around every
+    # GEMM / attention launch on the compute stream (kept out of `value`)
+    tr.dataloader = PackedDataLoader(reader, B, T, Sampler(shuffle=True, seed=0), feed="resident")
+    tr.dataloader.bind(rank, world, device)
+    if world > 1:
+        tr.engine.timing = []  # CUDA events around every all-gather / reduce-scatter (same pass)
+    with ops.KernelTimer() as kt:
+        for _ in range(args.steps):
+            tr.train_step(step)
+            step += 1
+        barrier_sync()
+    kern = kt.summary()
+    coll = tr.engine.collective_summary() if world > 1 else None
+    tr.engine.timing = None
 
     if rank != 0:
         return None
@@ -268,7 +302,8 @@ def run_ours(args):
         "clocks": clk.summary(),
         "e2e": {"value": round(tokens_step / (e2e_ms / 1000), 1), "unit": UNIT,
                 "ms_per_step": round(e2e_ms, 3),
-                "h2d_bytes_per_step": e2e_dl.h2d_bytes_per_step(), "d2h_bytes_per_step": 4},
+                "h2d_bytes_per_step": e2e_dl.h2d_bytes_per_step(), "d2h_bytes_per_step": 4,
+                "clocks": clk_e2e.summary()},
     }
     if args.cpu_baseline and world == 1:
         out["cpu_baseline"] = cpu_baseline(cfg, T, args)
