@@ -193,8 +193,9 @@ _work_cache: dict = {}
 
 
 def _work(n_floats: int, device):
-    """Reusable per-device scratch for the deterministic reductions."""
-    key = (device.index, "work")
+    """Reusable scratch for the deterministic reductions, one per (device, stream): kernels
+    on different streams (the backward's weight-gradient side stream) never share it."""
+    key = (device.index, torch.cuda.current_stream(device).cuda_stream)
     buf = _work_cache.get(key)
     if buf is None or buf.numel() < n_floats:
         buf = torch.empty(max(n_floats, 1 << 20), device=device, dtype=torch.float32)
