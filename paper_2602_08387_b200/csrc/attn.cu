@@ -80,13 +80,24 @@ struct Params {
 // dh = 128 runs one query tile per CTA (TILES = 1, warps 6-9 absent): the
 // 32 KB Q / K / V tiles leave room for 2 K/V stages and a double-buffered P
 // only for one tile in 227 KB of shared memory.
+#ifndef B2S_ATTN_FWD64_MODE
+#define B2S_ATTN_FWD64_MODE 0  // dh 64: 0 two ping-pong tiles per CTA (default, fastest measured);
+                               // 1 one tile per CTA, two CTAs per SM (2 K/V stages, 1 P buffer): 25% slower
+#endif
 template <int DH>
 struct Fwd {
-  static constexpr int TILES = DH == 64 ? 2 : 1;
+  static constexpr int MODE = DH == 64 ? B2S_ATTN_FWD64_MODE : 0;
+  static constexpr int TILES = (DH == 64 && MODE == 0) ? 2 : 1;
+  static constexpr int KVS = MODE == 2 ? 1 : 2;       // K / V smem stages
+  static constexpr int PB = MODE == 1 ? 1 : 2;        // P smem buffers per tile
+  static constexpr int MINB = MODE == 0 ? 1 : 2;      // CTAs per SM
+  static constexpr int TCOLS = MODE == 0 ? 512 : 256; // TMEM columns allocated
+  static constexpr int OCOL = MODE == 0 ? 256 : 128;  // first O column
   static constexpr int kThreads = 64 + 128 * TILES;
   static constexpr int kTileQ = BQ * DH * 2;  // Q / K / V tile bytes (DH/64 atoms)
-  static constexpr int kSmem = 1024 + TILES * kTileQ + 2 * kStages * kTileQ + TILES * 2 * kPBuf + 256;
-  static_assert(kSmem <= 232448, "forward tiles exceed shared memory");
+  static constexpr int kSmem = 1024 + TILES * kTileQ + 2 * KVS * kTileQ + TILES * PB * kPBuf + 256;
+  static_assert(kSmem * MINB <= 232448, "forward tiles exceed shared memory");
+  static_assert(KVS == 2, "S(j+1) is issued before PV(j): one K/V stage would deadlock");
 };
 constexpr float kRescaleThresh = 8.0f;  // log2 units
 
@@ -142,17 +153,18 @@ __device__ __forceinline__ float exp_pack(const uint32_t* v, int col0, int r, fl
 }
 
 template <int DH>
-__global__ void __launch_bounds__(Fwd<DH>::kThreads, 1)
+__global__ void __launch_bounds__(Fwd<DH>::kThreads, Fwd<DH>::MINB)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_o,
                     Params p) {
   using C = Fwd<DH>;
   constexpr int TILES = C::TILES, kTQ = C::kTileQ, NA = DH / 64;  // NA: 64-column atoms per tile
+  constexpr int KVS = C::KVS, PB = C::PB;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sQ = align1024(smem_raw);          // [TILES] tiles A, B
-  uint8_t* sK = sQ + TILES * kTQ;             // [kStages]
-  uint8_t* sV = sK + kStages * kTQ;           // [kStages]
-  uint8_t* sP = sV + kStages * kTQ;           // [tile][buf] x 32 KB (two 64-key atoms each)
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + TILES * 2 * kPBuf);
+  uint8_t* sK = sQ + TILES * kTQ;             // [KVS]
+  uint8_t* sV = sK + KVS * kTQ;               // [KVS]
+  uint8_t* sP = sV + KVS * kTQ;               // [tile][buf] x 32 KB (two 64-key atoms each)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + TILES * PB * kPBuf);
   uint64_t* q_full = bars;                    // 1
   uint64_t* k_full = bars + 1;                // [kStages]
   uint64_t* v_full = k_full + kStages;        // [kStages]
@@ -181,7 +193,7 @@ __global__ void __launch_bounds__(Fwd<DH>::kThreads, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tm_qkv);
     mbar_init(q_full, 1);
-    for (int s = 0; s < kStages; ++s) { mbar_init(&k_full[s], 1); mbar_init(&v_full[s], 1); mbar_init(&kv_empty[s], 1); }
+    for (int s = 0; s < KVS; ++s) { mbar_init(&k_full[s], 1); mbar_init(&v_full[s], 1); mbar_init(&kv_empty[s], 1); }
     for (int t = 0; t < 2; ++t) {
       mbar_init(&s_full[t], 1); mbar_init(&s_empty[t], 4);
       mbar_init(&p_full[2 * t], 4); mbar_init(&p_full[2 * t + 1], 4);
@@ -190,12 +202,12 @@ __global__ void __launch_bounds__(Fwd<DH>::kThreads, 1)
     }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc<512>(tslot);
+  if (warp == 1) tmem_alloc<C::TCOLS>(tslot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tslot;
-  // TMEM: S_A [0,128) S_B [128,256) O_A [256,256+DH) O_B [256+DH,256+2DH)
+  // TMEM: S_A [0,128) S_B [128,256) O_A [OCOL,OCOL+DH) O_B [OCOL+DH,OCOL+2DH)
 
   if (warp == 0) {
     if (lane == 0) {
@@ -205,8 +217,8 @@ __global__ void __launch_bounds__(Fwd<DH>::kThreads, 1)
         if (hasB) tma_load_2d(sQ + kTQ + a * kTile, &tm_qkv, q_full, h * DH + a * 64, b * p.T + qtB * BQ);
       }
       for (int j = 0; j < nkv; ++j) {
-        const int s = j % kStages;
-        mbar_wait(&kv_empty[s], ((j / kStages) & 1) ^ 1);
+        const int s = j % KVS;
+        mbar_wait(&kv_empty[s], ((j / KVS) & 1) ^ 1);
         const int r = b * p.T + j * BKV;
         mbar_arrive_expect_tx(&k_full[s], kTQ);
         for (int a = 0; a < NA; ++a)
@@ -223,8 +235,8 @@ __global__ void __launch_bounds__(Fwd<DH>::kThreads, 1)
       constexpr uint32_t idO = make_idesc_bf16(BQ, DH, false, true);
       const uint32_t aQ = smem_u32(sQ), aK = smem_u32(sK), aV = smem_u32(sV), aP = smem_u32(sP);
       auto issue_S = [&](int t, int j) {
-        const int s = j % kStages;
-        mbar_wait(&k_full[s], (j / kStages) & 1);
+        const int s = j % KVS;
+        mbar_wait(&k_full[s], (j / KVS) & 1);
         mbar_wait(&s_empty[t], (j & 1) ^ 1);
         tc_fence_after();
 #pragma unroll
@@ -236,17 +248,17 @@ __global__ void __launch_bounds__(Fwd<DH>::kThreads, 1)
         mma_commit_w(&s_full[t]);
       };
       auto issue_PV = [&](int t, int j, bool last) {
-        const int s = j % kStages;
-        mbar_wait(&v_full[s], (j / kStages) & 1);
-        mbar_wait(&p_full[2 * t + (j & 1)], (j >> 1) & 1);
+        const int s = j % KVS;
+        mbar_wait(&v_full[s], (j / KVS) & 1);
+        mbar_wait(&p_full[2 * t + (j % PB)], (j / PB) & 1);
         tc_fence_after();
-        const uint32_t pbase = aP + (2 * t + (j & 1)) * kPBuf;
+        const uint32_t pbase = aP + (PB * t + (j % PB)) * kPBuf;
         // V as an MN-major operand: 16 keys per K step (2 KB of 128-B rows), dh atoms LBO = 16 KB apart
 #pragma unroll
         for (int kk = 0; kk < BKV / 16; ++kk)
-          mma_bf16_ss_w(tbase + 256 + t * DH, make_sdesc(pbase + (kk >> 2) * kTile + (kk & 3) * 32, 16, 1024),
+          mma_bf16_ss_w(tbase + C::OCOL + t * DH, make_sdesc(pbase + (kk >> 2) * kTile + (kk & 3) * 32, 16, 1024),
                         make_sdesc(aV + s * kTQ + kk * 2048, kTile, 1024), idO, (j > 0 || kk > 0) ? 1u : 0u);
-        mma_commit_w(&p_empty[2 * t + (j & 1)]);
+        mma_commit_w(&p_empty[2 * t + (j % PB)]);
         mma_commit_w(&pv_done[t]);
         if (last) mma_commit_w(&o_done[t]);
       };
@@ -260,7 +272,7 @@ __global__ void __launch_bounds__(Fwd<DH>::kThreads, 1)
         if (j + 1 < nB) issue_S(1, j + 1);
         if (j < nA) issue_PV(0, j, j + 1 == nA);
         if (j < nB) issue_PV(1, j, j + 1 == nB);
-        mma_commit_w(&kv_empty[j % kStages]);  // K_j / V_j no longer read once these retire
+        mma_commit_w(&kv_empty[j % KVS]);  // K_j / V_j no longer read once these retire
       }
     }
     __syncwarp();
@@ -273,7 +285,7 @@ __global__ void __launch_bounds__(Fwd<DH>::kThreads, 1)
     const int nj = t == 0 ? nA : nB;
     const uint32_t lrow = (uint32_t)(q4 * 32) << 16;
     const uint32_t tS = tbase + lrow + t * BKV;
-    const uint32_t tO = tbase + lrow + 256 + t * DH;
+    const uint32_t tO = tbase + lrow + C::OCOL + t * DH;
     const float sl2 = p.scale_log2;
     float m = -INFINITY, l = 0.f;
     for (int j = 0; j < nj; ++j) {
@@ -324,9 +336,9 @@ __global__ void __launch_bounds__(Fwd<DH>::kThreads, 1)
         tmem_wait_st();
       }
       // P = 2^(s*sl2 - m_use) -> bf16 -> smem buffer (j & 1); row sum
-      const int pb = j & 1;
-      if (j >= 2) mbar_wait(&p_empty[2 * t + pb], ((j >> 1) - 1) & 1);
-      uint8_t* myP = sP + (2 * t + pb) * kPBuf;
+      const int pb = j % PB;
+      if (j >= PB) mbar_wait(&p_empty[2 * t + pb], ((j / PB) - 1) & 1);
+      uint8_t* myP = sP + (PB * t + pb) * kPBuf;
       float rs = 0.f;
       if (diag) {
         rs += exp_pack<true>(v, 0, r, sl2, m_use, myP);
@@ -378,7 +390,7 @@ __global__ void __launch_bounds__(Fwd<DH>::kThreads, 1)
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc<512>(tbase);
+    tmem_dealloc<C::TCOLS>(tbase);
   }
 }
 
@@ -477,9 +489,12 @@ __device__ __forceinline__ void p_ds(uint32_t* sv, uint32_t* dv, int q0, int r, 
 // columns) and Q / dO double-buffered. dh = 128: dV + dK take 256 columns, so
 // this kernel computes dK / dV only (single-buffered Q / dO to fit 227 KB of
 // smem) and attn_bwd_q_kernel produces dQ per query tile.
+#ifndef B2S_ATTN_BWD_SPLIT_DQ
+#define B2S_ATTN_BWD_SPLIT_DQ 0  // 1: dh = 64 also takes the separate query-tile dQ kernel
+#endif
 template <int DH>
 struct Bwd {
-  static constexpr bool DQ = DH == 64;        // dQ fused into the key-tile kernel
+  static constexpr bool DQ = DH == 64 && !B2S_ATTN_BWD_SPLIT_DQ;  // dQ fused into the key-tile kernel
   static constexpr int QS = DH == 64 ? 2 : 1; // Q / dO stages
   static constexpr int kTileQ = BQ * DH * 2;
   static constexpr int kSmem = 1024 + 2 * kTileQ /*K,V*/ + 2 * QS * kTileQ /*Q,dO*/ + 2 * kPBuf /*P^T,dS^T*/ +
