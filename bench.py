@@ -214,8 +214,10 @@ def run_ours(args):
     barrier_sync()
     # every step: its windows staged from the host memory map into pinned memory and
     # copied H2D, its loss copied D2H into pinned memory; the host reads step k's loss
-    # while step k+1 runs (one step of pipelining, like a training loop that logs)
-    lag = int(os.environ.get("B2S_E2E_LAG", "1"))  # steps between a loss's D2H and its host read
+    # while step k+lag runs (pipelined like a training loop that logs)
+    # steps between a loss's D2H and its host read: 2 keeps a host hiccup (GC, page faults)
+    # on one rank from stalling the collectives of the others
+    lag = int(os.environ.get("B2S_E2E_LAG", "2"))
     loss_host = [torch.empty(1, dtype=torch.float32, pin_memory=True) for _ in range(lag + 1)]
     loss_ev = [torch.cuda.Event() for _ in range(lag + 1)]
     e2e_losses = []
