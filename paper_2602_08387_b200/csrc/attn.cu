@@ -45,13 +45,6 @@ __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
   const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(p));
   return p + ((1024u - (a & 1023u)) & 1023u);
 }
-// 1-D bulk copy global -> shared, completion counted on `bar` (no tensor map).
-__device__ __forceinline__ void bulk_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_u32(dst)),
-               "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
-}
 __device__ __forceinline__ void named_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }

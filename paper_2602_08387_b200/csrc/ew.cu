@@ -5,6 +5,7 @@
 // row lives in registers), warp-shuffle reductions, deterministic two-stage
 // column reductions (no floating-point atomics except the embedding scatter).
 #include "common.cuh"
+#include "sm100.cuh"
 
 namespace b2s {
 namespace ew {
@@ -140,21 +141,57 @@ __global__ void __launch_bounds__(kRowThreads) norm_fwd_kernel(
 
 // Backward. dy bf16 [M,D]; dx fp32 accumulated in place (dx += ...), with a
 // bf16 copy of the updated dx (the next GEMM operand) when dx_bf16 != null.
-// dg/db partial sums per block into part[blockIdx][2][D] (db only for LN).
+// dg/db partial sums per block into part[blockIdx][3][D] (db only for LN).
+// Each row group (TPR threads) owns an S-stage shared-memory ring: one thread
+// bulk-copies (cp.async.bulk, mbarrier-tracked) the x, dx and dy rows of the
+// group's row S iterations ahead, so every SM keeps ~S x rows x 10 D bytes of
+// HBM reads in flight while the group reduces and writes the current row.
+template <int D, int TPR, bool RMS, typename T>
+struct NormBwd {
+  static constexpr int kGroups = kRowThreads / TPR;  // rows processed concurrently by the block
+  static constexpr int kStage = D * 8 + D * (int)sizeof(T);  // x fp32, dx fp32, dy
+  // ring stages per group: 3 while two blocks per SM still fit, else 2
+  static constexpr int S = 2 * kGroups * 3 * kStage <= 200 * 1024 ? 3 : 2;
+  static constexpr int kSmem = kGroups * S * kStage;
+  static constexpr int kChunk = D < 1024 ? D : 1024;  // columns reduced per smem pass (reuses the ring)
+  static_assert(kGroups * kChunk * 4 <= kSmem, "reduction scratch must fit in the ring");
+};
 template <int D, int TPR, bool RMS, typename T = __nv_bfloat16>
 __global__ void __launch_bounds__(kRowThreads) norm_bwd_kernel(
     const float* __restrict__ x, const T* __restrict__ dy, const T* __restrict__ g,
     const float* __restrict__ mean_in, const float* __restrict__ rstd_in, float* __restrict__ dx,
     T* __restrict__ dx_bf16, float* __restrict__ part, int64_t M, int want_dxsum) {
+  using K = NormBwd<D, TPR, RMS, T>;
   constexpr int V = D / (TPR * 4);
-  constexpr int kGroups = kRowThreads / TPR;  // rows processed concurrently by the block
-  constexpr int kChunk = 1024;                // columns reduced per smem pass
-  __shared__ float red[kGroups][kChunk];
+  constexpr int kGroups = K::kGroups, S = K::S, kChunk = K::kChunk;
+  extern __shared__ __align__(128) uint8_t ring[];
+  __shared__ __align__(8) uint64_t full[kGroups][S];
   __shared__ float scratch[32];
   int tog = 0;
   const int t = threadIdx.x % TPR, grp = threadIdx.x / TPR;
-  const int64_t r0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / TPR;
-  const int64_t nr = ((int64_t)gridDim.x * blockDim.x) / TPR;
+  const int64_t r0 = (int64_t)blockIdx.x * kGroups + grp;
+  const int64_t nr = (int64_t)gridDim.x * kGroups;
+  uint8_t* const mine = ring + grp * S * K::kStage;
+  if (t < S) sm100::mbar_init(&full[grp][t], 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();
+  auto issue = [&](int64_t row, int s) {
+    uint8_t* b = mine + s * K::kStage;
+    sm100::mbar_arrive_expect_tx(&full[grp][s], K::kStage);
+    sm100::bulk_load_1d(b, x + row * D, D * 4, &full[grp][s]);
+    sm100::bulk_load_1d(b + D * 4, dx + row * D, D * 4, &full[grp][s]);
+    sm100::bulk_load_1d(b + D * 8, dy + row * D, D * sizeof(T), &full[grp][s]);
+  };
+  auto group_sync = [&]() {
+    if constexpr (TPR == 32) __syncwarp();
+    else if constexpr (TPR == kRowThreads) __syncthreads();
+    else asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "n"(TPR) : "memory");
+  };
+  if (t == 0) {
+#pragma unroll
+    for (int s = 0; s < S; ++s)
+      if (r0 + s * nr < M) issue(r0 + s * nr, s);
+  }
   float gv[V][4], dg[V][4], db[V][4], ds[V][4];
 #pragma unroll
   for (int j = 0; j < V; ++j) {
@@ -162,25 +199,32 @@ __global__ void __launch_bounds__(kRowThreads) norm_bwd_kernel(
 #pragma unroll
     for (int u = 0; u < 4; ++u) { dg[j][u] = 0.f; db[j][u] = 0.f; ds[j][u] = 0.f; }
   }
-  // rows per group are equal for every group except the tail; loop bound must
-  // be uniform across the block when TPR spans the block (block_sum syncs)
-  // Two passes per row keep register use low enough for 2 CTAs/SM: pass 1 forms
-  // the row statistics, pass 2 re-reads x and dy (L1-resident) with dx.
-  for (int64_t row = r0; row < M; row += nr) {
-    const float mean = RMS ? 0.f : mean_in[row];
-    const float rstd = rstd_in[row];
+  // row statistics one row ahead, so their load latency overlaps the current row
+  float mean_n = 0.f, rstd_n = 0.f;
+  if (r0 < M) { mean_n = RMS ? 0.f : mean_in[r0]; rstd_n = rstd_in[r0]; }
+  int it = 0;
+  // the loop bound is uniform across the block when TPR spans the block (block_sum syncs)
+  for (int64_t row = r0; row < M; row += nr, ++it) {
+    const float mean = mean_n, rstd = rstd_n;
+    if (row + nr < M) { mean_n = RMS ? 0.f : mean_in[row + nr]; rstd_n = rstd_in[row + nr]; }
+    const int s = it % S;
+    sm100::mbar_wait(&full[grp][s], (it / S) & 1);
+    const uint8_t* b = mine + s * K::kStage;
+    const float* xs = reinterpret_cast<const float*>(b);
+    const float* dxs = reinterpret_cast<const float*>(b + D * 4);
+    const T* dys = reinterpret_cast<const T*>(b + D * 8);
     float s1 = 0.f, s2 = 0.f;
 #pragma unroll
     for (int j = 0; j < V; ++j) {
-      const float4 xv = ld4(x + row * D + t * 4 + j * TPR * 4);
+      const float4 xv = ld4(xs + t * 4 + j * TPR * 4);
       float d4[4];
-      ld_v4(dy + row * D + t * 4 + j * TPR * 4, d4);
-      const float xs[4] = {xv.x, xv.y, xv.z, xv.w};
+      ld_v4(dys + t * 4 + j * TPR * 4, d4);
+      const float xq[4] = {xv.x, xv.y, xv.z, xv.w};
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const float dyg = d4[u] * gv[j][u];
         s1 += dyg;
-        s2 += dyg * (xs[u] - mean) * rstd;
+        s2 += dyg * (xq[u] - mean) * rstd;
       }
     }
     s2 = row_sum<TPR>(s2, scratch, tog) * (1.f / D);
@@ -188,26 +232,29 @@ __global__ void __launch_bounds__(kRowThreads) norm_bwd_kernel(
     else s1 = 0.f;
 #pragma unroll
     for (int j = 0; j < V; ++j) {
-      const int64_t off = row * D + t * 4 + j * TPR * 4;
-      const float4 xv = ld4(x + off);
-      float4 o = ld4(dx + off);
+      const int c = t * 4 + j * TPR * 4;
+      const float4 xv = ld4(xs + c);
+      const float4 o = ld4(dxs + c);
       float d4[4];
-      ld_v4(dy + off, d4);
-      const float xs[4] = {xv.x, xv.y, xv.z, xv.w};
+      ld_v4(dys + c, d4);
+      const float xq[4] = {xv.x, xv.y, xv.z, xv.w};
       float os[4] = {o.x, o.y, o.z, o.w};
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const float xh = (xs[u] - mean) * rstd;
+        const float xh = (xq[u] - mean) * rstd;
         os[u] += rstd * (d4[u] * gv[j][u] - s1 - xh * s2);
         dg[j][u] += d4[u] * xh;
         db[j][u] += d4[u];
         ds[j][u] += os[u];
       }
-      st4(dx + off, make_float4(os[0], os[1], os[2], os[3]));
-      if (dx_bf16) st_v4(dx_bf16 + off, os);
+      st4(dx + row * D + c, make_float4(os[0], os[1], os[2], os[3]));
+      if (dx_bf16) st_v4(dx_bf16 + row * D + c, os);
     }
+    group_sync();  // every thread of the group is done reading stage s
+    if (t == 0 && row + S * nr < M) issue(row + S * nr, s);
   }
   // block-level reduction of dg, db, sum(dx) over the row groups -> part[block][pass]
+  float(*red)[kChunk] = reinterpret_cast<float(*)[kChunk]>(ring);
   for (int pass = 0; pass < 3; ++pass) {
     if ((pass == 1 && RMS) || (pass == 2 && !want_dxsum)) continue;
     for (int c0 = 0; c0 < D; c0 += kChunk) {
@@ -641,28 +688,42 @@ template <bool RMS, typename T = __nv_bfloat16>
 static int norm_bwd(const float* x, const void* dy, const void* g, const float* mean, const float* rstd,
                     float* dx, void* dx_bf16, float* dg, float* db, float* dxsum, float* work, int64_t M, int D,
                     cudaStream_t st) {
+  B2S_REQUIRE((((uintptr_t)x | (uintptr_t)dy | (uintptr_t)dx) & 15) == 0, B2S_EUNSUPPORTED,
+              "norm_bwd: x, dy and dx must be 16-byte aligned");
   unsigned grid = 0;
-  auto go = [&](auto kern, int tpr) {
-    int64_t blocks = (M * tpr + kRowThreads - 1) / kRowThreads;
-    const int64_t cap = tpr <= 128 ? kNormBwdMaxBlocks : kNumSMs * 2;
+  // persistent grid: as many blocks as are co-resident (the ring is the smem bound)
+  auto go = [&](auto kern, auto traits) {
+    using K = decltype(traits);
+    static int occ = 0;  // per instantiation
+    if (occ == 0) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, K::kSmem);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kRowThreads, K::kSmem);
+      if (occ < 1) occ = 1;
+    }
+    const int64_t blocks = (M + K::kGroups - 1) / K::kGroups;
+    int64_t cap = (int64_t)kNumSMs * occ;
+    if (cap > kNormBwdMaxBlocks) cap = kNormBwdMaxBlocks;
     grid = (unsigned)(blocks < cap ? blocks : cap);  // partial buffer: grid * 3 * D floats
-    kern<<<grid, kRowThreads, 0, st>>>(x, (const T*)dy, (const T*)g, mean, rstd, dx, (T*)dx_bf16, work, M,
-                                       dxsum != nullptr);
+    if (grid == 0) grid = 1;
+    kern<<<grid, kRowThreads, K::kSmem, st>>>(x, (const T*)dy, (const T*)g, mean, rstd, dx, (T*)dx_bf16, work, M,
+                                              dxsum != nullptr);
     return check_launch("norm_bwd");
   };
+#define B2S_NB(D_, TPR_) go(norm_bwd_kernel<D_, TPR_, RMS, T>, NormBwd<D_, TPR_, RMS, T>{})
   int rc;
   switch (D) {
-    case 128: rc = go(norm_bwd_kernel<128, 32, RMS, T>, 32); break;
-    case 256: rc = go(norm_bwd_kernel<256, 32, RMS, T>, 32); break;
-    case 512: rc = go(norm_bwd_kernel<512, 32, RMS, T>, 32); break;
-    case 768: rc = go(norm_bwd_kernel<768, 64, RMS, T>, 64); break;
-    case 1024: rc = go(norm_bwd_kernel<1024, 32, RMS, T>, 32); break;
-    case 2048: rc = go(norm_bwd_kernel<2048, 128, RMS, T>, 128); break;  // 2 rows in flight per block
-    case 4096: rc = go(norm_bwd_kernel<4096, 256, RMS, T>, 256); break;
+    case 128: rc = B2S_NB(128, 32); break;
+    case 256: rc = B2S_NB(256, 32); break;
+    case 512: rc = B2S_NB(512, 32); break;
+    case 768: rc = B2S_NB(768, 64); break;
+    case 1024: rc = B2S_NB(1024, 32); break;
+    case 2048: rc = B2S_NB(2048, 128); break;  // 2 rows in flight per block
+    case 4096: rc = B2S_NB(4096, 256); break;
     default:
       set_error("norm_bwd: unsupported hidden size %d", D);
       return B2S_EUNSUPPORTED;
   }
+#undef B2S_NB
   if (rc) return rc;
   if (!dg && !(db && !RMS) && !dxsum) return B2S_OK;
   reduce_parts_kernel<<<dim3((D + 31) / 32, 3), 1024, 0, st>>>(work, grid, D, dg, RMS ? nullptr : db, dxsum);

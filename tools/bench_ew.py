@@ -65,3 +65,8 @@ n = 124_000_000
 p, m_, v_, gr = (torch.randn(n, device=dev) for _ in range(4))
 pb = torch.empty(n, device=dev, dtype=torch.bfloat16)
 rec("adamw 124M", time_it(lambda: ops.adamw(p, m_, v_, gr, pb, 5, 1e-4, 0.9, 0.95, 1e-8, 0.1)), n * 30)
+dq = torch.randn(16384, 2304, device=dev).bfloat16()
+dhh = torch.randn(16384, 3072, device=dev).bfloat16()
+ob = torch.zeros(3072, device=dev)
+rec("colsum qkv_b (16384x2304 bf16)", time_it(lambda: ops.colsum_accumulate(dq, ob[:2304])), 16384 * 2304 * 2)
+rec("colsum fc_b (16384x3072 bf16)", time_it(lambda: ops.colsum_accumulate(dhh, ob)), 16384 * 3072 * 2)
