@@ -374,7 +374,7 @@ __global__ void __launch_bounds__(Fwd<DH>::kThreads, Fwd<DH>::MINB)
       if (q4 == 0 && lane == 0) {
         for (int a = 0; a < NA; ++a) tma_store_2d(&tm_o, sO + a * kTile, h * DH + a * 64, b * p.T + qt * BQ);
         bulk_commit();
-        bulk_wait<0>();
+        bulk_wait_read<0>();
       }
     }
     __syncwarp();
@@ -736,7 +736,7 @@ __global__ void __launch_bounds__(320, 1)
 #else
     if (nsteps > 0) { mbar_wait(&dq_full[(nsteps - 1) & 1], ((nsteps - 1) >> 1) & 1); if (lane == 0) mbar_arrive(&dq_empty[(nsteps - 1) & 1]); }
 #endif
-    if (DQ && lane == 0) bulk_wait<0>();  // this warp's add-reduces are complete before smem is reused / freed
+    if (DQ && lane == 0) bulk_wait_read<0>();  // this warp's add-reduces have read their staging smem (kernel exit orders their writes)
     __syncwarp();
     // dK (scaled) and dV -> bf16 -> smem (Q / dO stages are free) -> TMA store into dqkv
     mbar_wait(done, 0);
@@ -774,7 +774,7 @@ __global__ void __launch_bounds__(320, 1)
         tma_store_2d(&tm_dkv, sdV_out + a * kTile, (p.Hq + p.Hkv + kvh) * DH + a * 64, krow0);
       }
       bulk_commit();
-      bulk_wait<0>();
+      bulk_wait_read<0>();
     }
     __syncwarp();
   }
@@ -984,7 +984,7 @@ __global__ void __launch_bounds__(320, 1)
     if (ct == 0) {
       for (int a = 0; a < NA; ++a) tma_store_2d(&tm_dqkv, sQ + a * kTile, h * DH + a * 64, qrow0);
       bulk_commit();
-      bulk_wait<0>();
+      bulk_wait_read<0>();
     }
     __syncwarp();
   }

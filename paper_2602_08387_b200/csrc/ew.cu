@@ -4,6 +4,8 @@
 // for the row-wise ops with the hidden size a compile-time constant (so the
 // row lives in registers), warp-shuffle reductions, deterministic two-stage
 // column reductions (no floating-point atomics except the embedding scatter).
+#include <mutex>
+
 #include "common.cuh"
 #include "sm100.cuh"
 
@@ -305,15 +307,21 @@ __global__ void __launch_bounds__(1024) reduce_parts_kernel(const float* __restr
 }
 
 // ------------------------------------------------------------------ column sums
-// part[blockIdx.y][c] = sum over this block's rows of x[r][c] (bf16 or fp32 x).
-// 8 warps stride the rows; each lane owns one 16-byte column vector, so a warp
-// reads 512 contiguous bytes per row. Requires N, ld multiples of the vector.
+// out[c] += sum over rows of x[r][c] (bf16 or fp32 x), one launch. Block
+// (strip, part) sums rows [part * rows_per, ...) of a 32-vector column strip
+// into part[part][c]; the last block of each strip to finish (per-strip arrival
+// counter) adds the strip's partials in part order -- deterministic -- and
+// re-arms the counter. 8 warps stride the rows; each lane owns one 16-byte
+// column vector, so a warp reads 512 contiguous bytes per row. Requires N, ld
+// multiples of the vector.
 template <typename T>
 __global__ void __launch_bounds__(256) colsum_kernel(const T* __restrict__ x, int64_t M, int N, int64_t ld,
-                                                     int rows_per, float* __restrict__ part) {
+                                                     int rows_per, float* __restrict__ part,
+                                                     float* __restrict__ out, unsigned* __restrict__ arrivals) {
   constexpr int VEC = 16 / sizeof(T);
   constexpr int COLS = 32 * VEC;
   __shared__ float red[8][COLS];
+  __shared__ bool last;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int c = blockIdx.x * COLS + lane * VEC;
   const int64_t r0 = (int64_t)blockIdx.y * rows_per;
@@ -322,15 +330,40 @@ __global__ void __launch_bounds__(256) colsum_kernel(const T* __restrict__ x, in
 #pragma unroll
   for (int i = 0; i < VEC; ++i) acc[i] = 0.f;
   if (c < N) {
-    for (int64_t r = r0 + w; r < r1; r += 8) {
+    // four rows' 16-byte loads issued back to back before they are summed: the
+    // loop is latency-bound otherwise (one load in flight per lane)
+#ifndef B2S_COLSUM_U
+#define B2S_COLSUM_U 8
+#endif
+    constexpr int U = B2S_COLSUM_U;
+    int64_t r = r0 + w;
+    for (; r + 8 * (U - 1) < r1; r += 8 * U) {
+      uint4 q[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) q[u] = __ldcs(reinterpret_cast<const uint4*>(x + (r + 8 * u) * ld + c));
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if constexpr (sizeof(T) == 2) {
+          float f[8];
+          unpack8(*reinterpret_cast<const bf16x8*>(&q[u]), f);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) acc[i] += f[i];
+        } else {
+          acc[0] += __uint_as_float(q[u].x); acc[1] += __uint_as_float(q[u].y);
+          acc[2] += __uint_as_float(q[u].z); acc[3] += __uint_as_float(q[u].w);
+        }
+      }
+    }
+    for (; r < r1; r += 8) {
+      const uint4 q = __ldcs(reinterpret_cast<const uint4*>(x + r * ld + c));
       if constexpr (sizeof(T) == 2) {
         float f[8];
-        unpack8(*reinterpret_cast<const bf16x8*>(x + r * ld + c), f);
+        unpack8(*reinterpret_cast<const bf16x8*>(&q), f);
 #pragma unroll
         for (int i = 0; i < 8; ++i) acc[i] += f[i];
       } else {
-        float4 v = *reinterpret_cast<const float4*>(x + r * ld + c);
-        acc[0] += v.x; acc[1] += v.y; acc[2] += v.z; acc[3] += v.w;
+        acc[0] += __uint_as_float(q.x); acc[1] += __uint_as_float(q.y);
+        acc[2] += __uint_as_float(q.z); acc[3] += __uint_as_float(q.w);
       }
     }
   }
@@ -346,25 +379,40 @@ __global__ void __launch_bounds__(256) colsum_kernel(const T* __restrict__ x, in
       part[(int64_t)blockIdx.y * N + cc] = s;
     }
   }
-}
-// out[c] += sum_p part[p][c]: 32 columns x 32 part-groups per block, fixed order.
-__global__ void __launch_bounds__(1024) colsum_final_kernel(const float* __restrict__ part, int nparts, int N,
-                                                            float* __restrict__ out) {
-  __shared__ float red[32][33];
-  const int c = blockIdx.x * 32 + (threadIdx.x & 31), rg = threadIdx.x >> 5;
-  float acc = 0.f;
-  if (c < N) {
-#pragma unroll 4
-    for (int p = rg; p < nparts; p += 32) acc += part[(int64_t)p * N + c];
-  }
-  red[rg][threadIdx.x & 31] = acc;
+  __threadfence();  // publish this block's partials before counting its arrival
   __syncthreads();
-  if (rg == 0 && c < N) {
-    float s = 0.f;
+  if (threadIdx.x == 0) last = atomicAdd(&arrivals[blockIdx.x], 1u) == gridDim.y - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  // COLS columns x 8 part groups (fixed order within and across the groups)
+  const int nparts = gridDim.y;
+  constexpr int PG = 256 / COLS;  // part groups: 1 (bf16) or 2 (fp32)
+  const int k = threadIdx.x % COLS, g = threadIdx.x / COLS;
+  const int cc = blockIdx.x * COLS + k;
+  float s = 0.f;
+  if (cc < N) {
+    // 16 partials' loads in flight per batch (a serial chain of L2 round trips otherwise)
+    int q = g;
+    for (; q + 15 * PG < nparts; q += 16 * PG) {
+      float v[16];
 #pragma unroll
-    for (int k = 0; k < 32; ++k) s += red[k][threadIdx.x & 31];
-    out[c] += s;
+      for (int u = 0; u < 16; ++u) v[u] = __ldcg(part + (int64_t)(q + u * PG) * N + cc);
+#pragma unroll
+      for (int u = 0; u < 16; ++u) s += v[u];
+    }
+    for (; q < nparts; q += PG) s += __ldcg(part + (int64_t)q * N + cc);
   }
+  if constexpr (PG > 1) {
+    red[g][k] = s;
+    __syncthreads();
+    if (g == 0) {
+#pragma unroll
+      for (int j = 1; j < PG; ++j) s += red[j][k];
+    }
+  }
+  if (g == 0 && cc < N) out[cc] += s;
+  if (threadIdx.x == 0) arrivals[blockIdx.x] = 0u;  // re-armed for the next launch using this slot
 }
 
 // ------------------------------------------------------------------ embedding
@@ -684,6 +732,28 @@ static int norm_fwd(const float* x, const void* g, const void* b, void* y, float
 
 constexpr int kNormBwdMaxBlocks = kNumSMs * 4;
 
+// Per-device pool of zeroed colsum arrival counters (kColsumStrips per slot);
+// launches rotate through the slots so column sums in flight on different
+// streams never share one. Each launch leaves its counters at zero.
+constexpr int kColsumStrips = 1024, kColsumSlots = 64;
+static unsigned* colsum_slot() {
+  static unsigned* pool[64] = {};
+  static int next[64] = {};
+  static std::mutex mu;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  if (!pool[dev]) {
+    const size_t bytes = (size_t)kColsumSlots * kColsumStrips * sizeof(unsigned);
+    if (cudaMalloc(&pool[dev], bytes) != cudaSuccess) return nullptr;
+    cudaMemset(pool[dev], 0, bytes);
+    cudaDeviceSynchronize();
+  }
+  unsigned* p = pool[dev] + (size_t)kColsumStrips * next[dev];
+  next[dev] = (next[dev] + 1) % kColsumSlots;
+  return p;
+}
+
 template <bool RMS, typename T = __nv_bfloat16>
 static int norm_bwd(const float* x, const void* dy, const void* g, const float* mean, const float* rstd,
                     float* dx, void* dx_bf16, float* dg, float* db, float* dxsum, float* work, int64_t M, int D,
@@ -862,14 +932,22 @@ int b2s_colsum_accumulate(const void* d_x, int x_f32, int64_t M, int N, int64_t 
   cudaStream_t st = (cudaStream_t)stream;
   const int cols = 32 * vec;
   const int nblk = (N + cols - 1) / cols;
-  int nparts = (4 * kNumSMs + nblk - 1) / nblk;  // ~4 blocks per SM
+  B2S_REQUIRE(nblk <= ew::kColsumStrips, B2S_EUNSUPPORTED, "colsum: N = %d exceeds %d column strips", N,
+              ew::kColsumStrips);
+  unsigned* arrivals = ew::colsum_slot();
+  B2S_REQUIRE(arrivals != nullptr, B2S_ECUDA, "colsum: arrival counter allocation failed");
+  // four blocks per SM, rounded down so every block is co-resident in one wave
+  int nparts = 4 * kNumSMs / nblk;
   if (nparts > 256) nparts = 256;
+  if (nparts < 1) nparts = 1;
   const int rows_per = (int)((M + nparts - 1) / nparts);
   dim3 grid(nblk, nparts);
-  if (x_f32) ew::colsum_kernel<float><<<grid, 256, 0, st>>>((const float*)d_x, M, N, ld, rows_per, d_work);
-  else ew::colsum_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>((const __nv_bfloat16*)d_x, M, N, ld, rows_per, d_work);
-  ew::colsum_final_kernel<<<(N + 31) / 32, 1024, 0, st>>>(d_work, nparts, N, d_out);
-  return check_launch("colsum", 2);
+  if (x_f32)
+    ew::colsum_kernel<float><<<grid, 256, 0, st>>>((const float*)d_x, M, N, ld, rows_per, d_work, d_out, arrivals);
+  else
+    ew::colsum_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>((const __nv_bfloat16*)d_x, M, N, ld, rows_per, d_work,
+                                                           d_out, arrivals);
+  return check_launch("colsum");
 }
 int64_t b2s_colsum_work_floats(int N) { return 256LL * N; }
 

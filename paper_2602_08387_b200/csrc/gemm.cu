@@ -614,7 +614,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, EW>::kThreads, 1)
       }
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
-    if (lane == 0) bulk_wait<0>();
+    if (lane == 0) bulk_wait_read<0>();
     __syncwarp();
   }
 
