@@ -246,7 +246,7 @@ int b2s_attn_fwd(const void* d_qkv, void* d_o, float* d_lse, int B, int T, int H
                  b2s_stream_t stream);
 /* Backward of b2s_attn_fwd: writes dq, dk, dv into d_dqkv (same layout as
  * d_qkv). d_do: bf16 [B*T, Hq*dh]. d_work: b2s_attn_bwd_work_floats() floats
- * (fp32 dQ accumulator + rowsum(dO*O)). */
+ * (fp32 dQ accumulator, scaled rowsum(dO*O), log2-unit LSE). */
 int b2s_attn_bwd(const void* d_qkv, const void* d_o, const void* d_do, const float* d_lse, void* d_dqkv,
                  float* d_work, int B, int T, int Hq, int Hkv, int dh, b2s_stream_t stream);
 int64_t b2s_attn_bwd_work_floats(int B, int T, int Hq, int dh);

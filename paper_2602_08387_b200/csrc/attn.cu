@@ -55,6 +55,7 @@ struct Params {
   float scale;       // 1 / sqrt(dh)
   float* lse;        // [B, Hq, T]
   const float* dsum; // bwd: D = rowsum(dO * O), [B, Hq, T]
+  float* dq_acc;     // bwd (dh 64): fp32 dQ accumulator [B*T, Hq*dh]
 };
 
 // =====================================================================================
@@ -390,10 +391,15 @@ __global__ void __launch_bounds__(Fwd<DH>::kThreads, Fwd<DH>::MINB)
 // =====================================================================================
 // backward
 // =====================================================================================
-// D[b, h, q] = sum_d dO * O (row-wise), and zero the fp32 dQ accumulator (if any).
+// D'[b, h, q] = scale * sum_d dO * O (row-wise), lse2 = lse * log2(e), and zero
+// the fp32 dQ accumulator (if any). The backward then forms the already-scaled
+// dS' = scale * P (dP - D) = P * (scale * dP - D') with one FFMA, and
+// P = 2^(s * scale * log2(e) - lse2) with one FFMA, per element.
 template <int DH>
 __global__ void attn_bwd_prep_kernel(const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ dout,
-                                     float* __restrict__ dsum, float* __restrict__ dq_acc, int B, int T, int Hq) {
+                                     const float* __restrict__ lse, float* __restrict__ dsum,
+                                     float* __restrict__ lse2, float* __restrict__ dq_acc, int B, int T, int Hq,
+                                     float scale) {
   // DH/8 lanes per (row, head): each lane a 16-byte vector of o and dO
   constexpr int LPR = DH / 8;
   const int sub = threadIdx.x & (LPR - 1);
@@ -417,7 +423,9 @@ __global__ void attn_bwd_prep_kernel(const __nv_bfloat16* __restrict__ o, const 
     }
     if (sub == 0) {
       const int64_t b = row / T, t = row - b * T;
-      dsum[(b * Hq + h) * T + t] = acc;
+      const int64_t i = (b * Hq + h) * T + t;
+      dsum[i] = acc * scale;
+      lse2[i] = lse[i] * kLog2e;
     }
   }
 }
@@ -450,11 +458,12 @@ __global__ void attn_bwd_dq_kernel(const float* __restrict__ dq_acc, __nv_bfloat
 // into the fp32 accumulator) after publishing P/dS(t).
 constexpr int kBwdThreads = 320;
 
-// P^T = 2^(s*sl2 - lse2[q]) and dS^T = P^T (dP^T - D[q]) for 32 query columns of
-// one key row, in place in sv / dv (bit patterns of fp32). Mask = template branch.
+// P^T = 2^(s*sl2 - lse2[q]) and the scaled dS^T = P^T (scale dP^T - D'[q]) for
+// 32 query columns of one key row, in place in sv / dv (bit patterns of fp32).
+// Mask = template branch.
 template <bool DIAG>
-__device__ __forceinline__ void p_ds(uint32_t* sv, uint32_t* dv, int q0, int r, float sl2, const float* lse2,
-                                     const float* dd) {
+__device__ __forceinline__ void p_ds(uint32_t* sv, uint32_t* dv, int q0, int r, float sl2, float scale,
+                                     const float* lse2, const float* dd) {
   // the 32 columns' LSE / D values are the same for every thread: 16-byte
   // broadcast loads (8 + 8 LDS.128 instead of 64 scalar LDS)
   float ls[32], ds[32];
@@ -471,11 +480,11 @@ __device__ __forceinline__ void p_ds(uint32_t* sv, uint32_t* dv, int q0, int r, 
 #ifdef B2S_EXP_NOEXP
     float pv = __uint_as_float(sv[e]);
 #else
-    float pv = ex2(fmaf(__uint_as_float(sv[e]), sl2, -ls[e] * kLog2e));
+    float pv = ex2(fmaf(__uint_as_float(sv[e]), sl2, -ls[e]));
 #endif
     if (DIAG && q < r) pv = 0.f;  // query index below key index: masked
     sv[e] = __float_as_uint(pv);
-    dv[e] = __float_as_uint(pv * (__uint_as_float(dv[e]) - ds[e]));
+    dv[e] = __float_as_uint(pv * fmaf(__uint_as_float(dv[e]), scale, -ds[e]));
   }
 }
 // dh = 64: dQ fused (TMEM S^T 128 + dP^T 128 + dV 64 + dK 64 + dQ 2x64 = 512
@@ -485,12 +494,21 @@ __device__ __forceinline__ void p_ds(uint32_t* sv, uint32_t* dv, int q0, int r, 
 #ifndef B2S_ATTN_BWD_SPLIT_DQ
 #define B2S_ATTN_BWD_SPLIT_DQ 0  // 1: dh = 64 also takes the separate query-tile dQ kernel
 #endif
+#ifndef B2S_ATTN_BWD_DQ_RED
+#define B2S_ATTN_BWD_DQ_RED 0  // 1: dQ drained by red.global.add.v4.f32 from registers (no smem staging)
+#endif
+#ifndef B2S_ATTN_BWD_PT
+#define B2S_ATTN_BWD_PT 1  // dh 64: P^T goes to TMEM (dV by the TMEM-A MMA form), single-buffered dQ
+#endif
 template <int DH>
 struct Bwd {
   static constexpr bool DQ = DH == 64 && !B2S_ATTN_BWD_SPLIT_DQ;  // dQ fused into the key-tile kernel
+  // P^T in TMEM columns [448, 512) (freed by a single dQ buffer): no P^T shared-memory
+  // stores and no A-operand smem reads for dV -- the kernel is smem-bandwidth bound
+  static constexpr bool PT = DQ && B2S_ATTN_BWD_PT;
   static constexpr int QS = DH == 64 ? 2 : 1; // Q / dO stages
   static constexpr int kTileQ = BQ * DH * 2;
-  static constexpr int kSmem = 1024 + 2 * kTileQ /*K,V*/ + 2 * QS * kTileQ /*Q,dO*/ + 2 * kPBuf /*P^T,dS^T*/ +
+  static constexpr int kSmem = 1024 + 2 * kTileQ /*K,V*/ + 2 * QS * kTileQ /*Q,dO*/ + (PT ? 1 : 2) * kPBuf /*P^T,dS^T*/ +
                                (DQ ? 2 * kTile : 0) /*dQ fp32 staging: 8 warps x 4 KB*/ + 4 * BQ * 4 /*LSE, D x2*/ +
                                256;
   static_assert(kSmem <= 232448, "backward tiles exceed shared memory");
@@ -502,14 +520,14 @@ __global__ void __launch_bounds__(320, 1)
                     const __grid_constant__ CUtensorMap tm_dq, const __grid_constant__ CUtensorMap tm_dkv, Params p) {
   using C = Bwd<DH>;
   constexpr int kTQ = C::kTileQ, QS = C::QS, NA = DH / 64;
-  constexpr bool DQ = C::DQ;
+  constexpr bool DQ = C::DQ, PT = C::PT;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sK = align1024(smem_raw);
   uint8_t* sV = sK + kTQ;
   uint8_t* sQ = sV + kTQ;            // [QS]
   uint8_t* sdO = sQ + QS * kTQ;      // [QS]
-  uint8_t* sP = sdO + QS * kTQ;      // P^T  [128 keys][128 q] as two 64-column atoms
-  uint8_t* sdS = sP + kPBuf;         // dS^T
+  uint8_t* sP = sdO + QS * kTQ;      // P^T  [128 keys][128 q] as two 64-column atoms (smem P only)
+  uint8_t* sdS = sP + (PT ? 0 : kPBuf);  // dS^T
   uint8_t* sdQ = sdS + kPBuf;        // fp32 128 x 64 as two 32-column boxes (16 KB each), dh 64 only
   float* sLse = reinterpret_cast<float*>(sdQ + (DQ ? 2 * kTile : 0));  // [2][128] natural-log LSE (TMA bulk)
   float* sD = sLse + 2 * BQ;                                 // [2][128] rowsum(dO*O)
@@ -558,8 +576,12 @@ __global__ void __launch_bounds__(320, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tslot;
-  // dQ: [2] x 64 (dh 64 only)
+  // dQ: [2] x 64 (dh 64 only), or [1] x 64 + P^T (bf16 pairs) in [448, 512) with PT
   const uint32_t tS = tbase, tdP = tbase + 128, tdV = tbase + 256, tdK = tbase + 256 + DH, tdQ = tbase + 384;
+  const uint32_t tPT = tbase + 448;
+  // dQ buffer / barrier of step t, and how many times that buffer was used before
+  auto dq_buf = [&](int t) { return PT ? 0 : (t & 1); };
+  auto dq_use = [&](int t) { return PT ? t : (t >> 1); };
 
   if (warp == 0) {
     if (lane == 0) {
@@ -624,20 +646,23 @@ __global__ void __launch_bounds__(320, 1)
         for (int kk = 0; kk < BQ / 16; ++kk) {
           const uint64_t a_p = make_sdesc(aP + (kk >> 2) * kTile + (kk & 3) * 32, 16, 1024);
           const uint64_t a_ds = make_sdesc(adS + (kk >> 2) * kTile + (kk & 3) * 32, 16, 1024);
-          mma_bf16_ss_w(tdV, a_p, make_sdesc(do_ + kk * 2048, kTile, 1024), idKM, (t > 0 || kk > 0));
+          if constexpr (PT)
+            mma_bf16_ts_w(tdV, tPT + kk * 8, make_sdesc(do_ + kk * 2048, kTile, 1024), idKM, (t > 0 || kk > 0));
+          else
+            mma_bf16_ss_w(tdV, a_p, make_sdesc(do_ + kk * 2048, kTile, 1024), idKM, (t > 0 || kk > 0));
           mma_bf16_ss_w(tdK, a_ds, make_sdesc(q_ + kk * 2048, kTile, 1024), idKM, (t > 0 || kk > 0));
         }
         if constexpr (DQ) {
-          mbar_wait(&dq_empty[s], ((t >> 1) & 1) ^ 1);
+          mbar_wait(&dq_empty[dq_buf(t)], (dq_use(t) & 1) ^ 1);
           tc_fence_after();
 #pragma unroll
           for (int kk = 0; kk < BKV / 16; ++kk)
-            mma_bf16_ss_w(tdQ + s * DH, make_sdesc(adS + kk * 2048, kTile, 1024),
+            mma_bf16_ss_w(tdQ + dq_buf(t) * DH, make_sdesc(adS + kk * 2048, kTile, 1024),
                           make_sdesc(aK + kk * 2048, kTile, 1024), idMM, kk > 0);
         }
         mma_commit_w(&qd_empty[qs]);
         mma_commit_w(pds_empty);
-        if constexpr (DQ) mma_commit_w(&dq_full[s]);
+        if constexpr (DQ) mma_commit_w(&dq_full[dq_buf(t)]);
         if (QS == 1 && t + 1 < nsteps) issue_S(t + 1);
       }
       mma_commit_w(done);
@@ -656,27 +681,40 @@ __global__ void __launch_bounds__(320, 1)
     auto drain_dq = [&](int t) {
       if constexpr (!DQ) return;
       const int h = kvh * G + t / nq, i = kt + t % nq;
-      mbar_wait(&dq_full[t & 1], (t >> 1) & 1);
+      mbar_wait(&dq_full[dq_buf(t)], dq_use(t) & 1);
       tc_fence_after();
       uint32_t qv[32];
-      tmem_ld32(tdQ + lrow + (t & 1) * DH + half * 32, qv);
+      tmem_ld32(tdQ + lrow + dq_buf(t) * DH + half * 32, qv);
       tmem_wait_ld();
       tc_fence_before();
       __syncwarp();
+#if B2S_ATTN_BWD_DQ_RED
+      if (lane == 0) mbar_arrive(&dq_empty[dq_buf(t)]);
+      // straight from registers: 8 x 16-byte fp32 add-reductions into this thread's query row
+      float* dst = p.dq_acc + ((size_t)b * p.T + (size_t)i * BQ + r) * (p.Hq * DH) + h * DH + half * 32;
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst + 4 * c), "r"(qv[4 * c]),
+                     "r"(qv[4 * c + 1]), "r"(qv[4 * c + 2]), "r"(qv[4 * c + 3])
+                     : "memory");
+      return;
+#endif
       if (lane == 0) {
-        mbar_arrive(&dq_empty[t & 1]);
+        mbar_arrive(&dq_empty[dq_buf(t)]);
         bulk_wait_read<0>();  // this warp's previous add-reduce has read its staging tile
       }
       __syncwarp();
 #pragma unroll
       for (int c = 0; c < 8; ++c)
         *reinterpret_cast<float4*>(mystage + swz(lane, c)) =
-            make_float4(__uint_as_float(qv[4 * c]) * p.scale, __uint_as_float(qv[4 * c + 1]) * p.scale,
-                        __uint_as_float(qv[4 * c + 2]) * p.scale, __uint_as_float(qv[4 * c + 3]) * p.scale);
+            make_float4(__uint_as_float(qv[4 * c]), __uint_as_float(qv[4 * c + 1]), __uint_as_float(qv[4 * c + 2]),
+                        __uint_as_float(qv[4 * c + 3]));  // dS is pre-scaled
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) {
+#ifndef B2S_EXP_NO_DQ_REDUCE  // timing experiment only: dQ not accumulated
         tma_reduce_add_2d(&tm_dq, mystage, h * DH + half * 32, b * p.T + i * BQ + q4 * 32);
+#endif
         bulk_commit();
       }
     };
@@ -691,7 +729,7 @@ __global__ void __launch_bounds__(320, 1)
       // 168 registers per thread (3 warps on some SMSPs): two 32-column passes
 #pragma unroll
       for (int qq = 0; qq < 2; ++qq) {
-        uint32_t sv[32], dv[32];
+        uint32_t sv[32], dv[32], pt[16];
         tmem_ld32(tS + lrow + half * 64 + qq * 32, sv);
         tmem_ld32(tdP + lrow + half * 64 + qq * 32, dv);
         tmem_wait_ld();
@@ -700,9 +738,14 @@ __global__ void __launch_bounds__(320, 1)
           __syncwarp();
           if (lane == 0) mbar_arrive(st_empty);  // the next step's S^T / dP^T may overwrite TMEM
         }
-        if (diag) p_ds<true>(sv, dv, half * 64 + qq * 32, r, p.scale_log2, lse2, dd);
-        else p_ds<false>(sv, dv, half * 64 + qq * 32, r, p.scale_log2, lse2, dd);
+#ifndef B2S_EXP_NOCOMPUTE  // timing experiment only: protocol without the softmax math / P, dS stores
+        if (diag) p_ds<true>(sv, dv, half * 64 + qq * 32, r, p.scale_log2, p.scale, lse2, dd);
+        else p_ds<false>(sv, dv, half * 64 + qq * 32, r, p.scale_log2, p.scale, lse2, dd);
+#endif
+#ifndef B2S_EXP_NO_PDS_WAIT  // timing experiment only: races on sP / sdS
         if (qq == 0 && t > 0) mbar_wait(pds_empty, (t - 1) & 1);  // step t-1's MMAs released sP / sdS
+#endif
+#ifndef B2S_EXP_NOCOMPUTE
 #pragma unroll
         for (int k8 = 0; k8 < 4; ++k8) {
           uint4 w, z;
@@ -715,9 +758,21 @@ __global__ void __launch_bounds__(320, 1)
           z.z = pack_bf16x2(__uint_as_float(dv[8 * k8 + 4]), __uint_as_float(dv[8 * k8 + 5]));
           z.w = pack_bf16x2(__uint_as_float(dv[8 * k8 + 6]), __uint_as_float(dv[8 * k8 + 7]));
           const uint32_t off = half * kTile + swz(r, qq * 4 + k8);
-          *reinterpret_cast<uint4*>(sP + off) = w;
+          if constexpr (PT) {
+            pt[4 * k8 + 0] = w.x; pt[4 * k8 + 1] = w.y; pt[4 * k8 + 2] = w.z; pt[4 * k8 + 3] = w.w;
+          } else {
+            *reinterpret_cast<uint4*>(sP + off) = w;
+          }
           *reinterpret_cast<uint4*>(sdS + off) = z;
         }
+        if constexpr (PT) tmem_st16(tPT + lrow + half * 32 + qq * 16, pt);
+#else
+        if (lane == 99) *reinterpret_cast<uint32_t*>(sP) = sv[0] + dv[7];
+#endif
+      }
+      if constexpr (PT) {
+        tmem_wait_st();  // P^T is in TMEM before the MMA warp is told
+        tc_fence_before();
       }
       fence_proxy_async_smem();
       __syncwarp();
@@ -738,7 +793,7 @@ __global__ void __launch_bounds__(320, 1)
 #endif
     if (DQ && lane == 0) bulk_wait_read<0>();  // this warp's add-reduces have read their staging smem (kernel exit orders their writes)
     __syncwarp();
-    // dK (scaled) and dV -> bf16 -> smem (Q / dO stages are free) -> TMA store into dqkv
+    // dK (from the pre-scaled dS) and dV -> bf16 -> smem (Q / dO stages are free) -> TMA store into dqkv
     mbar_wait(done, 0);
     tc_fence_after();
     uint8_t* sdK_out = sQ;
@@ -753,10 +808,10 @@ __global__ void __launch_bounds__(320, 1)
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         uint4 w, z;
-        w.x = pack_bf16x2(__uint_as_float(kv[8 * c + 0]) * p.scale, __uint_as_float(kv[8 * c + 1]) * p.scale);
-        w.y = pack_bf16x2(__uint_as_float(kv[8 * c + 2]) * p.scale, __uint_as_float(kv[8 * c + 3]) * p.scale);
-        w.z = pack_bf16x2(__uint_as_float(kv[8 * c + 4]) * p.scale, __uint_as_float(kv[8 * c + 5]) * p.scale);
-        w.w = pack_bf16x2(__uint_as_float(kv[8 * c + 6]) * p.scale, __uint_as_float(kv[8 * c + 7]) * p.scale);
+        w.x = pack_bf16x2(__uint_as_float(kv[8 * c + 0]), __uint_as_float(kv[8 * c + 1]));
+        w.y = pack_bf16x2(__uint_as_float(kv[8 * c + 2]), __uint_as_float(kv[8 * c + 3]));
+        w.z = pack_bf16x2(__uint_as_float(kv[8 * c + 4]), __uint_as_float(kv[8 * c + 5]));
+        w.w = pack_bf16x2(__uint_as_float(kv[8 * c + 6]), __uint_as_float(kv[8 * c + 7]));
         z.x = pack_bf16x2(__uint_as_float(vv[8 * c + 0]), __uint_as_float(vv[8 * c + 1]));
         z.y = pack_bf16x2(__uint_as_float(vv[8 * c + 2]), __uint_as_float(vv[8 * c + 3]));
         z.z = pack_bf16x2(__uint_as_float(vv[8 * c + 4]), __uint_as_float(vv[8 * c + 5]));
@@ -919,7 +974,7 @@ __global__ void __launch_bounds__(320, 1)
     const int r = q4 * 32 + lane;      // query row
     const uint32_t lrow = (uint32_t)(q4 * 32) << 16;
     const size_t roff = ((size_t)b * p.Hq + h) * p.T + (size_t)i * BQ + r;
-    const float lse2 = p.lse[roff] * kLog2e;
+    const float lse2 = p.lse[roff];  // log2 units (prep kernel)
     const float dd = p.dsum[roff];
     const float sl2 = p.scale_log2;
     for (int j = 0; j < nkv; ++j) {
@@ -942,7 +997,7 @@ __global__ void __launch_bounds__(320, 1)
         for (int e = 0; e < 32; ++e) {
           float pv = ex2(fmaf(__uint_as_float(sv[e]), sl2, -lse2));
           if (diag && k0 + e > r) pv = 0.f;  // key after query: masked
-          dv[e] = __float_as_uint(pv * (__uint_as_float(dv[e]) - dd));
+          dv[e] = __float_as_uint(pv * fmaf(__uint_as_float(dv[e]), p.scale, -dd));  // scaled dS
         }
         if (qq == 0 && j > 0) mbar_wait(pds_empty, (j - 1) & 1);
 #pragma unroll
@@ -971,10 +1026,10 @@ __global__ void __launch_bounds__(320, 1)
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         uint4 w;
-        w.x = pack_bf16x2(__uint_as_float(qv[8 * c + 0]) * p.scale, __uint_as_float(qv[8 * c + 1]) * p.scale);
-        w.y = pack_bf16x2(__uint_as_float(qv[8 * c + 2]) * p.scale, __uint_as_float(qv[8 * c + 3]) * p.scale);
-        w.z = pack_bf16x2(__uint_as_float(qv[8 * c + 4]) * p.scale, __uint_as_float(qv[8 * c + 5]) * p.scale);
-        w.w = pack_bf16x2(__uint_as_float(qv[8 * c + 6]) * p.scale, __uint_as_float(qv[8 * c + 7]) * p.scale);
+        w.x = pack_bf16x2(__uint_as_float(qv[8 * c + 0]), __uint_as_float(qv[8 * c + 1]));
+        w.y = pack_bf16x2(__uint_as_float(qv[8 * c + 2]), __uint_as_float(qv[8 * c + 3]));
+        w.z = pack_bf16x2(__uint_as_float(qv[8 * c + 4]), __uint_as_float(qv[8 * c + 5]));
+        w.w = pack_bf16x2(__uint_as_float(qv[8 * c + 6]), __uint_as_float(qv[8 * c + 7]));
         const int chunk = col0 / 8 + c;
         *reinterpret_cast<uint4*>(sQ + (chunk >> 3) * kTile + swz(r, chunk & 7)) = w;
       }
@@ -1012,7 +1067,7 @@ int attn_fwd_dh(const void* d_qkv, void* d_o, float* d_lse, int B, int T, int Hq
   rc = encode_tma_2d(&to, d_o, 2, (uint64_t)Hq * DH, (uint64_t)B * T, (uint64_t)Hq * DH * 2, 64, 128, 128);
   if (rc) return rc;
   attn::Params p{B, T, Hq, Hkv, T / attn::BQ, attn::kLog2e / sqrtf((float)DH), 1.f / sqrtf((float)DH), d_lse,
-                 nullptr};
+                 nullptr, nullptr};
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(attn::attn_fwd_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
@@ -1031,8 +1086,10 @@ int attn_bwd_dh(const void* d_qkv, const void* d_o, const void* d_do, const floa
   const int64_t M = (int64_t)B * T;
   float* dq_acc = C::DQ ? d_work : nullptr;
   float* dsum = d_work + M * Hq * DH;
-  attn::attn_bwd_prep_kernel<DH><<<kNumSMs * 8, 256, 0, st>>>((const __nv_bfloat16*)d_o,
-                                                              (const __nv_bfloat16*)d_do, dsum, dq_acc, B, T, Hq);
+  float* lse2 = dsum + M * Hq;
+  attn::attn_bwd_prep_kernel<DH><<<kNumSMs * 8, 256, 0, st>>>(
+      (const __nv_bfloat16*)d_o, (const __nv_bfloat16*)d_do, d_lse, dsum, lse2, dq_acc, B, T, Hq,
+      1.f / sqrtf((float)DH));
   int rc = check_launch("attn_bwd_prep");
   if (rc) return rc;
   CUtensorMap tq, tdo, tdq, tdkv;
@@ -1044,8 +1101,8 @@ int attn_bwd_dh(const void* d_qkv, const void* d_o, const void* d_do, const floa
   if (rc) return rc;
   rc = encode_tma_2d(&tdkv, d_dqkv, 2, (uint64_t)ldq, (uint64_t)M, (uint64_t)ldq * 2, 64, 128, 128);
   if (rc) return rc;
-  attn::Params p{B, T, Hq, Hkv, T / attn::BQ, attn::kLog2e / sqrtf((float)DH), 1.f / sqrtf((float)DH),
-                 const_cast<float*>(d_lse), dsum};
+  attn::Params p{B, T, Hq, Hkv, T / attn::BQ, attn::kLog2e / sqrtf((float)DH), 1.f / sqrtf((float)DH), lse2,
+                 dsum, dq_acc};
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(attn::attn_bwd_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
@@ -1080,7 +1137,7 @@ extern "C" int b2s_attn_fwd(const void* d_qkv, void* d_o, float* d_lse, int B, i
 }
 
 extern "C" int64_t b2s_attn_bwd_work_floats(int B, int T, int Hq, int dh) {
-  return (int64_t)B * T * Hq * dh + (int64_t)B * Hq * T;
+  return (int64_t)B * T * Hq * dh + 2 * (int64_t)B * Hq * T;  // dQ acc | D' | lse2
 }
 
 extern "C" int b2s_attn_bwd(const void* d_qkv, const void* d_o, const void* d_do, const float* d_lse, void* d_dqkv,
