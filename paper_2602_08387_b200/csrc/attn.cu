@@ -78,18 +78,23 @@ struct Params {
 #define B2S_ATTN_FWD64_MODE 0  // dh 64: 0 two ping-pong tiles per CTA (default, fastest measured);
                                // 1 one tile per CTA, two CTAs per SM (2 K/V stages, 1 P buffer): 25% slower
 #endif
+#ifndef B2S_ATTN_FWD_PT
+#define B2S_ATTN_FWD_PT 1  // P in TMEM (PV by the TMEM-A MMA form) instead of shared memory
+#endif
 template <int DH>
 struct Fwd {
   static constexpr int MODE = DH == 64 ? B2S_ATTN_FWD64_MODE : 0;
+  static constexpr bool PT = B2S_ATTN_FWD_PT && MODE == 0;
   static constexpr int TILES = (DH == 64 && MODE == 0) ? 2 : 1;
   static constexpr int KVS = MODE == 2 ? 1 : 2;       // K / V smem stages
-  static constexpr int PB = MODE == 1 ? 1 : 2;        // P smem buffers per tile
+  static constexpr int PB = (MODE == 1 || PT) ? 1 : 2;  // P buffers per tile (smem, or one TMEM block)
   static constexpr int MINB = MODE == 0 ? 1 : 2;      // CTAs per SM
   static constexpr int TCOLS = MODE == 0 ? 512 : 256; // TMEM columns allocated
   static constexpr int OCOL = MODE == 0 ? 256 : 128;  // first O column
   static constexpr int kThreads = 64 + 128 * TILES;
   static constexpr int kTileQ = BQ * DH * 2;  // Q / K / V tile bytes (DH/64 atoms)
-  static constexpr int kSmem = 1024 + TILES * kTileQ + 2 * KVS * kTileQ + TILES * PB * kPBuf + 256;
+  static constexpr int PCOL = OCOL + TILES * DH;      // PT: P (bf16 pairs, 64 columns per tile)
+  static constexpr int kSmem = 1024 + TILES * kTileQ + 2 * KVS * kTileQ + (PT ? 0 : TILES * PB * kPBuf) + 256;
   static_assert(kSmem * MINB <= 232448, "forward tiles exceed shared memory");
   static_assert(KVS == 2, "S(j+1) is issued before PV(j): one K/V stage would deadlock");
 };
@@ -146,6 +151,27 @@ __device__ __forceinline__ float exp_pack(const uint32_t* v, int col0, int r, fl
   return (rs4[0] + rs4[1]) + (rs4[2] + rs4[3]);
 }
 
+// Same, for all BKV columns of the row, packed as bf16 pairs into out[0 .. BKV/2)
+// (out may alias v: pair k is written after v[2k], v[2k+1] are read).
+template <bool DIAG>
+__device__ __forceinline__ float exp_pack_regs(const uint32_t* v, int r, float sl2, float m, uint32_t* out) {
+  float rs4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+  for (int k8 = 0; k8 < BKV / 8; ++k8) {
+    float e[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float a = fmaf(__uint_as_float(v[k8 * 8 + i]), sl2, -m);
+      const float x = ex2(a);
+      e[i] = (DIAG && k8 * 8 + i > r) ? 0.f : x;
+    }
+    rs4[k8 & 3] += ((e[0] + e[1]) + (e[2] + e[3])) + ((e[4] + e[5]) + (e[6] + e[7]));
+#pragma unroll
+    for (int i = 0; i < 4; ++i) out[k8 * 4 + i] = pack_bf16x2(e[2 * i], e[2 * i + 1]);
+  }
+  return (rs4[0] + rs4[1]) + (rs4[2] + rs4[3]);
+}
+
 template <int DH>
 __global__ void __launch_bounds__(Fwd<DH>::kThreads, Fwd<DH>::MINB)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_o,
@@ -158,7 +184,7 @@ __global__ void __launch_bounds__(Fwd<DH>::kThreads, Fwd<DH>::MINB)
   uint8_t* sK = sQ + TILES * kTQ;             // [KVS]
   uint8_t* sV = sK + KVS * kTQ;               // [KVS]
   uint8_t* sP = sV + KVS * kTQ;               // [tile][buf] x 32 KB (two 64-key atoms each)
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + TILES * PB * kPBuf);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + (C::PT ? 0 : TILES * PB * kPBuf));
   uint64_t* q_full = bars;                    // 1
   uint64_t* k_full = bars + 1;                // [kStages]
   uint64_t* v_full = k_full + kStages;        // [kStages]
@@ -249,9 +275,14 @@ __global__ void __launch_bounds__(Fwd<DH>::kThreads, Fwd<DH>::MINB)
         const uint32_t pbase = aP + (PB * t + (j % PB)) * kPBuf;
         // V as an MN-major operand: 16 keys per K step (2 KB of 128-B rows), dh atoms LBO = 16 KB apart
 #pragma unroll
-        for (int kk = 0; kk < BKV / 16; ++kk)
-          mma_bf16_ss_w(tbase + C::OCOL + t * DH, make_sdesc(pbase + (kk >> 2) * kTile + (kk & 3) * 32, 16, 1024),
-                        make_sdesc(aV + s * kTQ + kk * 2048, kTile, 1024), idO, (j > 0 || kk > 0) ? 1u : 0u);
+        for (int kk = 0; kk < BKV / 16; ++kk) {
+          if constexpr (C::PT)  // P from TMEM: 16 keys = 8 columns of bf16 pairs per K step
+            mma_bf16_ts_w(tbase + C::OCOL + t * DH, tbase + C::PCOL + t * 64 + kk * 8,
+                          make_sdesc(aV + s * kTQ + kk * 2048, kTile, 1024), idO, (j > 0 || kk > 0) ? 1u : 0u);
+          else
+            mma_bf16_ss_w(tbase + C::OCOL + t * DH, make_sdesc(pbase + (kk >> 2) * kTile + (kk & 3) * 32, 16, 1024),
+                          make_sdesc(aV + s * kTQ + kk * 2048, kTile, 1024), idO, (j > 0 || kk > 0) ? 1u : 0u);
+        }
         mma_commit_w(&p_empty[2 * t + (j % PB)]);
         mma_commit_w(&pv_done[t]);
         if (last) mma_commit_w(&o_done[t]);
@@ -329,22 +360,34 @@ __global__ void __launch_bounds__(Fwd<DH>::kThreads, Fwd<DH>::MINB)
         }
         tmem_wait_st();
       }
-      // P = 2^(s*sl2 - m_use) -> bf16 -> smem buffer (j & 1); row sum
+      // P = 2^(s*sl2 - m_use) -> bf16 -> smem buffer (j & 1) or TMEM; row sum
       const int pb = j % PB;
-      if (j >= PB) mbar_wait(&p_empty[2 * t + pb], ((j / PB) - 1) & 1);
-      uint8_t* myP = sP + (PB * t + pb) * kPBuf;
       float rs = 0.f;
-      if (diag) {
-        rs += exp_pack<true>(v, 0, r, sl2, m_use, myP);
-        rs += exp_pack<true>(v + 64, 64, r, sl2, m_use, myP + kTile);
+      if constexpr (C::PT) {
+        // exponentials first (bf16 pairs packed over the S registers), then wait for
+        // PV(j-1) to release this tile's TMEM P block, then one TMEM store round
+        uint32_t* pk = v;
+        rs = diag ? exp_pack_regs<true>(v, r, sl2, m_use, pk) : exp_pack_regs<false>(v, r, sl2, m_use, pk);
+        if (j >= 1) mbar_wait(&p_empty[2 * t], (j - 1) & 1);
+        tc_fence_after();
+        tmem_st32(tbase + lrow + C::PCOL + t * 64, pk);
+        tmem_st32(tbase + lrow + C::PCOL + t * 64 + 32, pk + 32);
+        tmem_wait_st();
       } else {
-        rs += exp_pack<false>(v, 0, r, sl2, m_use, myP);
-        rs += exp_pack<false>(v + 64, 64, r, sl2, m_use, myP + kTile);
+        if (j >= PB) mbar_wait(&p_empty[2 * t + pb], ((j / PB) - 1) & 1);
+        uint8_t* myP = sP + (PB * t + pb) * kPBuf;
+        if (diag) {
+          rs += exp_pack<true>(v, 0, r, sl2, m_use, myP);
+          rs += exp_pack<true>(v + 64, 64, r, sl2, m_use, myP + kTile);
+        } else {
+          rs += exp_pack<false>(v, 0, r, sl2, m_use, myP);
+          rs += exp_pack<false>(v + 64, 64, r, sl2, m_use, myP + kTile);
+        }
+        fence_proxy_async_smem();
       }
       l = l * alpha + rs;
       m = m_use;
       tc_fence_before();
-      fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[2 * t + pb]);
     }
