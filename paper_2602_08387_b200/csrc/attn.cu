@@ -100,6 +100,11 @@ struct Fwd {
 };
 constexpr float kRescaleThresh = 8.0f;  // log2 units
 
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
 __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -162,7 +167,7 @@ __device__ __forceinline__ float exp_pack_regs(const uint32_t* v, int r, float s
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const float a = fmaf(__uint_as_float(v[k8 * 8 + i]), sl2, -m);
-      const float x = ex2(a);
+      const float x = ((B2S_EXP_POLY_MASK >> (k8 & 7)) & 1) ? ex2_poly(a) : ex2(a);
       e[i] = (DIAG && k8 * 8 + i > r) ? 0.f : x;
     }
     rs4[k8 & 3] += ((e[0] + e[1]) + (e[2] + e[3])) + ((e[4] + e[5]) + (e[6] + e[7]));
@@ -333,9 +338,10 @@ __global__ void __launch_bounds__(Fwd<DH>::kThreads, Fwd<DH>::MINB)
 #pragma unroll
         for (int i = 0; i < BKV; ++i)
           if (i <= r) mx8[i & 7] = fmaxf(mx8[i & 7], __uint_as_float(v[i]));
-      } else {
+      } else {  // three-input max (FMNMX3): two new elements per instruction
 #pragma unroll
-        for (int i = 0; i < BKV; ++i) mx8[i & 7] = fmaxf(mx8[i & 7], __uint_as_float(v[i]));
+        for (int i = 0; i < BKV / 2; ++i)
+          mx8[i & 7] = fmax3(mx8[i & 7], __uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
       }
       const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
                              fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
@@ -449,7 +455,7 @@ __global__ void attn_bwd_prep_kernel(const __nv_bfloat16* __restrict__ o, const 
   const int64_t nrows = (int64_t)B * T * Hq;
   for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / LPR; w < nrows;
        w += ((int64_t)gridDim.x * blockDim.x) / LPR) {
-    const int64_t row = w / Hq;
+    const int64_t row = (int64_t)((uint32_t)w / (uint32_t)Hq);  // B*T*Hq < 2^32 (host-checked)
     const int h = (int)(w - row * Hq);
     const int64_t off = row * Hq * DH + h * DH + sub * 8;
     float a[8], g[8];
@@ -465,7 +471,7 @@ __global__ void attn_bwd_prep_kernel(const __nv_bfloat16* __restrict__ o, const 
       *reinterpret_cast<float4*>(dq_acc + off + 4) = make_float4(0.f, 0.f, 0.f, 0.f);
     }
     if (sub == 0) {
-      const int64_t b = row / T, t = row - b * T;
+      const int64_t b = (int64_t)((uint32_t)row / (uint32_t)T), t = row - b * T;
       const int64_t i = (b * Hq + h) * T + t;
       dsum[i] = acc * scale;
       lse2[i] = lse[i] * kLog2e;
@@ -473,21 +479,23 @@ __global__ void attn_bwd_prep_kernel(const __nv_bfloat16* __restrict__ o, const 
   }
 }
 
-// dqkv[:, q heads] = bf16(dq_acc)  (dh = 64 path)
-__global__ void attn_bwd_dq_kernel(const float* __restrict__ dq_acc, __nv_bfloat16* __restrict__ dqkv, int64_t M,
-                                   int Hq, int64_t ldq) {
+// dqkv[:, q heads] = bf16(dq_acc)  (dh = 64 path). Blocks stride over rows (a row
+// is Hq*64 floats), so no 64-bit division per element.
+__global__ void __launch_bounds__(256) attn_bwd_dq_kernel(const float* __restrict__ dq_acc,
+                                                          __nv_bfloat16* __restrict__ dqkv, int64_t M, int Hq,
+                                                          int64_t ldq) {
   constexpr int DH = 64;
-  const int width = Hq * DH;
-  const int64_t nvec = M * width / 4;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nvec; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t e = i * 4;
-    const int64_t row = e / width;
-    const int c = (int)(e - row * width);
-    float4 v = *reinterpret_cast<const float4*>(dq_acc + e);
-    uint2 u;
-    u.x = pack_bf16x2(v.x, v.y);
-    u.y = pack_bf16x2(v.z, v.w);
-    *reinterpret_cast<uint2*>(dqkv + row * ldq + c) = u;
+  const int nv = Hq * DH / 4;  // float4 vectors per row
+  for (int64_t row = blockIdx.x; row < M; row += gridDim.x) {
+    const float* src = dq_acc + row * (int64_t)(Hq * DH);
+    __nv_bfloat16* dst = dqkv + row * ldq;
+    for (int v = threadIdx.x; v < nv; v += blockDim.x) {
+      const float4 a = __ldcs(reinterpret_cast<const float4*>(src) + v);
+      uint2 u;
+      u.x = pack_bf16x2(a.x, a.y);
+      u.y = pack_bf16x2(a.z, a.w);
+      *reinterpret_cast<uint2*>(dst + 4 * v) = u;
+    }
   }
 }
 
@@ -1159,7 +1167,8 @@ int attn_bwd_dh(const void* d_qkv, const void* d_o, const void* d_do, const floa
   rc = check_launch("attn_bwd");
   if (rc) return rc;
   if constexpr (C::DQ) {
-    attn::attn_bwd_dq_kernel<<<kNumSMs * 8, 256, 0, st>>>(dq_acc, (__nv_bfloat16*)d_dqkv, M, Hq, ldq);
+    attn::attn_bwd_dq_kernel<<<(unsigned)(M < kNumSMs * 16 ? M : kNumSMs * 16), 256, 0, st>>>(
+        dq_acc, (__nv_bfloat16*)d_dqkv, M, Hq, ldq);
     return check_launch("attn_bwd_dq");
   } else {
     attn::attn_bwd_q_kernel<DH><<<(unsigned)(B * Hq * (T / attn::BQ)), 320, attn::BwdQ<DH>::kSmem, st>>>(tq, tdo,
@@ -1188,6 +1197,7 @@ extern "C" int b2s_attn_bwd(const void* d_qkv, const void* d_o, const void* d_do
   B2S_REQUIRE(dh == 64 || dh == 128, B2S_EUNSUPPORTED, "attention: head dim %d not implemented (64, 128)", dh);
   B2S_REQUIRE(T % attn::BQ == 0 && T > 0, B2S_EUNSUPPORTED, "attention: T must be a multiple of 128");
   B2S_REQUIRE(Hkv > 0 && Hq % Hkv == 0, B2S_EINVAL, "attention: Hq must be a multiple of Hkv");
+  B2S_REQUIRE((int64_t)B * T * Hq < (1LL << 32), B2S_EUNSUPPORTED, "attention: B*T*Hq must be < 2^32");
   cudaStream_t st = (cudaStream_t)stream;
   return dh == 64 ? attn_bwd_dh<64>(d_qkv, d_o, d_do, d_lse, d_dqkv, d_work, B, T, Hq, Hkv, st)
                   : attn_bwd_dh<128>(d_qkv, d_o, d_do, d_lse, d_dqkv, d_work, B, T, Hq, Hkv, st);
