@@ -43,6 +43,34 @@ __device__ __forceinline__ void ld_v8(const __nv_bfloat16* p, float* f) {
 __device__ __forceinline__ void ld_v8(const float* p, float* f) { ld_v4(p, f); ld_v4(p + 4, f + 4); }
 __device__ __forceinline__ void st_v8(__nv_bfloat16* p, const float* f) { *reinterpret_cast<bf16x8*>(p) = pack8(f); }
 __device__ __forceinline__ void st_v8(float* p, const float* f) { st_v4(p, f); st_v4(p + 4, f + 4); }
+// streaming (evict-first) variants: data read / written once that should not push
+// still-needed lines out of L2
+__device__ __forceinline__ void st_v8_cs(__nv_bfloat16* p, const float* f) {
+  const bf16x8 v = pack8(f);
+  __stcs(reinterpret_cast<uint4*>(p), *reinterpret_cast<const uint4*>(&v));
+}
+__device__ __forceinline__ void st_v8_cs(float* p, const float* f) {
+  __stcs(reinterpret_cast<float4*>(p), make_float4(f[0], f[1], f[2], f[3]));
+  __stcs(reinterpret_cast<float4*>(p + 4), make_float4(f[4], f[5], f[6], f[7]));
+}
+__device__ __forceinline__ void ld_v8_cs(const __nv_bfloat16* p, float* f) {
+  const uint4 u = __ldcs(reinterpret_cast<const uint4*>(p));
+  unpack8(*reinterpret_cast<const bf16x8*>(&u), f);
+}
+__device__ __forceinline__ void ld_v8_cs(const float* p, float* f) {
+  const float4 a = __ldcs(reinterpret_cast<const float4*>(p)), b = __ldcs(reinterpret_cast<const float4*>(p + 4));
+  f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w; f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
+}
+__device__ __forceinline__ float ex2f(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
 __device__ __forceinline__ float to_f(__nv_bfloat16 v) { return bf2f(v); }
 __device__ __forceinline__ float to_f(float v) { return v; }
 __device__ __forceinline__ void from_f(__nv_bfloat16& d, float v) { d = f2bf(v); }
@@ -558,55 +586,57 @@ template <typename T>
 __global__ void __launch_bounds__(512) xent_kernel(T* __restrict__ logits, int64_t ld, int V,
                                                    const int64_t* __restrict__ target, float* __restrict__ loss,
                                                    float gscale, int64_t M, int write_grad) {
+  // log2 units throughout (y = x log2 e): one FFMA + one ex2 per element; the target
+  // column is corrected once per row instead of a compare-select per element
+  constexpr float L2E = 1.4426950408889634f;
   __shared__ float scratch[32];
+  const int nvec = V / 8;  // full 8-wide vectors
   const int64_t m = blockIdx.x;
   T* row = logits + m * ld;
-  const int nvec = V / 8;  // full 8-wide vectors
-  // one pass: per-thread online (max, sum of exp), then a block-wide merge
+  // one pass: per-thread online (max, sum of 2^(y - max)), then a block-wide merge
   float mx = -INFINITY, se = 0.f;
+  auto absorb = [&](const float* f) {
+    const float lm = fmax3(fmax3(f[0], f[1], f[2]), fmax3(f[3], f[4], f[5]), fmaxf(f[6], f[7]));
+    const float mn = fmaxf(mx, lm * L2E);
+    float acc = 0.f;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) acc += ex2f(fmaf(f[t], L2E, -mn));
+    se = se * ex2f(mx - mn) + acc;
+    mx = mn;
+  };
   for (int i = threadIdx.x; i < nvec; i += blockDim.x) {
     float f[8];
     ld_v8(row + i * 8, f);
-    float lm = f[0];
-#pragma unroll
-    for (int t = 1; t < 8; ++t) lm = fmaxf(lm, f[t]);
-    const float mn = fmaxf(mx, lm);
-    float acc = 0.f;
-#pragma unroll
-    for (int t = 0; t < 8; ++t) acc += __expf(f[t] - mn);
-    se = se * __expf(mx - mn) + acc;
-    mx = mn;
+    absorb(f);
   }
   for (int c = nvec * 8 + threadIdx.x; c < V; c += blockDim.x) {
-    const float f = to_f(row[c]);
-    const float mn = fmaxf(mx, f);
-    se = se * __expf(mx - mn) + __expf(f - mn);
+    const float y = to_f(row[c]) * L2E;
+    const float mn = fmaxf(mx, y);
+    se = se * ex2f(mx - mn) + ex2f(y - mn);
     mx = mn;
   }
   const float bmx = block_max(mx, scratch);
-  se = (mx == -INFINITY) ? 0.f : se * __expf(mx - bmx);
+  se = (mx == -INFINITY) ? 0.f : se * ex2f(mx - bmx);
   mx = bmx;
   se = block_sum(se, scratch);
-  const float lse = mx + __logf(se);
+  const float lse = (mx + __log2f(se)) * (1.f / L2E);
   const int64_t tgt = target[m];
   const float xt = to_f(row[tgt]);
   __syncthreads();
   if (threadIdx.x == 0) loss[m] = lse - xt;
   if (!write_grad) return;
-  const float inv = 1.f / se;
+  const float inv = gscale / se;  // softmax * gscale = 2^(y - max) * gscale / sum
   for (int i = threadIdx.x; i < nvec; i += blockDim.x) {
     float f[8];
-    ld_v8(row + i * 8, f);
+    ld_v8_cs(row + i * 8, f);  // last read of the row (pass 1 left it in L2)
 #pragma unroll
-    for (int t = 0; t < 8; ++t) {
-      const int c = i * 8 + t;
-      f[t] = (__expf(f[t] - mx) * inv - (c == tgt ? 1.f : 0.f)) * gscale;
-    }
-    st_v8(row + i * 8, f);
+    for (int t = 0; t < 8; ++t) f[t] = ex2f(fmaf(f[t], L2E, -mx)) * inv;
+    if ((uint64_t)(tgt - (int64_t)i * 8) < 8) f[tgt - (int64_t)i * 8] -= gscale;
+    st_v8_cs(row + i * 8, f);  // written once: keep other rows' pass-2 reads in L2
   }
   for (int c = nvec * 8 + threadIdx.x; c < ld; c += blockDim.x) {
     float g = 0.f;
-    if (c < V) g = (__expf(to_f(row[c]) - mx) * inv - (c == tgt ? 1.f : 0.f)) * gscale;
+    if (c < V) g = ex2f(fmaf(to_f(row[c]), L2E, -mx)) * inv - (c == tgt ? gscale : 0.f);
     from_f(row[c], g);
   }
 }

@@ -144,6 +144,7 @@ def test_cross_entropy(cuda, V, ld):
     M = 64
     logits = (torch.randn(M, ld, device=cuda) * 2).bfloat16()
     tgt = torch.randint(0, V, (M,), device=cuda)
+    tgt[0], tgt[1], tgt[2] = V - 1, 0, min(V - 1, (V // 8) * 8)  # last column, first, first tail column
     lf = logits.float()[:, :V].requires_grad_()
     ref = F.cross_entropy(lf, tgt, reduction="none")
     ref.sum().div(M).backward()
