@@ -141,7 +141,9 @@ int b2s_unpack_windows(const void* d_windows, int width, int batch, int64_t seq_
  * C: row-major [M][ldc], fp32 if c_f32 else bf16; accumulate!=0 adds into C.
  * d_bias: optional bf16 [N] added before the activation.
  * act: 0 none; 1 GELU-tanh (pre-activation written to d_aux as bf16);
- *      2 multiply by GELU-tanh'(d_aux) (fused activation backward).
+ *      2 multiply by GELU-tanh'(d_aux) (fused activation backward);
+ *      5 GELU-tanh with GELU-tanh'(pre-activation) written to d_aux (bf16), so that
+ *      the backward is 6: multiply by d_aux (a plain product epilogue).
  * Strides must keep rows 16-byte aligned (multiples of 8 bf16). */
 int b2s_gemm(const void* d_A, int a_mn_major, int64_t lda, const void* d_B, int b_mn_major,
              int64_t ldb, void* d_C, int64_t ldc, int c_f32, int M, int N, int K, int accumulate,

@@ -83,8 +83,9 @@ struct Epi {
   int accumulate;             // C += result (TMA add-reduce)
   const __nv_bfloat16* bias;  // [N] or null
   int act;                    // 0 none, 1 gelu-tanh (aux <- pre-activation), 2 x gelu'(aux),
-                              // 3 SwiGLU forward, 4 SwiGLU backward (see b2s_gemm_swiglu_*)
-  const __nv_bfloat16* aux_in;  // act=2: [M, ld_aux]; act=4: gu [M, ld_aux = 2F]
+                              // 3 SwiGLU forward, 4 SwiGLU backward (see b2s_gemm_swiglu_*),
+                              // 5 gelu-tanh (aux <- gelu'(pre-activation)), 6 x aux
+  const __nv_bfloat16* aux_in;  // act=2/6: [M, ld_aux]; act=4: gu [M, ld_aux = 2F]
   int64_t ld_aux;
   int glu_F;                  // act 3 / 4: the gate / up split F
 };
@@ -135,6 +136,22 @@ __device__ __forceinline__ float2 gelu_tanh_grad2(float a, float b) {
   const __half2 c_ = __hmul2(x, __hfma2(x2, __float2half2_rn(1.5f * k0 * k1), __float2half2_rn(0.5f * k0)));
   return __half22float2(__hfma2(c_, b_, a_));
 }
+// gelu(x) and gelu'(x) for the pair (a, b), sharing tanh(u): the forward stores
+// gelu' as the aux output so the backward epilogue is a single multiply (act 5 / 6).
+__device__ __forceinline__ void gelu_and_grad2(float a, float b, float2& g, uint32_t& dpacked) {
+  const float k0 = 0.7978845608f, k1 = 0.044715f;
+  const __half2 x = __floats2half2_rn(a, b);
+  const __half2 x2 = __hmul2(x, x);
+  const __half2 t = tanh_h2(__hmul2(x, __hfma2(x2, __float2half2_rn(k0 * k1), __float2half2_rn(k0))));
+  const __half2 half_ = __float2half2_rn(0.5f);
+  const __half2 hx = __hmul2(x, half_);
+  g = __half22float2(__hfma2(hx, t, hx));                                 // 0.5 x (1 + t)
+  const __half2 a_ = __hfma2(half_, t, half_);                           // 0.5 (1 + t)
+  const __half2 b_ = __hfma2(__hneg2(t), t, __float2half2_rn(1.f));       // 1 - t^2
+  const __half2 c_ = __hmul2(x, __hfma2(x2, __float2half2_rn(1.5f * k0 * k1), __float2half2_rn(0.5f * k0)));
+  const float2 d = __half22float2(__hfma2(c_, b_, a_));
+  dpacked = pack_bf16x2(d.x, d.y);
+}
 __device__ __forceinline__ float gelu_tanh_grad(float x) {
   const float k0 = 0.7978845608028654f, k1 = 0.044715f;
   float x2 = x * x;
@@ -170,6 +187,15 @@ __device__ __forceinline__ void stage_bf16(uint8_t* buf, int lane, const float* 
     w.w = pack_bf16x2(v[8 * c + 6], v[8 * c + 7]);
     const int pc = c ^ ((lane >> 1) & 3);
     *reinterpret_cast<uint4*>(buf + lane * 64 + pc * 16) = w;
+  }
+}
+// Same swizzled slot layout for 32 values already packed as 16 bf16 pairs.
+__device__ __forceinline__ void stage_bf16_packed(uint8_t* buf, int lane, const uint32_t* w16) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const int pc = c ^ ((lane >> 1) & 3);
+    *reinterpret_cast<uint4*>(buf + lane * 64 + pc * 16) =
+        make_uint4(w16[4 * c], w16[4 * c + 1], w16[4 * c + 2], w16[4 * c + 3]);
   }
 }
 __device__ __forceinline__ void stage_f32(uint8_t* buf, int lane, const float* v) {
@@ -403,7 +429,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, EW>::kThreads, 1)
     // the current one is processed), so the aux read latency is off the path.
     uint4 aux[4];
     auto load_aux = [&](int tile, int c) {
-      if (epi.act != 2) return;
+      if (epi.act != 2 && epi.act != 6) return;
       const int mn_ = tile % (num_m * num_n);
       const int row = (mn_ % num_m) * BM * CG + rank * BM + q * 32 + lane;
       const int col = (mn_ / num_m) * BN + c * 32;
@@ -556,7 +582,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, EW>::kThreads, 1)
           }
         }
         if (!live) {
-          if (epi.act == 2 && c + kEG < BN / 32) load_aux(tile, c + kEG);  // keep the prefetch chain going
+          if ((epi.act == 2 || epi.act == 6) && c + kEG < BN / 32) load_aux(tile, c + kEG);  // keep the chain going
           continue;
         }
         float v[32];
@@ -586,6 +612,29 @@ __global__ void __launch_bounds__(Cfg<BN, CG, EW>::kThreads, 1)
             v[i] = g.x;
             v[i + 1] = g.y;
           }
+        } else if (epi.act == 5) {  // GELU, aux <- gelu'(z) (bf16) for the backward's plain multiply
+          uint32_t dg[16];
+#pragma unroll
+          for (int i = 0; i < 32; i += 2) {
+            float2 g;
+            gelu_and_grad2(v[i], v[i + 1], g, dg[i / 2]);
+            v[i] = g.x;
+            v[i + 1] = g.y;
+          }
+          uint8_t* b = next_slot();
+          stage_bf16_packed(b, lane, dg);
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) { tma_store_2d(&tmAux, b, col0, rbase); bulk_commit(); }
+        } else if (epi.act == 6) {  // x aux (gelu' stored by the act-5 forward)
+#pragma unroll
+          for (int c8 = 0; c8 < 4; ++c8) {
+            float h[8];
+            unpack8(*reinterpret_cast<const bf16x8*>(&aux[c8]), h);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) v[c8 * 8 + j] *= h[j];
+          }
+          if (c + kEG < BN / 32) load_aux(tile, c + kEG);
         } else if (epi.act == 2) {
 #pragma unroll
           for (int c8 = 0; c8 < 4; ++c8) {
@@ -755,10 +804,10 @@ int gemm_run(const void* d_A, int a_mn_major, int64_t lda, const void* d_B, int 
               B2S_EUNSUPPORTED, "gemm: operands must be 16-byte aligned");
   B2S_REQUIRE((ldc * (c_f32 ? 4 : 2)) % 16 == 0 && N % 8 == 0, B2S_EUNSUPPORTED,
               "gemm: N and ldc must keep output rows 16B aligned");
-  B2S_REQUIRE(act == 0 || (act >= 1 && act <= 4 && d_aux && !c_f32 && (ld_aux * 2) % 16 == 0 &&
+  B2S_REQUIRE(act == 0 || (act >= 1 && act <= 6 && d_aux && !c_f32 && (ld_aux * 2) % 16 == 0 &&
                            ((uintptr_t)d_aux % 16) == 0),
               B2S_EINVAL, "gemm: activation epilogue needs an aligned bf16 aux buffer and bf16 output");
-  B2S_REQUIRE(!(accumulate && (act == 1 || act >= 3)), B2S_EINVAL,
+  B2S_REQUIRE(!(accumulate && (act == 1 || act == 3 || act == 4 || act == 5)), B2S_EINVAL,
               "gemm: accumulate with a GELU / SwiGLU epilogue is not supported");
   gemm::Choice ch = gemm::choose(M, N, K, accumulate && !d_bias && act == 0);
   if (act == 3) ch = gemm::Choice{256, 2, 1};  // the gate / up interleave needs CTA-pair 256-wide tiles
@@ -775,7 +824,7 @@ int gemm_run(const void* d_A, int a_mn_major, int64_t lda, const void* d_B, int 
   if (c_f32) rc = encode_tma_2d(&tc, d_C, 4, (uint64_t)c_width, (uint64_t)M, (uint64_t)ldc * 4, 32, 32, 128);
   else rc = encode_tma_2d(&tc, d_C, 2, (uint64_t)c_width, (uint64_t)M, (uint64_t)ldc * 2, 32, 32, 64);
   if (rc) return rc;
-  if (act == 1 || act == 2 || act == 3)
+  if (act == 1 || act == 2 || act == 3 || act == 5 || act == 6)
     rc = encode_tma_2d(&tx, d_aux, 2, (uint64_t)aux_width, (uint64_t)M, (uint64_t)ld_aux * 2, 32, 32, 64);
   else tx = tc;
   if (rc) return rc;
@@ -793,8 +842,9 @@ extern "C" int b2s_gemm(const void* d_A, int a_mn_major, int64_t lda, const void
                         int b_mn_major, int64_t ldb, void* d_C, int64_t ldc, int c_f32, int M,
                         int N, int K, int accumulate, const void* d_bias, int act, void* d_aux,
                         int64_t ld_aux, b2s_stream_t stream) {
-  B2S_REQUIRE(act >= 0 && act <= 2, B2S_EINVAL, "gemm: act must be 0, 1 or 2 (SwiGLU: b2s_gemm_swiglu_*)");
-  B2S_REQUIRE(!(accumulate && act == 1), B2S_EINVAL, "gemm: accumulate with GELU is not supported");
+  B2S_REQUIRE(act == 0 || act == 1 || act == 2 || act == 5 || act == 6, B2S_EINVAL,
+              "gemm: act must be 0, 1, 2, 5 or 6 (SwiGLU: b2s_gemm_swiglu_*)");
+  B2S_REQUIRE(!(accumulate && (act == 1 || act == 5)), B2S_EINVAL, "gemm: accumulate with GELU is not supported");
   return gemm_run(d_A, a_mn_major, lda, d_B, b_mn_major, ldb, d_C, ldc, c_f32, M, N, K, accumulate, d_bias, act,
                   d_aux, ld_aux, 0, N, N, (cudaStream_t)stream);
 }

@@ -363,7 +363,10 @@ class DecoderLM(torch.nn.Module):
                  bias=U.p("proj_b") if gpt2 else None)
         if gpt2:
             ops.layernorm_fwd_res(S.xa, S.ya, U.p("ln2_g"), U.p("ln2_b"), eps, S.ln_b, S.mean_b, S.rstd_b, S.xb)
-            ops.linear(S.ln_b, U.p("fc_w"), bias=U.p("fc_b"), out=S.h, act=1, aux=S.hpre)
+            # bf16: the epilogue stores gelu'(z) in hpre (act 5) so the backward multiplies by it
+            # (act 6); fp32 mode keeps z itself (act 1 / 2 on the SIMT kernel)
+            ops.linear(S.ln_b, U.p("fc_w"), bias=U.p("fc_b"), out=S.h, act=1 if self.precision == "fp32" else 5,
+                       aux=S.hpre)
             if with_output:
                 ops.gemm(S.h, U.p("fc2_w"), a_mn=False, b_mn=False, M=M, N=d, K=cfg.d_ff, out=S.yb,
                          bias=U.p("fc2_b"))
@@ -447,7 +450,8 @@ class DecoderLM(torch.nn.Module):
             # --- MLP (its output gradient is the residual gradient dx, bf16 copy in dxb)
             if gpt2:  # fc2_b's grad was summed by the norm backward that produced dx
                 ops.linear_wgrad(A.dxb, S.h, out=U.g("fc2_w"), accumulate=True)
-                ops.linear_dgrad(A.dxb, U.p("fc2_w"), out=A.dh, act=2, aux=S.hpre)
+                ops.linear_dgrad(A.dxb, U.p("fc2_w"), out=A.dh, act=2 if self.precision == "fp32" else 6,
+                                 aux=S.hpre)
                 ops.colsum_accumulate(A.dh, U.g("fc_b"))
                 ops.linear_wgrad(A.dh, S.ln_b, out=U.g("fc_w"), accumulate=True)
                 ops.linear_dgrad(A.dh, U.p("fc_w"), out=A.dln)

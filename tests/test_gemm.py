@@ -67,6 +67,17 @@ def test_gemm_epilogues(cuda, force):
     p = pre.float().requires_grad_()
     torch.nn.functional.gelu(p, approximate="tanh").backward(dy.float() @ w2.float())
     torch.testing.assert_close(dh.float(), p.grad, rtol=2e-2, atol=5e-2)
+    # act 5 / 6: the forward stores gelu'(z) instead of z, the backward multiplies by it
+    gd = torch.empty(M, N, device=cuda, dtype=torch.bfloat16)
+    y5 = ops.linear(x, w, bias=bias, act=5, aux=gd)
+    z = ref_pre.requires_grad_()
+    gz = torch.nn.functional.gelu(z, approximate="tanh")
+    torch.testing.assert_close(y5.float(), gz.detach(), rtol=1e-2, atol=2e-2)
+    gz.backward(torch.ones_like(gz))
+    torch.testing.assert_close(gd.float(), z.grad, rtol=1e-2, atol=2e-2)
+    dh6 = ops.linear_dgrad(dy, w2, act=6, aux=gd)
+    torch.testing.assert_close(dh6.float(), (dy.float() @ w2.float()) * gd.float(), rtol=1e-2, atol=2e-2)
+    torch.testing.assert_close(dh6.float(), p.grad, rtol=2e-2, atol=5e-2)
     # accumulate (fp32 and bf16) and wgrad
     acc = torch.randn(N, K, device=cuda)
     ref = acc + dy.new_tensor(0).float() + (torch.randn(0, device=cuda).sum())

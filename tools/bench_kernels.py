@@ -92,6 +92,9 @@ def bench_epilogues():
         ("fc.fwd plain", M, f, d, lambda: ops.linear(x, w_fc, out=h)),
         ("fc2.dgrad+dgelu", M, f, d, lambda: ops.linear_dgrad(dy, w_fc2, out=dh, act=2, aux=hpre)),
         ("fc2.dgrad plain", M, f, d, lambda: ops.linear_dgrad(dy, w_fc2, out=dh)),
+        ("fc.fwd+bias+gelu, aux=gelu' (act 5)", M, f, d,
+         lambda: ops.linear(x, w_fc, bias=b_fc, out=h, act=5, aux=hpre)),
+        ("fc2.dgrad x aux (act 6)", M, f, d, lambda: ops.linear_dgrad(dy, w_fc2, out=dh, act=6, aux=hpre)),
         ("fc2.fwd+bias+f32 resid add", M, d, f, lambda: ops.gemm(h, w_fc2, a_mn=False, b_mn=False, M=M, N=d, K=f,
                                                                   out=resid, accumulate=True, bias=b_d)),
         ("proj.fwd+bias+f32 resid add", M, d, d, lambda: ops.gemm(o, w_o, a_mn=False, b_mn=False, M=M, N=d, K=d,
