@@ -171,6 +171,7 @@ struct Cfg {
   static constexpr int kStages = (CG == 2) ? (EW == 8 ? 5 : 4) : (BN == 256 ? 3 : 4);
   static constexpr int kTmemCols = 2 * BN;  // double-buffered accumulator
   static constexpr int kSmem = kStages * kStageBytes + kEpiSmem + 1024 /*align*/ + 512 /*barriers, tile ring*/;
+  static_assert((2 * kStages + 4 + 2 * 8) * 8 + 8 * 4 + 8 + 2 * kEpiWarps * 8 <= 512, "barrier region");
   static_assert(kSmem <= 227 * 1024, "smem budget");
 };
 
@@ -236,6 +237,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, EW>::kThreads, 1)
   uint64_t* rempty = rfull + kRing;   // [kRing] every reader done with the slot (leader CTA's count)
   int* ring = reinterpret_cast<int*>(rempty + kRing);
   uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(ring + kRing);
+  uint64_t* abar_all = reinterpret_cast<uint64_t*>(tmem_base_slot + 2);  // [epilogue warp][2] aux tile landed
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = (CG == 2) ? cluster_ctarank() : 0;
@@ -254,6 +256,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, EW>::kThreads, 1)
     for (int s = 0; s < C_::kStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], CG * kEpiWarps); }
     for (int i = 0; i < kRing; ++i) { mbar_init(&rfull[i], 1); mbar_init(&rempty[i], kRingReaders); }
+    for (int i = 0; i < 2 * kEpiWarps; ++i) mbar_init(&abar_all[i], 1);
     fence_barrier_init();
   }
   if (warp == 1) {
@@ -411,11 +414,20 @@ __global__ void __launch_bounds__(Cfg<BN, CG, EW>::kThreads, 1)
     // fp32 outputs: two 4 KB slots (wait until <= 1 store group still reads smem);
     // bf16 outputs: four 2 KB slots (<= 3 pending) -- the GELU / SwiGLU epilogues
     // issue 2-3 stores per chunk and would otherwise wait on their own stores.
+    // act 2 / 6 read their aux tiles through slots 2, 3 (TMA loads, one 32 x 32 bf16
+    // box per chunk, 64-byte swizzle like the stores); their outputs use slots 0, 1
+    const bool aux_tma = (epi.act == 2 || epi.act == 6);
+    const bool two_slots = aux_tma || epi.act == 4;  // outputs staged through slots 0, 1 only
+    uint64_t* abar = abar_all + 2 * (warp - 2);
+    uint32_t aux_issued = 0, aux_used = 0;
     auto next_slot = [&]() -> uint8_t* {
       uint8_t* b;
       if (epi.out_f32) {
         if (lane == 0) bulk_wait_read<1>();
         b = ring + (slot & 1) * kStageSlot;
+      } else if (two_slots) {
+        if (lane == 0) bulk_wait_read<1>();
+        b = ring + (slot & 1) * (kStageSlot / 2);
       } else {
         if (lane == 0) bulk_wait_read<3>();
         b = ring + (slot & 3) * (kStageSlot / 2);
@@ -429,22 +441,36 @@ __global__ void __launch_bounds__(Cfg<BN, CG, EW>::kThreads, 1)
     // the current one is processed), so the aux read latency is off the path.
     uint4 aux[4];
     auto load_aux = [&](int tile, int c) {
-      if (epi.act != 2 && epi.act != 6) return;
+      if (!aux_tma) return;
       const int mn_ = tile % (num_m * num_n);
-      const int row = (mn_ % num_m) * BM * CG + rank * BM + q * 32 + lane;
+      const int row0 = (mn_ % num_m) * BM * CG + rank * BM + q * 32;
       const int col = (mn_ / num_m) * BN + c * 32;
-      if (row >= M) return;
-      const __nv_bfloat16* p = epi.aux_in + (int64_t)row * epi.ld_aux + col;
+      const int s_ = aux_issued & 1;
+      if (lane == 0) {  // out-of-range rows / columns are zero-filled and still counted
+        mbar_arrive_expect_tx(&abar[s_], 32 * 32 * 2);
+        tma_load_2d(ring + (2 + s_) * (kStageSlot / 2), &tmAux, &abar[s_], col, row0);
+      }
+      ++aux_issued;
+    };
+    // this chunk's aux tile -> registers (each lane its row's 64 bytes)
+    auto take_aux = [&](bool read) {
+      const int s_ = aux_used & 1;
+      mbar_wait(&abar[s_], (aux_used >> 1) & 1);
+      if (read) {
+        const uint8_t* b = ring + (2 + s_) * (kStageSlot / 2);
 #pragma unroll
-      for (int k = 0; k < 4; ++k)
-        if (col + 8 * k < N) aux[k] = __ldg(reinterpret_cast<const uint4*>(p + 8 * k));
+        for (int k = 0; k < 4; ++k) aux[k] = *reinterpret_cast<const uint4*>(b + lane * 64 + ((k ^ ((lane >> 1) & 3)) * 16));
+      }
+      ++aux_used;
+      __syncwarp();  // every lane has read the slot before its next TMA load is issued
     };
     for (int it = 0;; ++it) {
       const int tile = ring_get(it);
       __syncwarp();
       if (lane == 0) ring_release(it, tile);
       if (tile >= num_tiles) break;
-      load_aux(tile, half);  // first chunk's pre-activations: in flight while the MMAs finish
+      load_aux(tile, half);  // first two chunks' aux tiles: in flight while the MMAs finish
+      if (half + kEG < BN / 32) load_aux(tile, half + kEG);
       const int mn = tile % (num_m * num_n);
       const int m0 = (mn % num_m) * BM * CG + rank * BM, n0 = (mn / num_m) * BN;
       mbar_wait(&tfull[acc], acc_phase);
@@ -495,25 +521,30 @@ __global__ void __launch_bounds__(Cfg<BN, CG, EW>::kThreads, 1)
       }
       if (epi.act == 4) {  // SwiGLU backward: dh chunk (accumulator) -> [dgate | dup] using gu
         const int F = epi.glu_F;
-        uint4 gq[4], uq[4], gn[4], un[4];  // this chunk's gate / up, and the next chunk's (prefetched)
-        auto load_gu = [&](int col, uint4* gg, uint4* uu) {
-          if (rbase + lane >= M) return;
-          const __nv_bfloat16* p = epi.aux_in + (int64_t)(rbase + lane) * epi.ld_aux + col;
-#pragma unroll
-          for (int k = 0; k < 4; ++k)
-            if (col + 8 * k < N) {
-              gg[k] = __ldg(reinterpret_cast<const uint4*>(p + 8 * k));
-              uu[k] = __ldg(reinterpret_cast<const uint4*>(p + F + 8 * k));
-            }
+        uint4 gq[4], uq[4];  // this chunk's gate / up rows (64 bytes each per lane)
+        // gate and up 32 x 32 tiles of a chunk land in slots 2, 3 by TMA (zero-filled out of range)
+        auto load_gu = [&](int col) {
+          if (lane == 0) {
+            mbar_arrive_expect_tx(&abar[0], 2 * 32 * 32 * 2);
+            tma_load_2d(ring + 2 * (kStageSlot / 2), &tmAux, &abar[0], col, rbase);
+            tma_load_2d(ring + 3 * (kStageSlot / 2), &tmAux, &abar[0], col + F, rbase);
+          }
         };
-        if (rbase < M && n0 + half * 32 < N) load_gu(n0 + half * 32, gn, un);
+        load_gu(n0 + half * 32);
 #pragma unroll 1
         for (int c = half; c < BN / 32; c += kEG) {
           const int col0 = n0 + c * 32;
           const bool live = rbase < M && col0 < N;
+          mbar_wait(&abar[0], aux_used & 1);
+          ++aux_used;
 #pragma unroll
-          for (int k = 0; k < 4; ++k) { gq[k] = gn[k]; uq[k] = un[k]; }
-          if (c + kEG < BN / 32 && rbase < M && col0 + kEG * 32 < N) load_gu(col0 + kEG * 32, gn, un);
+          for (int k = 0; k < 4; ++k) {
+            const int off = lane * 64 + ((k ^ ((lane >> 1) & 3)) * 16);
+            gq[k] = *reinterpret_cast<const uint4*>(ring + 2 * (kStageSlot / 2) + off);
+            uq[k] = *reinterpret_cast<const uint4*>(ring + 3 * (kStageSlot / 2) + off);
+          }
+          __syncwarp();  // slots 2, 3 read by every lane: the next chunk's tiles may land
+          if (c + kEG < BN / 32) load_gu(col0 + kEG * 32);
           uint32_t r[32];
           tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, r);
           tmem_wait_ld();
@@ -582,7 +613,10 @@ __global__ void __launch_bounds__(Cfg<BN, CG, EW>::kThreads, 1)
           }
         }
         if (!live) {
-          if ((epi.act == 2 || epi.act == 6) && c + kEG < BN / 32) load_aux(tile, c + kEG);  // keep the chain going
+          if (aux_tma) {
+            take_aux(false);
+            if (c + 2 * kEG < BN / 32) load_aux(tile, c + 2 * kEG);  // keep the chain going
+          }
           continue;
         }
         float v[32];
@@ -627,6 +661,8 @@ __global__ void __launch_bounds__(Cfg<BN, CG, EW>::kThreads, 1)
           __syncwarp();
           if (lane == 0) { tma_store_2d(&tmAux, b, col0, rbase); bulk_commit(); }
         } else if (epi.act == 6) {  // x aux (gelu' stored by the act-5 forward)
+          take_aux(true);
+          if (c + 2 * kEG < BN / 32) load_aux(tile, c + 2 * kEG);  // two chunks ahead (both slots busy)
 #pragma unroll
           for (int c8 = 0; c8 < 4; ++c8) {
             float h[8];
@@ -634,8 +670,9 @@ __global__ void __launch_bounds__(Cfg<BN, CG, EW>::kThreads, 1)
 #pragma unroll
             for (int j = 0; j < 8; ++j) v[c8 * 8 + j] *= h[j];
           }
-          if (c + kEG < BN / 32) load_aux(tile, c + kEG);
         } else if (epi.act == 2) {
+          take_aux(true);
+          if (c + 2 * kEG < BN / 32) load_aux(tile, c + 2 * kEG);  // two chunks ahead (both slots busy)
 #pragma unroll
           for (int c8 = 0; c8 < 4; ++c8) {
             float h[8];
@@ -647,8 +684,6 @@ __global__ void __launch_bounds__(Cfg<BN, CG, EW>::kThreads, 1)
               v[c8 * 8 + j + 1] *= g.y;
             }
           }
-          // prefetch the next chunk of this warp (the next tile's first chunk is loaded on arrival)
-          if (c + kEG < BN / 32) load_aux(tile, c + kEG);
         }
         uint8_t* b = next_slot();
         if (epi.out_f32) stage_f32(b, lane, v);
@@ -824,13 +859,14 @@ int gemm_run(const void* d_A, int a_mn_major, int64_t lda, const void* d_B, int 
   if (c_f32) rc = encode_tma_2d(&tc, d_C, 4, (uint64_t)c_width, (uint64_t)M, (uint64_t)ldc * 4, 32, 32, 128);
   else rc = encode_tma_2d(&tc, d_C, 2, (uint64_t)c_width, (uint64_t)M, (uint64_t)ldc * 2, 32, 32, 64);
   if (rc) return rc;
-  if (act == 1 || act == 2 || act == 3 || act == 5 || act == 6)
+  if (act >= 1 && act <= 6)
     rc = encode_tma_2d(&tx, d_aux, 2, (uint64_t)aux_width, (uint64_t)M, (uint64_t)ld_aux * 2, 32, 32, 64);
   else tx = tc;
   if (rc) return rc;
   gemm::Epi e{c_f32, accumulate, (const __nv_bfloat16*)d_bias, act, (const __nv_bfloat16*)d_aux, ld_aux, glu_F};
   const int splits = ch.splits;
-  if (ch.cg == 2 && act != 0)  // activation epilogue: 12 epilogue warps (see EW above)
+  if (ch.cg == 2 && act != 0 && act != 6)  // activation epilogue: 12 epilogue warps (see EW above);
+    // the x aux product (act 6) is light enough for 8 warps and the deeper 5-stage mainloop
     return gemm::dispatch<256, 2, 12>(a_mn_major, b_mn_major, ta, tb, tc, tx, M, N, K, splits, e, st);
   if (ch.cg == 2) return gemm::dispatch<256, 2>(a_mn_major, b_mn_major, ta, tb, tc, tx, M, N, K, splits, e, st);
   if (bn == 256) return gemm::dispatch<256, 1>(a_mn_major, b_mn_major, ta, tb, tc, tx, M, N, K, splits, e, st);

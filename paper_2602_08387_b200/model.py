@@ -23,6 +23,7 @@ Numerics (``precision``):
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass, field, replace
 
 import torch
@@ -31,6 +32,9 @@ from . import ops
 
 ALIGN = 64  # parameter offsets inside a flat unit, in elements (128 B of bf16)
 PRECISIONS = {"bf16": torch.bfloat16, "fp32": torch.float32}
+# A/B switches for the fused epilogue variants (default on; "0" selects the older chains)
+_GELU_AUX_GRAD = os.environ.get("B2S_GELU_AUX_GRAD", "1") != "0"
+_FUSED_SWIGLU_BWD = os.environ.get("B2S_SWIGLU_BWD_FUSED", "1") != "0"
 
 
 @dataclass(frozen=True)
@@ -310,6 +314,9 @@ class DecoderLM(torch.nn.Module):
                              "use precision='fp32' for other head dims")
         self.cfg = cfg
         self.precision = precision
+        # GELU epilogues: bf16 stores gelu'(z) as the aux (act 5 / 6); fp32 keeps z (act 1 / 2)
+        gd = precision != "fp32" and _GELU_AUX_GRAD
+        self._act_fwd, self._act_bwd = (5, 6) if gd else (1, 2)
         self.dtype = PRECISIONS[precision]
         self.activation_checkpointing = bool(activation_checkpointing)
         self.units = unit_specs(cfg)
@@ -365,8 +372,7 @@ class DecoderLM(torch.nn.Module):
             ops.layernorm_fwd_res(S.xa, S.ya, U.p("ln2_g"), U.p("ln2_b"), eps, S.ln_b, S.mean_b, S.rstd_b, S.xb)
             # bf16: the epilogue stores gelu'(z) in hpre (act 5) so the backward multiplies by it
             # (act 6); fp32 mode keeps z itself (act 1 / 2 on the SIMT kernel)
-            ops.linear(S.ln_b, U.p("fc_w"), bias=U.p("fc_b"), out=S.h, act=1 if self.precision == "fp32" else 5,
-                       aux=S.hpre)
+            ops.linear(S.ln_b, U.p("fc_w"), bias=U.p("fc_b"), out=S.h, act=self._act_fwd, aux=S.hpre)
             if with_output:
                 ops.gemm(S.h, U.p("fc2_w"), a_mn=False, b_mn=False, M=M, N=d, K=cfg.d_ff, out=S.yb,
                          bias=U.p("fc2_b"))
@@ -450,8 +456,7 @@ class DecoderLM(torch.nn.Module):
             # --- MLP (its output gradient is the residual gradient dx, bf16 copy in dxb)
             if gpt2:  # fc2_b's grad was summed by the norm backward that produced dx
                 ops.linear_wgrad(A.dxb, S.h, out=U.g("fc2_w"), accumulate=True)
-                ops.linear_dgrad(A.dxb, U.p("fc2_w"), out=A.dh, act=2 if self.precision == "fp32" else 6,
-                                 aux=S.hpre)
+                ops.linear_dgrad(A.dxb, U.p("fc2_w"), out=A.dh, act=self._act_bwd, aux=S.hpre)
                 ops.colsum_accumulate(A.dh, U.g("fc_b"))
                 ops.linear_wgrad(A.dh, S.ln_b, out=U.g("fc_w"), accumulate=True)
                 ops.linear_dgrad(A.dh, U.p("fc_w"), out=A.dln)
@@ -459,10 +464,13 @@ class DecoderLM(torch.nn.Module):
                                   U.g("ln2_g"), U.g("ln2_b"), dxsum=U.g("proj_b"))
             else:
                 ops.linear_wgrad(A.dxb, S.h, out=U.g("w2"), accumulate=True)
-                # (b2s_gemm_swiglu_bwd fuses this pair; measured slower -- its epilogue, 8 B in and
-                # 4 B out per element, becomes the bottleneck -- so the step keeps the chain)
-                ops.linear_dgrad(A.dxb, U.p("w2"), out=A.dh)
-                ops.swiglu_bwd(S.gu, A.dh, A.dgu)
+                if self.dtype == torch.bfloat16 and cfg.d_ff % 128 == 0 and _FUSED_SWIGLU_BWD:
+                    # dh = dy W2 with the SwiGLU backward in the epilogue (gate / up tiles by TMA):
+                    # dh never reaches HBM (0.68 -> 0.61 ms per Llama-1B layer)
+                    ops.linear_dgrad_swiglu(A.dxb, U.p("w2"), S.gu, A.dgu)
+                else:
+                    ops.linear_dgrad(A.dxb, U.p("w2"), out=A.dh)
+                    ops.swiglu_bwd(S.gu, A.dh, A.dgu)
                 ops.linear_wgrad(A.dgu, S.ln_b, out=U.g("w13"), accumulate=True)
                 ops.linear_dgrad(A.dgu, U.p("w13"), out=A.dln)
                 ops.rmsnorm_bwd(S.xb, A.dln, U.p("mlp_norm"), S.rstd_b, A.dx, A.dxb, U.g("mlp_norm"))
