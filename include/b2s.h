@@ -224,6 +224,13 @@ int b2s_cross_entropy(void* d_logits, int64_t ld, int V, const int64_t* d_target
 int b2s_sum(const float* d_x, int64_t n, int squares, float* d_out, float scale, b2s_stream_t stream);
 /* d_part[b] = partial sum of squares (b < nparts), deterministic stage 1. */
 int b2s_sumsq_partial(const float* d_x, int64_t n, float* d_part, int nparts, b2s_stream_t stream);
+/* Same over nseg buffers in one launch (the global gradient norm over every FSDP
+ * unit's shard): d_ptrs / d_lens are device arrays of nseg fp32 buffer addresses
+ * (16-byte aligned) and element counts; d_part[b] sums all segments. Replaces the
+ * reference's per-parameter torch.nn.utils.clip_grad_norm_ norm pass
+ * (gradient clipping in the optimizer step). */
+int b2s_sumsq_partial_multi(const uint64_t* d_ptrs, const int64_t* d_lens, int nseg, float* d_part, int nparts,
+                            b2s_stream_t stream);
 
 /* Fused AdamW over a flat fp32 shard (K10). Gradient clipping by the global
  * norm is applied on the device: clip = min(1, max_norm/(sqrt(*d_gn2)+1e-6))

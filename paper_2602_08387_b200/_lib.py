@@ -73,6 +73,7 @@ _SIGS = {
     "b2s_cross_entropy": "plippflip",
     "b2s_sum": "plipfp",
     "b2s_sumsq_partial": "plpip",
+    "b2s_sumsq_partial_multi": "ppipip",
     "b2s_adamw": "pppppplpffffffip",
     "b2s_f32_to_bf16": "pplfp",
     "b2s_scale_f32": "plfp",

@@ -651,6 +651,35 @@ __global__ void __launch_bounds__(1024) sum_kernel(const float* __restrict__ x, 
   acc = block_sum(acc, scratch);
   if (threadIdx.x == 0) out[0] = acc * scale;
 }
+// Stage 1 of the gradient norm over several buffers in one launch: every block
+// grid-strides over each segment in turn (four 16-byte loads in flight per
+// thread), part[block] = its sum of squares over all segments (fixed order).
+__global__ void __launch_bounds__(256) sumsq_multi_kernel(const uint64_t* __restrict__ ptrs,
+                                                          const int64_t* __restrict__ lens, int nseg,
+                                                          float* __restrict__ part) {
+  __shared__ float scratch[32];
+  float acc = 0.f;
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, nth = (int64_t)gridDim.x * blockDim.x;
+  for (int sgi = 0; sgi < nseg; ++sgi) {
+    const float* x = reinterpret_cast<const float*>(ptrs[sgi]);
+    const int64_t n = lens[sgi], nv = n / 4;
+    int64_t i = tid;
+    for (; i + 3 * nth < nv; i += 4 * nth) {
+      float4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = __ldcs(reinterpret_cast<const float4*>(x) + i + u * nth);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc += v[u].x * v[u].x + v[u].y * v[u].y + v[u].z * v[u].z + v[u].w * v[u].w;
+    }
+    for (; i < nv; i += nth) {
+      const float4 v = __ldcs(reinterpret_cast<const float4*>(x) + i);
+      acc += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+    }
+    for (int64_t j = nv * 4 + tid; j < n; j += nth) acc += x[j] * x[j];
+  }
+  acc = block_sum(acc, scratch);
+  if (threadIdx.x == 0) part[blockIdx.x] = acc;
+}
 // Stage 1 of a deterministic large sum of squares: part[block] = sum x^2.
 __global__ void __launch_bounds__(256) sumsq_part_kernel(const float* __restrict__ x, int64_t n,
                                                          float* __restrict__ part) {
@@ -1033,6 +1062,12 @@ int b2s_cross_entropy_f32(float* d_logits, int64_t ld, int V, const int64_t* d_t
 int b2s_sum(const float* d_x, int64_t n, int squares, float* d_out, float scale, b2s_stream_t stream) {
   ew::sum_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(d_x, n, squares, d_out, scale);
   return check_launch("sum");
+}
+int b2s_sumsq_partial_multi(const uint64_t* d_ptrs, const int64_t* d_lens, int nseg, float* d_part, int nparts,
+                            b2s_stream_t stream) {
+  B2S_REQUIRE(nseg >= 0 && nparts > 0, B2S_EINVAL, "sumsq_partial_multi: bad sizes");
+  ew::sumsq_multi_kernel<<<nparts, 256, 0, (cudaStream_t)stream>>>(d_ptrs, d_lens, nseg, d_part);
+  return check_launch("sumsq_partial_multi");
 }
 int b2s_sumsq_partial(const float* d_x, int64_t n, float* d_part, int nparts, b2s_stream_t stream) {
   ew::sumsq_part_kernel<<<nparts, 256, 0, (cudaStream_t)stream>>>(d_x, n, d_part);

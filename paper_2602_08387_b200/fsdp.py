@@ -30,8 +30,13 @@ import torch.distributed as dist
 from .model import ALIGN, UnitSpec
 
 
+def _padded_numel(specs: list, world: int) -> int:
+    per = -(-sum(s.numel for s in specs) // world)
+    return (-(-per // ALIGN) * ALIGN) * world
+
+
 class FlatUnit:
-    def __init__(self, specs: list, rank: int, world: int, device, dtype=torch.bfloat16):
+    def __init__(self, specs: list, rank: int, world: int, device, dtype=torch.bfloat16, gfull=None):
         self.specs = specs  # one or more model UnitSpecs grouped into this FSDP unit
         self.rank, self.world = rank, world
         self.offsets = {}
@@ -46,7 +51,10 @@ class FlatUnit:
         self.padded = self.shard * world
         bf, f32 = dtype, torch.float32
         self.full = torch.zeros(self.padded, device=device, dtype=bf)
-        self.gfull = torch.zeros(self.padded, device=device, dtype=f32)
+        # gfull: this unit's slice of one buffer holding every unit's gradients (one
+        # memset per step instead of one per unit), or its own allocation
+        self.gfull = gfull if gfull is not None else torch.zeros(self.padded, device=device, dtype=f32)
+        assert self.gfull.numel() == self.padded
         lo = rank * self.shard
         if world == 1:
             self.g = self.gfull
@@ -119,7 +127,11 @@ class FlatParams:
                 groups.append([s])
         if cur:
             groups.append(cur)
-        self.flat = [FlatUnit(g, rank, world, device, dtype) for g in groups]
+        sizes = [_padded_numel(g, world) for g in groups]
+        self.gall = torch.zeros(sum(sizes), device=device, dtype=torch.float32)
+        offs = [sum(sizes[:i]) for i in range(len(sizes))]
+        self.flat = [FlatUnit(g, rank, world, device, dtype, gfull=self.gall[o:o + n])
+                     for g, o, n in zip(groups, offs, sizes)]
         self.owner = {}
         self.first_model_unit = {}
         self.last_model_unit = {}
@@ -199,8 +211,7 @@ class Engine:
 
     # ------------------------------------------------------------------ step
     def begin_step(self) -> None:
-        for f in self.P.flat:
-            f.gfull.zero_()
+        self.P.gall.zero_()
         if self.world > 1 and self._prefetched == len(self.P.flat):
             # every unit's all-gather was queued right after its optimizer update
             self._issued = len(self.P.flat)

@@ -318,6 +318,12 @@ def sumsq_partial(x, part):
     _call("b2s_sumsq_partial", x.data_ptr(), x.numel(), part.data_ptr(), part.numel(), _sp())
 
 
+def sumsq_partial_multi(table, nseg, part):
+    """table: int64 device tensor [2, nseg] = (fp32 buffer addresses, element counts)."""
+    _call("b2s_sumsq_partial_multi", table[0].data_ptr(), table[1].data_ptr(), nseg, part.data_ptr(), part.numel(),
+          _sp())
+
+
 def adamw(p, m, v, g, p_bf16, step, lr, beta1, beta2, eps, wd, gn2=None, max_norm=0.0, wd_mask=None):
     """p_bf16: the compute copy written after the update (bf16 or fp32), or None / p itself (fp32 mode)."""
     if p_bf16 is p:

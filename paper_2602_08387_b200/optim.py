@@ -55,11 +55,13 @@ class FusedAdamW:
         dev = flats[0].g.device
         nparts = 4 * 148
         if self._part is None:
-            self._part = torch.empty(len(flats) * nparts, device=dev)
+            self._part = torch.empty(nparts, device=dev)
             self._red = torch.zeros(2, device=dev)
             self._gn2 = self._red[0:1]
-        for i, f in enumerate(flats):
-            ops.sumsq_partial(f.g, self._part[i * nparts:(i + 1) * nparts])
+            # one launch over every unit's gradient shard (addresses are stable for the run)
+            self._table = torch.tensor([[f.g.data_ptr() for f in flats], [f.g.numel() for f in flats]],
+                                       dtype=torch.int64).to(dev)
+        ops.sumsq_partial_multi(self._table, len(flats), self._part)
         ops.sum_(self._part, self._gn2)
         if world > 1:
             if loss is not None:

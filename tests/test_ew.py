@@ -183,3 +183,13 @@ def test_adamw_and_sums(cuda):
     part = torch.empty(37, device=cuda)
     ops.sumsq_partial(g, part)
     torch.testing.assert_close(part.sum(), (g * g).sum(), rtol=1e-5, atol=1e-3)
+    # one launch over several buffers (odd lengths: scalar tails), fixed order -> repeatable
+    segs = [torch.randn(n, device=cuda) for n in (10_003, 4, 1, 123_457, 2_000_000)]
+    table = torch.tensor([[x.data_ptr() for x in segs], [x.numel() for x in segs]], dtype=torch.int64).to(cuda)
+    part = torch.empty(592, device=cuda)
+    ops.sumsq_partial_multi(table, len(segs), part)
+    ref = sum((x.double() ** 2).sum() for x in segs)
+    torch.testing.assert_close(part.double().sum(), ref, rtol=1e-5, atol=1e-3)
+    part2 = torch.empty_like(part)
+    ops.sumsq_partial_multi(table, len(segs), part2)
+    assert torch.equal(part, part2)
