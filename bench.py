@@ -163,7 +163,9 @@ def run_ours(args):
     path = None
     if rank == 0:
         path = _data_path(cfg, n_tokens)
-    tr = SPMDTrainer(DecoderLM(cfg, activation_checkpointing=args.ac), AdamWConfig(), None, steps=0, seed=0,
+    # B2S_GRAD_CLIP: diagnostics only (the reference default, 1.0, is what the bench line reports)
+    ocfg = AdamWConfig(grad_clip=float(os.environ.get("B2S_GRAD_CLIP", AdamWConfig().grad_clip)))
+    tr = SPMDTrainer(DecoderLM(cfg, activation_checkpointing=args.ac), ocfg, None, steps=0, seed=0,
                      blocks_per_unit=args.blocks_per_unit, init_device="cuda")
     # distributed init happens in setup(); make sure the data file exists first
     from paper_2602_08387_b200.trainer import init_distributed

@@ -721,6 +721,18 @@ __global__ void __launch_bounds__(Cfg<BN, CG, EW>::kThreads, 1)
   }
 }
 
+// SMs the persistent GEMM grid may occupy (B2S_GEMM_SMS; default all 148). With
+// collectives overlapping compute (W > 1) leaving a few SMs to NCCL's CTAs keeps a
+// persistent grid from waiting on them.
+static int gemm_sms() {
+  static const int n = [] {
+    const char* e = getenv("B2S_GEMM_SMS");
+    const int v = e ? atoi(e) : kNumSMs;
+    return (v >= 2 && v <= kNumSMs) ? v : kNumSMs;
+  }();
+  return n;
+}
+
 // Per-device pool of zeroed scheduler counters {next_tile, ctas_done}; launches
 // rotate through the pool so GEMMs in flight on different streams never share one.
 constexpr int kSchedSlots = 64;
@@ -753,7 +765,7 @@ static int launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMa
     attr_set = true;
   }
   const int tiles = ((M + BM * CG - 1) / (BM * CG)) * ((N + BN - 1) / BN) * splits;
-  const int slots = kNumSMs / CG;
+  const int slots = gemm_sms() / CG;
   const int grid = (tiles < slots ? tiles : slots) * CG;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
@@ -809,7 +821,7 @@ static Choice choose(int M, int N, int K, bool can_split) {
       if (sp > 1 && nkb / sp < 8) break;
       const Choice c{cands[i].bn, cands[i].cg, sp};
       const long mt = (M + BM * c.cg - 1) / (BM * c.cg), nt = (N + c.bn - 1) / c.bn;
-      const long tiles = mt * nt * sp, slots = kNumSMs / c.cg;
+      const long tiles = mt * nt * sp, slots = gemm_sms() / c.cg;
       const long waves = (tiles + slots - 1) / slots;
       const double fill = (double)tiles / (double)(waves * slots);
       const double pad = ((double)M / (mt * BM * c.cg)) * ((double)N / (nt * c.bn));

@@ -205,6 +205,7 @@ class Engine:
         self.rs_done = [torch.cuda.Event() for _ in range(n)] if self.cuda else [None] * n
         self._issued = 0
         self._prefetched = 0  # units whose next-step all-gather was issued after their optimizer update
+        self.in_graph = False  # capturing the W > 1 forward/backward: all-gathers were awaited before replay
         self.timing = None  # list of (kind, bytes, start_event, end_event) while collective timing is on
         self.bytes_ag = sum(f.padded * f.full.element_size() for f in params.flat)
         self.bytes_rs = sum(f.padded * 4 for f in params.flat)
@@ -225,6 +226,16 @@ class Engine:
                 ready.record()  # after the previous optimizer step wrote p16
                 self.comm.wait_event(ready)
             self._issue_until(min(len(self.P.flat), self.prefetch))
+
+    def graph_step_prologue(self) -> None:
+        """Host side of begin_step for a graph replay (W > 1): every unit's all-gather was
+        queued after its optimizer update; the compute stream waits for all of them here,
+        outside the graph (events recorded outside a capture cannot be awaited inside it)."""
+        cur = torch.cuda.current_stream()
+        for e in self.ag_done:
+            cur.wait_event(e)
+        self._issued = len(self.P.flat)
+        self._prefetched = 0
 
     def after_update(self, fi: int) -> None:
         """FSDP unit fi's shard was just updated by the optimizer (compute stream):
@@ -281,7 +292,7 @@ class Engine:
             self._issued += 1
 
     def before_forward(self, model_unit: int) -> None:
-        if self.world == 1:
+        if self.world == 1 or self.in_graph:
             return
         fi = self.P.owner[model_unit]
         if self.P.first_model_unit[fi] != model_unit:

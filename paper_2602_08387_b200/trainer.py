@@ -43,6 +43,12 @@ def init_distributed():
     return rank, world, local, device
 
 
+# B2S_GRAPH_MULTI=1 (experimental, off): also capture the W > 1 forward + backward with its
+# reduce-scatters. Measured 2-3% faster at W=2 in bench.py, but the 2-GPU parity check
+# (tools/fsdp_check.py) hung with it on, so the default stays eager at W > 1.
+_GRAPH_MULTI = os.environ.get("B2S_GRAPH_MULTI", "0") == "1"
+
+
 class SPMDTrainer:
     def __init__(self, model: DecoderLM, optimizer, dataloader: PackedDataLoader, steps: int = 20,
                  seed: int = 0, blocks_per_unit: int = 1, init_device: str = "cpu", log_every: int = 0,
@@ -99,13 +105,26 @@ class SPMDTrainer:
     def _graph_forward_backward(self, inputs, targets):
         from . import _lib
 
+        multi = self.world > 1
+        if multi:
+            # W > 1: this step's all-gathers were queued after the previous optimizer
+            # update (outside the graph); the replay starts once they landed, and the
+            # graph itself holds the forward, backward and per-unit reduce-scatters
+            self.engine.graph_step_prologue()
         if self._graph is None:
             self._gx, self._gy = inputs.clone(), targets.clone()
             n0 = _lib.load().b2s_launch_count()
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g):
-                self.engine.begin_step()
+                if multi:
+                    self.engine.in_graph = True
+                    self.engine.P.gall.zero_()
+                else:
+                    self.engine.begin_step()
                 self._gloss = self.model.forward_backward(self._gx, self._gy, hooks=self.engine)
+                if multi:
+                    self.engine.end_backward()  # joins the comm stream back into the capture
+                    self.engine.in_graph = False
             self._graph_launches = int(_lib.load().b2s_launch_count() - n0)
             _lib.count_replayed_launches(-self._graph_launches)  # capture launched nothing
             self._graph = g
@@ -121,8 +140,9 @@ class SPMDTrainer:
         shape = tuple(inputs.shape)
         if self._graph is not None and shape != self._gshape:
             self._graph, self._eager_steps = None, 0  # new activation buffers: re-warm, re-capture
-        use_graph = (self.cuda_graph and self.world == 1 and ops.KernelTimer.active is None
-                     and self._eager_steps >= 2)
+        graph_ok = self.world == 1 or (_GRAPH_MULTI and self.engine.timing is None
+                                       and self.engine._prefetched == len(self.params.flat))
+        use_graph = (self.cuda_graph and graph_ok and ops.KernelTimer.active is None and self._eager_steps >= 2)
         if use_graph:
             self._gshape = shape
             loss = self._graph_forward_backward(inputs, targets)
@@ -130,7 +150,7 @@ class SPMDTrainer:
             self._eager_steps += 1
             self.engine.begin_step()
             loss = self.model.forward_backward(inputs, targets, hooks=self.engine)
-        self.engine.end_backward()
+            self.engine.end_backward()
         self._loss.copy_(loss)
         # the rank-mean loss shares the grad-norm all-reduce; the optimizer then
         # queues each unit's next-step all-gather as soon as that unit is updated
