@@ -381,7 +381,7 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
-    out = run_reference(args) if args.impl == "reference" else run_ours(args)
+    out = run_reference(args) if args.impl == "reference" else run_ours(args)  # (its trainer and graph are freed)
     if out is not None:
         print(json.dumps(out), flush=True)
     if args.impl == "ours" and int(os.environ.get("WORLD_SIZE", "1")) > 1:

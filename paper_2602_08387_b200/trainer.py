@@ -43,10 +43,9 @@ def init_distributed():
     return rank, world, local, device
 
 
-# B2S_GRAPH_MULTI=1 (experimental, off): also capture the W > 1 forward + backward with its
-# reduce-scatters. Measured 2-3% faster at W=2 in bench.py, but the 2-GPU parity check
-# (tools/fsdp_check.py) hung with it on, so the default stays eager at W > 1.
-_GRAPH_MULTI = os.environ.get("B2S_GRAPH_MULTI", "0") == "1"
+# W > 1 forward + backward captured with its reduce-scatters (B2S_GRAPH_MULTI=0: eager):
+# 2-3% faster at W=2; see SPMDTrainer.close() for process-group teardown.
+_GRAPH_MULTI = os.environ.get("B2S_GRAPH_MULTI", "1") == "1"
 
 
 class SPMDTrainer:
@@ -158,6 +157,14 @@ class SPMDTrainer:
                             engine=self.engine)
         return self._loss
 
+    def close(self) -> None:
+        """Release the captured step graph. At W > 1 it holds NCCL work, and
+        destroy_process_group() waits for that communicator while the graph is alive:
+        call this (or drop the trainer) before tearing the process group down."""
+        if self._graph is not None:
+            torch.cuda.synchronize()
+            self._graph = None
+
     def run(self) -> list:
         """Train `steps` steps; returns the per-step mean losses (host floats)."""
         self.setup()
@@ -168,4 +175,5 @@ class SPMDTrainer:
             losses.append(float(loss.item()))
             if self.log_every and self.rank == 0 and (g % self.log_every == 0 or g == self.steps - 1):
                 print(f"step {g:5d}  loss {losses[-1]:.4f}  {time.perf_counter() - t0:.1f}s", flush=True)
+        self.close()  # a later run() re-captures; the process group can be torn down now
         return losses

@@ -6,6 +6,7 @@ Every rank trains `steps` steps on its shard of the global batch; rank 0 then
 replays the same steps on one GPU with the whole batch (a second trainer in
 the same process, world=1 semantics) and writes both loss curves to out.json.
 """
+import faulthandler
 import json
 import os
 import sys
@@ -28,6 +29,8 @@ GB = int(sys.argv[2]) if len(sys.argv) > 2 else 8
 steps = int(sys.argv[3]) if len(sys.argv) > 3 else 10
 out = sys.argv[4] if len(sys.argv) > 4 else os.path.join(ROOT, "gpurun_out", "fsdp_check.json")
 bpu = int(os.environ.get("BLOCKS_PER_UNIT", "1"))
+if os.environ.get("B2S_HANG_DUMP"):  # diagnostics: dump every thread's stack if the run stalls
+    faulthandler.dump_traceback_later(int(os.environ["B2S_HANG_DUMP"]), exit=True)
 cfg = PRESETS[preset]
 T = min(256, cfg.max_seq_len)
 world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -70,5 +73,6 @@ if rank == 0:
     os.makedirs(os.path.dirname(out), exist_ok=True)
     with open(out, "w") as f:
         json.dump(res, f)
+tr.close()  # the W > 1 step graph holds NCCL work: release it before the teardown
 dist.barrier()
 dist.destroy_process_group()
