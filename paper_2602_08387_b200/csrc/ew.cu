@@ -361,7 +361,7 @@ __global__ void __launch_bounds__(256) colsum_kernel(const T* __restrict__ x, in
     // four rows' 16-byte loads issued back to back before they are summed: the
     // loop is latency-bound otherwise (one load in flight per lane)
 #ifndef B2S_COLSUM_U
-#define B2S_COLSUM_U 8
+#define B2S_COLSUM_U 16
 #endif
     constexpr int U = B2S_COLSUM_U;
     int64_t r = r0 + w;
