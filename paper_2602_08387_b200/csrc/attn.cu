@@ -78,6 +78,9 @@ struct Params {
 #define B2S_ATTN_FWD64_MODE 0  // dh 64: 0 two ping-pong tiles per CTA (default, fastest measured);
                                // 1 one tile per CTA, two CTAs per SM (2 K/V stages, 1 P buffer): 25% slower
 #endif
+#ifndef B2S_ATTN_FWD128_TILES
+#define B2S_ATTN_FWD128_TILES 2  // dh 128: 2 = two query tiles per CTA with P aliasing S; 1 = one tile
+#endif
 #ifndef B2S_ATTN_FWD_PT
 #define B2S_ATTN_FWD_PT 1  // P in TMEM (PV by the TMEM-A MMA form) instead of shared memory
 #endif
@@ -85,7 +88,10 @@ template <int DH>
 struct Fwd {
   static constexpr int MODE = DH == 64 ? B2S_ATTN_FWD64_MODE : 0;
   static constexpr bool PT = B2S_ATTN_FWD_PT && MODE == 0;
-  static constexpr int TILES = (DH == 64 && MODE == 0) ? 2 : 1;
+  // dh 128 with P in TMEM: two ping-pong query tiles, P aliasing the tile's S columns
+  // (S / O of two tiles fill all 512 columns); S_t(j+1) is issued behind PV_t(j)
+  static constexpr bool ALIAS = DH == 128 && PT && B2S_ATTN_FWD128_TILES == 2;
+  static constexpr int TILES = ((DH == 64 && MODE == 0) || ALIAS) ? 2 : 1;
   static constexpr int KVS = MODE == 2 ? 1 : 2;       // K / V smem stages
   static constexpr int PB = (MODE == 1 || PT) ? 1 : 2;  // P buffers per tile (smem, or one TMEM block)
   static constexpr int MINB = MODE == 0 ? 1 : 2;      // CTAs per SM
@@ -94,6 +100,7 @@ struct Fwd {
   static constexpr int kThreads = 64 + 128 * TILES;
   static constexpr int kTileQ = BQ * DH * 2;  // Q / K / V tile bytes (DH/64 atoms)
   static constexpr int PCOL = OCOL + TILES * DH;      // PT: P (bf16 pairs, 64 columns per tile)
+  static constexpr int pcol(int t) { return ALIAS ? t * BKV : PCOL + t * 64; }
   static constexpr int kSmem = 1024 + TILES * kTileQ + 2 * KVS * kTileQ + (PT ? 0 : TILES * PB * kPBuf) + 256;
   static_assert(kSmem * MINB <= 232448, "forward tiles exceed shared memory");
   static_assert(KVS == 2, "S(j+1) is issued before PV(j): one K/V stage would deadlock");
@@ -282,7 +289,7 @@ __global__ void __launch_bounds__(Fwd<DH>::kThreads, Fwd<DH>::MINB)
 #pragma unroll
         for (int kk = 0; kk < BKV / 16; ++kk) {
           if constexpr (C::PT)  // P from TMEM: 16 keys = 8 columns of bf16 pairs per K step
-            mma_bf16_ts_w(tbase + C::OCOL + t * DH, tbase + C::PCOL + t * 64 + kk * 8,
+            mma_bf16_ts_w(tbase + C::OCOL + t * DH, tbase + C::pcol(t) + kk * 8,
                           make_sdesc(aV + s * kTQ + kk * 2048, kTile, 1024), idO, (j > 0 || kk > 0) ? 1u : 0u);
           else
             mma_bf16_ss_w(tbase + C::OCOL + t * DH, make_sdesc(pbase + (kk >> 2) * kTile + (kk & 3) * 32, 16, 1024),
@@ -296,12 +303,21 @@ __global__ void __launch_bounds__(Fwd<DH>::kThreads, Fwd<DH>::MINB)
       issue_S(0, 0);
       if (nB > 0) issue_S(1, 0);
       for (int j = 0; j < nkv; ++j) {
-        // QK^T of block j+1 goes in as soon as each softmax group holds S(j) in
-        // registers, so it is ready when the group finishes block j
-        if (j + 1 < nA) issue_S(0, j + 1);
-        if (j + 1 < nB) issue_S(1, j + 1);
-        if (j < nA) issue_PV(0, j, j + 1 == nA);
-        if (j < nB) issue_PV(1, j, j + 1 == nB);
+        if constexpr (C::ALIAS) {
+          // P_t(j) lives in S_t's columns: S_t(j+1) goes in behind PV_t(j) (the tensor
+          // pipe runs one CTA's MMAs in order), while the other tile's softmax runs
+          if (j < nA) issue_PV(0, j, j + 1 == nA);
+          if (j + 1 < nA) issue_S(0, j + 1);
+          if (j < nB) issue_PV(1, j, j + 1 == nB);
+          if (j + 1 < nB) issue_S(1, j + 1);
+        } else {
+          // QK^T of block j+1 goes in as soon as each softmax group holds S(j) in
+          // registers, so it is ready when the group finishes block j
+          if (j + 1 < nA) issue_S(0, j + 1);
+          if (j + 1 < nB) issue_S(1, j + 1);
+          if (j < nA) issue_PV(0, j, j + 1 == nA);
+          if (j < nB) issue_PV(1, j, j + 1 == nB);
+        }
         mma_commit_w(&kv_empty[j % KVS]);  // K_j / V_j no longer read once these retire
       }
     }
@@ -376,8 +392,8 @@ __global__ void __launch_bounds__(Fwd<DH>::kThreads, Fwd<DH>::MINB)
         rs = diag ? exp_pack_regs<true>(v, r, sl2, m_use, pk) : exp_pack_regs<false>(v, r, sl2, m_use, pk);
         if (j >= 1) mbar_wait(&p_empty[2 * t], (j - 1) & 1);
         tc_fence_after();
-        tmem_st32(tbase + lrow + C::PCOL + t * 64, pk);
-        tmem_st32(tbase + lrow + C::PCOL + t * 64 + 32, pk + 32);
+        tmem_st32(tbase + lrow + C::pcol(t), pk);
+        tmem_st32(tbase + lrow + C::pcol(t) + 32, pk + 32);
         tmem_wait_st();
       } else {
         if (j >= PB) mbar_wait(&p_empty[2 * t + pb], ((j / PB) - 1) & 1);
