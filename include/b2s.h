@@ -149,6 +149,14 @@ int b2s_gemm(const void* d_A, int a_mn_major, int64_t lda, const void* d_B, int 
              int64_t ldb, void* d_C, int64_t ldc, int c_f32, int M, int N, int K, int accumulate,
              const void* d_bias, int act, void* d_aux, int64_t ld_aux, b2s_stream_t stream);
 
+/* b2s_gemm (bf16 C, act 0 / 2 / 6) that also writes the per-32-row column sums of the
+ * stored (bf16-rounded) C: d_colsum_part [ceil(M/32)][N] fp32. Summing its rows
+ * (b2s_colsum_accumulate, fp32) gives the bias gradient of a dgrad without re-reading C --
+ * the reference's autograd bias grad, dbias = dY.sum(0). */
+int b2s_gemm_colsum(const void* d_A, int a_mn_major, int64_t lda, const void* d_B, int b_mn_major, int64_t ldb,
+                    void* d_C, int64_t ldc, int M, int N, int K, int act, void* d_aux, int64_t ld_aux,
+                    float* d_colsum_part, b2s_stream_t stream);
+
 /* Llama MLP with the SwiGLU fused into the GEMM epilogues (bf16).
  * Forward: gu = x @ W13^T ([M, 2F] = gate | up, kept for the backward) and
  * h = silu(gate) * up ([M, F]) from one GEMM -- each CTA-pair tile holds 128

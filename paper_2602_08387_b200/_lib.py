@@ -54,6 +54,7 @@ _SIGS = {
     "b2s_tokenizer_encode": "pplplp",
     "b2s_tokenize_corpus": "pplppiiiipp",
     "b2s_gemm": "pilpilpliiiiipiplp",
+    "b2s_gemm_colsum": "pilpilpliiiiplpp",
     "b2s_gemm_swiglu_fwd": "plplplpliiip",
     "b2s_gemm_swiglu_bwd": "plplplpliiip",
     "b2s_layernorm_fwd": "ppppppplifp",

@@ -88,6 +88,8 @@ struct Epi {
   const __nv_bfloat16* aux_in;  // act=2/6: [M, ld_aux]; act=4: gu [M, ld_aux = 2F]
   int64_t ld_aux;
   int glu_F;                  // act 3 / 4: the gate / up split F
+  float* colsum_part;         // bf16 generic epilogue: per-32-row column sums of the stored C,
+                              // [ceil(M/32)][N] fp32 (the bias gradient of a dgrad), or null
 };
 
 __device__ __forceinline__ float silu_sig(float g, float& sg) {
@@ -695,6 +697,25 @@ __global__ void __launch_bounds__(Cfg<BN, CG, EW>::kThreads, 1)
           else tma_store_2d(&tmC, b, col0, rbase);
           bulk_commit();
         }
+        if (epi.colsum_part && !epi.out_f32) {
+          // column sums of the staged (bf16-rounded) 32 x 32 tile: lane l sums columns
+          // 2(l & 15), +1 over rows 16 (l >> 4) .. +15, then the two row halves combine
+          const int cw = lane & 15, rh = lane >> 4;
+          float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+          for (int r = 0; r < 16; ++r) {
+            const int row = rh * 16 + r;
+            const uint32_t w = *reinterpret_cast<const uint32_t*>(
+                b + row * 64 + (((cw >> 2) ^ ((row >> 1) & 3)) * 16) + (cw & 3) * 4);
+            s0 += __uint_as_float(w << 16);
+            s1 += __uint_as_float(w & 0xffff0000u);
+          }
+          s0 += __shfl_xor_sync(0xffffffffu, s0, 16);
+          s1 += __shfl_xor_sync(0xffffffffu, s1, 16);
+          const int col = col0 + 2 * cw;
+          if (lane < 16 && col < N)
+            *reinterpret_cast<float2*>(epi.colsum_part + (int64_t)(rbase >> 5) * N + col) = make_float2(s0, s1);
+        }
       }
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
@@ -841,7 +862,8 @@ namespace {
 // act 4: N = F, C = dgu [M, 2F] of width c_width, aux = gu).
 int gemm_run(const void* d_A, int a_mn_major, int64_t lda, const void* d_B, int b_mn_major, int64_t ldb, void* d_C,
              int64_t ldc, int c_f32, int M, int N, int K, int accumulate, const void* d_bias, int act, void* d_aux,
-             int64_t ld_aux, int glu_F, int64_t c_width, int64_t aux_width, cudaStream_t st) {
+             int64_t ld_aux, int glu_F, int64_t c_width, int64_t aux_width, cudaStream_t st,
+             float* d_colsum_part = nullptr) {
   using namespace b2s;
   B2S_REQUIRE(M > 0 && N > 0 && K > 0, B2S_EINVAL, "gemm: empty shape %d x %d x %d", M, N, K);
   B2S_REQUIRE(d_A && d_B && d_C, B2S_EINVAL, "gemm: null operand");
@@ -875,7 +897,8 @@ int gemm_run(const void* d_A, int a_mn_major, int64_t lda, const void* d_B, int 
     rc = encode_tma_2d(&tx, d_aux, 2, (uint64_t)aux_width, (uint64_t)M, (uint64_t)ld_aux * 2, 32, 32, 64);
   else tx = tc;
   if (rc) return rc;
-  gemm::Epi e{c_f32, accumulate, (const __nv_bfloat16*)d_bias, act, (const __nv_bfloat16*)d_aux, ld_aux, glu_F};
+  gemm::Epi e{c_f32, accumulate, (const __nv_bfloat16*)d_bias, act, (const __nv_bfloat16*)d_aux, ld_aux, glu_F,
+              d_colsum_part};
   const int splits = ch.splits;
   if (ch.cg == 2 && act != 0 && act != 6)  // activation epilogue: 12 epilogue warps (see EW above);
     // the x aux product (act 6) is light enough for 8 warps and the deeper 5-stage mainloop
@@ -895,6 +918,15 @@ extern "C" int b2s_gemm(const void* d_A, int a_mn_major, int64_t lda, const void
   B2S_REQUIRE(!(accumulate && (act == 1 || act == 5)), B2S_EINVAL, "gemm: accumulate with GELU is not supported");
   return gemm_run(d_A, a_mn_major, lda, d_B, b_mn_major, ldb, d_C, ldc, c_f32, M, N, K, accumulate, d_bias, act,
                   d_aux, ld_aux, 0, N, N, (cudaStream_t)stream);
+}
+
+extern "C" int b2s_gemm_colsum(const void* d_A, int a_mn_major, int64_t lda, const void* d_B, int b_mn_major,
+                               int64_t ldb, void* d_C, int64_t ldc, int M, int N, int K, int act, void* d_aux,
+                               int64_t ld_aux, float* d_colsum_part, b2s_stream_t stream) {
+  B2S_REQUIRE(act == 0 || act == 2 || act == 6, B2S_EINVAL, "gemm_colsum: act must be 0, 2 or 6");
+  B2S_REQUIRE(d_colsum_part && ((uintptr_t)d_colsum_part % 8) == 0, B2S_EINVAL, "gemm_colsum: null / misaligned partials");
+  return gemm_run(d_A, a_mn_major, lda, d_B, b_mn_major, ldb, d_C, ldc, 0, M, N, K, 0, nullptr, act, d_aux, ld_aux, 0, N,
+                  N, (cudaStream_t)stream, d_colsum_part);
 }
 
 extern "C" int b2s_gemm_swiglu_fwd(const void* d_x, int64_t ldx, const void* d_w13, int64_t ldw, void* d_gu,

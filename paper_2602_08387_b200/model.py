@@ -456,8 +456,8 @@ class DecoderLM(torch.nn.Module):
             # --- MLP (its output gradient is the residual gradient dx, bf16 copy in dxb)
             if gpt2:  # fc2_b's grad was summed by the norm backward that produced dx
                 ops.linear_wgrad(A.dxb, S.h, out=U.g("fc2_w"), accumulate=True)
-                ops.linear_dgrad(A.dxb, U.p("fc2_w"), out=A.dh, act=self._act_bwd, aux=S.hpre)
-                ops.colsum_accumulate(A.dh, U.g("fc_b"))
+                # fc_b's gradient = colsum(dh), from the dgrad epilogue's per-32-row partials
+                ops.linear_dgrad(A.dxb, U.p("fc2_w"), out=A.dh, act=self._act_bwd, aux=S.hpre, colsum_out=U.g("fc_b"))
                 ops.linear_wgrad(A.dh, S.ln_b, out=U.g("fc_w"), accumulate=True)
                 ops.linear_dgrad(A.dh, U.p("fc_w"), out=A.dln)
                 ops.layernorm_bwd(S.xb, A.dln, U.p("ln2_g"), S.mean_b, S.rstd_b, A.dx, A.dxb,

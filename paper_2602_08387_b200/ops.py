@@ -144,12 +144,45 @@ def linear(x, w, bias=None, out=None, act=0, aux=None, accumulate=False):
                 accumulate=accumulate)
 
 
-def linear_dgrad(dy, w, out=None, act=0, aux=None, accumulate=False):
-    """dx = dy @ w: dy [M,N], w [N,K] -> [M,K]."""
+def linear_dgrad(dy, w, out=None, act=0, aux=None, accumulate=False, colsum_out=None):
+    """dx = dy @ w: dy [M,N], w [N,K] -> [M,K].
+
+    colsum_out (fp32 [K], bf16 path): also ``colsum_out += dx.sum(0)`` (the bias gradient of
+    the layer whose output gradient dx is), from per-32-row partial sums the GEMM epilogue
+    writes -- dx is not read back."""
     M, N = dy.shape
     K = w.shape[1]
-    return gemm(dy, w, a_mn=False, b_mn=True, M=M, N=K, K=N, out=out, act=act, aux=aux,
-                accumulate=accumulate)
+    if colsum_out is None or dy.dtype != torch.bfloat16 or accumulate:
+        out = gemm(dy, w, a_mn=False, b_mn=True, M=M, N=K, K=N, out=out, act=act, aux=aux,
+                   accumulate=accumulate)
+        if colsum_out is not None:
+            colsum_accumulate(out, colsum_out)
+        return out
+    _dev(dy, w, out, aux, colsum_out)
+    if out is None:
+        out = torch.empty(M, K, device=dy.device, dtype=torch.bfloat16)
+    rb = (M + 31) // 32
+    part = _colsum_part(rb * K, dy.device)[: rb * K].view(rb, K)
+    ld_aux = aux.stride(0) if aux is not None else 0
+    _timed("gemm", 2.0 * M * N * K, lambda: _call(
+        "b2s_gemm_colsum", dy.data_ptr(), 0, dy.stride(0), w.data_ptr(), 1, w.stride(0), out.data_ptr(), out.stride(0),
+        M, K, N, act, _ptr(aux), ld_aux, part.data_ptr(), _sp()),
+        detail=(M, K, N, "K", "MN", "bf16", "", "", act))
+    colsum_accumulate(part, colsum_out)
+    return out
+
+
+_colsum_part_cache = {}
+
+
+def _colsum_part(n, device):
+    """Per-(device, stream) scratch for the GEMM-epilogue column-sum partials."""
+    key = (device.index, torch.cuda.current_stream(device).cuda_stream)
+    buf = _colsum_part_cache.get(key)
+    if buf is None or buf.numel() < n:
+        buf = torch.empty(n, device=device, dtype=torch.float32)
+        _colsum_part_cache[key] = buf
+    return buf
 
 
 def linear_swiglu(x, w13, gu, h):

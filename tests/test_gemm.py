@@ -78,6 +78,13 @@ def test_gemm_epilogues(cuda, force):
     dh6 = ops.linear_dgrad(dy, w2, act=6, aux=gd)
     torch.testing.assert_close(dh6.float(), (dy.float() @ w2.float()) * gd.float(), rtol=1e-2, atol=2e-2)
     torch.testing.assert_close(dh6.float(), p.grad, rtol=2e-2, atol=5e-2)
+    # dgrad with the bias-gradient column sums from the epilogue (rows not a multiple of 32)
+    for act_, aux_ in ((0, None), (6, gd)):
+        cs = torch.full((N,), 0.5, device=cuda)
+        dhc = ops.linear_dgrad(dy, w2, act=act_, aux=aux_, colsum_out=cs)
+        ref_dh = ops.linear_dgrad(dy, w2, act=act_, aux=aux_)
+        assert torch.equal(dhc, ref_dh)
+        torch.testing.assert_close(cs, 0.5 + ref_dh.float().sum(0), rtol=1e-4, atol=1e-3)
     # accumulate (fp32 and bf16) and wgrad
     acc = torch.randn(N, K, device=cuda)
     ref = acc + dy.new_tensor(0).float() + (torch.randn(0, device=cuda).sum())

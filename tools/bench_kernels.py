@@ -85,6 +85,7 @@ def bench_epilogues():
     b_d = torch.randn(d, device="cuda", generator=g).bfloat16()
     resid = torch.zeros(M, d, device="cuda")
     dh = torch.empty(M, f, device="cuda", dtype=torch.bfloat16)
+    b_acc = torch.zeros(f, device="cuda")
     o = torch.randn(M, d, device="cuda", generator=g).bfloat16()
     w_o = torch.randn(d, d, device="cuda", generator=g).bfloat16()
     cases = [
@@ -95,6 +96,10 @@ def bench_epilogues():
         ("fc.fwd+bias+gelu, aux=gelu' (act 5)", M, f, d,
          lambda: ops.linear(x, w_fc, bias=b_fc, out=h, act=5, aux=hpre)),
         ("fc2.dgrad x aux (act 6)", M, f, d, lambda: ops.linear_dgrad(dy, w_fc2, out=dh, act=6, aux=hpre)),
+        ("fc2.dgrad x aux (act 6) + fc_b colsum partials", M, f, d,
+         lambda: ops.linear_dgrad(dy, w_fc2, out=dh, act=6, aux=hpre, colsum_out=b_acc)),
+        ("fc2.dgrad x aux (act 6), then colsum kernel", M, f, d,
+         lambda: (ops.linear_dgrad(dy, w_fc2, out=dh, act=6, aux=hpre), ops.colsum_accumulate(dh, b_acc))),
         ("fc2.fwd+bias+f32 resid add", M, d, f, lambda: ops.gemm(h, w_fc2, a_mn=False, b_mn=False, M=M, N=d, K=f,
                                                                   out=resid, accumulate=True, bias=b_d)),
         ("proj.fwd+bias+f32 resid add", M, d, d, lambda: ops.gemm(o, w_o, a_mn=False, b_mn=False, M=M, N=d, K=d,
