@@ -78,6 +78,9 @@ struct Params {
 #define B2S_ATTN_FWD64_MODE 0  // dh 64: 0 two ping-pong tiles per CTA (default, fastest measured);
                                // 1 one tile per CTA, two CTAs per SM (2 K/V stages, 1 P buffer): 25% slower
 #endif
+#ifndef B2S_ATTN_FWD64_KVS
+#define B2S_ATTN_FWD64_KVS 2  // dh 64 K / V stages (2..4)
+#endif
 #ifndef B2S_ATTN_FWD128_TILES
 #define B2S_ATTN_FWD128_TILES 2  // dh 128: 2 = two query tiles per CTA with P aliasing S; 1 = one tile
 #endif
@@ -92,7 +95,8 @@ struct Fwd {
   // (S / O of two tiles fill all 512 columns); S_t(j+1) is issued behind PV_t(j)
   static constexpr bool ALIAS = DH == 128 && PT && B2S_ATTN_FWD128_TILES == 2;
   static constexpr int TILES = ((DH == 64 && MODE == 0) || ALIAS) ? 2 : 1;
-  static constexpr int KVS = MODE == 2 ? 1 : 2;       // K / V smem stages
+  // K / V smem stages (dh 64 with P in TMEM has room for more)
+  static constexpr int KVS = MODE == 2 ? 1 : ((DH == 64 && PT) ? B2S_ATTN_FWD64_KVS : 2);
   static constexpr int PB = (MODE == 1 || PT) ? 1 : 2;  // P buffers per tile (smem, or one TMEM block)
   static constexpr int MINB = MODE == 0 ? 1 : 2;      // CTAs per SM
   static constexpr int TCOLS = MODE == 0 ? 512 : 256; // TMEM columns allocated
@@ -103,7 +107,7 @@ struct Fwd {
   static constexpr int pcol(int t) { return ALIAS ? t * BKV : PCOL + t * 64; }
   static constexpr int kSmem = 1024 + TILES * kTileQ + 2 * KVS * kTileQ + (PT ? 0 : TILES * PB * kPBuf) + 256;
   static_assert(kSmem * MINB <= 232448, "forward tiles exceed shared memory");
-  static_assert(KVS == 2, "S(j+1) is issued before PV(j): one K/V stage would deadlock");
+  static_assert(KVS >= 2 && KVS <= 4, "S(j+1) is issued before PV(j): one K/V stage would deadlock");
 };
 constexpr float kRescaleThresh = 8.0f;  // log2 units
 
@@ -198,10 +202,11 @@ __global__ void __launch_bounds__(Fwd<DH>::kThreads, Fwd<DH>::MINB)
   uint8_t* sP = sV + KVS * kTQ;               // [tile][buf] x 32 KB (two 64-key atoms each)
   uint64_t* bars = reinterpret_cast<uint64_t*>(sP + (C::PT ? 0 : TILES * PB * kPBuf));
   uint64_t* q_full = bars;                    // 1
-  uint64_t* k_full = bars + 1;                // [kStages]
-  uint64_t* v_full = k_full + kStages;        // [kStages]
-  uint64_t* kv_empty = v_full + kStages;      // [kStages]
-  uint64_t* s_full = kv_empty + kStages;      // [2] per tile
+  constexpr int kKV = 4;                      // barrier slots per K / V array (>= KVS)
+  uint64_t* k_full = bars + 1;                // [KVS]
+  uint64_t* v_full = k_full + kKV;            // [KVS]
+  uint64_t* kv_empty = v_full + kKV;          // [KVS]
+  uint64_t* s_full = kv_empty + kKV;          // [2] per tile
   uint64_t* s_empty = s_full + 2;             // [2]
   uint64_t* p_full = s_empty + 2;             // [tile][buf]: per buffer, so a group running a block
                                               // ahead of the MMA warp cannot alias a barrier phase
