@@ -352,7 +352,7 @@ def run_reference(args):
         return None
     cfg = PRESETS[args.config]
     T = args.seq
-    warm = min(args.warmup, 1)
+    warm = min(args.warmup, 3)  # CPU steps are ~2.5 s each; more warm-up buys nothing
     tps, threads, dt = _oracle_step_timer(cfg, T, 1, args.steps, warm)
     return {"metric": METRIC, "value": round(tps, 2), "unit": UNIT, "n_gpus": int(os.environ.get("WORLD_SIZE", 1)),
             "steps": args.steps, "warmup": warm, "ms_per_step": round(dt * 1000 / args.steps, 1),
