@@ -583,7 +583,7 @@ __global__ void swiglu_bwd_kernel(const T* __restrict__ gu, const T* __restrict_
 // One block per row of bf16 logits [M, ld] (first V columns valid). Writes
 // loss[m] = logsumexp - logit[target] (fp32) and, in place over the logits,
 // dlogits = (softmax - onehot) * gscale (columns >= V zeroed).
-template <typename T>
+template <typename T, int U = 1>
 __global__ void __launch_bounds__(512) xent_kernel(T* __restrict__ logits, int64_t ld, int V,
                                                    const int64_t* __restrict__ target, float* __restrict__ loss,
                                                    float gscale, int64_t M, int write_grad) {
@@ -605,7 +605,17 @@ __global__ void __launch_bounds__(512) xent_kernel(T* __restrict__ logits, int64
     se = se * ex2f(mx - mn) + acc;
     mx = mn;
   };
-  for (int i = threadIdx.x; i < nvec; i += blockDim.x) {
+  int i0 = threadIdx.x;
+  if (U > 1) {  // U row vectors in flight per thread before their exponentials
+    for (; i0 + (U - 1) * (int)blockDim.x < nvec; i0 += U * blockDim.x) {
+      float f[U][8];
+#pragma unroll
+      for (int u = 0; u < U; ++u) ld_v8(row + (int64_t)(i0 + u * blockDim.x) * 8, f[u]);
+#pragma unroll
+      for (int u = 0; u < U; ++u) absorb(f[u]);
+    }
+  }
+  for (int i = i0; i < nvec; i += blockDim.x) {
     float f[8];
     ld_v8(row + i * 8, f);
     absorb(f);
@@ -993,8 +1003,12 @@ int cross_entropy(void* d_logits, int64_t ld, int V, const int64_t* d_target, fl
                                                                    d_loss_rows, grad_scale, write_grad);
     return check_launch("cross_entropy");
   }
-  ew::xent_kernel<T><<<(unsigned)M, 512, 0, st>>>((T*)d_logits, ld, V, d_target, d_loss_rows, grad_scale, M,
-                                                  write_grad);
+  // B2S_XENT_UNROLL = 1 / 2 / 4 / 8: row vectors in flight per thread in the first pass
+  // (GPT-2 logits: 659 / 665 / 648 us for 1 / 2 / 4, profiles/r1_xent_smem_ab.jsonl)
+  static const int un = getenv("B2S_XENT_UNROLL") ? atoi(getenv("B2S_XENT_UNROLL")) : 4;
+  auto kern = un == 8 ? ew::xent_kernel<T, 8>
+              : un == 4 ? ew::xent_kernel<T, 4> : un == 2 ? ew::xent_kernel<T, 2> : ew::xent_kernel<T, 1>;
+  kern<<<(unsigned)M, 512, 0, st>>>((T*)d_logits, ld, V, d_target, d_loss_rows, grad_scale, M, write_grad);
   return check_launch("cross_entropy");
 }
 template <typename T>
