@@ -583,7 +583,7 @@ __global__ void swiglu_bwd_kernel(const T* __restrict__ gu, const T* __restrict_
 // One block per row of bf16 logits [M, ld] (first V columns valid). Writes
 // loss[m] = logsumexp - logit[target] (fp32) and, in place over the logits,
 // dlogits = (softmax - onehot) * gscale (columns >= V zeroed).
-template <typename T, int U = 1>
+template <typename T, int U = 1, int U2 = 1>
 __global__ void __launch_bounds__(512) xent_kernel(T* __restrict__ logits, int64_t ld, int V,
                                                    const int64_t* __restrict__ target, float* __restrict__ loss,
                                                    float gscale, int64_t M, int write_grad) {
@@ -637,7 +637,23 @@ __global__ void __launch_bounds__(512) xent_kernel(T* __restrict__ logits, int64
   if (threadIdx.x == 0) loss[m] = lse - xt;
   if (!write_grad) return;
   const float inv = gscale / se;  // softmax * gscale = 2^(y - max) * gscale / sum
-  for (int i = threadIdx.x; i < nvec; i += blockDim.x) {
+  int j0 = threadIdx.x;
+  if (U2 > 1) {  // U2 row vectors in flight per thread before their exponentials / stores
+    for (; j0 + (U2 - 1) * (int)blockDim.x < nvec; j0 += U2 * blockDim.x) {
+      float f[U2][8];
+#pragma unroll
+      for (int u = 0; u < U2; ++u) ld_v8_cs(row + (int64_t)(j0 + u * blockDim.x) * 8, f[u]);
+#pragma unroll
+      for (int u = 0; u < U2; ++u) {
+        const int i = j0 + u * blockDim.x;
+#pragma unroll
+        for (int t = 0; t < 8; ++t) f[u][t] = ex2f(fmaf(f[u][t], L2E, -mx)) * inv;
+        if ((uint64_t)(tgt - (int64_t)i * 8) < 8) f[u][tgt - (int64_t)i * 8] -= gscale;
+        st_v8_cs(row + (int64_t)i * 8, f[u]);
+      }
+    }
+  }
+  for (int i = j0; i < nvec; i += blockDim.x) {
     float f[8];
     ld_v8_cs(row + i * 8, f);  // last read of the row (pass 1 left it in L2)
 #pragma unroll
@@ -1006,8 +1022,13 @@ int cross_entropy(void* d_logits, int64_t ld, int V, const int64_t* d_target, fl
   // B2S_XENT_UNROLL = 1 / 2 / 4 / 8: row vectors in flight per thread in the first pass
   // (GPT-2 logits: 659 / 665 / 648 us for 1 / 2 / 4, profiles/r1_xent_smem_ab.jsonl)
   static const int un = getenv("B2S_XENT_UNROLL") ? atoi(getenv("B2S_XENT_UNROLL")) : 4;
-  auto kern = un == 8 ? ew::xent_kernel<T, 8>
-              : un == 4 ? ew::xent_kernel<T, 4> : un == 2 ? ew::xent_kernel<T, 2> : ew::xent_kernel<T, 1>;
+  // B2S_XENT_UNROLL2 = 1 / 2 / 4: the same for the gradient pass
+  static const int un2 = getenv("B2S_XENT_UNROLL2") ? atoi(getenv("B2S_XENT_UNROLL2")) : 1;
+  auto kern = un == 8   ? ew::xent_kernel<T, 8>
+              : un == 2 ? ew::xent_kernel<T, 2>
+              : un == 1 ? ew::xent_kernel<T, 1>
+              : un2 == 2 ? ew::xent_kernel<T, 4, 2>
+              : un2 == 4 ? ew::xent_kernel<T, 4, 4> : ew::xent_kernel<T, 4>;
   kern<<<(unsigned)M, 512, 0, st>>>((T*)d_logits, ld, V, d_target, d_loss_rows, grad_scale, M, write_grad);
   return check_launch("cross_entropy");
 }
