@@ -1123,8 +1123,10 @@ int b2s_colsum_accumulate(const void* d_x, int x_f32, int64_t M, int N, int64_t 
               ew::kColsumStrips);
   unsigned* arrivals = ew::colsum_slot();
   B2S_REQUIRE(arrivals != nullptr, B2S_ECUDA, "colsum: arrival counter allocation failed");
-  // four blocks per SM, rounded down so every block is co-resident in one wave
-  int nparts = 4 * kNumSMs / nblk;
+  // B2S_COLSUM_BPS (default four) blocks per SM, rounded down so every block is
+  // co-resident in one wave
+  static const int bps = getenv("B2S_COLSUM_BPS") ? atoi(getenv("B2S_COLSUM_BPS")) : 4;
+  int nparts = (bps >= 1 && bps <= 8 ? bps : 4) * kNumSMs / nblk;
   if (nparts > 256) nparts = 256;
   if (nparts < 1) nparts = 1;
   const int rows_per = (int)((M + nparts - 1) / nparts);
