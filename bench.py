@@ -316,6 +316,11 @@ def run_ours(args):
     return out
 
 
+# CPU sample per reference step: (sequences, tokens) sized so one oracle step takes a few
+# seconds on the GPU box's host cores (the full 1B step at 1 x 4096 tokens takes ~40 s there)
+REF_SAMPLE = {"tiny-gpt2": (8, 256), "gpt2-124m": (1, 2048), "llama-1b": (1, 512), "llama-8b": None}
+
+
 def _oracle_step_timer(cfg, T, B, steps, warmup):
     """Time OracleTrainer steps (CPU fp32) on synthetic samples; returns (tokens/s, threads, secs)."""
     import torch
@@ -336,12 +341,55 @@ def _oracle_step_timer(cfg, T, B, steps, warmup):
     return B * T * steps / dt, torch.get_num_threads(), dt
 
 
+def _data_path_baseline(cfg, B, T):
+    """The packed-data feed on the host: the oracle restatement of PackedReader.get_sample
+    (packed_data.py:196-203) over B windows of T+1 tokens, stacked and widened to int64, and the
+    Fisher-Yates make_permutation (packed_data.py:257-282) in C; timed on one core."""
+    import numpy as np
+
+    from oracle import packed_oracle as orc
+    from paper_2602_08387_b200.packed import open_packed
+
+    path = _data_path(cfg, max(1 << 22, 64 * B * T + 1))
+    r = open_packed(path)
+    payload = np.asarray(r.payload)
+    n = r.sample_count(T)
+    rng = np.random.default_rng(0)
+    reps, t0 = 0, time.perf_counter()
+    while time.perf_counter() - t0 < 1.0:
+        ids = rng.integers(0, n, B)
+        x, y = orc.batch_windows(payload, ids, T)
+        reps += 1
+    dt = time.perf_counter() - t0
+    import ctypes
+
+    lib = ctypes.CDLL(os.path.join(ROOT, "oracle", "_build", "liboracle.so"))
+    np_perm = 1 << 20
+    out = np.empty(np_perm, dtype=np.uint64)
+    t1 = time.perf_counter()
+    lib.oracle_permutation(ctypes.c_uint64(np_perm), ctypes.c_uint64(0), out.ctypes.data_as(ctypes.c_void_p))
+    dp = time.perf_counter() - t1
+    return {"get_sample_batch_tokens_per_s": round(reps * B * T / dt, 1), "batch": f"{B} x {T + 1} tokens, "
+            f"width {r.token_width}", "make_permutation_elems_per_s": round(np_perm / dp, 1),
+            "cores": 1, "kind": "port", "sample": f"{reps} batches in {dt:.2f} s (oracle/packed_oracle.py "
+            f"batch_windows); make_permutation(2^20, 0) in {dp * 1e3:.1f} ms (oracle/permutation_oracle.c)"}
+
+
 def cpu_baseline(cfg, T, args):
-    tps, threads, dt = _oracle_step_timer(cfg, T, 1, 1, 0)
-    return {"value": round(tps, 2), "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"CPU fp32 oracle (oracle/model_oracle.py) of the same {args.config} step: 1 sequence x {T} "
-                      f"tokens, 1 step ({dt:.1f} s), torch threads={threads}, "
-                      f"host cpus={len(os.sched_getaffinity(0))}"}
+    smp = REF_SAMPLE.get(args.config)
+    if smp is None:
+        return None
+    Bs, Ts = smp[0], min(T, smp[1])
+    tps, threads, dt = _oracle_step_timer(cfg, Ts, Bs, 1, 0)
+    out = {"value": round(tps, 2), "unit": UNIT, "cores": threads, "kind": "port",
+           "sample": f"CPU fp32 oracle (oracle/model_oracle.py) of the {args.config} training step "
+                     f"(fwd+bwd+clip+AdamW, all layers): {Bs} x {Ts} tokens, 1 step ({dt:.1f} s), "
+                     f"torch threads={threads}, host cpus={len(os.sched_getaffinity(0))}"}
+    try:
+        out["data_path"] = _data_path_baseline(cfg, args.batch, T)
+    except Exception as e:  # the step number above stands on its own
+        out["data_path"] = {"error": str(e)[:200]}
+    return out
 
 
 def run_reference(args):
@@ -351,34 +399,79 @@ def run_reference(args):
     if rank != 0:
         return None
     cfg = PRESETS[args.config]
-    T = args.seq
-    warm = min(args.warmup, 3)  # CPU steps are ~2.5 s each; more warm-up buys nothing
-    tps, threads, dt = _oracle_step_timer(cfg, T, 1, args.steps, warm)
+    smp = REF_SAMPLE.get(args.config)
+    if smp is None:
+        return {"impl": "reference", "unavailable": f"{args.config}: the fp32 CPU oracle needs ~130 GB of host "
+                                                      "memory for its parameters and AdamW state"}
+    Bs, Ts = smp[0], min(args.seq, smp[1])
+    warm = min(args.warmup, 1)  # CPU steps take seconds; one warm-up allocates the AdamW state
+    tps, threads, dt = _oracle_step_timer(cfg, Ts, Bs, args.steps, warm)
+    sample = (f"{args.steps} steps of {Bs} x {Ts} tokens after {warm} warm-up, full {cfg.n_layer}-layer "
+              f"{args.config} fp32 step (fwd+bwd+clip+AdamW) on the host cores; the reference has no training "
+              "step (SPEC.md:12), so its arm is the CPU fp32 oracle (oracle/model_oracle.py)")
+    if Ts < args.seq:
+        sample += (f"; seq {Ts} instead of {args.seq} bounds the run (attention is 12*L*d*T of the "
+                   f"{cfg.flops_per_token(args.seq) / 1e9:.2f} GF/token, so the shorter sample favours the CPU)")
     return {"metric": METRIC, "value": round(tps, 2), "unit": UNIT, "n_gpus": int(os.environ.get("WORLD_SIZE", 1)),
             "steps": args.steps, "warmup": warm, "ms_per_step": round(dt * 1000 / args.steps, 1),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic token ids; random-init weights", "impl": "reference",
-            "config": {"workload": f"{args.config} training step (fwd+bwd+AdamW), seq {T}, 1 seq/step sample",
-                       "model": args.config, "global_batch": 1, "seq_len": T, "parallelism": "cpu"},
+            "config": {"workload": f"{args.config} FSDP training step (fwd+bwd+AdamW), seq {args.seq}, "
+                                   f"{args.batch} seqs/GPU (CPU sample {Bs} x {Ts})",
+                       "model": args.config, "global_batch": Bs, "seq_len": Ts, "parallelism": "cpu"},
             "cpu_baseline": {"value": round(tps, 2), "unit": UNIT, "cores": threads, "kind": "port",
-                             "sample": f"{args.steps} steps of 1 x {T} tokens after {warm} warm-up; the reference "
-                                       "has no training step (SPEC.md:12), so its arm is the CPU fp32 oracle"},
+                             "sample": sample},
             "e2e": {"value": round(tps, 2), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+# per-config workload defaults (BASELINE.json configs / SURVEY §8(a)): sequences per GPU, seq len, AC
+CONFIGS = {
+    "tiny-gpt2": (8, 256, False),
+    "gpt2-124m": (8, 2048, False),   # configs[1]
+    "llama-1b": (4, 4096, False),    # configs[2]: the north-star target
+    "llama-8b": (2, 4096, True),     # configs[3]: per-block activation checkpointing
+}
+
+
+def _free_port() -> int:
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _self_launch(args) -> int:
+    """`python bench.py --gpus N` (N > 1, not under torchrun): re-exec as N ranks, one per GPU."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "VERSION")  # keeps NCCL's version / init line visible
+    return subprocess.call(cmd, env=env)
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="gpt2-124m")
-    ap.add_argument("--batch", type=int, default=8, help="sequences per GPU per step")
-    ap.add_argument("--seq", type=int, default=2048)
+    ap.add_argument("--config", default="llama-1b", choices=sorted(CONFIGS))
+    ap.add_argument("--batch", type=int, default=None, help="sequences per GPU per step (default: per config)")
+    ap.add_argument("--seq", type=int, default=None, help="sequence length (default: per config)")
     ap.add_argument("--blocks-per-unit", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
-    ap.add_argument("--ac", action="store_true", help="per-block activation checkpointing (the 8B config)")
+    ap.add_argument("--ac", action="store_true", default=None, help="per-block activation checkpointing")
     args = ap.parse_args()
+    B0, T0, ac0 = CONFIGS[args.config]
+    args.batch = B0 if args.batch is None else args.batch
+    args.seq = T0 if args.seq is None else args.seq
+    args.ac = ac0 if args.ac is None else args.ac
+    world = int(os.environ.get("WORLD_SIZE", "0"))
+    if world == 0 and args.gpus > 1:
+        sys.exit(_self_launch(args))
+    if world and world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU")
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
     out = run_reference(args) if args.impl == "reference" else run_ours(args)  # (its trainer and graph are freed)
@@ -387,9 +480,11 @@ def main():
     if args.impl == "ours" and int(os.environ.get("WORLD_SIZE", "1")) > 1:
         import torch.distributed as dist
 
+        from paper_2602_08387_b200.trainer import destroy_process_group
+
         if dist.is_initialized():
             dist.barrier()
-            dist.destroy_process_group()
+            destroy_process_group()
 
 
 if __name__ == "__main__":

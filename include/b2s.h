@@ -46,6 +46,9 @@ const char* b2s_last_error(void);
 int b2s_abi_version(void);
 /* Number of CUDA kernels this library has launched since it was loaded. */
 uint64_t b2s_launch_count(void);
+/* cudaMemsetAsync of `bytes` bytes at device pointer `dst` to `value` on `stream` (a memset
+   node, not a kernel: zeroes the gradient / residual-gradient accumulators inside the step). */
+int b2s_memset_async(void* dst, int value, uint64_t bytes, void* stream);
 
 /* ------------------------------------------------------------------ */
 /* Packed data path (CFPKD001)                                         */

@@ -17,6 +17,9 @@ unpinned" (no reference test or golden vector exists for it); the packed
 data path (oracle/packed_oracle.py) is pinned to reference goldens.
 
 Parameters use the product's flat naming 'unit.param' (model.unit_specs).
+The module is device-agnostic: the headline-shape tests move it to the GPU and
+run it in true fp32 (TF32 off) as the fp32 reference of the bf16 step, where the
+CPU would take minutes per step.
 """
 
 from __future__ import annotations
@@ -50,7 +53,7 @@ class OracleModel(torch.nn.Module):
         else:
             inv = 1.0 / (c.rope_theta ** (torch.arange(0, dh, 2, dtype=torch.float64) / dh))
             ang = torch.arange(T, dtype=torch.float64)[:, None] * inv[None]
-            cos, sin = ang.cos().float(), ang.sin().float()
+            cos, sin = ang.cos().float().to(tok.device), ang.sin().float().to(tok.device)
 
         def rope(t):  # t [B, h, T, dh], rotate-half pairing
             t1, t2 = t[..., : dh // 2], t[..., dh // 2:]
@@ -59,7 +62,7 @@ class OracleModel(torch.nn.Module):
         def rms(t, g):
             return t * torch.rsqrt(t.pow(2).mean(-1, keepdim=True) + c.norm_eps) * g
 
-        mask = torch.ones(T, T, dtype=torch.bool).tril()
+        mask = torch.ones(T, T, dtype=torch.bool, device=tok.device).tril()
         for i in range(c.n_layer):
             u = f"block{i}."
             if gpt2:

@@ -41,6 +41,7 @@ _lib = None
 # (device or host; passed as int), `i` = int, `l` = int64, `u` = uint64, `f` = float.
 _SIGS = {
     "b2s_abi_version": "",
+    "b2s_memset_async": "piup",
     "b2s_token_width_for_vocab": "up",
     "b2s_sample_count": "ulp",
     "b2s_splitmix64": "uup",

@@ -119,6 +119,14 @@ const char* b2s_last_error(void) { return b2s::g_err; }
 int b2s_abi_version(void) { return 1; }
 uint64_t b2s_launch_count(void) { return b2s::g_launches.load(); }
 
+int b2s_memset_async(void* dst, int value, uint64_t bytes, void* stream) {
+  B2S_REQUIRE(dst || bytes == 0, B2S_EINVAL, "dst is null");
+  if (bytes == 0) return B2S_OK;
+  const cudaError_t e = cudaMemsetAsync(dst, value, (size_t)bytes, (cudaStream_t)stream);
+  B2S_REQUIRE(e == cudaSuccess, B2S_ECUDA, "cudaMemsetAsync: %s", cudaGetErrorString(e));
+  return B2S_OK;
+}
+
 int b2s_token_width_for_vocab(uint64_t vocab_size, int* h_width) {
   B2S_REQUIRE(h_width, B2S_EINVAL, "h_width is null");
   B2S_REQUIRE(vocab_size >= 1, B2S_EINVAL, "vocab_size must be positive, got %llu",

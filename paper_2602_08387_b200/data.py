@@ -58,7 +58,15 @@ class PackedDataLoader:
         self._order = None
         self._dev = None
 
-    def bind(self, rank: int, world: int, device) -> "PackedDataLoader":
+    def bind(self, rank: int, world: int, device, vocab_size: int | None = None) -> "PackedDataLoader":
+        """Attach to (rank, world, device). With ``vocab_size`` (the trainer passes the model's),
+        a corpus holding any token id >= vocab_size is rejected here: the embedding and
+        cross-entropy kernels index weight rows by token id and would otherwise read or
+        scatter-add outside the tables."""
+        if vocab_size is not None:
+            mx = self.dataset.max_token()
+            if mx >= vocab_size:
+                raise ValueError(f"dataset holds token id {mx}, outside the model's vocabulary of {vocab_size}")
         self.rank, self.world, self.device = rank, world, torch.device(device)
         n = self.dataset.sample_count(self.seq_len)
         self._order = self.sampler.order(n)

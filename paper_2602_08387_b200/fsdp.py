@@ -27,6 +27,7 @@ from __future__ import annotations
 import torch
 import torch.distributed as dist
 
+from . import ops
 from .model import ALIGN, UnitSpec
 
 
@@ -212,7 +213,10 @@ class Engine:
 
     # ------------------------------------------------------------------ step
     def begin_step(self) -> None:
-        self.P.gall.zero_()
+        if self.P.gall.is_cuda:
+            ops.zero_(self.P.gall)
+        else:  # the gloo host-logic tests (tests/test_fsdp_cpu.py) run the engine without a GPU
+            self.P.gall.zero_()
         if self.world > 1 and self._prefetched == len(self.P.flat):
             # every unit's all-gather was queued right after its optimizer update
             self._issued = len(self.P.flat)

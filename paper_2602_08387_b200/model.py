@@ -440,7 +440,7 @@ class DecoderLM(torch.nn.Module):
         g_head = E.g("wte") if cfg.tie_embeddings else Hd.g("lm_head")
         ops.linear_wgrad(A.logits, A.ln_f, out=g_head, accumulate=True)
         ops.linear_dgrad(A.logits, w_head, out=A.dln)
-        A.dx.zero_()
+        ops.zero_(A.dx)
         if gpt2:
             # the updated dx is the output gradient of the last block's fc2 -> its bias grad
             ops.layernorm_bwd(xf, A.dln, Hd.p("lnf_g"), A.mean_f, A.rstd_f, A.dx, A.dxb,

@@ -88,6 +88,14 @@ def _ptr(t):
     return 0 if t is None else t.data_ptr()
 
 
+def zero_(t):
+    """t.zero_() as a cudaMemsetAsync on the current stream (no fill kernel in the step)."""
+    _dev(t)
+    assert t.is_contiguous()
+    _call("b2s_memset_async", t.data_ptr(), 0, t.numel() * t.element_size(), _sp())
+    return t
+
+
 # ---------------------------------------------------------------------------- GEMM
 
 

@@ -192,6 +192,13 @@ class PackedReader:
         lo = s * seq_len
         return self._payload[lo:lo + seq_len + 1]
 
+    def max_token(self) -> int:
+        """Largest token id in the payload (-1 if empty); one host scan, cached (the reader is
+        immutable). The training feed checks it against the model's vocabulary once."""
+        if getattr(self, "_max_token", None) is None:
+            self._max_token = int(self._payload.max()) if self.token_count else -1
+        return self._max_token
+
     def close(self) -> None:
         self._payload = self._spans = None
         self._mm = None

@@ -16,12 +16,15 @@ collectives. A step is:
 
 from __future__ import annotations
 
+import atexit
 import os
 import time
+import weakref
 
 import torch
 import torch.distributed as dist
 
+from . import ops
 from .data import PackedDataLoader
 from .fsdp import Engine, FlatParams
 from .model import DecoderLM, param_initializer
@@ -42,6 +45,27 @@ def init_distributed():
         dist.init_process_group("nccl", device_id=device)
     return rank, world, local, device
 
+
+# trainers that may hold a captured step graph with NCCL work in it (W > 1)
+_LIVE = weakref.WeakSet()
+
+
+def release_graphs() -> None:
+    """Release every live trainer's captured step graph (see SPMDTrainer.close)."""
+    for tr in list(_LIVE):
+        tr.close()
+
+
+def destroy_process_group() -> None:
+    """Tear down NCCL safely: captured graphs holding NCCL work are released first, otherwise
+    torch's destroy_process_group() waits on the communicator they keep alive."""
+    release_graphs()
+    if dist.is_initialized():
+        dist.destroy_process_group()
+
+
+# interpreter exit: release graphs before torch's own process-group teardown
+atexit.register(release_graphs)
 
 # W > 1 forward + backward captured with its reduce-scatters (B2S_GRAPH_MULTI=0: eager):
 # 2-3% faster at W=2; see SPMDTrainer.close() for process-group teardown.
@@ -89,10 +113,12 @@ class SPMDTrainer:
         self.model.attach(self.params)
         self.engine = Engine(self.params, self.group, self.world)
         self.optimizer = FusedAdamW(self.opt_cfg)
-        self.dataloader.bind(self.rank, self.world, self.device)
+        self.dataloader.bind(self.rank, self.world, self.device, vocab_size=cfg.vocab_size)
         if self.dataloader.seq_len > cfg.max_seq_len:
             raise ValueError(f"seq_len {self.dataloader.seq_len} exceeds the model's {cfg.max_seq_len}")
         self._loss = torch.zeros(1, device=self.device)
+        if self.world > 1:
+            _LIVE.add(self)
         self._ready = True
         return self
 
@@ -117,7 +143,7 @@ class SPMDTrainer:
             with torch.cuda.graph(g):
                 if multi:
                     self.engine.in_graph = True
-                    self.engine.P.gall.zero_()
+                    ops.zero_(self.engine.P.gall)
                 else:
                     self.engine.begin_step()
                 self._gloss = self.model.forward_backward(self._gx, self._gy, hooks=self.engine)
