@@ -114,24 +114,37 @@ class ClockSampler:
 
 
 def _gemm_traffic(config):
-    """dram bytes (read + write) per GEMM launch from the committed ncu capture, or None."""
+    """Measured DRAM bytes (read + write) per step of the GEMM class, from the committed ncu pass
+    over one step of this config (tools/gpu/r2_raster.sh -> profiles/r2_<config>_step_metrics.csv),
+    or None when no capture of this config is committed."""
     import csv
     import io
 
-    path = os.path.join(ROOT, "profiles", "r1_gemm_dram_tensor_metrics.csv")
-    if config != "gpt2-124m" or not os.path.exists(path):
+    path = os.path.join(ROOT, "profiles", f"r2_{config.replace('-', '')}_step_metrics.csv")
+    if not os.path.exists(path):
         return None
     text = open(path).read()
     rows = list(csv.reader(io.StringIO(text[text.index('"ID"'):])))
     h = rows[0]
-    iI, iM, iV, iU = h.index("ID"), h.index("Metric Name"), h.index("Metric Value"), h.index("Metric Unit")
+    iN, iM, iV, iU = h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Value"), h.index("Metric Unit")
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-    tot, ids = 0.0, set()
+    tot = 0.0
     for r in rows[1:]:
-        if r[iM] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+        if "gemm_kernel" in r[iN] and r[iM] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
             tot += float(r[iV].replace(",", "")) * scale.get(r[iU], 1)
-            ids.add(r[iI])
-    return round(tot / max(1, len(ids)))
+    return {"bytes_per_step": round(tot), "src": os.path.relpath(path, ROOT)}
+
+
+def _gemm_algorithmic_bytes(detail):
+    """Minimum DRAM bytes of one GEMM launch (operands read once, outputs written once)."""
+    M, N, K, _, _, out, acc, bias, act = detail
+    if act == "swiglu":  # x [M,K], w13 [2F,K] -> gu [M,2F] + h [M,F]
+        return 2 * (M * K + N * K) + 2 * M * N + M * N
+    if act == "dswiglu":  # dy [M,K], w2, gu [M,2F] in -> dgu [M,2F] out
+        return 2 * (M * K + N * K) + 4 * M * N + 4 * M * N
+    c = (4 if out == "f32" else 2) * M * N * (2 if acc else 1)
+    aux = 2 * M * N if act in (5, 6, 1, 2) else 0
+    return 2 * (M * K + N * K) + c + aux
 
 
 def _data_path(cfg, n_tokens):
@@ -259,6 +272,8 @@ def run_ours(args):
             step += 1
         barrier_sync()
     kern = kt.summary()
+    gemm_alg_bytes = sum(_gemm_algorithmic_bytes(det) * n for (kind, det), n, _ms, _tf in kt.detail()
+                         if kind == "gemm") / args.steps
     coll = tr.engine.collective_summary() if world > 1 else None
     tr.engine.timing = None
 
@@ -292,7 +307,11 @@ def run_ours(args):
         "loss_last": round(loss_dev, 4),
         "roofline": {"bound": "tensor", "kernel": "b2s gemm (tcgen05)", "achieved": round(gemm_tf, 1),
                      "peak": peaks["bf16_sust"], "unit": "TFLOP/s", "frac": round(gemm_tf / peaks["bf16_sust"], 3),
-                     "traffic": _gemm_traffic(args.config),
+                     "frac_vs_burst_peak": round(gemm_tf / peaks["bf16"], 3),
+                     "traffic": (_gemm_traffic(args.config) or {}).get("bytes_per_step"),
+                     "traffic_unit": "DRAM bytes per step, all GEMM launches (ncu, committed capture)",
+                     "traffic_src": (_gemm_traffic(args.config) or {}).get("src"),
+                     "algorithmic_bytes_per_step": round(gemm_alg_bytes),
                      "peak_src": f"{peaks['src']} bf16 sustained (kernel timed inside a long step)",
                      "achieved_src": "sum of algorithmic GEMM FLOPs / sum of CUDA-event launch durations over "
                                      f"{args.steps} instrumented steps",

@@ -19,7 +19,12 @@
 // the MMA and epilogue warps -- and to the peer CTA of a pair), so CTAs that
 // start late (SMs busy with NCCL kernels on the comm stream) take fewer tiles
 // instead of stretching the kernel.
+#include <algorithm>
+#include <map>
 #include <mutex>
+#include <string.h>
+#include <tuple>
+#include <vector>
 #include <stdio.h>
 #include <stdlib.h>
 #include <cuda_fp16.h>
@@ -210,6 +215,27 @@ __device__ __forceinline__ void stage_f32(uint8_t* buf, int lane, const float* v
   }
 }
 
+// Tile raster (host-chosen, see choose_raster): tile index mn -> (m block, n block).
+// raster > 0: groups of `raster` M blocks; inside a group the M block varies fastest and the
+//   group sweeps every N block before the next group starts.
+// raster < 0: the same with the roles of M and N swapped (groups of -raster N blocks).
+// Tiles are handed out in index order, so the ~74 tiles in flight at once (one per CTA pair)
+// form a (group x span) rectangle: the operand blocks they share are loaded from DRAM once and
+// hit in L2 for the rest of the wave. raster = num_m is the plain M-fastest order.
+__device__ __forceinline__ void tile_mn(int mn, int num_m, int num_n, int raster, int& mi, int& ni) {
+  if (raster > 0) {
+    const int gt = raster * num_n, g = mn / gt, local = mn - g * gt;
+    const int gm = min(raster, num_m - g * raster);
+    mi = g * raster + local % gm;
+    ni = local / gm;
+  } else {
+    const int G = -raster, gt = G * num_m, g = mn / gt, local = mn - g * gt;
+    const int gn = min(G, num_n - g * G);
+    ni = g * G + local % gn;
+    mi = local / gn;
+  }
+}
+
 // CG = 1: one CTA computes a 128 x BN tile.
 // CG = 2: a CTA pair (cluster of 2) computes a 256 x BN tile with
 //   tcgen05.mma.cta_group::2 (M = 256): each CTA stages its 128 rows of A and
@@ -221,7 +247,7 @@ template <int BN, int CG, bool A_MN, bool B_MN, int EW>
 __global__ void __launch_bounds__(Cfg<BN, CG, EW>::kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmAux,
-                int M, int N, int K, int splits, Epi epi, int* __restrict__ sched) {
+                int M, int N, int K, int splits, int raster, Epi epi, int* __restrict__ sched) {
   using C_ = Cfg<BN, CG, EW>;
   constexpr int kEpiWarps = C_::kEpiWarps, kEpiSmem = C_::kEpiSmem;
   constexpr int kEG = kEpiWarps / 4;  // epilogue warps per TMEM lane quarter
@@ -314,11 +340,12 @@ __global__ void __launch_bounds__(Cfg<BN, CG, EW>::kThreads, 1)
         if (tile >= num_tiles) break;
         if (leader) next = sched ? tstride + atomicAdd(sched, 1) : tile + tstride;
         const int mn = tile % (num_m * num_n), ks = tile / (num_m * num_n);
-        const int m0 = (mn % num_m) * BM * CG + rank * BM;
+        int mi, ni;
+        tile_mn(mn, num_m, num_n, raster, mi, ni);
+        const int m0 = mi * BM * CG + rank * BM;
         // act 3 (SwiGLU forward, CTA pairs): tile n covers gate rows [128n, 128n+128) (leader)
         // and the matching up rows [F + 128n, ...) (peer), so each accumulator holds both
-        const int n0 = epi.act == 3 ? (rank ? epi.glu_F : 0) + (mn / num_m) * (BN / 2)
-                                    : (mn / num_m) * BN + rank * BNc;
+        const int n0 = epi.act == 3 ? (rank ? epi.glu_F : 0) + ni * (BN / 2) : ni * BN + rank * BNc;
         const int kb0 = ks * kb_per, kb1 = min(num_kb_all, kb0 + kb_per);
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
@@ -444,9 +471,10 @@ __global__ void __launch_bounds__(Cfg<BN, CG, EW>::kThreads, 1)
     uint4 aux[4];
     auto load_aux = [&](int tile, int c) {
       if (!aux_tma) return;
-      const int mn_ = tile % (num_m * num_n);
-      const int row0 = (mn_ % num_m) * BM * CG + rank * BM + q * 32;
-      const int col = (mn_ / num_m) * BN + c * 32;
+      int mi_, ni_;
+      tile_mn(tile % (num_m * num_n), num_m, num_n, raster, mi_, ni_);
+      const int row0 = mi_ * BM * CG + rank * BM + q * 32;
+      const int col = ni_ * BN + c * 32;
       const int s_ = aux_issued & 1;
       if (lane == 0) {  // out-of-range rows / columns are zero-filled and still counted
         mbar_arrive_expect_tx(&abar[s_], 32 * 32 * 2);
@@ -473,13 +501,14 @@ __global__ void __launch_bounds__(Cfg<BN, CG, EW>::kThreads, 1)
       if (tile >= num_tiles) break;
       load_aux(tile, half);  // first two chunks' aux tiles: in flight while the MMAs finish
       if (half + kEG < BN / 32) load_aux(tile, half + kEG);
-      const int mn = tile % (num_m * num_n);
-      const int m0 = (mn % num_m) * BM * CG + rank * BM, n0 = (mn / num_m) * BN;
+      int mi, ni;
+      tile_mn(tile % (num_m * num_n), num_m, num_n, raster, mi, ni);
+      const int m0 = mi * BM * CG + rank * BM, n0 = ni * BN;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const int rbase = m0 + q * 32;
       if (epi.act == 3) {  // SwiGLU forward: gate chunk c with up chunk c + BN/64 of the same rows
-        const int F = epi.glu_F, h0 = (mn / num_m) * (BN / 2);
+        const int F = epi.glu_F, h0 = ni * (BN / 2);
 #pragma unroll 1
         for (int c = half; c < BN / 64; c += kEG) {
           uint32_t rg[32], ru[32];
@@ -774,6 +803,74 @@ static int* sched_slot() {
   return p;
 }
 
+// Raster choice by a wave model of L2 reuse. Tiles run in index order, `slots` at a time
+// (one per CTA / CTA pair). A wave loads every distinct A block (BM*CG rows x K) and B block
+// (BN rows x K) its tiles touch once -- concurrent tiles stream the same K slices in near
+// lockstep -- and a block the previous wave also touched is still in L2 with probability
+// min(1, budget / bytes of that wave's blocks). The candidate with the fewest modelled DRAM
+// bytes wins: M-grouped or N-grouped, group sizes 1, 2, 4, ... (the full extent is the plain
+// M- / N-fastest order). Cached per shape.
+static int choose_raster(int num_m, int num_n, double a_blk, double b_blk, int slots) {
+  static std::mutex mu;
+  static std::map<std::tuple<int, int, long long, long long, int>, int> cache;
+  const auto key = std::make_tuple(num_m, num_n, (long long)a_blk, (long long)b_blk, slots);
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+  }
+  const double budget = 48e6;  // of the 126 MB L2: two dies, outputs stream through it too
+  const int total = num_m * num_n;
+  auto cost = [&](int raster) {
+    std::vector<int> seenA(num_m, -2), seenB(num_n, -2);  // last wave that touched the block
+    double bytes = 0.0, prev_bytes = 0.0;
+    for (int w0 = 0, w = 0; w0 < total; w0 += slots, ++w) {
+      double wave_bytes = 0.0, load = 0.0;
+      const double f = prev_bytes > 0 ? std::min(1.0, budget / prev_bytes) : 0.0;
+      for (int t = w0; t < std::min(total, w0 + slots); ++t) {
+        int mi, ni;
+        if (raster > 0) {
+          const int gt = raster * num_n, g = t / gt, l = t - g * gt, gm = std::min(raster, num_m - g * raster);
+          mi = g * raster + l % gm;
+          ni = l / gm;
+        } else {
+          const int G = -raster, gt = G * num_m, g = t / gt, l = t - g * gt, gn = std::min(G, num_n - g * G);
+          ni = g * G + l % gn;
+          mi = l / gn;
+        }
+        if (seenA[mi] != w) {
+          load += a_blk * (seenA[mi] == w - 1 ? 1.0 - f : 1.0);
+          seenA[mi] = w;
+          wave_bytes += a_blk;
+        }
+        if (seenB[ni] != w) {
+          load += b_blk * (seenB[ni] == w - 1 ? 1.0 - f : 1.0);
+          seenB[ni] = w;
+          wave_bytes += b_blk;
+        }
+      }
+      bytes += load;
+      prev_bytes = wave_bytes;
+    }
+    return bytes;
+  };
+  int best = num_m;  // M-fastest
+  double best_cost = cost(best);
+  for (int g = 1;; g *= 2) {
+    const bool more_m = g < num_m, more_n = g < num_n;
+    if (!more_m && !more_n) break;
+    if (more_m) {
+      const double c = cost(g);
+      if (c < best_cost * 0.98) { best_cost = c; best = g; }
+    }
+    const double c = cost(-std::min(g, num_n));
+    if (c < best_cost * 0.98) { best_cost = c; best = -std::min(g, num_n); }
+  }
+  std::lock_guard<std::mutex> lock(mu);
+  cache[key] = best;
+  return best;
+}
+
 template <int BN, int CG, bool A_MN, bool B_MN, int EW>
 static int launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc,
                   const CUtensorMap& tx, int M, int N, int K, int splits, const Epi& e, cudaStream_t st) {
@@ -804,7 +901,16 @@ static int launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMa
   static const bool static_sched = getenv("B2S_GEMM_STATIC") && atoi(getenv("B2S_GEMM_STATIC")) != 0;
   int* sched = static_sched ? nullptr : sched_slot();
   if (!static_sched && !sched) { set_error("gemm: scheduler counter allocation failed"); return B2S_ECUDA; }
-  cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, tx, M, N, K, splits, e, sched);
+  const int num_m = (M + BM * CG - 1) / (BM * CG), num_n = (N + BN - 1) / BN;
+  // B2S_GEMM_RASTER (tests / A-B runs): "mfast" = plain M-fastest order, an integer = that raster
+  // (clamped to the tile grid); read per launch like B2S_GEMM_FORCE
+  const char* rs = getenv("B2S_GEMM_RASTER");
+  const double kbytes = 2.0 * ((K + splits - 1) / splits);
+  int raster;
+  if (rs && strcmp(rs, "mfast") == 0) raster = num_m;
+  else if (rs && atoi(rs) != 0) raster = atoi(rs) > 0 ? std::min(atoi(rs), num_m) : -std::min(-atoi(rs), num_n);
+  else raster = choose_raster(num_m, num_n, BM * CG * kbytes, BN * kbytes, slots);
+  cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, tx, M, N, K, splits, raster, e, sched);
   return check_launch("gemm");
 }
 

@@ -32,8 +32,13 @@ for s in range(W):
     tr.train_step(s)
 torch.cuda.synchronize()
 n0 = _lib.load().b2s_launch_count()
+rng = os.environ.get("PROFILE_RANGE")  # ncu --profile-from-start off: capture exactly this step
+if rng:
+    torch.cuda.cudart().cudaProfilerStart()
 tr.train_step(W)
 torch.cuda.synchronize()
+if rng:
+    torch.cuda.cudart().cudaProfilerStop()
 print(f"launches_per_step {_lib.load().b2s_launch_count() - n0} loss {tr._loss.item():.4f}")
 if os.environ.get("KTIMER"):
     from paper_2602_08387_b200 import ops
