@@ -464,9 +464,7 @@ def _self_launch(args) -> int:
     """`python bench.py --gpus N` (N > 1, not under torchrun): re-exec as N ranks, one per GPU."""
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
            "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
-    env = dict(os.environ)
-    env.setdefault("NCCL_DEBUG", "VERSION")  # keeps NCCL's version / init line visible
-    return subprocess.call(cmd, env=env)
+    return subprocess.call(cmd, env=dict(os.environ))
 
 
 def main():
