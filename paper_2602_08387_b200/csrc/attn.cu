@@ -8,19 +8,17 @@
 // [B*T, Hq*dh] bf16 (the O-projection GEMM's A operand) and the per-row
 // log-sum-exp lse[B, Hq, T] (fp32, natural log) is kept for the backward.
 //
-// Forward CTA = (batch, q head, 128-query tile); roles: warp0 TMA, warp1 MMA,
-// warps 2..5 softmax (one query row per thread, the row is a TMEM lane).
-//   S_j = Q K_j^T  -> TMEM (double-buffered, M=128 N=128 K=64)
-//   P_j = exp2(S_j * scale*log2e - m_j) -> bf16 -> swizzled smem
-//   PV_j = P_j V_j -> TMEM (M=128 N=64 K=128, V as an MN-major operand)
-//   O   = O * 2^(m_{j-1} - m_j) + PV_j   (fp32, registers)
-// S_{j+1} is issued before PV_j, so QK^T of the next block overlaps softmax.
+// Forward: persistent, one CTA per SM working through (batch, q head, pair of 128-query
+// tiles) items heaviest first (see "forward (persistent)" below): S = QK^T and O = PV in TMEM,
+// P = 2^(S*scale*log2e - m) in TMEM (TMEM-A MMA form), lazy O rescale, one MMA issuer per
+// query tile and the two tiles' softmax warpgroups alternating on the MUFU.
 //
 // Backward CTA = (batch, kv head, 128-key tile), looping over the q heads of
 // its group and the causal query tiles: S^T = K Q^T, dP^T = V dO^T (TMEM),
 // P^T and dS^T = P^T (dP^T - D) to smem (thread = key row), then
 // dV += P^T dO, dK += dS^T Q (TMEM accumulators across the loop) and
 // dQ_i = dS K (TMEM) -> fp32 smem -> TMA add-reduce into a dQ accumulator.
+#include <mutex>
 #include "common.cuh"
 #include "sm100.cuh"
 
@@ -48,6 +46,9 @@ __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
 __device__ __forceinline__ void named_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
+__device__ __forceinline__ void named_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
 
 struct Params {
   int B, T, Hq, Hkv, nqt;
@@ -56,58 +57,73 @@ struct Params {
   float* lse;        // [B, Hq, T]
   const float* dsum; // bwd: D = rowsum(dO * O), [B, Hq, T]
   float* dq_acc;     // bwd (dh 64): fp32 dQ accumulator [B*T, Hq*dh]
+  int* sched;        // persistent kernels: {next work item, CTAs done} (zero between launches)
 };
 
-// =====================================================================================
-// forward
-// =====================================================================================
-// CTA = (batch, q head, pair of 128-query tiles A = 2p, B = 2p+1). Two softmax
-// warpgroups (warps 2-5 -> tile A, warps 6-9 -> tile B) share each K/V block
-// and the MMA warp ping-pongs between them:
-//   S_A(0) S_B(0) | PV_A(j) S_A(j+1) PV_B(j) S_B(j+1) | ...
-// O accumulates in TMEM (PV MMAs chain with accumulate=1). A softmax thread
-// only rescales its O row (tcgen05.ld / st) when its running max grows by
-// more than 2^8 -- otherwise P is formed against the stale max and stays
-// <= 256 -- so the softmax loop never waits for the PV MMA it just enabled.
-// P is double-buffered in smem per tile so P(j+1) can be written while
-// PV(j) still reads P(j).
-// dh = 128 runs one query tile per CTA (TILES = 1, warps 6-9 absent): the
-// 32 KB Q / K / V tiles leave room for 2 K/V stages and a double-buffered P
-// only for one tile in 227 KB of shared memory.
-#ifndef B2S_ATTN_FWD64_MODE
-#define B2S_ATTN_FWD64_MODE 0  // dh 64: 0 two ping-pong tiles per CTA (default, fastest measured);
-                               // 1 one tile per CTA, two CTAs per SM (2 K/V stages, 1 P buffer): 25% slower
+// Timeline tracing of the forward's roles (experiment builds: -DB2S_ATTN_TRACE; see
+// tools/attn_trace.py): lane 0 of each warp of CTAs 0..kTraceCtas-1 records (clock64, event).
+#ifdef B2S_ATTN_TRACE
+constexpr int kTraceCtas = 4, kTraceRecs = 8192;
+__device__ unsigned long long g_trace[kTraceCtas][18][kTraceRecs][2];
+#define TRACE(ev, aux)                                                                              \
+  do {                                                                                              \
+    if (blockIdx.x < kTraceCtas && lane == 0 && tr_n < kTraceRecs) {                                \
+      g_trace[blockIdx.x][warp][tr_n][0] = clock64();                                               \
+      g_trace[blockIdx.x][warp][tr_n][1] = ((unsigned long long)(ev) << 32) | (unsigned)(aux);     \
+      ++tr_n;                                                                                       \
+    }                                                                                               \
+  } while (0)
+#else
+#define TRACE(ev, aux) \
+  do {                 \
+  } while (0)
 #endif
+
+// =====================================================================================
+// forward (persistent)
+// =====================================================================================
+// Grid = one CTA per SM. A work item is (batch, q head, pair of 128-query tiles A = 2p,
+// B = 2p+1); items are numbered heaviest pair first and handed out by a global atomic
+// counter (longest-processing-time order: the tail is one light item, and CTAs that start
+// late -- SMs held by NCCL kernels on the comm stream -- take fewer items). The producer
+// warp fetches the next item index one item ahead and publishes it through a smem ring to
+// the MMA and softmax warps, so the next item's Q / K / V loads and its first QK^T run
+// while the current item's last blocks and epilogue finish (a non-persistent grid exposes
+// that prologue once per item: ~10% of the dh-64 forward).
+// Roles: warp0 TMA, warp1 MMA, warps 2-5 softmax of tile A, warps 6-9 of tile B (one
+// query row per thread, the row is a TMEM lane). Per KV block j of an item:
+//   S_t(j) = Q_t K_j^T -> TMEM;  P_t = 2^(S_t*scale*log2e - m) -> bf16 -> TMEM;
+//   O_t += P_t V_j (TMEM-A MMA form, V as an MN-major operand).
+// O accumulates in TMEM; a softmax thread rescales its O row (tcgen05.ld / st) only when
+// its running max grows by more than 2^8 -- otherwise P is formed against the stale max and
+// stays <= 256 -- so the softmax loop rarely waits on the PV MMA it just enabled.
+// TMEM columns: dh 64: S_A [0,128) S_B [128,256) O_A [256,320) O_B [320,384) P_A [384,448)
+//   P_B [448,512); MMA order S_A(j+1) S_B(j+1) PV_A(j) PV_B(j).
+// dh 128: S_A [0,128) S_B [128,256) O_A [256,384) O_B [384,512), P_t written over S_t's
+//   columns; MMA order PV_A(j) S_A(j+1) PV_B(j) S_B(j+1) (the tensor pipe runs one CTA's
+//   MMAs in issue order, so S_t(j+1) overwrites P_t(j) only after PV_t(j) read it).
+// The item's O is normalised by the softmax warps, staged through that item's Q buffer
+// (Q is double-buffered across items) and written by TMA.
 #ifndef B2S_ATTN_FWD64_KVS
-#define B2S_ATTN_FWD64_KVS 2  // dh 64 K / V stages (2..4)
-#endif
-#ifndef B2S_ATTN_FWD128_TILES
-#define B2S_ATTN_FWD128_TILES 2  // dh 128: 2 = two query tiles per CTA with P aliasing S; 1 = one tile
-#endif
-#ifndef B2S_ATTN_FWD_PT
-#define B2S_ATTN_FWD_PT 1  // P in TMEM (PV by the TMEM-A MMA form) instead of shared memory
+#define B2S_ATTN_FWD64_KVS 4
 #endif
 template <int DH>
 struct Fwd {
-  static constexpr int MODE = DH == 64 ? B2S_ATTN_FWD64_MODE : 0;
-  static constexpr bool PT = B2S_ATTN_FWD_PT && MODE == 0;
-  // dh 128 with P in TMEM: two ping-pong query tiles, P aliasing the tile's S columns
-  // (S / O of two tiles fill all 512 columns); S_t(j+1) is issued behind PV_t(j)
-  static constexpr bool ALIAS = DH == 128 && PT && B2S_ATTN_FWD128_TILES == 2;
-  static constexpr int TILES = ((DH == 64 && MODE == 0) || ALIAS) ? 2 : 1;
-  // K / V smem stages (dh 64 with P in TMEM has room for more)
-  static constexpr int KVS = MODE == 2 ? 1 : ((DH == 64 && PT) ? B2S_ATTN_FWD64_KVS : 2);
-  static constexpr int PB = (MODE == 1 || PT) ? 1 : 2;  // P buffers per tile (smem, or one TMEM block)
-  static constexpr int MINB = MODE == 0 ? 1 : 2;      // CTAs per SM
-  static constexpr int TCOLS = MODE == 0 ? 512 : 256; // TMEM columns allocated
-  static constexpr int OCOL = MODE == 0 ? 256 : 128;  // first O column
-  static constexpr int kThreads = 64 + 128 * TILES;
-  static constexpr int kTileQ = BQ * DH * 2;  // Q / K / V tile bytes (DH/64 atoms)
-  static constexpr int PCOL = OCOL + TILES * DH;      // PT: P (bf16 pairs, 64 columns per tile)
-  static constexpr int pcol(int t) { return ALIAS ? t * BKV : PCOL + t * 64; }
-  static constexpr int kSmem = 1024 + TILES * kTileQ + 2 * KVS * kTileQ + (PT ? 0 : TILES * PB * kPBuf) + 256;
-  static_assert(kSmem * MINB <= 232448, "forward tiles exceed shared memory");
-  static_assert(KVS >= 2 && KVS <= 4, "S(j+1) is issued before PV(j): one K/V stage would deadlock");
+  static constexpr bool ALIAS = DH == 128;      // P over S (dh 128: O takes 2 x 128 columns)
+  // K / V stages: the K load of block j + KVS waits for both tiles' PV(j); two stages leave it
+  // about one softmax period of TMA latency, which is not enough at dh 64 (dh 128 has no room)
+  static constexpr int KVS = DH == 64 ? B2S_ATTN_FWD64_KVS : 2;
+  static constexpr int kThreads = 352;          // TMA, MMA(A), 8 softmax warps, MMA(B)
+  static constexpr int kTileQ = BQ * DH * 2;    // Q / K / V tile bytes (DH/64 swizzle atoms)
+  static constexpr int OCOL = 256;              // first O column
+  static constexpr int pcol(int t) { return ALIAS ? t * BKV : OCOL + 2 * DH + t * 64; }
+  static constexpr int kRing = 4;               // item-index ring depth
+  // Q buffers (item-level double buffering; dh 128 has room for one: the next item's Q then
+  // loads once the current item's O stores have read their staging)
+  static constexpr int QB = DH == 64 ? 2 : 1;
+  static constexpr int kSmem = 1024 + QB * 2 * kTileQ /*Q: QB items x 2 tiles*/ + 2 * KVS * kTileQ + 512;
+  static_assert(kSmem <= 232448, "forward tiles exceed shared memory");
+  static_assert(KVS >= 2 && KVS <= 4, "K / V stages: 2..4 barrier slots");
 };
 constexpr float kRescaleThresh = 8.0f;  // log2 units
 
@@ -122,63 +138,20 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
-// 2^x on the FMA / ALU pipes (no MUFU): x = n + f, n = rint(x) by the 1.5*2^23
-// magic add, f in [-0.5, 0.5], 2^f by a degree-3 minimax polynomial (max
-// relative error 1.0e-4, well below the bf16 rounding P is stored with), the
-// exponent added as integer n << 23. x is clamped to >= -127 (2^-127 ~ 0).
-// Offloads part of the softmax exponentials from the 16/clk/SM MUFU unit.
-__device__ __forceinline__ float ex2_poly(float x) {
-  x = fmaxf(x, -127.f);
-  const float j = x + 12582912.f;
-  const float f = x - (j - 12582912.f);
-  float p = fmaf(fmaf(fmaf(0.05500891f, f, 0.242211f), f, 0.69328293f), f, 1.0f);
-  return __int_as_float(__float_as_int(p) + (__float_as_int(j) << 23));
-}
-#ifndef B2S_EXP_POLY_MASK
-#define B2S_EXP_POLY_MASK 0x00  // 8-column groups (bitmask) using ex2_poly; 0: measured fastest (the softmax is latency-, not MUFU-bound)
-#endif
-
-// P = 2^(s*sl2 - m) for 64 columns of one row -> bf16 -> swizzled smem; returns
-// the row sum. The causal mask is a template branch so off-diagonal blocks run
-// the mask-free instruction stream.
-template <bool DIAG>
-__device__ __forceinline__ float exp_pack(const uint32_t* v, int col0, int r, float sl2, float m,
-                                          uint8_t* dst) {
-  // row sum as 4 independent partial sums combined by a tree: a single serial
-  // FADD chain over 64 elements would be longer than the MUFU work it follows
-  float rs4[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-  for (int k8 = 0; k8 < 8; ++k8) {
-    float e[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const float a = fmaf(__uint_as_float(v[k8 * 8 + i]), sl2, -m);
-      const float x = ((B2S_EXP_POLY_MASK >> k8) & 1) ? ex2_poly(a) : ex2(a);
-      e[i] = (DIAG && col0 + k8 * 8 + i > r) ? 0.f : x;
-    }
-    rs4[k8 & 3] += ((e[0] + e[1]) + (e[2] + e[3])) + ((e[4] + e[5]) + (e[6] + e[7]));
-    uint4 w;
-    w.x = pack_bf16x2(e[0], e[1]);
-    w.y = pack_bf16x2(e[2], e[3]);
-    w.z = pack_bf16x2(e[4], e[5]);
-    w.w = pack_bf16x2(e[6], e[7]);
-    *reinterpret_cast<uint4*>(dst + swz(r, k8)) = w;
-  }
-  return (rs4[0] + rs4[1]) + (rs4[2] + rs4[3]);
-}
-
-// Same, for all BKV columns of the row, packed as bf16 pairs into out[0 .. BKV/2)
-// (out may alias v: pair k is written after v[2k], v[2k+1] are read).
+// P = 2^(s*sl2 - m) for all BKV columns of one row, packed as bf16 pairs into out[0 .. BKV/2)
+// (out may alias v: pair k is written after v[2k], v[2k+1] are read); returns the row sum.
+// The causal mask is a template branch so off-diagonal blocks run the mask-free stream.
 template <bool DIAG>
 __device__ __forceinline__ float exp_pack_regs(const uint32_t* v, int r, float sl2, float m, uint32_t* out) {
+  // row sum as 4 independent partial sums combined by a tree: a single serial FADD chain
+  // over 128 elements would be longer than the MUFU work it follows
   float rs4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
   for (int k8 = 0; k8 < BKV / 8; ++k8) {
     float e[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      const float a = fmaf(__uint_as_float(v[k8 * 8 + i]), sl2, -m);
-      const float x = ((B2S_EXP_POLY_MASK >> (k8 & 7)) & 1) ? ex2_poly(a) : ex2(a);
+      const float x = ex2(fmaf(__uint_as_float(v[k8 * 8 + i]), sl2, -m));
       e[i] = (DIAG && k8 * 8 + i > r) ? 0.f : x;
     }
     rs4[k8 & 3] += ((e[0] + e[1]) + (e[2] + e[3])) + ((e[4] + e[5]) + (e[6] + e[7]));
@@ -189,272 +162,355 @@ __device__ __forceinline__ float exp_pack_regs(const uint32_t* v, int r, float s
 }
 
 template <int DH>
-__global__ void __launch_bounds__(Fwd<DH>::kThreads, Fwd<DH>::MINB)
+__global__ void __launch_bounds__(Fwd<DH>::kThreads, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_o,
                     Params p) {
   using C = Fwd<DH>;
-  constexpr int TILES = C::TILES, kTQ = C::kTileQ, NA = DH / 64;  // NA: 64-column atoms per tile
-  constexpr int KVS = C::KVS, PB = C::PB;
+  constexpr int kTQ = C::kTileQ, NA = DH / 64, KVS = C::KVS, R = C::kRing, QB = C::QB;  // NA: atoms per tile
+  constexpr int kThreadsMMA2 = C::kThreads - 32;  // first thread of the tile-B MMA warp
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* sQ = align1024(smem_raw);          // [TILES] tiles A, B
-  uint8_t* sK = sQ + TILES * kTQ;             // [KVS]
-  uint8_t* sV = sK + KVS * kTQ;               // [KVS]
-  uint8_t* sP = sV + KVS * kTQ;               // [tile][buf] x 32 KB (two 64-key atoms each)
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + (C::PT ? 0 : TILES * PB * kPBuf));
-  uint64_t* q_full = bars;                    // 1
-  constexpr int kKV = 4;                      // barrier slots per K / V array (>= KVS)
-  uint64_t* k_full = bars + 1;                // [KVS]
-  uint64_t* v_full = k_full + kKV;            // [KVS]
-  uint64_t* kv_empty = v_full + kKV;          // [KVS]
-  uint64_t* s_full = kv_empty + kKV;          // [2] per tile
-  uint64_t* s_empty = s_full + 2;             // [2]
-  uint64_t* p_full = s_empty + 2;             // [tile][buf]: per buffer, so a group running a block
-                                              // ahead of the MMA warp cannot alias a barrier phase
-  uint64_t* p_empty = p_full + 4;             // [tile][buf]
-  uint64_t* o_done = p_empty + 4;             // [2] last PV of the tile retired
-  uint64_t* pv_done = o_done + 2;             // [2] each PV retired (rescale fence)
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(pv_done + 2);
+  uint8_t* sQ = align1024(smem_raw);  // [item buffer][tile]
+  uint8_t* sK = sQ + QB * 2 * kTQ;    // [KVS]
+  uint8_t* sV = sK + KVS * kTQ;       // [KVS]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + KVS * kTQ);
+  uint64_t* q_full = bars;             // [2] item buffer loaded
+  uint64_t* q_empty = bars + 2;        // [2] item buffer's O staging read by the stores (2 tiles)
+  uint64_t* k_full = bars + 4;         // [KVS]
+  uint64_t* v_full = k_full + 4;       // [KVS]
+  uint64_t* kv_empty = v_full + 4;     // [KVS]
+  uint64_t* s_full = kv_empty + 4;     // [tile]
+  uint64_t* s_empty = s_full + 2;      // [tile]
+  uint64_t* p_full = s_empty + 2;      // [tile]
+  uint64_t* p_empty = p_full + 2;      // [tile] PV retired: P may be rewritten
+  uint64_t* pv_done = p_empty + 2;     // [tile] each PV retired (rescale fence)
+  uint64_t* o_done = pv_done + 2;      // [tile] the item's last PV retired
+  uint64_t* r_full = o_done + 2;       // [R] item index published
+  uint64_t* r_empty = r_full + R;      // [R] read by the MMA warp and the 8 softmax warps
+  int* ring = reinterpret_cast<int*>(r_empty + R);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(ring + R);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int npair = (p.nqt + TILES - 1) / TILES;
+#ifdef B2S_ATTN_TRACE
+  int tr_n = 0;
+#endif
+  const int npair = (p.nqt + 1) / 2;
   const int nbh = p.B * p.Hq;
-  const int pr = npair - 1 - (int)(blockIdx.x / nbh);  // heaviest pairs first
-  const int bh = blockIdx.x % nbh;
-  const int b = bh / p.Hq, h = bh % p.Hq;
-  const int kvh = h / (p.Hq / p.Hkv);
-  const int qtA = TILES * pr, qtB = TILES * pr + 1;
-  const bool hasB = TILES == 2 && qtB < p.nqt;
-  const int nA = qtA + 1, nB = hasB ? qtB + 1 : 0;
-  const int nkv = hasB ? nB : nA;
+  const int nitems = npair * nbh;
+  // item w -> (query tiles, batch, head); heaviest pairs first
+  auto decode = [&](int w, int& qtA, int& nA, int& nB, int& b, int& h) {
+    const int pr = npair - 1 - w / nbh, bh = w % nbh;
+    b = bh / p.Hq;
+    h = bh % p.Hq;
+    qtA = 2 * pr;
+    nA = qtA + 1;
+    nB = qtA + 1 < p.nqt ? qtA + 2 : 0;
+  };
+  auto ring_get = [&](int it) -> int {
+    mbar_wait(&r_full[it % R], (it / R) & 1);
+    return *reinterpret_cast<volatile int*>(&ring[it % R]);
+  };
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tm_qkv);
-    mbar_init(q_full, 1);
-    for (int s = 0; s < KVS; ++s) { mbar_init(&k_full[s], 1); mbar_init(&v_full[s], 1); mbar_init(&kv_empty[s], 1); }
+    tma_prefetch(&tm_o);
+    for (int i = 0; i < 2; ++i) { mbar_init(&q_full[i], 1); mbar_init(&q_empty[i], 2); }
+    for (int s = 0; s < KVS; ++s) { mbar_init(&k_full[s], 1); mbar_init(&v_full[s], 1); mbar_init(&kv_empty[s], 2); }
     for (int t = 0; t < 2; ++t) {
       mbar_init(&s_full[t], 1); mbar_init(&s_empty[t], 4);
-      mbar_init(&p_full[2 * t], 4); mbar_init(&p_full[2 * t + 1], 4);
-      mbar_init(&o_done[t], 1); mbar_init(&pv_done[t], 1);
-      mbar_init(&p_empty[2 * t], 1); mbar_init(&p_empty[2 * t + 1], 1);
+      mbar_init(&p_full[t], 4); mbar_init(&p_empty[t], 1);
+      mbar_init(&pv_done[t], 1); mbar_init(&o_done[t], 1);
     }
+    for (int i = 0; i < R; ++i) { mbar_init(&r_full[i], 1); mbar_init(&r_empty[i], 10); }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc<C::TCOLS>(tslot);
+  if (warp == 1) tmem_alloc<512>(tslot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tslot;
-  // TMEM: S_A [0,128) S_B [128,256) O_A [OCOL,OCOL+DH) O_B [OCOL+DH,OCOL+2DH)
 
   if (warp == 0) {
+    // ------------------------------------------------ producer: item ring + TMA loads
     if (lane == 0) {
-      mbar_arrive_expect_tx(q_full, hasB ? 2 * kTQ : kTQ);
-      for (int a = 0; a < NA; ++a) {
-        tma_load_2d(sQ + a * kTile, &tm_qkv, q_full, h * DH + a * 64, b * p.T + qtA * BQ);
-        if (hasB) tma_load_2d(sQ + kTQ + a * kTile, &tm_qkv, q_full, h * DH + a * 64, b * p.T + qtB * BQ);
-      }
-      for (int j = 0; j < nkv; ++j) {
-        const int s = j % KVS;
-        mbar_wait(&kv_empty[s], ((j / KVS) & 1) ^ 1);
-        const int r = b * p.T + j * BKV;
-        mbar_arrive_expect_tx(&k_full[s], kTQ);
-        for (int a = 0; a < NA; ++a)
-          tma_load_2d(sK + s * kTQ + a * kTile, &tm_qkv, &k_full[s], (p.Hq + kvh) * DH + a * 64, r);
-        mbar_arrive_expect_tx(&v_full[s], kTQ);
-        for (int a = 0; a < NA; ++a)
-          tma_load_2d(sV + s * kTQ + a * kTile, &tm_qkv, &v_full[s], (p.Hq + p.Hkv + kvh) * DH + a * 64, r);
+      int next = blockIdx.x;  // first item static, later ones from the counter
+      uint32_t kv = 0;        // K / V blocks loaded by this CTA
+      for (int it = 0;; ++it) {
+        const int slot = it % R;
+        mbar_wait(&r_empty[slot], ((it / R) & 1) ^ 1);
+        const int w = next < nitems ? next : nitems;
+        ring[slot] = w;
+        mbar_arrive(&r_full[slot]);
+        if (w >= nitems) break;
+        next = gridDim.x + atomicAdd(p.sched, 1);  // latency hidden behind this item's loads
+        int qtA, nA, nB, b, h;
+        decode(w, qtA, nA, nB, b, h);
+        const int kvh = h / (p.Hq / p.Hkv);
+        const int qb = it % QB;
+        mbar_wait(&q_empty[qb], ((it / QB) & 1) ^ 1);
+        mbar_arrive_expect_tx(&q_full[qb], (nB ? 2 : 1) * kTQ);
+        for (int a = 0; a < NA; ++a) {
+          tma_load_2d(sQ + (2 * qb) * kTQ + a * kTile, &tm_qkv, &q_full[qb], h * DH + a * 64, b * p.T + qtA * BQ);
+          if (nB)
+            tma_load_2d(sQ + (2 * qb + 1) * kTQ + a * kTile, &tm_qkv, &q_full[qb], h * DH + a * 64,
+                        b * p.T + (qtA + 1) * BQ);
+        }
+        const int nkv = nB ? nB : nA;
+        for (int j = 0; j < nkv; ++j, ++kv) {
+          const int s = kv % KVS;
+          mbar_wait(&kv_empty[s], ((kv / KVS) & 1) ^ 1);
+          const int r = b * p.T + j * BKV;
+          mbar_arrive_expect_tx(&k_full[s], kTQ);
+          for (int a = 0; a < NA; ++a)
+            tma_load_2d(sK + s * kTQ + a * kTile, &tm_qkv, &k_full[s], (p.Hq + kvh) * DH + a * 64, r);
+          mbar_arrive_expect_tx(&v_full[s], kTQ);
+          for (int a = 0; a < NA; ++a)
+            tma_load_2d(sV + s * kTQ + a * kTile, &tm_qkv, &v_full[s], (p.Hq + p.Hkv + kvh) * DH + a * 64, r);
+        }
       }
     }
     __syncwarp();
-  } else if (warp == 1) {
-    {  // whole warp, converged; one lane elected per tcgen05 instruction
-      constexpr uint32_t idS = make_idesc_bf16(BQ, BKV, false, false);
-      constexpr uint32_t idO = make_idesc_bf16(BQ, DH, false, true);
-      const uint32_t aQ = smem_u32(sQ), aK = smem_u32(sK), aV = smem_u32(sV), aP = smem_u32(sP);
-      auto issue_S = [&](int t, int j) {
-        const int s = j % KVS;
-        mbar_wait(&k_full[s], (j / KVS) & 1);
-        mbar_wait(&s_empty[t], (j & 1) ^ 1);
+  } else if (warp == 1 || warp == kThreadsMMA2 / 32) {
+    // ------------------------------------------------ MMA issuers: warp 1 tile A, the last warp tile B
+    // (whole warp, one lane elected per op). One issuer per tile: a single in-order issuer
+    // for both tiles stalls one tile's QK^T / PV behind the other tile's softmax.
+    const int tt = warp == 1 ? 0 : 1;
+    constexpr uint32_t idS = make_idesc_bf16(BQ, BKV, false, false);
+    constexpr uint32_t idO = make_idesc_bf16(BQ, DH, false, true);
+    const uint32_t aQ = smem_u32(sQ), aK = smem_u32(sK), aV = smem_u32(sV);
+    const uint32_t tSt = tbase + tt * BKV, tOt = tbase + C::OCOL + tt * DH, tPt = tbase + C::pcol(tt);
+    uint32_t kv = 0;   // K / V blocks consumed (the producer's order)
+    uint32_t ns = 0;   // S MMAs issued for this tile (s_empty phases)
+    uint32_t np = 0;   // PV MMAs issued for this tile (p_full phases)
+    for (int it = 0;; ++it) {
+      const int w = ring_get(it);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&r_empty[it % R]);
+      if (w >= nitems) break;
+      int qtA, nA, nB, b, h;
+      decode(w, qtA, nA, nB, b, h);
+      const int qb = it % QB;
+      const int nkv = nB ? nB : nA;
+      const int nt = tt == 0 ? nA : nB;
+      const uint32_t kv0 = kv;
+      auto issue_S = [&](int j) {
+        const uint32_t g = kv0 + j, s = g % KVS;
+        TRACE(10, g);
+        mbar_wait(&k_full[s], (g / KVS) & 1);
+        TRACE(12, g);
+        mbar_wait(&s_empty[tt], (ns & 1) ^ 1);
+        TRACE(14, g);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < DH / 16; ++kk) {
           const uint32_t ko = (kk >> 2) * kTile + (kk & 3) * 32;  // atom, then 16-element K step
-          mma_bf16_ss_w(tbase + t * BKV, make_sdesc(aQ + t * kTQ + ko, 16, 1024),
+          mma_bf16_ss_w(tSt, make_sdesc(aQ + (2 * qb + tt) * kTQ + ko, 16, 1024),
                         make_sdesc(aK + s * kTQ + ko, 16, 1024), idS, kk > 0);
         }
-        mma_commit_w(&s_full[t]);
+        mma_commit_w(&s_full[tt]);
+        ++ns;
       };
-      auto issue_PV = [&](int t, int j, bool last) {
-        const int s = j % KVS;
-        mbar_wait(&v_full[s], (j / KVS) & 1);
-        mbar_wait(&p_full[2 * t + (j % PB)], (j / PB) & 1);
+      auto issue_PV = [&](int j, bool last) {
+        const uint32_t g = kv0 + j, s = g % KVS;
+        TRACE(20, g);
+        mbar_wait(&v_full[s], (g / KVS) & 1);
+        TRACE(22, g);
+        mbar_wait(&p_full[tt], np & 1);
+        TRACE(24, g);
         tc_fence_after();
-        const uint32_t pbase = aP + (PB * t + (j % PB)) * kPBuf;
-        // V as an MN-major operand: 16 keys per K step (2 KB of 128-B rows), dh atoms LBO = 16 KB apart
+        // V as an MN-major operand: 16 keys per K step (2 KB of 128-B rows), dh atoms 16 KB apart;
+        // P from TMEM: 16 keys = 8 columns of bf16 pairs per K step
 #pragma unroll
-        for (int kk = 0; kk < BKV / 16; ++kk) {
-          if constexpr (C::PT)  // P from TMEM: 16 keys = 8 columns of bf16 pairs per K step
-            mma_bf16_ts_w(tbase + C::OCOL + t * DH, tbase + C::pcol(t) + kk * 8,
-                          make_sdesc(aV + s * kTQ + kk * 2048, kTile, 1024), idO, (j > 0 || kk > 0) ? 1u : 0u);
-          else
-            mma_bf16_ss_w(tbase + C::OCOL + t * DH, make_sdesc(pbase + (kk >> 2) * kTile + (kk & 3) * 32, 16, 1024),
-                          make_sdesc(aV + s * kTQ + kk * 2048, kTile, 1024), idO, (j > 0 || kk > 0) ? 1u : 0u);
-        }
-        mma_commit_w(&p_empty[2 * t + (j % PB)]);
-        mma_commit_w(&pv_done[t]);
-        if (last) mma_commit_w(&o_done[t]);
+        for (int kk = 0; kk < BKV / 16; ++kk)
+          mma_bf16_ts_w(tOt, tPt + kk * 8, make_sdesc(aV + s * kTQ + kk * 2048, kTile, 1024), idO,
+                        (j > 0 || kk > 0) ? 1u : 0u);
+        mma_commit_w(&p_empty[tt]);
+        mma_commit_w(&pv_done[tt]);
+        if (last) mma_commit_w(&o_done[tt]);
+        mma_commit_w(&kv_empty[s]);  // this tile's reads of K_j / V_j retired
+        ++np;
       };
-      mbar_wait(q_full, 0);
-      issue_S(0, 0);
-      if (nB > 0) issue_S(1, 0);
-      for (int j = 0; j < nkv; ++j) {
-        if constexpr (C::ALIAS) {
-          // P_t(j) lives in S_t's columns: S_t(j+1) goes in behind PV_t(j) (the tensor
-          // pipe runs one CTA's MMAs in order), while the other tile's softmax runs
-          if (j < nA) issue_PV(0, j, j + 1 == nA);
-          if (j + 1 < nA) issue_S(0, j + 1);
-          if (j < nB) issue_PV(1, j, j + 1 == nB);
-          if (j + 1 < nB) issue_S(1, j + 1);
-        } else {
-          // QK^T of block j+1 goes in as soon as each softmax group holds S(j) in
-          // registers, so it is ready when the group finishes block j
-          if (j + 1 < nA) issue_S(0, j + 1);
-          if (j + 1 < nB) issue_S(1, j + 1);
-          if (j < nA) issue_PV(0, j, j + 1 == nA);
-          if (j < nB) issue_PV(1, j, j + 1 == nB);
+      if (nt > 0) {
+        mbar_wait(&q_full[qb], (it / QB) & 1);
+        issue_S(0);
+        for (int j = 0; j < nt; ++j) {
+          if constexpr (C::ALIAS) {  // P_t(j) lives in S_t's columns: S_t(j+1) goes in behind PV_t(j)
+            issue_PV(j, j + 1 == nt);
+            if (j + 1 < nt) issue_S(j + 1);
+          } else {  // QK^T(j+1) as soon as the softmax holds S(j) in registers
+            if (j + 1 < nt) issue_S(j + 1);
+            issue_PV(j, j + 1 == nt);
+          }
         }
-        mma_commit_w(&kv_empty[j % KVS]);  // K_j / V_j no longer read once these retire
       }
+      // blocks of the item this tile does not use: release their K / V stage once it has been
+      // loaded (so this arrival cannot count toward the stage's previous use)
+      for (int j = nt; j < nkv; ++j) {
+        const uint32_t g = kv0 + j, s = g % KVS;
+        mbar_wait(&k_full[s], (g / KVS) & 1);
+        mbar_wait(&v_full[s], (g / KVS) & 1);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&kv_empty[s]);
+      }
+      kv += nkv;
     }
     __syncwarp();
   } else {
-    // ------------------------------------------------ softmax warpgroups
-    const int t = (warp - 2) >> 2;  // 0: tile A, 1: tile B
+    // ------------------------------------------------ softmax warpgroups (tile t = 0: A, 1: B)
+    const int t = (warp - 2) >> 2;
     const int q4 = warp & 3;
     const int r = q4 * 32 + lane;
-    const int qt = t == 0 ? qtA : qtB;
-    const int nj = t == 0 ? nA : nB;
     const uint32_t lrow = (uint32_t)(q4 * 32) << 16;
     const uint32_t tS = tbase + lrow + t * BKV;
     const uint32_t tO = tbase + lrow + C::OCOL + t * DH;
     const float sl2 = p.scale_log2;
-    float m = -INFINITY, l = 0.f;
-    for (int j = 0; j < nj; ++j) {
-      mbar_wait(&s_full[t], j & 1);
-      tc_fence_after();
-      const bool diag = (j == qt);
-      // the whole 128-column S row in registers: one TMEM round trip per block
-      uint32_t v[BKV];
-#pragma unroll
-      for (int c = 0; c < BKV / 32; ++c) tmem_ld32(tS + c * 32, v + c * 32);
-      tmem_wait_ld();
-      tc_fence_before();
+    uint32_t ns = 0;    // S blocks consumed by this tile (s_full / p phases)
+    uint32_t nitm = 0;  // items with blocks for this tile (o_done phase)
+    const int my_turn = 3 + t, other_turn = 4 - t;
+    if (t == 1) named_arrive(3, 256);  // tile A goes first
+    for (int it = 0;; ++it) {
+      const int w = ring_get(it);
       __syncwarp();
-      if (lane == 0) mbar_arrive(&s_empty[t]);  // S(j) is in registers: QK^T(j+1) may overwrite it
-      // row max over 8 independent partial maxima (short dependency chains)
-      float mx8[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) mx8[u] = -INFINITY;
-      if (diag) {
-#pragma unroll
-        for (int i = 0; i < BKV; ++i)
-          if (i <= r) mx8[i & 7] = fmaxf(mx8[i & 7], __uint_as_float(v[i]));
-      } else {  // three-input max (FMNMX3): two new elements per instruction
-#pragma unroll
-        for (int i = 0; i < BKV / 2; ++i)
-          mx8[i & 7] = fmax3(mx8[i & 7], __uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
+      if (lane == 0) mbar_arrive(&r_empty[it % R]);
+      if (w >= nitems) break;
+      int qtA, nA, nB, b, h;
+      decode(w, qtA, nA, nB, b, h);
+      const int qb = it % QB;
+      const int qt = qtA + t;
+      const int nj = t == 0 ? nA : nB;
+      const int nturns = nB ? nB : nA;
+      float m = -INFINITY, l = 0.f;
+      for (int j = nj; j < nturns; ++j) {  // turns without a block of this tile: pass them on
+        named_sync(my_turn, 256);
+        named_arrive(other_turn, 256);
       }
-      const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
-                             fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
-      const float m_cand = mx * sl2;
-      // lazy rescale: keep the old max unless the new one exceeds it by > 2^8
-      float m_use = m;
-      bool resc = false;
-      if (m_cand > m + kRescaleThresh) { m_use = m_cand; resc = (j > 0); }
-      const float alpha = ex2(m - m_use);  // 0 on the first block (m = -inf)
-      if (__any_sync(0xffffffffu, resc)) {
-        // O must not be in flight: wait for the previous PV of this tile, then O *= alpha
-        mbar_wait(&pv_done[t], (j - 1) & 1);
+      for (int j = 0; j < nj; ++j, ++ns) {
+        TRACE(30, ns);
+        mbar_wait(&s_full[t], ns & 1);
+        TRACE(31, ns);
         tc_fence_after();
+        const bool diag = (j == qt);
+        // the whole 128-column S row in registers: one TMEM round trip per block
+        uint32_t v[BKV];
 #pragma unroll
-        for (int c = 0; c < DH / 16; ++c) {
-          uint32_t o[16];
-          tmem_ld16(tO + c * 16, o);
-          tmem_wait_ld();
+        for (int c = 0; c < BKV / 32; ++c) tmem_ld32(tS + c * 32, v + c * 32);
+        tmem_wait_ld();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&s_empty[t]);  // S(j) is in registers: QK^T(j+1) may overwrite it
+        TRACE(32, ns);
+        // row max over 8 independent partial maxima (short dependency chains)
+        float mx8[8];
 #pragma unroll
-          for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * (resc ? alpha : 1.f));
-          tmem_st16(tO + c * 16, o);
+        for (int u = 0; u < 8; ++u) mx8[u] = -INFINITY;
+        if (diag) {
+#pragma unroll
+          for (int i = 0; i < BKV; ++i)
+            if (i <= r) mx8[i & 7] = fmaxf(mx8[i & 7], __uint_as_float(v[i]));
+        } else {  // three-input max (FMNMX3): two new elements per instruction
+#pragma unroll
+          for (int i = 0; i < BKV / 2; ++i)
+            mx8[i & 7] = fmax3(mx8[i & 7], __uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
         }
-        tmem_wait_st();
-      }
-      // P = 2^(s*sl2 - m_use) -> bf16 -> smem buffer (j & 1) or TMEM; row sum
-      const int pb = j % PB;
-      float rs = 0.f;
-      if constexpr (C::PT) {
-        // exponentials first (bf16 pairs packed over the S registers), then wait for
-        // PV(j-1) to release this tile's TMEM P block, then one TMEM store round
+        const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                               fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
+        const float m_cand = mx * sl2;
+        // lazy rescale: keep the old max unless the new one exceeds it by > 2^8
+        float m_use = m;
+        bool resc = false;
+        if (m_cand > m + kRescaleThresh) { m_use = m_cand; resc = (j > 0); }
+        const float alpha = ex2(m - m_use);  // 0 on the first block (m = -inf)
+        if (__any_sync(0xffffffffu, resc)) {
+          // O must not be in flight: wait for the previous PV of this tile, then O *= alpha
+          mbar_wait(&pv_done[t], (ns - 1) & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int c = 0; c < DH / 16; ++c) {
+            uint32_t o[16];
+            tmem_ld16(tO + c * 16, o);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * (resc ? alpha : 1.f));
+            tmem_st16(tO + c * 16, o);
+          }
+          tmem_wait_st();
+        }
+        // exponentials first (bf16 pairs packed over the S registers), then wait for PV(j-1)
+        // to release this tile's TMEM P block, then one TMEM store round
         uint32_t* pk = v;
-        rs = diag ? exp_pack_regs<true>(v, r, sl2, m_use, pk) : exp_pack_regs<false>(v, r, sl2, m_use, pk);
-        if (j >= 1) mbar_wait(&p_empty[2 * t], (j - 1) & 1);
+        TRACE(33, ns);
+        named_sync(my_turn, 256);
+        TRACE(37, ns);
+        const float rs = diag ? exp_pack_regs<true>(v, r, sl2, m_use, pk) : exp_pack_regs<false>(v, r, sl2, m_use, pk);
+        named_arrive(other_turn, 256);
+        TRACE(34, ns);
+        if (ns > 0) mbar_wait(&p_empty[t], (ns - 1) & 1);
+        TRACE(35, ns);
         tc_fence_after();
         tmem_st32(tbase + lrow + C::pcol(t), pk);
         tmem_st32(tbase + lrow + C::pcol(t) + 32, pk + 32);
         tmem_wait_st();
-      } else {
-        if (j >= PB) mbar_wait(&p_empty[2 * t + pb], ((j / PB) - 1) & 1);
-        uint8_t* myP = sP + (PB * t + pb) * kPBuf;
-        if (diag) {
-          rs += exp_pack<true>(v, 0, r, sl2, m_use, myP);
-          rs += exp_pack<true>(v + 64, 64, r, sl2, m_use, myP + kTile);
-        } else {
-          rs += exp_pack<false>(v, 0, r, sl2, m_use, myP);
-          rs += exp_pack<false>(v + 64, 64, r, sl2, m_use, myP + kTile);
+        l = l * alpha + rs;
+        m = m_use;
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[t]);
+        TRACE(36, ns);
+      }
+      if (nj > 0) {
+        // epilogue: O (TMEM) / l -> bf16 -> this tile's Q buffer (all its MMAs retired) -> TMA store
+        mbar_wait(&o_done[t], nitm & 1);
+        ++nitm;
+        tc_fence_after();
+        uint8_t* sO = sQ + (2 * qb + t) * kTQ;
+        const float inv = 1.f / l;
+#pragma unroll
+        for (int c = 0; c < DH / 32; ++c) {
+          uint32_t o[32];
+          tmem_ld32(tO + c * 32, o);
+          tmem_wait_ld();
+#pragma unroll
+          for (int k8 = 0; k8 < 4; ++k8) {
+            uint4 w4;
+            w4.x = pack_bf16x2(__uint_as_float(o[8 * k8 + 0]) * inv, __uint_as_float(o[8 * k8 + 1]) * inv);
+            w4.y = pack_bf16x2(__uint_as_float(o[8 * k8 + 2]) * inv, __uint_as_float(o[8 * k8 + 3]) * inv);
+            w4.z = pack_bf16x2(__uint_as_float(o[8 * k8 + 4]) * inv, __uint_as_float(o[8 * k8 + 5]) * inv);
+            w4.w = pack_bf16x2(__uint_as_float(o[8 * k8 + 6]) * inv, __uint_as_float(o[8 * k8 + 7]) * inv);
+            *reinterpret_cast<uint4*>(sO + (c >> 1) * kTile + swz(r, (c & 1) * 4 + k8)) = w4;
+          }
         }
+        tc_fence_before();  // O read out: the next item's first PV may overwrite it
+        p.lse[((size_t)b * p.Hq + h) * p.T + qt * BQ + r] = (m + log2f(l)) * (1.f / kLog2e);
         fence_proxy_async_smem();
-      }
-      l = l * alpha + rs;
-      m = m_use;
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full[2 * t + pb]);
-    }
-    if (nj > 0) {
-      // epilogue: O (TMEM) / l -> bf16 -> this tile's Q buffer (all MMAs retired) -> TMA store
-      mbar_wait(&o_done[t], 0);
-      tc_fence_after();
-      uint8_t* sO = sQ + t * kTQ;
-      const float inv = 1.f / l;
-#pragma unroll
-      for (int c = 0; c < DH / 32; ++c) {
-        uint32_t o[32];
-        tmem_ld32(tO + c * 32, o);
-        tmem_wait_ld();
-#pragma unroll
-        for (int k8 = 0; k8 < 4; ++k8) {
-          uint4 w;
-          w.x = pack_bf16x2(__uint_as_float(o[8 * k8 + 0]) * inv, __uint_as_float(o[8 * k8 + 1]) * inv);
-          w.y = pack_bf16x2(__uint_as_float(o[8 * k8 + 2]) * inv, __uint_as_float(o[8 * k8 + 3]) * inv);
-          w.z = pack_bf16x2(__uint_as_float(o[8 * k8 + 4]) * inv, __uint_as_float(o[8 * k8 + 5]) * inv);
-          w.w = pack_bf16x2(__uint_as_float(o[8 * k8 + 6]) * inv, __uint_as_float(o[8 * k8 + 7]) * inv);
-          *reinterpret_cast<uint4*>(sO + (c >> 1) * kTile + swz(r, (c & 1) * 4 + k8)) = w;
+        named_sync(1 + t, 128);
+        if (q4 == 0 && lane == 0) {
+          for (int a = 0; a < NA; ++a) tma_store_2d(&tm_o, sO + a * kTile, h * DH + a * 64, b * p.T + qt * BQ);
+          bulk_commit();
+          bulk_wait_read<0>();  // the staging (this item's Q buffer) may be reloaded
+          mbar_arrive(&q_empty[qb]);
         }
+      } else if (q4 == 0 && lane == 0) {
+        mbar_arrive(&q_empty[qb]);  // no tile B in this item: nothing staged
       }
-      p.lse[((size_t)b * p.Hq + h) * p.T + qt * BQ + r] = (m + log2f(l)) * (1.f / kLog2e);
-      fence_proxy_async_smem();
-      named_sync(1 + t, 128);
-      if (q4 == 0 && lane == 0) {
-        for (int a = 0; a < NA; ++a) tma_store_2d(&tm_o, sO + a * kTile, h * DH + a * 64, b * p.T + qt * BQ);
-        bulk_commit();
-        bulk_wait_read<0>();
-      }
+      __syncwarp();
     }
+    if (t == 0) named_sync(3, 256);  // consume tile B's last hand-over: no barrier left pending
+    if (q4 == 0 && lane == 0) bulk_wait<0>();  // the last item's O stores complete
     __syncwarp();
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc<C::TCOLS>(tbase);
+    tmem_dealloc<512>(tbase);
+  }
+  // every CTA has fetched its sentinel: the last one out re-arms the counter for the next launch
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(p.sched + 1, 1) == (int)gridDim.x - 1) {
+      p.sched[0] = 0;
+      p.sched[1] = 0;
+      __threadfence();
+    }
   }
 }
 
@@ -549,11 +605,7 @@ __device__ __forceinline__ void p_ds(uint32_t* sv, uint32_t* dv, int q0, int r, 
 #pragma unroll
   for (int e = 0; e < 32; ++e) {
     const int q = q0 + e;
-#ifdef B2S_EXP_NOEXP
-    float pv = __uint_as_float(sv[e]);
-#else
     float pv = ex2(fmaf(__uint_as_float(sv[e]), sl2, -ls[e]));
-#endif
     if (DIAG && q < r) pv = 0.f;  // query index below key index: masked
     sv[e] = __float_as_uint(pv);
     dv[e] = __float_as_uint(pv * fmaf(__uint_as_float(dv[e]), scale, -ds[e]));
@@ -563,21 +615,12 @@ __device__ __forceinline__ void p_ds(uint32_t* sv, uint32_t* dv, int q0, int r, 
 // columns) and Q / dO double-buffered. dh = 128: dV + dK take 256 columns, so
 // this kernel computes dK / dV only (single-buffered Q / dO to fit 227 KB of
 // smem) and attn_bwd_q_kernel produces dQ per query tile.
-#ifndef B2S_ATTN_BWD_SPLIT_DQ
-#define B2S_ATTN_BWD_SPLIT_DQ 0  // 1: dh = 64 also takes the separate query-tile dQ kernel
-#endif
-#ifndef B2S_ATTN_BWD_DQ_RED
-#define B2S_ATTN_BWD_DQ_RED 0  // 1: dQ drained by red.global.add.v4.f32 from registers (no smem staging)
-#endif
-#ifndef B2S_ATTN_BWD_PT
-#define B2S_ATTN_BWD_PT 1  // dh 64: P^T goes to TMEM (dV by the TMEM-A MMA form), single-buffered dQ
-#endif
 template <int DH>
 struct Bwd {
-  static constexpr bool DQ = DH == 64 && !B2S_ATTN_BWD_SPLIT_DQ;  // dQ fused into the key-tile kernel
+  static constexpr bool DQ = DH == 64;  // dQ fused into the key-tile kernel
   // P^T in TMEM columns [448, 512) (freed by a single dQ buffer): no P^T shared-memory
   // stores and no A-operand smem reads for dV -- the kernel is smem-bandwidth bound
-  static constexpr bool PT = DQ && B2S_ATTN_BWD_PT;
+  static constexpr bool PT = DQ;
   static constexpr int QS = DH == 64 ? 2 : 1; // Q / dO stages
   static constexpr int kTileQ = BQ * DH * 2;
   static constexpr int kSmem = 1024 + 2 * kTileQ /*K,V*/ + 2 * QS * kTileQ /*Q,dO*/ + (PT ? 1 : 2) * kPBuf /*P^T,dS^T*/ +
@@ -708,7 +751,7 @@ __global__ void __launch_bounds__(320, 1)
       mbar_wait(kv_full, 0);
       issue_S(0);
       for (int t = 0; t < nsteps; ++t) {
-        const int s = t & 1, qs = t % QS;
+        const int qs = t % QS;
         const uint32_t q_ = aQ + qs * kTQ, do_ = adO + qs * kTQ;
         // with a single Q / dO stage, S(t+1) needs this step's dV / dK MMAs to have read Q(t) / dO(t)
         if (QS == 2 && t + 1 < nsteps) issue_S(t + 1);
@@ -760,17 +803,6 @@ __global__ void __launch_bounds__(320, 1)
       tmem_wait_ld();
       tc_fence_before();
       __syncwarp();
-#if B2S_ATTN_BWD_DQ_RED
-      if (lane == 0) mbar_arrive(&dq_empty[dq_buf(t)]);
-      // straight from registers: 8 x 16-byte fp32 add-reductions into this thread's query row
-      float* dst = p.dq_acc + ((size_t)b * p.T + (size_t)i * BQ + r) * (p.Hq * DH) + h * DH + half * 32;
-#pragma unroll
-      for (int c = 0; c < 8; ++c)
-        asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst + 4 * c), "r"(qv[4 * c]),
-                     "r"(qv[4 * c + 1]), "r"(qv[4 * c + 2]), "r"(qv[4 * c + 3])
-                     : "memory");
-      return;
-#endif
       if (lane == 0) {
         mbar_arrive(&dq_empty[dq_buf(t)]);
         bulk_wait_read<0>();  // this warp's previous add-reduce has read its staging tile
@@ -784,9 +816,7 @@ __global__ void __launch_bounds__(320, 1)
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) {
-#ifndef B2S_EXP_NO_DQ_REDUCE  // timing experiment only: dQ not accumulated
         tma_reduce_add_2d(&tm_dq, mystage, h * DH + half * 32, b * p.T + i * BQ + q4 * 32);
-#endif
         bulk_commit();
       }
     };
@@ -810,14 +840,9 @@ __global__ void __launch_bounds__(320, 1)
           __syncwarp();
           if (lane == 0) mbar_arrive(st_empty);  // the next step's S^T / dP^T may overwrite TMEM
         }
-#ifndef B2S_EXP_NOCOMPUTE  // timing experiment only: protocol without the softmax math / P, dS stores
         if (diag) p_ds<true>(sv, dv, half * 64 + qq * 32, r, p.scale_log2, p.scale, lse2, dd);
         else p_ds<false>(sv, dv, half * 64 + qq * 32, r, p.scale_log2, p.scale, lse2, dd);
-#endif
-#ifndef B2S_EXP_NO_PDS_WAIT  // timing experiment only: races on sP / sdS
         if (qq == 0 && t > 0) mbar_wait(pds_empty, (t - 1) & 1);  // step t-1's MMAs released sP / sdS
-#endif
-#ifndef B2S_EXP_NOCOMPUTE
 #pragma unroll
         for (int k8 = 0; k8 < 4; ++k8) {
           uint4 w, z;
@@ -838,9 +863,6 @@ __global__ void __launch_bounds__(320, 1)
           *reinterpret_cast<uint4*>(sdS + off) = z;
         }
         if constexpr (PT) tmem_st16(tPT + lrow + half * 32 + qq * 16, pt);
-#else
-        if (lane == 99) *reinterpret_cast<uint32_t*>(sP) = sv[0] + dv[7];
-#endif
       }
       if constexpr (PT) {
         tmem_wait_st();  // P^T is in TMEM before the MMA warp is told
@@ -852,17 +874,9 @@ __global__ void __launch_bounds__(320, 1)
         mbar_arrive(pds_full);
         mbar_arrive(&st_ld_empty[t & 1]);
       }
-#ifndef B2S_EXP_NODQ
       if (t > 0) drain_dq(t - 1);
-#else
-      if (t > 0) { mbar_wait(&dq_full[(t - 1) & 1], ((t - 1) >> 1) & 1); tc_fence_after(); __syncwarp(); if (lane == 0) mbar_arrive(&dq_empty[(t - 1) & 1]); }
-#endif
     }
-#ifndef B2S_EXP_NODQ
     if (nsteps > 0) drain_dq(nsteps - 1);
-#else
-    if (nsteps > 0) { mbar_wait(&dq_full[(nsteps - 1) & 1], ((nsteps - 1) >> 1) & 1); if (lane == 0) mbar_arrive(&dq_empty[(nsteps - 1) & 1]); }
-#endif
     if (DQ && lane == 0) bulk_wait_read<0>();  // this warp's add-reduces have read their staging smem (kernel exit orders their writes)
     __syncwarp();
     // dK (from the pre-scaled dS) and dV -> bf16 -> smem (Q / dO stages are free) -> TMA store into dqkv
@@ -1129,6 +1143,26 @@ __global__ void __launch_bounds__(320, 1)
 using namespace b2s;
 
 namespace {
+// Per-device pool of zeroed work-item counters {next, ctas_done} for the persistent kernels;
+// launches rotate through it so kernels in flight on different streams never share one.
+static int* sched_slot() {
+  constexpr int kSlots = 64;
+  static int* pool[64] = {};
+  static int next[64] = {};
+  static std::mutex mu;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  if (!pool[dev]) {
+    if (cudaMalloc(&pool[dev], kSlots * 2 * sizeof(int)) != cudaSuccess) return nullptr;
+    cudaMemset(pool[dev], 0, kSlots * 2 * sizeof(int));
+    cudaDeviceSynchronize();
+  }
+  int* p = pool[dev] + 2 * next[dev];
+  next[dev] = (next[dev] + 1) % kSlots;
+  return p;
+}
+
 template <int DH>
 int attn_fwd_dh(const void* d_qkv, void* d_o, float* d_lse, int B, int T, int Hq, int Hkv, cudaStream_t st) {
   using C = attn::Fwd<DH>;
@@ -1138,14 +1172,17 @@ int attn_fwd_dh(const void* d_qkv, void* d_o, float* d_lse, int B, int T, int Hq
   if (rc) return rc;
   rc = encode_tma_2d(&to, d_o, 2, (uint64_t)Hq * DH, (uint64_t)B * T, (uint64_t)Hq * DH * 2, 64, 128, 128);
   if (rc) return rc;
+  int* sched = sched_slot();
+  B2S_REQUIRE(sched, B2S_ECUDA, "attention: work-item counter allocation failed");
   attn::Params p{B, T, Hq, Hkv, T / attn::BQ, attn::kLog2e / sqrtf((float)DH), 1.f / sqrtf((float)DH), d_lse,
-                 nullptr, nullptr};
+                 nullptr, nullptr, sched};
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(attn::attn_fwd_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
     attr = true;
   }
-  const unsigned grid = (unsigned)(B * Hq * ((T / attn::BQ + C::TILES - 1) / C::TILES));
+  const int items = B * Hq * ((T / attn::BQ + 1) / 2);
+  const unsigned grid = (unsigned)(items < kNumSMs ? items : kNumSMs);
   attn::attn_fwd_kernel<DH><<<grid, C::kThreads, C::kSmem, st>>>(tq, to, p);
   return check_launch("attn_fwd");
 }
@@ -1174,7 +1211,7 @@ int attn_bwd_dh(const void* d_qkv, const void* d_o, const void* d_do, const floa
   rc = encode_tma_2d(&tdkv, d_dqkv, 2, (uint64_t)ldq, (uint64_t)M, (uint64_t)ldq * 2, 64, 128, 128);
   if (rc) return rc;
   attn::Params p{B, T, Hq, Hkv, T / attn::BQ, attn::kLog2e / sqrtf((float)DH), 1.f / sqrtf((float)DH), lse2,
-                 dsum, dq_acc};
+                 dsum, dq_acc, nullptr};
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(attn::attn_bwd_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
@@ -1208,6 +1245,13 @@ extern "C" int b2s_attn_fwd(const void* d_qkv, void* d_o, float* d_lse, int B, i
   return dh == 64 ? attn_fwd_dh<64>(d_qkv, d_o, d_lse, B, T, Hq, Hkv, st)
                   : attn_fwd_dh<128>(d_qkv, d_o, d_lse, B, T, Hq, Hkv, st);
 }
+
+#ifdef B2S_ATTN_TRACE
+// experiment builds only (not declared in b2s.h): copy the forward's timeline records to host
+extern "C" int b2s_attn_trace_read(void* host, int64_t bytes) {
+  return cudaMemcpyFromSymbol(host, attn::g_trace, (size_t)bytes) == cudaSuccess ? 0 : -3;
+}
+#endif
 
 extern "C" int64_t b2s_attn_bwd_work_floats(int B, int T, int Hq, int dh) {
   return (int64_t)B * T * Hq * dh + 2 * (int64_t)B * Hq * T;  // dQ acc | D' | lse2
