@@ -171,6 +171,13 @@ int b2s_gemm_swiglu_fwd(const void* d_x, int64_t ldx, const void* d_w13, int64_t
                         void* d_h, int64_t ld_h, int M, int F, int K, b2s_stream_t stream);
 int b2s_gemm_swiglu_bwd(const void* d_dy, int64_t ld_dy, const void* d_w2, int64_t ldw, const void* d_gu,
                         int64_t ld_gu, void* d_dgu, int64_t ld_dgu, int M, int F, int K, b2s_stream_t stream);
+/* Fused QKV projection + rotary embedding (Llama): out = x @ W^T ([M, N], bf16) with columns
+ * [0, rope_cols) -- the q and k heads, width dh in {64, 128} -- rotated in the epilogue
+ * (rotate-half pairs j, j + dh/2; fp32 tables cos / sin [T, dh/2] at position row % T), the
+ * same result as b2s_gemm followed by b2s_rope. N % 256 == 0. */
+int b2s_gemm_rope(const void* d_x, int64_t ldx, const void* d_w, int64_t ldw, void* d_out, int64_t ldo, int M,
+                  int N, int K, const float* d_cos, const float* d_sin, int T, int dh, int rope_cols,
+                  b2s_stream_t stream);
 
 /* ------------------------------------------------------------------ */
 /* Bandwidth-bound kernels (K2-K4, K8-K11); no reference counterpart    */
@@ -270,6 +277,12 @@ int b2s_attn_fwd(const void* d_qkv, void* d_o, float* d_lse, int B, int T, int H
 int b2s_attn_bwd(const void* d_qkv, const void* d_o, const void* d_do, const float* d_lse, void* d_dqkv,
                  float* d_work, int B, int T, int Hq, int Hkv, int dh, b2s_stream_t stream);
 int64_t b2s_attn_bwd_work_floats(int B, int T, int Hq, int dh);
+/* b2s_attn_bwd for rotary-embedded q / k: also rotates the q and k heads of d_dqkv back
+ * (inverse of b2s_rope with the same tables), i.e. the gradient w.r.t. the projection output.
+ * dh 64 folds the dq rotation into the dq conversion pass. */
+int b2s_attn_bwd_rope(const void* d_qkv, const void* d_o, const void* d_do, const float* d_lse, void* d_dqkv,
+                      float* d_work, int B, int T, int Hq, int Hkv, int dh, const float* d_cos, const float* d_sin,
+                      b2s_stream_t stream);
 
 /* ------------------------------------------------------------------ */
 /* fp32 mode (north star: per-step losses/gradients within 1e-4 of the  */

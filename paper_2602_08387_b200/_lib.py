@@ -58,6 +58,7 @@ _SIGS = {
     "b2s_gemm_colsum": "pilpilpliiiiplpp",
     "b2s_gemm_swiglu_fwd": "plplplpliiip",
     "b2s_gemm_swiglu_bwd": "plplplpliiip",
+    "b2s_gemm_rope": "plplpliiippiiip",
     "b2s_layernorm_fwd": "ppppppplifp",
     "b2s_rmsnorm_fwd": "ppppplifp",
     "b2s_layernorm_fwd_res": "pppppppplifp",
@@ -81,6 +82,7 @@ _SIGS = {
     "b2s_scale_f32": "plfp",
     "b2s_attn_fwd": "pppiiiiip",
     "b2s_attn_bwd": "ppppppiiiiip",
+    "b2s_attn_bwd_rope": "ppppppiiiiippp",
     # fp32 mode (same argument order as the bf16 entry points)
     "b2s_gemm_f32": "pilpilpliiiipiplp",
     "b2s_layernorm_fwd_f32": "ppppppplifp",

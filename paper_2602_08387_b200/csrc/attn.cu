@@ -556,22 +556,58 @@ __global__ void attn_bwd_prep_kernel(const __nv_bfloat16* __restrict__ o, const 
   }
 }
 
-// dqkv[:, q heads] = bf16(dq_acc)  (dh = 64 path). Blocks stride over rows (a row
-// is Hq*64 floats), so no 64-bit division per element.
+// dqkv[:, q heads] = bf16(dq_acc)  (dh = 64 path), with ROPE the inverse rotary embedding
+// applied on the way (the forward rotated q after the QKV projection, so dq w.r.t. the
+// projection output is dq rotated back: pairs (j, j + 32), position row % T). Blocks stride
+// over rows (a row is Hq*64 floats), so no 64-bit division per element.
+template <bool ROPE>
 __global__ void __launch_bounds__(256) attn_bwd_dq_kernel(const float* __restrict__ dq_acc,
                                                           __nv_bfloat16* __restrict__ dqkv, int64_t M, int Hq,
-                                                          int64_t ldq) {
+                                                          int64_t ldq, int T, const float* __restrict__ cos_t,
+                                                          const float* __restrict__ sin_t) {
   constexpr int DH = 64;
-  const int nv = Hq * DH / 4;  // float4 vectors per row
-  for (int64_t row = blockIdx.x; row < M; row += gridDim.x) {
-    const float* src = dq_acc + row * (int64_t)(Hq * DH);
-    __nv_bfloat16* dst = dqkv + row * ldq;
-    for (int v = threadIdx.x; v < nv; v += blockDim.x) {
-      const float4 a = __ldcs(reinterpret_cast<const float4*>(src) + v);
-      uint2 u;
-      u.x = pack_bf16x2(a.x, a.y);
-      u.y = pack_bf16x2(a.z, a.w);
-      *reinterpret_cast<uint2*>(dst + 4 * v) = u;
+  if constexpr (!ROPE) {
+    const int nv = Hq * DH / 4;  // float4 vectors per row
+    for (int64_t row = blockIdx.x; row < M; row += gridDim.x) {
+      const float* src = dq_acc + row * (int64_t)(Hq * DH);
+      __nv_bfloat16* dst = dqkv + row * ldq;
+      for (int v = threadIdx.x; v < nv; v += blockDim.x) {
+        const float4 a = __ldcs(reinterpret_cast<const float4*>(src) + v);
+        uint2 u;
+        u.x = pack_bf16x2(a.x, a.y);
+        u.y = pack_bf16x2(a.z, a.w);
+        *reinterpret_cast<uint2*>(dst + 4 * v) = u;
+      }
+    }
+  } else {
+    const int nv = Hq * 8;  // 4 rotation pairs per thread-step: head v / 8, pairs 4 (v % 8) .. + 3
+    for (int64_t row = blockIdx.x; row < M; row += gridDim.x) {
+      const float* src = dq_acc + row * (int64_t)(Hq * DH);
+      __nv_bfloat16* dst = dqkv + row * ldq;
+      const int t = (int)(row % T);
+      for (int v = threadIdx.x; v < nv; v += blockDim.x) {
+        const int h = v >> 3, j0 = (v & 7) * 4;
+        const float4 a = __ldcs(reinterpret_cast<const float4*>(src + h * DH + j0));
+        const float4 b = __ldcs(reinterpret_cast<const float4*>(src + h * DH + j0 + 32));
+        const float4 c = __ldg(reinterpret_cast<const float4*>(cos_t + (int64_t)t * 32 + j0));
+        const float4 sn = __ldg(reinterpret_cast<const float4*>(sin_t + (int64_t)t * 32 + j0));
+        // inverse rotation: s -> -s (the rope kernel's inverse form)
+        const float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+        const float cv[4] = {c.x, c.y, c.z, c.w}, sv[4] = {-sn.x, -sn.y, -sn.z, -sn.w};
+        float oa[4], ob[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          oa[k] = av[k] * cv[k] - bv[k] * sv[k];
+          ob[k] = bv[k] * cv[k] + av[k] * sv[k];
+        }
+        uint2 ua, ub;
+        ua.x = pack_bf16x2(oa[0], oa[1]);
+        ua.y = pack_bf16x2(oa[2], oa[3]);
+        ub.x = pack_bf16x2(ob[0], ob[1]);
+        ub.y = pack_bf16x2(ob[2], ob[3]);
+        *reinterpret_cast<uint2*>(dst + h * DH + j0) = ua;
+        *reinterpret_cast<uint2*>(dst + h * DH + j0 + 32) = ub;
+      }
     }
   }
 }
@@ -1189,7 +1225,8 @@ int attn_fwd_dh(const void* d_qkv, void* d_o, float* d_lse, int B, int T, int Hq
 
 template <int DH>
 int attn_bwd_dh(const void* d_qkv, const void* d_o, const void* d_do, const float* d_lse, void* d_dqkv,
-                float* d_work, int B, int T, int Hq, int Hkv, cudaStream_t st) {
+                float* d_work, int B, int T, int Hq, int Hkv, cudaStream_t st, const float* rope_cos = nullptr,
+                const float* rope_sin = nullptr) {
   using C = attn::Bwd<DH>;
   const int ldq = (Hq + 2 * Hkv) * DH;
   const int64_t M = (int64_t)B * T;
@@ -1225,8 +1262,13 @@ int attn_bwd_dh(const void* d_qkv, const void* d_o, const void* d_do, const floa
   rc = check_launch("attn_bwd");
   if (rc) return rc;
   if constexpr (C::DQ) {
-    attn::attn_bwd_dq_kernel<<<(unsigned)(M < kNumSMs * 16 ? M : kNumSMs * 16), 256, 0, st>>>(
-        dq_acc, (__nv_bfloat16*)d_dqkv, M, Hq, ldq);
+    const unsigned g = (unsigned)(M < kNumSMs * 16 ? M : kNumSMs * 16);
+    if (rope_cos)
+      attn::attn_bwd_dq_kernel<true><<<g, 256, 0, st>>>(dq_acc, (__nv_bfloat16*)d_dqkv, M, Hq, ldq, T, rope_cos,
+                                                        rope_sin);
+    else
+      attn::attn_bwd_dq_kernel<false><<<g, 256, 0, st>>>(dq_acc, (__nv_bfloat16*)d_dqkv, M, Hq, ldq, T, nullptr,
+                                                         nullptr);
     return check_launch("attn_bwd_dq");
   } else {
     attn::attn_bwd_q_kernel<DH><<<(unsigned)(B * Hq * (T / attn::BQ)), 320, attn::BwdQ<DH>::kSmem, st>>>(tq, tdo,
@@ -1266,4 +1308,32 @@ extern "C" int b2s_attn_bwd(const void* d_qkv, const void* d_o, const void* d_do
   cudaStream_t st = (cudaStream_t)stream;
   return dh == 64 ? attn_bwd_dh<64>(d_qkv, d_o, d_do, d_lse, d_dqkv, d_work, B, T, Hq, Hkv, st)
                   : attn_bwd_dh<128>(d_qkv, d_o, d_do, d_lse, d_dqkv, d_work, B, T, Hq, Hkv, st);
+}
+
+// Backward of attention applied to rotary-embedded q / k (Llama): dq, dk w.r.t. the projection
+// output, i.e. b2s_attn_bwd followed by the inverse rotation of the q and k heads of d_dqkv.
+// dh 64: dq is rotated back inside the dq conversion pass (no extra pass over the q heads) and
+// one b2s_rope launch covers the k heads only; dh 128: b2s_rope over q and k heads.
+extern "C" int b2s_rope(void* d_qkv, int64_t M, int T, int64_t ld, int nheads, int dh, const float* d_cos,
+                        const float* d_sin, int inverse, b2s_stream_t stream);
+extern "C" int b2s_attn_bwd_rope(const void* d_qkv, const void* d_o, const void* d_do, const float* d_lse,
+                                 void* d_dqkv, float* d_work, int B, int T, int Hq, int Hkv, int dh, const float* d_cos,
+                                 const float* d_sin, b2s_stream_t stream) {
+  B2S_REQUIRE(dh == 64 || dh == 128, B2S_EUNSUPPORTED, "attention: head dim %d not implemented (64, 128)", dh);
+  B2S_REQUIRE(T % attn::BQ == 0 && T > 0, B2S_EUNSUPPORTED, "attention: T must be a multiple of 128");
+  B2S_REQUIRE(Hkv > 0 && Hq % Hkv == 0, B2S_EINVAL, "attention: Hq must be a multiple of Hkv");
+  B2S_REQUIRE((int64_t)B * T * Hq < (1LL << 32), B2S_EUNSUPPORTED, "attention: B*T*Hq must be < 2^32");
+  B2S_REQUIRE(d_cos && d_sin && ((uintptr_t)d_cos % 16) == 0 && ((uintptr_t)d_sin % 16) == 0, B2S_EINVAL,
+              "attn_bwd_rope: null / misaligned rotary tables");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t M = (int64_t)B * T, ld = (int64_t)(Hq + 2 * Hkv) * dh;
+  int rc;
+  if (dh == 64) {
+    rc = attn_bwd_dh<64>(d_qkv, d_o, d_do, d_lse, d_dqkv, d_work, B, T, Hq, Hkv, st, d_cos, d_sin);
+    if (rc) return rc;
+    return b2s_rope((__nv_bfloat16*)d_dqkv + (int64_t)Hq * dh, M, T, ld, Hkv, dh, d_cos, d_sin, 1, stream);
+  }
+  rc = attn_bwd_dh<128>(d_qkv, d_o, d_do, d_lse, d_dqkv, d_work, B, T, Hq, Hkv, st);
+  if (rc) return rc;
+  return b2s_rope(d_dqkv, M, T, ld, Hq + Hkv, dh, d_cos, d_sin, 1, stream);
 }

@@ -95,6 +95,12 @@ struct Epi {
   int glu_F;                  // act 3 / 4: the gate / up split F
   float* colsum_part;         // bf16 generic epilogue: per-32-row column sums of the stored C,
                               // [ceil(M/32)][N] fp32 (the bias gradient of a dgrad), or null
+  // act 7 (RoPE on the fused QKV projection, see b2s_gemm_rope): columns [0, rope_cols) are
+  // heads of width rope_dh rotated (rotate-half pairs j, j + dh/2) by the fp32 tables
+  // cos / sin [T, dh/2] at position row % T; the rest (the V heads) is stored as is
+  const float* rope_cos;
+  const float* rope_sin;
+  int rope_T, rope_dh, rope_cols;
 };
 
 __device__ __forceinline__ float silu_sig(float g, float& sg) {
@@ -550,6 +556,71 @@ __global__ void __launch_bounds__(Cfg<BN, CG, EW>::kThreads, 1)
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         continue;
       }
+      if (epi.act == 7) {  // RoPE: a head's two halves (chunks k and k + dh/64) rotated together
+        const int dh = epi.rope_dh, hc = dh / 64;  // chunk pairs per head
+        const int units = BN / dh;
+        const int tpos = rbase % epi.rope_T, rlane = (rbase + lane) % epi.rope_T;
+        (void)tpos;
+#pragma unroll 1
+        for (int u = half; u < units; u += kEG) {
+#pragma unroll 1
+          for (int k = 0; k < hc; ++k) {
+            const int ca = u * (dh / 32) + k, cb = ca + hc;  // TMEM chunks of the pair halves
+            const int col_a = n0 + ca * 32, col_b = n0 + cb * 32;
+            uint32_t ra[32], rb[32];
+            tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + ca * 32, ra);
+            tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + cb * 32, rb);
+            tmem_wait_ld();
+            if (u + kEG >= units && k + 1 == hc) {  // this warp's last chunks read: release the accumulator
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) {
+                if constexpr (CG == 2) mbar_arrive_cluster_relaxed(mapa_shared(smem_u32(&tempty[acc]), 0));
+                else mbar_arrive(&tempty[acc]);
+              }
+            }
+            if (rbase >= M || col_a >= N) continue;
+            float va[32], vb[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {  // what the unfused path stores and the rope kernel re-reads
+              va[i] = __bfloat162float(__float2bfloat16_rn(__uint_as_float(ra[i])));
+              vb[i] = __bfloat162float(__float2bfloat16_rn(__uint_as_float(rb[i])));
+            }
+            if (col_a < epi.rope_cols) {
+              const float* cp = epi.rope_cos + (int64_t)rlane * (dh / 2) + k * 32;
+              const float* sp = epi.rope_sin + (int64_t)rlane * (dh / 2) + k * 32;
+#pragma unroll
+              for (int i4 = 0; i4 < 8; ++i4) {
+                const float4 c4 = __ldg(reinterpret_cast<const float4*>(cp) + i4);
+                const float4 s4 = __ldg(reinterpret_cast<const float4*>(sp) + i4);
+                const float cc[4] = {c4.x, c4.y, c4.z, c4.w}, ss[4] = {s4.x, s4.y, s4.z, s4.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  const int i = 4 * i4 + e;
+                  const float a = va[i], b = vb[i];
+                  va[i] = a * cc[e] - b * ss[e];
+                  vb[i] = b * cc[e] + a * ss[e];
+                }
+              }
+            }
+            const float* outs[2] = {va, vb};
+            const int cols[2] = {col_a, col_b};
+#pragma unroll
+            for (int o = 0; o < 2; ++o) {
+              uint8_t* b = next_slot();
+              stage_bf16(b, lane, outs[o]);
+              fence_proxy_async_smem();
+              __syncwarp();
+              if (lane == 0) {
+                tma_store_2d(&tmC, b, cols[o], rbase);
+                bulk_commit();
+              }
+            }
+          }
+        }
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        continue;
+      }
       if (epi.act == 4) {  // SwiGLU backward: dh chunk (accumulator) -> [dgate | dup] using gu
         const int F = epi.glu_F;
         uint4 gq[4], uq[4];  // this chunk's gate / up rows (64 bytes each per lane)
@@ -969,7 +1040,8 @@ namespace {
 int gemm_run(const void* d_A, int a_mn_major, int64_t lda, const void* d_B, int b_mn_major, int64_t ldb, void* d_C,
              int64_t ldc, int c_f32, int M, int N, int K, int accumulate, const void* d_bias, int act, void* d_aux,
              int64_t ld_aux, int glu_F, int64_t c_width, int64_t aux_width, cudaStream_t st,
-             float* d_colsum_part = nullptr) {
+             float* d_colsum_part = nullptr, const float* rope_cos = nullptr, const float* rope_sin = nullptr,
+             int rope_T = 0, int rope_dh = 0, int rope_cols = 0) {
   using namespace b2s;
   B2S_REQUIRE(M > 0 && N > 0 && K > 0, B2S_EINVAL, "gemm: empty shape %d x %d x %d", M, N, K);
   B2S_REQUIRE(d_A && d_B && d_C, B2S_EINVAL, "gemm: null operand");
@@ -979,14 +1051,15 @@ int gemm_run(const void* d_A, int a_mn_major, int64_t lda, const void* d_B, int 
               B2S_EUNSUPPORTED, "gemm: operands must be 16-byte aligned");
   B2S_REQUIRE((ldc * (c_f32 ? 4 : 2)) % 16 == 0 && N % 8 == 0, B2S_EUNSUPPORTED,
               "gemm: N and ldc must keep output rows 16B aligned");
-  B2S_REQUIRE(act == 0 || (act >= 1 && act <= 6 && d_aux && !c_f32 && (ld_aux * 2) % 16 == 0 &&
-                           ((uintptr_t)d_aux % 16) == 0),
+  B2S_REQUIRE(act == 0 || act == 7 ||
+                  (act >= 1 && act <= 6 && d_aux && !c_f32 && (ld_aux * 2) % 16 == 0 && ((uintptr_t)d_aux % 16) == 0),
               B2S_EINVAL, "gemm: activation epilogue needs an aligned bf16 aux buffer and bf16 output");
-  B2S_REQUIRE(!(accumulate && (act == 1 || act == 3 || act == 4 || act == 5)), B2S_EINVAL,
+  B2S_REQUIRE(!(accumulate && (act == 1 || act == 3 || act == 4 || act == 5 || act == 7)), B2S_EINVAL,
               "gemm: accumulate with a GELU / SwiGLU epilogue is not supported");
   gemm::Choice ch = gemm::choose(M, N, K, accumulate && !d_bias && act == 0);
   if (act == 3) ch = gemm::Choice{256, 2, 1};  // the gate / up interleave needs CTA-pair 256-wide tiles
   if (act == 4) ch.splits = 1;
+  if (act == 7) ch = gemm::Choice{256, 2, 1};  // a 256-wide tile holds whole heads (dh 64 / 128)
   const int bn = ch.bn, bnc = ch.bn / ch.cg;
   CUtensorMap ta, tb, tc, tx;
   int rc;
@@ -1004,9 +1077,9 @@ int gemm_run(const void* d_A, int a_mn_major, int64_t lda, const void* d_B, int 
   else tx = tc;
   if (rc) return rc;
   gemm::Epi e{c_f32, accumulate, (const __nv_bfloat16*)d_bias, act, (const __nv_bfloat16*)d_aux, ld_aux, glu_F,
-              d_colsum_part};
+              d_colsum_part, rope_cos, rope_sin, rope_T, rope_dh, rope_cols};
   const int splits = ch.splits;
-  if (ch.cg == 2 && act != 0 && act != 6)  // activation epilogue: 12 epilogue warps (see EW above);
+  if (ch.cg == 2 && act != 0 && act != 6 && act != 7)  // activation epilogue: 12 epilogue warps (see EW above);
     // the x aux product (act 6) is light enough for 8 warps and the deeper 5-stage mainloop
     return gemm::dispatch<256, 2, 12>(a_mn_major, b_mn_major, ta, tb, tc, tx, M, N, K, splits, e, st);
   if (ch.cg == 2) return gemm::dispatch<256, 2>(a_mn_major, b_mn_major, ta, tb, tc, tx, M, N, K, splits, e, st);
@@ -1049,4 +1122,16 @@ extern "C" int b2s_gemm_swiglu_bwd(const void* d_dy, int64_t ld_dy, const void* 
   B2S_REQUIRE(F > 0 && F % 8 == 0, B2S_EUNSUPPORTED, "gemm_swiglu_bwd: F must be a multiple of 8");
   return gemm_run(d_dy, 0, ld_dy, d_w2, 1, ldw, d_dgu, ld_dgu, 0, M, F, K, 0, nullptr, 4, const_cast<void*>(d_gu),
                   ld_gu, F, 2 * F, 2 * F, (cudaStream_t)stream);
+}
+
+extern "C" int b2s_gemm_rope(const void* d_x, int64_t ldx, const void* d_w, int64_t ldw, void* d_out, int64_t ldo,
+                             int M, int N, int K, const float* d_cos, const float* d_sin, int T, int dh, int rope_cols,
+                             b2s_stream_t stream) {
+  B2S_REQUIRE(dh == 64 || dh == 128, B2S_EUNSUPPORTED, "gemm_rope: head dim must be 64 or 128, got %d", dh);
+  B2S_REQUIRE(N % 256 == 0 && rope_cols % dh == 0 && rope_cols <= N, B2S_EUNSUPPORTED,
+              "gemm_rope: N (%d) must be a multiple of 256 and rope_cols (%d) of dh", N, rope_cols);
+  B2S_REQUIRE(d_cos && d_sin && T > 0 && ((uintptr_t)d_cos % 16) == 0 && ((uintptr_t)d_sin % 16) == 0, B2S_EINVAL,
+              "gemm_rope: null / misaligned tables");
+  return gemm_run(d_x, 0, ldx, d_w, 0, ldw, d_out, ldo, 0, M, N, K, 0, nullptr, 7, nullptr, 0, 0, N, N,
+                  (cudaStream_t)stream, nullptr, d_cos, d_sin, T, dh, rope_cols);
 }

@@ -362,8 +362,11 @@ class DecoderLM(torch.nn.Module):
                 ops.rmsnorm_fwd(S.xa, U.p("attn_norm"), eps, S.ln_a, S.rstd_a)
             else:
                 ops.rmsnorm_fwd_res(pending[0], pending[1], U.p("attn_norm"), eps, S.ln_a, S.rstd_a, S.xa)
-            ops.linear(S.ln_a, U.p("wqkv"), out=S.qkv)
-            ops.rope(S.qkv, T, H + Hkv, dh, *rope)
+            if self.dtype == torch.bfloat16:  # RoPE on q / k in the projection's epilogue
+                ops.linear_rope(S.ln_a, U.p("wqkv"), S.qkv, T, dh, (H + Hkv) * dh, *rope)
+            else:
+                ops.linear(S.ln_a, U.p("wqkv"), out=S.qkv)
+                ops.rope(S.qkv, T, H + Hkv, dh, *rope)
         ops.attn_fwd(S.qkv, B, T, H, Hkv, dh, o=S.o, lse=S.lse)
         # y1 = o @ Wo^T (+ bias); the next norm adds it into the residual: xb = xa + y1
         ops.gemm(S.o, U.p("proj_w" if gpt2 else "wo"), a_mn=False, b_mn=False, M=M, N=d, K=H * dh, out=S.ya,
@@ -478,9 +481,12 @@ class DecoderLM(torch.nn.Module):
             wo = "proj_w" if gpt2 else "wo"
             ops.linear_wgrad(A.dxb, S.o, out=U.g(wo), accumulate=True)
             ops.linear_dgrad(A.dxb, U.p(wo), out=A.do)
-            ops.attn_bwd(S.qkv, S.o, A.do, S.lse, B, T, H, Hkv, dh, dqkv=A.dqkv, work=A.attn_work)
-            if not gpt2:
-                ops.rope(A.dqkv, T, H + Hkv, dh, *rope, inverse=True)
+            if not gpt2 and self.dtype == torch.bfloat16:  # dq / dk rotated back inside (b2s_attn_bwd_rope)
+                ops.attn_bwd(S.qkv, S.o, A.do, S.lse, B, T, H, Hkv, dh, dqkv=A.dqkv, work=A.attn_work, rope=rope)
+            else:
+                ops.attn_bwd(S.qkv, S.o, A.do, S.lse, B, T, H, Hkv, dh, dqkv=A.dqkv, work=A.attn_work)
+                if not gpt2:
+                    ops.rope(A.dqkv, T, H + Hkv, dh, *rope, inverse=True)
             wq = "qkv_w" if gpt2 else "wqkv"
             if gpt2:
                 ops.colsum_accumulate(A.dqkv, U.g("qkv_b"))

@@ -204,6 +204,18 @@ def linear_swiglu(x, w13, gu, h):
     return gu, h
 
 
+def linear_rope(x, w, out, T, dh, rope_cols, cos, sin):
+    """out = x @ w^T with the rotary embedding applied to columns [0, rope_cols) in the epilogue
+    (the Llama QKV projection: q and k heads rotated, v heads as is)."""
+    _dev(x, w, out, cos, sin)
+    M, K = x.shape
+    N = w.shape[0]
+    _timed("gemm", 2.0 * M * N * K, lambda: _call(
+        "b2s_gemm_rope", x.data_ptr(), x.stride(0), w.data_ptr(), w.stride(0), out.data_ptr(), out.stride(0), M, N, K,
+        cos.data_ptr(), sin.data_ptr(), T, dh, rope_cols, _sp()), detail=(M, N, K, "K", "K", "bf16", "", "", "rope"))
+    return out
+
+
 def linear_dgrad_swiglu(dy, w2, gu, dgu):
     """dgu = SwiGLU backward of dh = dy @ w2 (dy [M, d], w2 [d, F]) without materialising dh."""
     _dev(dy, w2, gu, dgu)
@@ -397,12 +409,22 @@ def attn_fwd(qkv, B, T, Hq, Hkv, dh, o=None, lse=None):
     return o, lse
 
 
-def attn_bwd(qkv, o, do, lse, B, T, Hq, Hkv, dh, dqkv=None, work=None):
-    """dq/dk/dv of causal attention, written into a [B*T, (Hq+2Hkv)*dh] buffer."""
+def attn_bwd(qkv, o, do, lse, B, T, Hq, Hkv, dh, dqkv=None, work=None, rope=None):
+    """dq/dk/dv of causal attention, written into a [B*T, (Hq+2Hkv)*dh] buffer.
+
+    rope=(cos, sin) (bf16 path): q / k carried the rotary embedding, so dq and dk are rotated
+    back (the gradient w.r.t. the projection output) by b2s_attn_bwd_rope."""
     dqkv = torch.empty_like(qkv) if dqkv is None else dqkv
     n = _lib.load().b2s_attn_bwd_work_floats(B, T, Hq, dh)
     work = _work(n, qkv.device) if work is None else work
     flops = 10.0 * B * Hq * dh * T * T / 2  # S, dP, dV, dK, dQ over the lower triangle
+    if rope is not None:
+        assert qkv.dtype == torch.bfloat16
+        cos, sin = rope
+        _timed("attn_bwd", flops, lambda: _call("b2s_attn_bwd_rope", qkv.data_ptr(), o.data_ptr(), do.data_ptr(),
+                                                lse.data_ptr(), dqkv.data_ptr(), work.data_ptr(), B, T, Hq, Hkv, dh,
+                                                cos.data_ptr(), sin.data_ptr(), _sp()))
+        return dqkv
     _timed("attn_bwd", flops, lambda: _call("b2s_attn_bwd" + _sfx(qkv), qkv.data_ptr(), o.data_ptr(), do.data_ptr(),
                                             lse.data_ptr(), dqkv.data_ptr(), work.data_ptr(), B, T, Hq, Hkv, dh,
                                             _sp()))

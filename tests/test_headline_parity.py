@@ -308,3 +308,50 @@ def test_two_layer_headline_step_matches_oracle(cuda, tmp_path, name, B, T):
         gg = gpu[key].to(cuda)[: g.shape[0]] if g.dim() else gpu[key].to(cuda)
         cos = torch.nn.functional.cosine_similarity(gg.reshape(-1).double(), g.reshape(-1).double(), dim=0)
         assert cos >= 0.995, (key, float(cos))
+
+
+# ----------------------------------------------------------------------------- fused RoPE
+@pytest.mark.parametrize("name,M,T", [("llama-1b", 4 * 4096, 4096), ("llama-8b", 2 * 4096, 4096),
+                                      ("tiny-llama", 2 * 256, 256)])
+def test_qkv_gemm_rope_epilogue(cuda, name, M, T):
+    """b2s_gemm_rope (RoPE in the QKV GEMM epilogue) == b2s_gemm then b2s_rope, at the step shapes."""
+    from paper_2602_08387_b200 import ops
+    from paper_2602_08387_b200.model import PRESETS, rope_tables
+
+    cfg = PRESETS[name]
+    d, H, Hkv, dh = cfg.d_model, cfg.n_head, cfg.n_kv_head, cfg.head_dim
+    N = cfg.qkv_dim
+    x, w = _rnd((M, d), 21), _rnd((N, d), 22, d ** -0.5)
+    cos, sin = rope_tables(cfg, T, cuda)
+    ref = ops.linear(x, w)
+    ops.rope(ref, T, H + Hkv, dh, cos, sin)
+    out = torch.empty_like(ref)
+    ops.linear_rope(x, w, out, T, dh, (H + Hkv) * dh, cos, sin)
+    # same bf16 input to the same fp32 rotation: equal up to one bf16 rounding of a contraction
+    diff = (out.float() - ref.float()).abs()
+    assert float(diff.max()) <= 2 ** -7 * float(ref.float().abs().max()), float(diff.max())
+    assert float((diff > 0).float().mean()) < 1e-3
+    torch.testing.assert_close(out[:, (H + Hkv) * dh:], ref[:, (H + Hkv) * dh:], rtol=0, atol=0)  # v untouched
+
+
+@pytest.mark.parametrize("B,T,Hq,Hkv,dh", [(1, 4096, 32, 8, 64), (1, 4096, 32, 8, 128), (2, 256, 4, 2, 64)])
+def test_attn_bwd_rope(cuda, B, T, Hq, Hkv, dh):
+    """b2s_attn_bwd_rope == b2s_attn_bwd followed by the inverse rotation of the q and k heads."""
+    from dataclasses import replace as _r
+
+    from paper_2602_08387_b200 import ops
+    from paper_2602_08387_b200.model import PRESETS, rope_tables
+
+    cfg = _r(PRESETS["llama-1b"], d_model=Hq * dh, n_head=Hq, n_kv_head=Hkv)
+    cos, sin = rope_tables(cfg, T, cuda)
+    qkv = _inputs(B, T, Hq, Hkv, dh, "unit", seed=5)
+    o, lse = ops.attn_fwd(qkv, B, T, Hq, Hkv, dh)
+    g = torch.Generator(device="cuda").manual_seed(6)
+    do = torch.randn(B * T, Hq * dh, device="cuda", generator=g).bfloat16()
+    ref = ops.attn_bwd(qkv, o, do, lse, B, T, Hq, Hkv, dh).clone()
+    ops.rope(ref, T, Hq + Hkv, dh, cos, sin, inverse=True)
+    got = ops.attn_bwd(qkv, o, do, lse, B, T, Hq, Hkv, dh, rope=(cos, sin))
+    # dq: the fused path rotates the fp32 accumulator (one bf16 rounding instead of two)
+    scale = float(ref.float().abs().max())
+    assert float((got.float() - ref.float()).abs().max()) <= 2 ** -7 * scale
+    torch.testing.assert_close(got[:, Hq * dh:], ref[:, Hq * dh:], rtol=0, atol=0)  # dk (same kernel), dv
