@@ -583,7 +583,9 @@ __global__ void swiglu_bwd_kernel(const T* __restrict__ gu, const T* __restrict_
 // One block per row of bf16 logits [M, ld] (first V columns valid). Writes
 // loss[m] = logsumexp - logit[target] (fp32) and, in place over the logits,
 // dlogits = (softmax - onehot) * gscale (columns >= V zeroed).
-template <typename T, int U = 1, int U2 = 1>
+// The first pass keeps U row vectors in flight per thread before their exponentials (GPT-2
+// logits: 659 / 665 / 648 / 720 us for U = 1 / 2 / 4 / 8, profiles/r1_xent_smem_ab.jsonl).
+template <typename T, int U = 4>
 __global__ void __launch_bounds__(512) xent_kernel(T* __restrict__ logits, int64_t ld, int V,
                                                    const int64_t* __restrict__ target, float* __restrict__ loss,
                                                    float gscale, int64_t M, int write_grad) {
@@ -637,22 +639,7 @@ __global__ void __launch_bounds__(512) xent_kernel(T* __restrict__ logits, int64
   if (threadIdx.x == 0) loss[m] = lse - xt;
   if (!write_grad) return;
   const float inv = gscale / se;  // softmax * gscale = 2^(y - max) * gscale / sum
-  int j0 = threadIdx.x;
-  if (U2 > 1) {  // U2 row vectors in flight per thread before their exponentials / stores
-    for (; j0 + (U2 - 1) * (int)blockDim.x < nvec; j0 += U2 * blockDim.x) {
-      float f[U2][8];
-#pragma unroll
-      for (int u = 0; u < U2; ++u) ld_v8_cs(row + (int64_t)(j0 + u * blockDim.x) * 8, f[u]);
-#pragma unroll
-      for (int u = 0; u < U2; ++u) {
-        const int i = j0 + u * blockDim.x;
-#pragma unroll
-        for (int t = 0; t < 8; ++t) f[u][t] = ex2f(fmaf(f[u][t], L2E, -mx)) * inv;
-        if ((uint64_t)(tgt - (int64_t)i * 8) < 8) f[u][tgt - (int64_t)i * 8] -= gscale;
-        st_v8_cs(row + (int64_t)i * 8, f[u]);
-      }
-    }
-  }
+  const int j0 = threadIdx.x;
   for (int i = j0; i < nvec; i += blockDim.x) {
     float f[8];
     ld_v8_cs(row + i * 8, f);  // last read of the row (pass 1 left it in L2)
@@ -668,85 +655,6 @@ __global__ void __launch_bounds__(512) xent_kernel(T* __restrict__ logits, int64
   }
 }
 
-// Shared-memory-resident variant for rows of at most kXentSmemMax bytes (GPT-2's
-// 50304-wide bf16 rows: 98.25 KB): the row arrives by kXentChunks cp.async.bulk
-// copies (the max pass starts on the first chunk while the rest land), the sum pass
-// overwrites each logit in shared memory with its bf16 2^(y - max), and the gradient
-// pass scales those -- each logit is read from HBM once and exponentiated once
-// (the two-pass kernel above re-reads the row through L2 and runs ex2 twice per
-// element). Two blocks per SM: one block's loads overlap the other's math and stores.
-constexpr int kXentSmemMax = 110 * 1024, kXentChunks = 4;
-__global__ void __launch_bounds__(512, 2) xent_smem_kernel(__nv_bfloat16* __restrict__ logits, int64_t ld, int V,
-                                                          const int64_t* __restrict__ target,
-                                                          float* __restrict__ loss, float gscale, int write_grad) {
-  constexpr float L2E = 1.4426950408889634f;
-  extern __shared__ __align__(128) uint8_t xrow[];
-  __shared__ float scratch[32];
-  __shared__ uint64_t bar[kXentChunks];
-  const int nvec = V / 8;
-  const int64_t m = blockIdx.x;
-  __nv_bfloat16* row = logits + m * ld;
-  // chunk c covers 16-byte vectors [c * cv, min((c + 1) * cv, ld / 8))
-  const int lv = (int)(ld / 8), cv = (lv + kXentChunks - 1) / kXentChunks;
-  if (threadIdx.x == 0) {
-    for (int c = 0; c < kXentChunks; ++c) sm100::mbar_init(&bar[c], 1);
-    sm100::fence_barrier_init();
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int c = 0; c < kXentChunks; ++c) {
-      const int v0 = c * cv, nv = min(cv, lv - v0);
-      if (nv <= 0) break;
-      sm100::mbar_arrive_expect_tx(&bar[c], (uint32_t)nv * 16);
-      sm100::bulk_load_1d(xrow + (size_t)v0 * 16, row + (int64_t)v0 * 8, (uint32_t)nv * 16, &bar[c]);
-    }
-  }
-  const int64_t tgt = target[m];
-  uint4* sv = reinterpret_cast<uint4*>(xrow);
-  __nv_bfloat16* sh = reinterpret_cast<__nv_bfloat16*>(xrow);
-  float mx = -INFINITY;
-  for (int c = 0; c < kXentChunks; ++c) {
-    const int v0 = c * cv, v1 = min(v0 + cv, nvec);
-    if (v0 >= lv) break;
-    sm100::mbar_wait(&bar[c], 0);
-    for (int i = v0 + threadIdx.x; i < v1; i += 512) {
-      float f[8];
-      unpack8(*reinterpret_cast<const bf16x8*>(&sv[i]), f);
-      mx = fmaxf(mx, fmax3(fmax3(f[0], f[1], f[2]), fmax3(f[3], f[4], f[5]), fmaxf(f[6], f[7])));
-    }
-  }
-  const float xt = to_f(sh[tgt]);
-  const int ct = nvec * 8 + threadIdx.x;  // V - 8 nvec < 8 tail columns: at most one per thread
-  const float tv = ct < V ? to_f(sh[ct]) : -INFINITY;
-  mx = fmaxf(mx, tv);
-  mx = block_max(mx, scratch) * L2E;
-  const float te = ct < V ? ex2f(fmaf(tv, L2E, -mx)) : 0.f;
-  float se = te;
-  for (int i = threadIdx.x; i < nvec; i += 512) {
-    float f[8];
-    unpack8(*reinterpret_cast<const bf16x8*>(&sv[i]), f);
-#pragma unroll
-    for (int t = 0; t < 8; ++t) {
-      f[t] = ex2f(fmaf(f[t], L2E, -mx));
-      se += f[t];
-    }
-    *reinterpret_cast<bf16x8*>(&sv[i]) = pack8(f);  // this thread's own vector: no barrier needed
-  }
-  se = block_sum(se, scratch);
-  if (threadIdx.x == 0) loss[m] = (mx + __log2f(se)) * (1.f / L2E) - xt;
-  if (!write_grad) return;
-  const float inv = gscale / se;
-  for (int i = threadIdx.x; i < nvec; i += 512) {
-    float f[8];
-    unpack8(*reinterpret_cast<const bf16x8*>(&sv[i]), f);
-#pragma unroll
-    for (int t = 0; t < 8; ++t) f[t] *= inv;
-    // the target column from the fp32 exponential (p - 1 cancels when p is near 1)
-    if ((uint64_t)(tgt - (int64_t)i * 8) < 8) f[tgt - (int64_t)i * 8] = ex2f(fmaf(xt, L2E, -mx)) * inv - gscale;
-    st_v8_cs(row + (int64_t)i * 8, f);
-  }
-  for (int c = ct; c < ld; c += 512) from_f(row[c], c < V ? te * inv - (c == tgt ? gscale : 0.f) : 0.f);
-}
 
 // ------------------------------------------------------------------ reductions
 // Deterministic sum of n floats (optionally of squares) into out[0] (overwrite).
@@ -1007,28 +915,7 @@ template <typename T>
 int cross_entropy(void* d_logits, int64_t ld, int V, const int64_t* d_target, float* d_loss_rows,
                   float grad_scale, int64_t M, int write_grad, cudaStream_t st) {
   B2S_REQUIRE(ld % 8 == 0 && V <= ld, B2S_EUNSUPPORTED, "cross_entropy: ld must be a multiple of 8 >= V");
-  // B2S_XENT_SMEM=1: shared-memory-resident single-read kernel for bf16 rows <= 110 KB
-  static const bool smem = getenv("B2S_XENT_SMEM") && atoi(getenv("B2S_XENT_SMEM")) != 0;
-  if (std::is_same<T, __nv_bfloat16>::value && smem && ld * 2 <= ew::kXentSmemMax) {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(ew::xent_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, ew::kXentSmemMax);
-      attr = true;
-    }
-    ew::xent_smem_kernel<<<(unsigned)M, 512, (size_t)ld * 2, st>>>((__nv_bfloat16*)d_logits, ld, V, d_target,
-                                                                   d_loss_rows, grad_scale, write_grad);
-    return check_launch("cross_entropy");
-  }
-  // B2S_XENT_UNROLL = 1 / 2 / 4 / 8: row vectors in flight per thread in the first pass
-  // (GPT-2 logits: 659 / 665 / 648 us for 1 / 2 / 4, profiles/r1_xent_smem_ab.jsonl)
-  static const int un = getenv("B2S_XENT_UNROLL") ? atoi(getenv("B2S_XENT_UNROLL")) : 4;
-  // B2S_XENT_UNROLL2 = 1 / 2 / 4: the same for the gradient pass
-  static const int un2 = getenv("B2S_XENT_UNROLL2") ? atoi(getenv("B2S_XENT_UNROLL2")) : 1;
-  auto kern = un == 8   ? ew::xent_kernel<T, 8>
-              : un == 2 ? ew::xent_kernel<T, 2>
-              : un == 1 ? ew::xent_kernel<T, 1>
-              : un2 == 2 ? ew::xent_kernel<T, 4, 2>
-              : un2 == 4 ? ew::xent_kernel<T, 4, 4> : ew::xent_kernel<T, 4>;
+  auto kern = ew::xent_kernel<T, 4>;
   kern<<<(unsigned)M, 512, 0, st>>>((T*)d_logits, ld, V, d_target, d_loss_rows, grad_scale, M, write_grad);
   return check_launch("cross_entropy");
 }
@@ -1123,10 +1010,10 @@ int b2s_colsum_accumulate(const void* d_x, int x_f32, int64_t M, int N, int64_t 
               ew::kColsumStrips);
   unsigned* arrivals = ew::colsum_slot();
   B2S_REQUIRE(arrivals != nullptr, B2S_ECUDA, "colsum: arrival counter allocation failed");
-  // B2S_COLSUM_BPS (default four) blocks per SM, rounded down so every block is
-  // co-resident in one wave
-  static const int bps = getenv("B2S_COLSUM_BPS") ? atoi(getenv("B2S_COLSUM_BPS")) : 4;
-  int nparts = (bps >= 1 && bps <= 8 ? bps : 4) * kNumSMs / nblk;
+  // about four blocks per SM (2..8 measured: 2-4 best, profiles/r1_colsum_bps_sweep.jsonl). No
+  // block waits on another -- the last block of a column strip to arrive reduces the strip's
+  // partials -- so co-residency is not required
+  int nparts = 4 * kNumSMs / nblk;
   if (nparts > 256) nparts = 256;
   if (nparts < 1) nparts = 1;
   const int rows_per = (int)((M + nparts - 1) / nparts);

@@ -54,6 +54,9 @@ rec("swiglu_bwd 1B", time_it(lambda: ops.swiglu_bwd(gu, dh, dgu)), M * F * 2 * 5
 qkv = torch.randn(M, cfg.qkv_dim, device=dev).bfloat16()
 cos, sin = rope_tables(cfg, 4096, dev)
 nh = cfg.n_head + cfg.n_kv_head
+rec("rope 1B (k heads only, the backward's remaining launch)",
+    time_it(lambda: ops.rope(qkv[:, cfg.n_head * cfg.head_dim:], 4096, cfg.n_kv_head, cfg.head_dim, cos, sin)),
+    M * cfg.n_kv_head * cfg.head_dim * 2 * 2)
 rec("rope 1B (q+k heads)", time_it(lambda: ops.rope(qkv, 4096, nh, cfg.head_dim, cos, sin)),
     M * nh * cfg.head_dim * 2 * 2)
 V = 50257
@@ -61,6 +64,18 @@ logits = torch.randn(16384, 50304, device=dev).bfloat16()
 tgt = torch.randint(0, V, (16384,), device=dev)
 rec("cross_entropy GPT-2", time_it(lambda: ops.cross_entropy(logits, V, tgt, grad_scale=1.0 / 16384)),
     16384 * 50304 * 2 * 3)
+del logits
+V1 = cfg.vocab_size
+logits = torch.randn(16384, cfg.padded_vocab, device=dev).bfloat16()
+tgt = torch.randint(0, V1, (16384,), device=dev)
+rec("cross_entropy Llama-1B", time_it(lambda: ops.cross_entropy(logits, V1, tgt, grad_scale=1.0 / 16384)),
+    16384 * cfg.padded_vocab * 2 * 3)
+del logits
+wte = torch.randn(cfg.padded_vocab, cfg.d_model, device=dev).bfloat16()
+tok = torch.randint(0, V1, (16384,), device=dev)
+xe = torch.empty(16384, cfg.d_model, device=dev)
+rec("embedding_fwd Llama-1B", time_it(lambda: ops.embedding_fwd(tok, wte, None, 4096, out=xe)),
+    16384 * cfg.d_model * (2 + 4))
 n = 124_000_000
 p, m_, v_, gr = (torch.randn(n, device=dev) for _ in range(4))
 pb = torch.empty(n, device=dev, dtype=torch.bfloat16)
