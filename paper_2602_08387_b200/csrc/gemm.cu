@@ -249,7 +249,10 @@ __device__ __forceinline__ void tile_mn(int mn, int num_m, int num_n, int raster
 //   the leader alone issues the MMAs, and commits multicast to both CTAs.
 //   Each CTA's TMEM holds its own 128 x BN half of the accumulator, which its
 //   own epilogue warps drain. Per-SM operand traffic drops by 1/3.
-template <int BN, int CG, bool A_MN, bool B_MN, int EW>
+// SPEC selects a specialised epilogue at compile time (0: the generic bias / GELU / aux-product
+// / column-sum epilogue, 3: SwiGLU forward, 4: SwiGLU backward, 7: RoPE), so each instantiation
+// carries only its own epilogue's registers.
+template <int BN, int CG, bool A_MN, bool B_MN, int EW, int SPEC>
 __global__ void __launch_bounds__(Cfg<BN, CG, EW>::kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmAux,
@@ -351,7 +354,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, EW>::kThreads, 1)
         const int m0 = mi * BM * CG + rank * BM;
         // act 3 (SwiGLU forward, CTA pairs): tile n covers gate rows [128n, 128n+128) (leader)
         // and the matching up rows [F + 128n, ...) (peer), so each accumulator holds both
-        const int n0 = epi.act == 3 ? (rank ? epi.glu_F : 0) + ni * (BN / 2) : ni * BN + rank * BNc;
+        const int n0 = SPEC == 3 ? (rank ? epi.glu_F : 0) + ni * (BN / 2) : ni * BN + rank * BNc;
         const int kb0 = ks * kb_per, kb1 = min(num_kb_all, kb0 + kb_per);
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
@@ -513,7 +516,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, EW>::kThreads, 1)
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const int rbase = m0 + q * 32;
-      if (epi.act == 3) {  // SwiGLU forward: gate chunk c with up chunk c + BN/64 of the same rows
+      if constexpr (SPEC == 3) {  // SwiGLU forward: gate chunk c with up chunk c + BN/64 of the same rows
         const int F = epi.glu_F, h0 = ni * (BN / 2);
 #pragma unroll 1
         for (int c = half; c < BN / 64; c += kEG) {
@@ -556,7 +559,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, EW>::kThreads, 1)
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         continue;
       }
-      if (epi.act == 7) {  // RoPE: a head's two halves (chunks k and k + dh/64) rotated together
+      if constexpr (SPEC == 7) {  // RoPE: a head's two halves (chunks k and k + dh/64) rotated together
         const int dh = epi.rope_dh, hc = dh / 64;  // chunk pairs per head
         const int units = BN / dh;
         const int tpos = rbase % epi.rope_T, rlane = (rbase + lane) % epi.rope_T;
@@ -621,7 +624,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, EW>::kThreads, 1)
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         continue;
       }
-      if (epi.act == 4) {  // SwiGLU backward: dh chunk (accumulator) -> [dgate | dup] using gu
+      if constexpr (SPEC == 4) {  // SwiGLU backward: dh chunk (accumulator) -> [dgate | dup] using gu
         const int F = epi.glu_F;
         uint4 gq[4], uq[4];  // this chunk's gate / up rows (64 bytes each per lane)
         // gate and up 32 x 32 tiles of a chunk land in slots 2, 3 by TMA (zero-filled out of range)
@@ -690,6 +693,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, EW>::kThreads, 1)
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         continue;
       }
+if constexpr (SPEC == 0) {
 #pragma unroll 1
       for (int c = half; c < BN / 32; c += kEG) {
         const int col0 = n0 + c * 32;
@@ -817,6 +821,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, EW>::kThreads, 1)
             *reinterpret_cast<float2*>(epi.colsum_part + (int64_t)(rbase >> 5) * N + col) = make_float2(s0, s1);
         }
       }
+      }
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
     if (lane == 0) bulk_wait_read<0>();
@@ -942,11 +947,11 @@ static int choose_raster(int num_m, int num_n, double a_blk, double b_blk, int s
   return best;
 }
 
-template <int BN, int CG, bool A_MN, bool B_MN, int EW>
+template <int BN, int CG, bool A_MN, bool B_MN, int EW, int SPEC>
 static int launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc,
                   const CUtensorMap& tx, int M, int N, int K, int splits, const Epi& e, cudaStream_t st) {
   using C_ = Cfg<BN, CG, EW>;
-  auto kern = gemm_kernel<BN, CG, A_MN, B_MN, EW>;
+  auto kern = gemm_kernel<BN, CG, A_MN, B_MN, EW, SPEC>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::kSmem);
@@ -985,14 +990,14 @@ static int launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMa
   return check_launch("gemm");
 }
 
-template <int BN, int CG, int EW = 8>
+template <int BN, int CG, int EW = 8, int SPEC = 0>
 static int dispatch(bool amn, bool bmn, const CUtensorMap& ta, const CUtensorMap& tb,
                     const CUtensorMap& tc, const CUtensorMap& tx, int M, int N, int K,
                     int splits, const Epi& e, cudaStream_t st) {
-  if (!amn && !bmn) return launch<BN, CG, false, false, EW>(ta, tb, tc, tx, M, N, K, splits, e, st);
-  if (!amn && bmn) return launch<BN, CG, false, true, EW>(ta, tb, tc, tx, M, N, K, splits, e, st);
-  if (amn && !bmn) return launch<BN, CG, true, false, EW>(ta, tb, tc, tx, M, N, K, splits, e, st);
-  return launch<BN, CG, true, true, EW>(ta, tb, tc, tx, M, N, K, splits, e, st);
+  if (!amn && !bmn) return launch<BN, CG, false, false, EW, SPEC>(ta, tb, tc, tx, M, N, K, splits, e, st);
+  if (!amn && bmn) return launch<BN, CG, false, true, EW, SPEC>(ta, tb, tc, tx, M, N, K, splits, e, st);
+  if (amn && !bmn) return launch<BN, CG, true, false, EW, SPEC>(ta, tb, tc, tx, M, N, K, splits, e, st);
+  return launch<BN, CG, true, true, EW, SPEC>(ta, tb, tc, tx, M, N, K, splits, e, st);
 }
 
 // Tile choice: (BN, CTA group, split-K) maximising filled SM slots in the last
@@ -1058,7 +1063,7 @@ int gemm_run(const void* d_A, int a_mn_major, int64_t lda, const void* d_B, int 
               "gemm: accumulate with a GELU / SwiGLU epilogue is not supported");
   gemm::Choice ch = gemm::choose(M, N, K, accumulate && !d_bias && act == 0);
   if (act == 3) ch = gemm::Choice{256, 2, 1};  // the gate / up interleave needs CTA-pair 256-wide tiles
-  if (act == 4) ch.splits = 1;
+  if (act == 4) ch = gemm::Choice{256, 2, 1};
   if (act == 7) ch = gemm::Choice{256, 2, 1};  // a 256-wide tile holds whole heads (dh 64 / 128)
   const int bn = ch.bn, bnc = ch.bn / ch.cg;
   CUtensorMap ta, tb, tc, tx;
@@ -1079,7 +1084,12 @@ int gemm_run(const void* d_A, int a_mn_major, int64_t lda, const void* d_B, int 
   gemm::Epi e{c_f32, accumulate, (const __nv_bfloat16*)d_bias, act, (const __nv_bfloat16*)d_aux, ld_aux, glu_F,
               d_colsum_part, rope_cos, rope_sin, rope_T, rope_dh, rope_cols};
   const int splits = ch.splits;
-  if (ch.cg == 2 && act != 0 && act != 6 && act != 7)  // activation epilogue: 12 epilogue warps (see EW above);
+  // specialised epilogues: SwiGLU forward (x, W13 both K-major), SwiGLU backward (W2 MN-major),
+  // RoPE (K-major); all on 256-wide CTA-pair tiles
+  if (act == 3) return gemm::launch<256, 2, false, false, 12, 3>(ta, tb, tc, tx, M, N, K, splits, e, st);
+  if (act == 4) return gemm::launch<256, 2, false, true, 12, 4>(ta, tb, tc, tx, M, N, K, splits, e, st);
+  if (act == 7) return gemm::launch<256, 2, false, false, 8, 7>(ta, tb, tc, tx, M, N, K, splits, e, st);
+  if (ch.cg == 2 && act != 0 && act != 6)  // activation epilogue: 12 epilogue warps (see EW above);
     // the x aux product (act 6) is light enough for 8 warps and the deeper 5-stage mainloop
     return gemm::dispatch<256, 2, 12>(a_mn_major, b_mn_major, ta, tb, tc, tx, M, N, K, splits, e, st);
   if (ch.cg == 2) return gemm::dispatch<256, 2>(a_mn_major, b_mn_major, ta, tb, tc, tx, M, N, K, splits, e, st);

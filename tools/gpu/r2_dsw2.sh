@@ -1,0 +1,4 @@
+for i in 1 2; do
+python tools/one_swiglu_bwd.py
+B2S_LIB=paper_2602_08387_b200/csrc/build/var_ew8/libb2s.so python tools/one_swiglu_bwd.py
+done
