@@ -621,6 +621,7 @@ __global__ void __launch_bounds__(256) attn_bwd_dq_kernel(const float* __restric
 // double-buffered in TMEM: the compute warps drain dQ(t-1) (TMA add-reduce
 // into the fp32 accumulator) after publishing P/dS(t).
 constexpr int kBwdThreads = 320;
+constexpr int kBwdGroups = 8;  // (batch, kv head) groups per chunk of the backward grid
 
 // P^T = 2^(s*sl2 - lse2[q]) and the scaled dS^T = P^T (scale dP^T - D'[q]) for
 // 32 query columns of one key row, in place in sv / dv (bit patterns of fp32).
@@ -698,9 +699,18 @@ __global__ void __launch_bounds__(320, 1)
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 18);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // Block order: the (batch, kv head) groups in chunks of kBwdGroups; inside a chunk,
+  // heaviest key tile first (kt = 0 has the most query tiles). A chunk's dQ accumulator rows
+  // (kBwdGroups x T x G heads x dh fp32, 32 MB at the Llama-1B shape) stay in L2 while its
+  // key tiles add into them; all groups at once (134 MB) made every add-reduce a DRAM
+  // read-modify-write (1.6 GB of DRAM traffic per launch).
   const int nbk = p.B * p.Hkv;
-  const int kt = (int)(blockIdx.x / nbk);  // kt = 0 has the most query tiles: launched first
-  const int bk = blockIdx.x % nbk;
+  const int gc = nbk < kBwdGroups ? nbk : kBwdGroups;  // groups per chunk (the last may be smaller)
+  const int chunk = (int)(blockIdx.x / (gc * p.nqt));
+  const int in_chunk = (int)(blockIdx.x - chunk * gc * p.nqt);
+  const int gcur = min(gc, nbk - chunk * gc);  // groups in this chunk
+  const int kt = in_chunk / gcur;
+  const int bk = chunk * gc + in_chunk % gcur;
   const int b = bk / p.Hkv, kvh = bk % p.Hkv;
   const int G = p.Hq / p.Hkv;
   const int nq = p.nqt - kt;  // query tiles i = kt .. nqt-1
