@@ -485,9 +485,9 @@ def main():
     args.seq = T0 if args.seq is None else args.seq
     args.ac = ac0 if args.ac is None else args.ac
     world = int(os.environ.get("WORLD_SIZE", "0"))
-    if world == 0 and args.gpus > 1:
+    if world == 0 and args.gpus > 1 and args.impl == "ours":  # (the CPU reference arm runs on rank 0 only)
         sys.exit(_self_launch(args))
-    if world and world != args.gpus:
+    if world and world != args.gpus and args.impl == "ours":
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU")
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
