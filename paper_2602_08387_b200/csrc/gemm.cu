@@ -256,7 +256,7 @@ template <int BN, int CG, bool A_MN, bool B_MN, int EW, int SPEC>
 __global__ void __launch_bounds__(Cfg<BN, CG, EW>::kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmAux,
-                int M, int N, int K, int splits, int raster, Epi epi, int* __restrict__ sched) {
+                int M, int N, int K, int splits, int raster, int l2hints, Epi epi, int* __restrict__ sched) {
   using C_ = Cfg<BN, CG, EW>;
   constexpr int kEpiWarps = C_::kEpiWarps, kEpiSmem = C_::kEpiSmem;
   constexpr int kEG = kEpiWarps / 4;  // epilogue warps per TMEM lane quarter
@@ -325,6 +325,8 @@ __global__ void __launch_bounds__(Cfg<BN, CG, EW>::kThreads, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
+      // L2 policies of the A / B loads (l2hints: 2 bits per operand, see launch())
+      const uint64_t polA = l2_policy(l2hints & 3), polB = l2_policy((l2hints >> 2) & 3);
       // first tile static (blockIdx), later ones from the counter; the atomic for
       // tile i+1 is issued when tile i starts loading, so its latency is hidden
       const int tstride = gridDim.x / CG;
@@ -364,15 +366,15 @@ __global__ void __launch_bounds__(Cfg<BN, CG, EW>::kThreads, 1)
           if constexpr (CG == 1) {
             if constexpr (A_MN) {
 #pragma unroll
-              for (int j = 0; j < BM / 64; ++j) tma_load_2d(sa + j * (64 * BK * 2), &tmA, &full[stage], m0 + 64 * j, k0);
+              for (int j = 0; j < BM / 64; ++j) tma_load_2d_hint(sa + j * (64 * BK * 2), &tmA, &full[stage], m0 + 64 * j, k0, polA);
             } else {
-              tma_load_2d(sa, &tmA, &full[stage], k0, m0);
+              tma_load_2d_hint(sa, &tmA, &full[stage], k0, m0, polA);
             }
             if constexpr (B_MN) {
 #pragma unroll
-              for (int j = 0; j < BNc / 64; ++j) tma_load_2d(sb + j * (64 * BK * 2), &tmB, &full[stage], n0 + 64 * j, k0);
+              for (int j = 0; j < BNc / 64; ++j) tma_load_2d_hint(sb + j * (64 * BK * 2), &tmB, &full[stage], n0 + 64 * j, k0, polB);
             } else {
-              tma_load_2d(sb, &tmB, &full[stage], k0, n0);
+              tma_load_2d_hint(sb, &tmB, &full[stage], k0, n0, polB);
             }
             mbar_arrive_expect_tx(&full[stage], C_::kStageBytes);
           } else {
@@ -380,15 +382,15 @@ __global__ void __launch_bounds__(Cfg<BN, CG, EW>::kThreads, 1)
             if (leader) mbar_arrive_expect_tx(&full[stage], 2 * C_::kStageBytes);
             if constexpr (A_MN) {
 #pragma unroll
-              for (int j = 0; j < BM / 64; ++j) tma_load_2d_pair(sa + j * (64 * BK * 2), &tmA, bar, m0 + 64 * j, k0);
+              for (int j = 0; j < BM / 64; ++j) tma_load_2d_pair_hint(sa + j * (64 * BK * 2), &tmA, bar, m0 + 64 * j, k0, polA);
             } else {
-              tma_load_2d_pair(sa, &tmA, bar, k0, m0);
+              tma_load_2d_pair_hint(sa, &tmA, bar, k0, m0, polA);
             }
             if constexpr (B_MN) {
 #pragma unroll
-              for (int j = 0; j < BNc / 64; ++j) tma_load_2d_pair(sb + j * (64 * BK * 2), &tmB, bar, n0 + 64 * j, k0);
+              for (int j = 0; j < BNc / 64; ++j) tma_load_2d_pair_hint(sb + j * (64 * BK * 2), &tmB, bar, n0 + 64 * j, k0, polB);
             } else {
-              tma_load_2d_pair(sb, &tmB, bar, k0, n0);
+              tma_load_2d_pair_hint(sb, &tmB, bar, k0, n0, polB);
             }
           }
           if (++stage == C_::kStages) { stage = 0; phase ^= 1; }
@@ -986,7 +988,21 @@ static int launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMa
   if (rs && strcmp(rs, "mfast") == 0) raster = num_m;
   else if (rs && atoi(rs) != 0) raster = atoi(rs) > 0 ? std::min(atoi(rs), num_m) : -std::min(-atoi(rs), num_n);
   else raster = choose_raster(num_m, num_n, BM * CG * kbytes, BN * kbytes, slots);
-  cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, tx, M, N, K, splits, raster, e, sched);
+  // L2 hints for the rasters where one operand is streamed through exactly once and the other
+  // is re-read by every wave: raster 1 (each M block meets all N blocks back to back) streams A
+  // and re-reads B, raster -1 the reverse. The streamed operand is loaded evict_first when the
+  // re-read one is at most 40 MB, so the streamed bytes stop pushing it out (e.g. the long-K
+  // down-projection, whose W2 otherwise returns from DRAM once per wave). (evict_last on the
+  // re-read operand was measured worse: the sticky lines outlive the kernel.)
+  // B2S_GEMM_L2HINT=0 disables them (A/B runs).
+  int l2hints = 0;
+  static const bool hints_on = !(getenv("B2S_GEMM_L2HINT") && atoi(getenv("B2S_GEMM_L2HINT")) == 0);
+  if (hints_on && (long long)num_m * num_n > slots && splits == 1) {
+    const double a_tot = (double)M * K * 2, b_tot = (double)N * K * 2;
+    if (raster == 1 && num_n <= slots && b_tot <= 40e6) l2hints = 1;
+    else if (raster == -1 && num_m <= slots && a_tot <= 40e6) l2hints = 1 << 2;
+  }
+  cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, tx, M, N, K, splits, raster, l2hints, e, sched);
   return check_launch("gemm");
 }
 
