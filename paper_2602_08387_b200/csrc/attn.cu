@@ -104,15 +104,12 @@ __device__ unsigned long long g_trace[kTraceCtas][18][kTraceRecs][2];
 //   MMAs in issue order, so S_t(j+1) overwrites P_t(j) only after PV_t(j) read it).
 // The item's O is normalised by the softmax warps, staged through that item's Q buffer
 // (Q is double-buffered across items) and written by TMA.
-#ifndef B2S_ATTN_FWD64_KVS
-#define B2S_ATTN_FWD64_KVS 4
-#endif
 template <int DH>
 struct Fwd {
   static constexpr bool ALIAS = DH == 128;      // P over S (dh 128: O takes 2 x 128 columns)
   // K / V stages: the K load of block j + KVS waits for both tiles' PV(j); two stages leave it
   // about one softmax period of TMA latency, which is not enough at dh 64 (dh 128 has no room)
-  static constexpr int KVS = DH == 64 ? B2S_ATTN_FWD64_KVS : 2;
+  static constexpr int KVS = DH == 64 ? 4 : 2;
   static constexpr int kThreads = 352;          // TMA, MMA(A), 8 softmax warps, MMA(B)
   static constexpr int kTileQ = BQ * DH * 2;    // Q / K / V tile bytes (DH/64 swizzle atoms)
   static constexpr int OCOL = 256;              // first O column

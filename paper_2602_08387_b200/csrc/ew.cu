@@ -361,10 +361,7 @@ __global__ void __launch_bounds__(256) colsum_kernel(const T* __restrict__ x, in
   if (c < N) {
     // four rows' 16-byte loads issued back to back before they are summed: the
     // loop is latency-bound otherwise (one load in flight per lane)
-#ifndef B2S_COLSUM_U
-#define B2S_COLSUM_U 16
-#endif
-    constexpr int U = B2S_COLSUM_U;
+    constexpr int U = 16;
     int64_t r = r0 + w;
     for (; r + 8 * (U - 1) < r1; r += 8 * U) {
       uint4 q[U];

@@ -849,17 +849,9 @@ if constexpr (SPEC == 0) {
   }
 }
 
-// SMs the persistent GEMM grid may occupy (B2S_GEMM_SMS; default all 148). With
-// collectives overlapping compute (W > 1) leaving a few SMs to NCCL's CTAs keeps a
-// persistent grid from waiting on them.
-static int gemm_sms() {
-  static const int n = [] {
-    const char* e = getenv("B2S_GEMM_SMS");
-    const int v = e ? atoi(e) : kNumSMs;
-    return (v >= 2 && v <= kNumSMs) ? v : kNumSMs;
-  }();
-  return n;
-}
+// SMs the persistent GEMM grid occupies: all of them (reserving some for NCCL's CTAs at W > 1
+// was measured slower; the dynamic tile counter already lets late CTAs take fewer).
+static int gemm_sms() { return kNumSMs; }
 
 // Per-device pool of zeroed scheduler counters {next_tile, ctas_done}; launches
 // rotate through the pool so GEMMs in flight on different streams never share one.
@@ -975,10 +967,8 @@ static int launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMa
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  // B2S_GEMM_STATIC=1: static strided tile schedule (A/B comparisons)
-  static const bool static_sched = getenv("B2S_GEMM_STATIC") && atoi(getenv("B2S_GEMM_STATIC")) != 0;
-  int* sched = static_sched ? nullptr : sched_slot();
-  if (!static_sched && !sched) { set_error("gemm: scheduler counter allocation failed"); return B2S_ECUDA; }
+  int* sched = sched_slot();
+  if (!sched) { set_error("gemm: scheduler counter allocation failed"); return B2S_ECUDA; }
   const int num_m = (M + BM * CG - 1) / (BM * CG), num_n = (N + BN - 1) / BN;
   // B2S_GEMM_RASTER (tests / A-B runs): "mfast" = plain M-fastest order, an integer = that raster
   // (clamped to the tile grid); read per launch like B2S_GEMM_FORCE

@@ -23,7 +23,6 @@ Numerics (``precision``):
 from __future__ import annotations
 
 import math
-import os
 from dataclasses import dataclass, field, replace
 
 import torch
@@ -32,9 +31,6 @@ from . import ops
 
 ALIGN = 64  # parameter offsets inside a flat unit, in elements (128 B of bf16)
 PRECISIONS = {"bf16": torch.bfloat16, "fp32": torch.float32}
-# A/B switches for the fused epilogue variants (default on; "0" selects the older chains)
-_GELU_AUX_GRAD = os.environ.get("B2S_GELU_AUX_GRAD", "1") != "0"
-_FUSED_SWIGLU_BWD = os.environ.get("B2S_SWIGLU_BWD_FUSED", "1") != "0"
 
 
 @dataclass(frozen=True)
@@ -315,7 +311,7 @@ class DecoderLM(torch.nn.Module):
         self.cfg = cfg
         self.precision = precision
         # GELU epilogues: bf16 stores gelu'(z) as the aux (act 5 / 6); fp32 keeps z (act 1 / 2)
-        gd = precision != "fp32" and _GELU_AUX_GRAD
+        gd = precision != "fp32"
         self._act_fwd, self._act_bwd = (5, 6) if gd else (1, 2)
         self.dtype = PRECISIONS[precision]
         self.activation_checkpointing = bool(activation_checkpointing)
@@ -467,7 +463,7 @@ class DecoderLM(torch.nn.Module):
                                   U.g("ln2_g"), U.g("ln2_b"), dxsum=U.g("proj_b"))
             else:
                 ops.linear_wgrad(A.dxb, S.h, out=U.g("w2"), accumulate=True)
-                if self.dtype == torch.bfloat16 and cfg.d_ff % 128 == 0 and _FUSED_SWIGLU_BWD:
+                if self.dtype == torch.bfloat16 and cfg.d_ff % 128 == 0:
                     # dh = dy W2 with the SwiGLU backward in the epilogue (gate / up tiles by TMA):
                     # dh never reaches HBM (0.68 -> 0.61 ms per Llama-1B layer)
                     ops.linear_dgrad_swiglu(A.dxb, U.p("w2"), S.gu, A.dgu)

@@ -97,14 +97,6 @@ class SPMDTrainer:
             return self
         self.rank, self.world, self.local_rank, self.device = init_distributed()
         self.group = dist.group.WORLD if self.world > 1 else None
-        max_ctas = int(os.environ.get("B2S_FSDP_MAX_CTAS", "0"))
-        if self.world > 1 and max_ctas > 0:
-            # FSDP collectives on their own communicator with a bounded number of NCCL CTAs:
-            # they overlap compute, so fewer SMs taken from the GEMMs can beat raw bandwidth
-            opts = dist.ProcessGroupNCCL.Options()
-            opts.config.max_ctas = max_ctas
-            opts.config.min_ctas = 1
-            self.group = dist.new_group(backend="nccl", pg_options=opts)
         cfg = self.model.cfg
         self.params = FlatParams(self.model.units, self.rank, self.world, self.device, self.blocks_per_unit,
                                  dtype=self.model.dtype)
