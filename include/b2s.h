@@ -49,6 +49,13 @@ uint64_t b2s_launch_count(void);
 /* cudaMemsetAsync of `bytes` bytes at device pointer `dst` to `value` on `stream` (a memset
    node, not a kernel: zeroes the gradient / residual-gradient accumulators inside the step). */
 int b2s_memset_async(void* dst, int value, uint64_t bytes, void* stream);
+/* Native CUDA-graph capture of the work issued to `stream` between begin and end (thread-local
+ * capture mode); end instantiates it into *h_exec, launched by b2s_graph_launch and freed by
+ * b2s_graph_destroy. Used for the single-GPU training step. */
+int b2s_graph_capture_begin(void* stream);
+int b2s_graph_capture_end(void* stream, void** h_exec);
+int b2s_graph_launch(void* exec, void* stream);
+int b2s_graph_destroy(void* exec);
 
 /* ------------------------------------------------------------------ */
 /* Packed data path (CFPKD001)                                         */

@@ -42,6 +42,10 @@ _lib = None
 _SIGS = {
     "b2s_abi_version": "",
     "b2s_memset_async": "piup",
+    "b2s_graph_capture_begin": "p",
+    "b2s_graph_capture_end": "pp",
+    "b2s_graph_launch": "pp",
+    "b2s_graph_destroy": "p",
     "b2s_token_width_for_vocab": "up",
     "b2s_sample_count": "ulp",
     "b2s_splitmix64": "uup",

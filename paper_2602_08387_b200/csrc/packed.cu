@@ -127,6 +127,37 @@ int b2s_memset_async(void* dst, int value, uint64_t bytes, void* stream) {
   return B2S_OK;
 }
 
+// Native CUDA-graph capture of a stream's work (the W = 1 training step): the replay is a bare
+// cudaGraphLaunch, so the step's launch list holds only this library's kernels and memsets
+// (torch.cuda.CUDAGraph's replay adds two RNG-offset fill kernels per launch).
+int b2s_graph_capture_begin(void* stream) {
+  const cudaError_t e = cudaStreamBeginCapture((cudaStream_t)stream, cudaStreamCaptureModeThreadLocal);
+  B2S_REQUIRE(e == cudaSuccess, B2S_ECUDA, "cudaStreamBeginCapture: %s", cudaGetErrorString(e));
+  return B2S_OK;
+}
+int b2s_graph_capture_end(void* stream, void** h_exec) {
+  B2S_REQUIRE(h_exec, B2S_EINVAL, "h_exec is null");
+  cudaGraph_t g = nullptr;
+  cudaError_t e = cudaStreamEndCapture((cudaStream_t)stream, &g);
+  B2S_REQUIRE(e == cudaSuccess && g, B2S_ECUDA, "cudaStreamEndCapture: %s", cudaGetErrorString(e));
+  cudaGraphExec_t x = nullptr;
+  e = cudaGraphInstantiate(&x, g, 0);
+  cudaGraphDestroy(g);
+  B2S_REQUIRE(e == cudaSuccess, B2S_ECUDA, "cudaGraphInstantiate: %s", cudaGetErrorString(e));
+  *h_exec = (void*)x;
+  return B2S_OK;
+}
+int b2s_graph_launch(void* exec, void* stream) {
+  B2S_REQUIRE(exec, B2S_EINVAL, "exec is null");
+  const cudaError_t e = cudaGraphLaunch((cudaGraphExec_t)exec, (cudaStream_t)stream);
+  B2S_REQUIRE(e == cudaSuccess, B2S_ECUDA, "cudaGraphLaunch: %s", cudaGetErrorString(e));
+  return B2S_OK;
+}
+int b2s_graph_destroy(void* exec) {
+  if (exec) cudaGraphExecDestroy((cudaGraphExec_t)exec);
+  return B2S_OK;
+}
+
 int b2s_token_width_for_vocab(uint64_t vocab_size, int* h_width) {
   B2S_REQUIRE(h_width, B2S_EINVAL, "h_width is null");
   B2S_REQUIRE(vocab_size >= 1, B2S_EINVAL, "vocab_size must be positive, got %llu",

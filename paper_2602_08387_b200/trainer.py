@@ -72,6 +72,29 @@ atexit.register(release_graphs)
 _GRAPH_MULTI = os.environ.get("B2S_GRAPH_MULTI", "1") == "1"
 
 
+class _NativeGraph:
+    """An instantiated CUDA graph captured through the library's C-ABI (b2s_graph_*): replayed
+    with a bare cudaGraphLaunch, so a W = 1 step launches only b2s kernels and memsets."""
+
+    def __init__(self, exec_handle: int):
+        self.exec = exec_handle
+
+    def replay(self) -> None:
+        from . import _lib
+
+        _lib.call("b2s_graph_launch", self.exec, _lib.stream_ptr())
+
+    def __del__(self):
+        try:
+            from . import _lib
+
+            if self.exec:
+                _lib.load().b2s_graph_destroy(self.exec)
+                self.exec = None
+        except Exception:
+            pass
+
+
 class SPMDTrainer:
     def __init__(self, model: DecoderLM, optimizer, dataloader: PackedDataLoader, steps: int = 20,
                  seed: int = 0, blocks_per_unit: int = 1, init_device: str = "cpu", log_every: int = 0,
@@ -132,16 +155,36 @@ class SPMDTrainer:
             self._gx, self._gy = inputs.clone(), targets.clone()
             n0 = _lib.load().b2s_launch_count()
             g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g):
-                if multi:
+            if multi:
+                with torch.cuda.graph(g):
                     self.engine.in_graph = True
                     ops.zero_(self.engine.P.gall)
-                else:
-                    self.engine.begin_step()
-                self._gloss = self.model.forward_backward(self._gx, self._gy, hooks=self.engine)
-                if multi:
+                    self._gloss = self.model.forward_backward(self._gx, self._gy, hooks=self.engine)
                     self.engine.end_backward()  # joins the comm stream back into the capture
                     self.engine.in_graph = False
+            else:
+                # W = 1: native capture on a side stream (a capture cannot use the legacy default
+                # stream). One eager pass on that stream first fills the per-stream scratch
+                # caches, so nothing is allocated while capturing; the replay's zeroing of the
+                # gradients makes the pass harmless.
+                import ctypes
+
+                cur = torch.cuda.current_stream()
+                cs = self._cap_stream = getattr(self, "_cap_stream", None) or torch.cuda.Stream()
+                cs.wait_stream(cur)
+                handle = (ctypes.c_void_p * 1)()
+                with torch.cuda.stream(cs):
+                    self.engine.begin_step()
+                    self.model.forward_backward(self._gx, self._gy, hooks=self.engine)
+                    n0 = _lib.load().b2s_launch_count()
+                    _lib.call("b2s_graph_capture_begin", cs.cuda_stream)
+                    try:
+                        self.engine.begin_step()
+                        self._gloss = self.model.forward_backward(self._gx, self._gy, hooks=self.engine)
+                    finally:
+                        _lib.call("b2s_graph_capture_end", cs.cuda_stream, ctypes.addressof(handle))
+                cur.wait_stream(cs)
+                g = _NativeGraph(handle[0])
             self._graph_launches = int(_lib.load().b2s_launch_count() - n0)
             _lib.count_replayed_launches(-self._graph_launches)  # capture launched nothing
             self._graph = g
