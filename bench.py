@@ -295,11 +295,7 @@ def run_ours(args):
         "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (uniform token ids, CFPKD001 packed file); "
                                                           "random-init weights",
-        "config": {"workload": f"{args.config} FSDP training step (fwd+bwd+AdamW), seq {T}, "
-                               f"{B} seqs/GPU", "model": args.config, "global_batch": world * B, "seq_len": T,
-                   "parallelism": f"fsdp{world}", "blocks_per_unit": args.blocks_per_unit,
-                   "activation_checkpointing": args.ac,
-                   "l2": "working set (weights + activations) >> 126 MB L2; no explicit flush"},
+        "config": workload_config(args, world),
         "tokens_per_sec_per_gpu": round(per_gpu, 1),
         "mfu": round(mfu, 4),
         "mfu_vs_sustained_peak": round(per_gpu * fpt / (peaks["bf16_sust"] * 1e12), 4),
@@ -338,6 +334,15 @@ def run_ours(args):
 # CPU sample per reference step: (sequences, tokens) sized so one oracle step takes a few
 # seconds on the GPU box's host cores (the full 1B step at 1 x 4096 tokens takes ~40 s there)
 REF_SAMPLE = {"tiny-gpt2": (8, 256), "gpt2-124m": (1, 2048), "llama-1b": (1, 512), "llama-8b": None}
+
+
+def workload_config(args, world):
+    """The bench line's `config` (both arms: the reference arm times a CPU sample of this workload)."""
+    return {"workload": f"{args.config} FSDP training step (fwd+bwd+AdamW), seq {args.seq}, {args.batch} seqs/GPU",
+            "model": args.config, "global_batch": world * args.batch, "seq_len": args.seq,
+            "parallelism": f"fsdp{world}", "blocks_per_unit": args.blocks_per_unit,
+            "activation_checkpointing": args.ac,
+            "l2": "working set (weights + activations) >> 126 MB L2; no explicit flush"}
 
 
 def _oracle_step_timer(cfg, T, B, steps, warmup):
@@ -423,7 +428,7 @@ def run_reference(args):
         return {"impl": "reference", "unavailable": f"{args.config}: the fp32 CPU oracle needs ~130 GB of host "
                                                       "memory for its parameters and AdamW state"}
     Bs, Ts = smp[0], min(args.seq, smp[1])
-    warm = min(args.warmup, 1)  # CPU steps take seconds; one warm-up allocates the AdamW state
+    warm = args.warmup  # the same K / W as our arm (a step is a few seconds here)
     tps, threads, dt = _oracle_step_timer(cfg, Ts, Bs, args.steps, warm)
     sample = (f"{args.steps} steps of {Bs} x {Ts} tokens after {warm} warm-up, full {cfg.n_layer}-layer "
               f"{args.config} fp32 step (fwd+bwd+clip+AdamW) on the host cores; the reference has no training "
@@ -435,9 +440,7 @@ def run_reference(args):
             "steps": args.steps, "warmup": warm, "ms_per_step": round(dt * 1000 / args.steps, 1),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic token ids; random-init weights", "impl": "reference",
-            "config": {"workload": f"{args.config} FSDP training step (fwd+bwd+AdamW), seq {args.seq}, "
-                                   f"{args.batch} seqs/GPU (CPU sample {Bs} x {Ts})",
-                       "model": args.config, "global_batch": Bs, "seq_len": Ts, "parallelism": "cpu"},
+            "config": workload_config(args, int(os.environ.get("WORLD_SIZE", 1))),
             "cpu_baseline": {"value": round(tps, 2), "unit": UNIT, "cores": threads, "kind": "port",
                              "sample": sample},
             "e2e": {"value": round(tps, 2), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
