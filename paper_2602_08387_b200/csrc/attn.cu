@@ -655,10 +655,14 @@ struct Bwd {
   // P^T in TMEM columns [448, 512) (freed by a single dQ buffer): no P^T shared-memory
   // stores and no A-operand smem reads for dV -- the kernel is smem-bandwidth bound
   static constexpr bool PT = DQ;
-  static constexpr int QS = DH == 64 ? 2 : 1; // Q / dO stages
+  // Q / dO stages. A stage is freed when step t's dV / dK / dQ MMAs retire and its next
+  // TMA load takes ~1700 clk (L2 / DRAM) -- longer than a step -- so dh 64 keeps two loads in
+  // flight ahead of the step being computed (three stages; two left S(t+1) waiting on its Q).
+  static constexpr int QS = DH == 64 ? 3 : 1;
+  static constexpr int LS = 4;  // lse / D stages (512 B each, loaded LS - 1 steps ahead)
   static constexpr int kTileQ = BQ * DH * 2;
   static constexpr int kSmem = 1024 + 2 * kTileQ /*K,V*/ + 2 * QS * kTileQ /*Q,dO*/ + (PT ? 1 : 2) * kPBuf /*P^T,dS^T*/ +
-                               (DQ ? 2 * kTile : 0) /*dQ fp32 staging: 8 warps x 4 KB*/ + 4 * BQ * 4 /*LSE, D x2*/ +
+                               (DQ ? 2 * kTile : 0) /*dQ fp32 staging: 8 warps x 4 KB*/ + 2 * LS * BQ * 4 /*LSE, D*/ +
                                256;
   static_assert(kSmem <= 232448, "backward tiles exceed shared memory");
 };
@@ -668,7 +672,7 @@ __global__ void __launch_bounds__(320, 1)
     attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
                     const __grid_constant__ CUtensorMap tm_dq, const __grid_constant__ CUtensorMap tm_dkv, Params p) {
   using C = Bwd<DH>;
-  constexpr int kTQ = C::kTileQ, QS = C::QS, NA = DH / 64;
+  constexpr int kTQ = C::kTileQ, QS = C::QS, LS = C::LS, NA = DH / 64;
   constexpr bool DQ = C::DQ, PT = C::PT;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sK = align1024(smem_raw);
@@ -678,24 +682,27 @@ __global__ void __launch_bounds__(320, 1)
   uint8_t* sP = sdO + QS * kTQ;      // P^T  [128 keys][128 q] as two 64-column atoms (smem P only)
   uint8_t* sdS = sP + (PT ? 0 : kPBuf);  // dS^T
   uint8_t* sdQ = sdS + kPBuf;        // fp32 128 x 64 as two 32-column boxes (16 KB each), dh 64 only
-  float* sLse = reinterpret_cast<float*>(sdQ + (DQ ? 2 * kTile : 0));  // [2][128] natural-log LSE (TMA bulk)
-  float* sD = sLse + 2 * BQ;                                 // [2][128] rowsum(dO*O)
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sD + 2 * BQ);
+  float* sLse = reinterpret_cast<float*>(sdQ + (DQ ? 2 * kTile : 0));  // [LS][128] natural-log LSE (TMA bulk)
+  float* sD = sLse + LS * BQ;                                // [LS][128] rowsum(dO*O)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sD + LS * BQ);
   uint64_t* kv_full = bars;
-  uint64_t* qd_full = bars + 1;   // [2]
-  uint64_t* qd_empty = bars + 3;  // [2]
-  uint64_t* st_full = bars + 5;
-  uint64_t* st_empty = bars + 6;
-  uint64_t* pds_full = bars + 7;
-  uint64_t* pds_empty = bars + 8;
-  uint64_t* dq_full = bars + 9;   // [2]
-  uint64_t* dq_empty = bars + 11; // [2]
-  uint64_t* done = bars + 13;
-  uint64_t* st_ld_full = bars + 14;   // [2] lse / D of a step landed
-  uint64_t* st_ld_empty = bars + 16;  // [2] all compute warps done with them
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 18);
+  uint64_t* qd_full = bars + 1;        // [QS]
+  uint64_t* qd_empty = qd_full + QS;   // [QS]
+  uint64_t* st_full = qd_empty + QS;
+  uint64_t* st_empty = st_full + 1;
+  uint64_t* pds_full = st_full + 2;
+  uint64_t* pds_empty = st_full + 3;
+  uint64_t* dq_full = st_full + 4;     // [2]
+  uint64_t* dq_empty = dq_full + 2;    // [2]
+  uint64_t* done = dq_empty + 2;
+  uint64_t* st_ld_full = done + 1;         // [LS] lse / D of a step landed
+  uint64_t* st_ld_empty = st_ld_full + LS; // [LS] all compute warps done with them
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(st_ld_empty + LS);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#ifdef B2S_ATTN_TRACE
+  int tr_n = 0;
+#endif
   // Block order: the (batch, kv head) groups in chunks of kBwdGroups; inside a chunk,
   // heaviest key tile first (kt = 0 has the most query tiles). A chunk's dQ accumulator rows
   // (kBwdGroups x T x G heads x dh fp32, 32 MB at the Llama-1B shape) stay in L2 while its
@@ -718,15 +725,14 @@ __global__ void __launch_bounds__(320, 1)
     tma_prefetch(&tm_qkv);
     tma_prefetch(&tm_do);
     mbar_init(kv_full, 1);
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(&qd_full[s], 1); mbar_init(&qd_empty[s], 1); mbar_init(&dq_full[s], 1); mbar_init(&dq_empty[s], 8);
-    }
+    for (int s = 0; s < QS; ++s) { mbar_init(&qd_full[s], 1); mbar_init(&qd_empty[s], 1); }
+    for (int s = 0; s < 2; ++s) { mbar_init(&dq_full[s], 1); mbar_init(&dq_empty[s], 8); }
     mbar_init(st_full, 1);
     mbar_init(st_empty, 8);
     mbar_init(pds_full, 8);
     mbar_init(pds_empty, 1);
     mbar_init(done, 1);
-    for (int s = 0; s < 2; ++s) { mbar_init(&st_ld_full[s], 1); mbar_init(&st_ld_empty[s], 8); }
+    for (int s = 0; s < LS; ++s) { mbar_init(&st_ld_full[s], 1); mbar_init(&st_ld_empty[s], 8); }
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<512>(tslot);
@@ -750,14 +756,15 @@ __global__ void __launch_bounds__(320, 1)
       }
       for (int t = 0; t < nsteps; ++t) {
         const int h = kvh * G + t / nq, i = kt + t % nq;
-        const int s = t & 1;
-        mbar_wait(&st_ld_empty[s], ((t >> 1) & 1) ^ 1);
+        const int s = t % LS;
+        mbar_wait(&st_ld_empty[s], ((t / LS) & 1) ^ 1);
         const size_t off = ((size_t)b * p.Hq + h) * p.T + (size_t)i * BQ;
         mbar_arrive_expect_tx(&st_ld_full[s], 2 * BQ * 4);
         bulk_load_1d(sLse + s * BQ, p.lse + off, BQ * 4, &st_ld_full[s]);
         bulk_load_1d(sD + s * BQ, p.dsum + off, BQ * 4, &st_ld_full[s]);
         const int qs = t % QS;
         mbar_wait(&qd_empty[qs], ((t / QS) & 1) ^ 1);
+        TRACE(70, t);
         mbar_arrive_expect_tx(&qd_full[qs], 2 * kTQ);
         for (int a = 0; a < NA; ++a) {
           tma_load_2d(sQ + qs * kTQ + a * kTile, &tm_qkv, &qd_full[qs], h * DH + a * 64, b * p.T + i * BQ);
@@ -776,7 +783,9 @@ __global__ void __launch_bounds__(320, 1)
       auto issue_S = [&](int t) {
         const int qs = t % QS;
         mbar_wait(&qd_full[qs], (t / QS) & 1);
+        TRACE(71, t);
         if (t > 0) mbar_wait(st_empty, (t - 1) & 1);
+        TRACE(72, t);
         tc_fence_after();
         const uint32_t q_ = aQ + qs * kTQ, do_ = adO + qs * kTQ;
 #pragma unroll
@@ -790,6 +799,7 @@ __global__ void __launch_bounds__(320, 1)
           mma_bf16_ss_w(tdP, make_sdesc(aV + ko, 16, 1024), make_sdesc(do_ + ko, 16, 1024), idSS, kk > 0);
         }
         mma_commit_w(st_full);
+        TRACE(50, t);
       };
       mbar_wait(kv_full, 0);
       issue_S(0);
@@ -797,8 +807,9 @@ __global__ void __launch_bounds__(320, 1)
         const int qs = t % QS;
         const uint32_t q_ = aQ + qs * kTQ, do_ = adO + qs * kTQ;
         // with a single Q / dO stage, S(t+1) needs this step's dV / dK MMAs to have read Q(t) / dO(t)
-        if (QS == 2 && t + 1 < nsteps) issue_S(t + 1);
+        if (QS >= 2 && t + 1 < nsteps) issue_S(t + 1);
         mbar_wait(pds_full, t & 1);
+        TRACE(51, t);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < BQ / 16; ++kk) {
@@ -818,6 +829,7 @@ __global__ void __launch_bounds__(320, 1)
             mma_bf16_ss_w(tdQ + dq_buf(t) * DH, make_sdesc(adS + kk * 2048, kTile, 1024),
                           make_sdesc(aK + kk * 2048, kTile, 1024), idMM, kk > 0);
         }
+        TRACE(52, t);
         mma_commit_w(&qd_empty[qs]);
         mma_commit_w(pds_empty);
         if constexpr (DQ) mma_commit_w(&dq_full[dq_buf(t)]);
@@ -840,6 +852,7 @@ __global__ void __launch_bounds__(320, 1)
       if constexpr (!DQ) return;
       const int h = kvh * G + t / nq, i = kt + t % nq;
       mbar_wait(&dq_full[dq_buf(t)], dq_use(t) & 1);
+      TRACE(67, t);
       tc_fence_after();
       uint32_t qv[32];
       tmem_ld32(tdQ + lrow + dq_buf(t) * DH + half * 32, qv);
@@ -866,18 +879,23 @@ __global__ void __launch_bounds__(320, 1)
     for (int t = 0; t < nsteps; ++t) {
       const int i = kt + t % nq;
       const bool diag = (i == kt);
-      mbar_wait(&st_ld_full[t & 1], (t >> 1) & 1);
-      const float* lse2 = sLse + (t & 1) * BQ;  // natural log; p_ds folds in log2(e)
-      const float* dd = sD + (t & 1) * BQ;
+      mbar_wait(&st_ld_full[t % LS], (t / LS) & 1);
+      const float* lse2 = sLse + (t % LS) * BQ;  // natural log; p_ds folds in log2(e)
+      const float* dd = sD + (t % LS) * BQ;
       mbar_wait(st_full, t & 1);
+      TRACE(60, t);
       tc_fence_after();
-      // 168 registers per thread (3 warps on some SMSPs): two 32-column passes
+      // Two 32-column passes. Both passes' S^T / dP^T are read from TMEM (and st_empty released,
+      // so S(t+1) / dP(t+1) can start) before waiting for step t-1's MMAs to free P^T / dS^T:
+      // the packed bf16 results wait in registers.
+      uint32_t pw[2][16], zw[2][16];
 #pragma unroll
       for (int qq = 0; qq < 2; ++qq) {
-        uint32_t sv[32], dv[32], pt[16];
+        uint32_t sv[32], dv[32];
         tmem_ld32(tS + lrow + half * 64 + qq * 32, sv);
         tmem_ld32(tdP + lrow + half * 64 + qq * 32, dv);
         tmem_wait_ld();
+        TRACE(61 + 3 * qq, t);
         if (qq == 1) {
           tc_fence_before();
           __syncwarp();
@@ -885,27 +903,27 @@ __global__ void __launch_bounds__(320, 1)
         }
         if (diag) p_ds<true>(sv, dv, half * 64 + qq * 32, r, p.scale_log2, p.scale, lse2, dd);
         else p_ds<false>(sv, dv, half * 64 + qq * 32, r, p.scale_log2, p.scale, lse2, dd);
-        if (qq == 0 && t > 0) mbar_wait(pds_empty, (t - 1) & 1);  // step t-1's MMAs released sP / sdS
+        TRACE(62 + 3 * qq, t);
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          pw[qq][k] = pack_bf16x2(__uint_as_float(sv[2 * k]), __uint_as_float(sv[2 * k + 1]));
+          zw[qq][k] = pack_bf16x2(__uint_as_float(dv[2 * k]), __uint_as_float(dv[2 * k + 1]));
+        }
+      }
+      if (t > 0) mbar_wait(pds_empty, (t - 1) & 1);  // step t-1's MMAs released P^T / dS^T
+      TRACE(63, t);
+#pragma unroll
+      for (int qq = 0; qq < 2; ++qq) {
 #pragma unroll
         for (int k8 = 0; k8 < 4; ++k8) {
-          uint4 w, z;
-          w.x = pack_bf16x2(__uint_as_float(sv[8 * k8 + 0]), __uint_as_float(sv[8 * k8 + 1]));
-          w.y = pack_bf16x2(__uint_as_float(sv[8 * k8 + 2]), __uint_as_float(sv[8 * k8 + 3]));
-          w.z = pack_bf16x2(__uint_as_float(sv[8 * k8 + 4]), __uint_as_float(sv[8 * k8 + 5]));
-          w.w = pack_bf16x2(__uint_as_float(sv[8 * k8 + 6]), __uint_as_float(sv[8 * k8 + 7]));
-          z.x = pack_bf16x2(__uint_as_float(dv[8 * k8 + 0]), __uint_as_float(dv[8 * k8 + 1]));
-          z.y = pack_bf16x2(__uint_as_float(dv[8 * k8 + 2]), __uint_as_float(dv[8 * k8 + 3]));
-          z.z = pack_bf16x2(__uint_as_float(dv[8 * k8 + 4]), __uint_as_float(dv[8 * k8 + 5]));
-          z.w = pack_bf16x2(__uint_as_float(dv[8 * k8 + 6]), __uint_as_float(dv[8 * k8 + 7]));
           const uint32_t off = half * kTile + swz(r, qq * 4 + k8);
-          if constexpr (PT) {
-            pt[4 * k8 + 0] = w.x; pt[4 * k8 + 1] = w.y; pt[4 * k8 + 2] = w.z; pt[4 * k8 + 3] = w.w;
-          } else {
-            *reinterpret_cast<uint4*>(sP + off) = w;
-          }
-          *reinterpret_cast<uint4*>(sdS + off) = z;
+          if constexpr (!PT)
+            *reinterpret_cast<uint4*>(sP + off) =
+                make_uint4(pw[qq][4 * k8], pw[qq][4 * k8 + 1], pw[qq][4 * k8 + 2], pw[qq][4 * k8 + 3]);
+          *reinterpret_cast<uint4*>(sdS + off) =
+              make_uint4(zw[qq][4 * k8], zw[qq][4 * k8 + 1], zw[qq][4 * k8 + 2], zw[qq][4 * k8 + 3]);
         }
-        if constexpr (PT) tmem_st16(tPT + lrow + half * 32 + qq * 16, pt);
+        if constexpr (PT) tmem_st16(tPT + lrow + half * 32 + qq * 16, pw[qq]);
       }
       if constexpr (PT) {
         tmem_wait_st();  // P^T is in TMEM before the MMA warp is told
@@ -915,9 +933,11 @@ __global__ void __launch_bounds__(320, 1)
       __syncwarp();
       if (lane == 0) {
         mbar_arrive(pds_full);
-        mbar_arrive(&st_ld_empty[t & 1]);
+        mbar_arrive(&st_ld_empty[t % LS]);
       }
+      TRACE(66, t);
       if (t > 0) drain_dq(t - 1);
+      TRACE(68, t);
     }
     if (nsteps > 0) drain_dq(nsteps - 1);
     if (DQ && lane == 0) bulk_wait_read<0>();  // this warp's add-reduces have read their staging smem (kernel exit orders their writes)

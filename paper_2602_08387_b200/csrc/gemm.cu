@@ -177,7 +177,8 @@ template <int BN, int CG, int EW = 8>
 struct Cfg {
   static constexpr int kEpiWarps = EW;
   static constexpr int kThreads = 64 + 32 * EW;
-  static constexpr int kEpiSmem = kEpiWarps * 2 * kStageSlot;
+  static constexpr int kRing = 2 * kStageSlot;  // per-warp staging ring
+  static constexpr int kEpiSmem = kEpiWarps * kRing;
   static constexpr int kABytes = BM * BK * 2;          // this CTA's 128 rows of A
   static constexpr int kBBytes = (BN / CG) * BK * 2;   // this CTA's share of B's BN rows
   static constexpr int kStageBytes = kABytes + kBBytes;
@@ -445,7 +446,9 @@ __global__ void __launch_bounds__(Cfg<BN, CG, EW>::kThreads, 1)
     // ------------------------------------------------ epilogue warps 2..9
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int half = (warp - 2) >> 2;  // this warp owns chunks half, half + kEG, ... of each tile
-    uint8_t* ring = epi_smem + (warp - 2) * 2 * kStageSlot;
+    uint8_t* ring = epi_smem + (warp - 2) * C_::kRing;
+    // L2 policies of the C stores and the aux loads / stores (l2hints bits 4-5, 6-7; see launch())
+    const uint64_t polC = l2_policy((l2hints >> 4) & 3), polX = l2_policy((l2hints >> 6) & 3);
     int slot = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -489,7 +492,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, EW>::kThreads, 1)
       const int s_ = aux_issued & 1;
       if (lane == 0) {  // out-of-range rows / columns are zero-filled and still counted
         mbar_arrive_expect_tx(&abar[s_], 32 * 32 * 2);
-        tma_load_2d(ring + (2 + s_) * (kStageSlot / 2), &tmAux, &abar[s_], col, row0);
+        tma_load_2d_hint(ring + (2 + s_) * (kStageSlot / 2), &tmAux, &abar[s_], col, row0, polX);
       }
       ++aux_issued;
     };
@@ -553,7 +556,8 @@ __global__ void __launch_bounds__(Cfg<BN, CG, EW>::kThreads, 1)
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
-              tma_store_2d(o == 2 ? &tmAux : &tmC, b, cols[o], rbase);
+              if (o == 2) tma_store_2d_hint(&tmAux, b, cols[o], rbase, polX);
+              else tma_store_2d_hint(&tmC, b, cols[o], rbase, polC);
               bulk_commit();
             }
           }
@@ -617,7 +621,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, EW>::kThreads, 1)
               fence_proxy_async_smem();
               __syncwarp();
               if (lane == 0) {
-                tma_store_2d(&tmC, b, cols[o], rbase);
+                tma_store_2d_hint(&tmC, b, cols[o], rbase, polC);
                 bulk_commit();
               }
             }
@@ -633,8 +637,8 @@ __global__ void __launch_bounds__(Cfg<BN, CG, EW>::kThreads, 1)
         auto load_gu = [&](int col) {
           if (lane == 0) {
             mbar_arrive_expect_tx(&abar[0], 2 * 32 * 32 * 2);
-            tma_load_2d(ring + 2 * (kStageSlot / 2), &tmAux, &abar[0], col, rbase);
-            tma_load_2d(ring + 3 * (kStageSlot / 2), &tmAux, &abar[0], col + F, rbase);
+            tma_load_2d_hint(ring + 2 * (kStageSlot / 2), &tmAux, &abar[0], col, rbase, polX);
+            tma_load_2d_hint(ring + 3 * (kStageSlot / 2), &tmAux, &abar[0], col + F, rbase, polX);
           }
         };
         load_gu(n0 + half * 32);
@@ -687,7 +691,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, EW>::kThreads, 1)
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
-              tma_store_2d(&tmC, b, col0 + o * F, rbase);
+              tma_store_2d_hint(&tmC, b, col0 + o * F, rbase, polC);
               bulk_commit();
             }
           }
@@ -746,7 +750,7 @@ if constexpr (SPEC == 0) {
           stage_bf16(b, lane, v);
           fence_proxy_async_smem();
           __syncwarp();
-          if (lane == 0) { tma_store_2d(&tmAux, b, col0, rbase); bulk_commit(); }
+          if (lane == 0) { tma_store_2d_hint(&tmAux, b, col0, rbase, polX); bulk_commit(); }
 #pragma unroll
           for (int i = 0; i < 32; i += 2) {  // GELU of the bf16-rounded pre-activation (what the backward sees)
             const float2 g = gelu_tanh2(__bfloat162float(__float2bfloat16_rn(v[i])),
@@ -767,7 +771,7 @@ if constexpr (SPEC == 0) {
           stage_bf16_packed(b, lane, dg);
           fence_proxy_async_smem();
           __syncwarp();
-          if (lane == 0) { tma_store_2d(&tmAux, b, col0, rbase); bulk_commit(); }
+          if (lane == 0) { tma_store_2d_hint(&tmAux, b, col0, rbase, polX); bulk_commit(); }
         } else if (epi.act == 6) {  // x aux (gelu' stored by the act-5 forward)
           take_aux(true);
           if (c + 2 * kEG < BN / 32) load_aux(tile, c + 2 * kEG);  // two chunks ahead (both slots busy)
@@ -800,7 +804,7 @@ if constexpr (SPEC == 0) {
         __syncwarp();
         if (lane == 0) {
           if (epi.accumulate) tma_reduce_add_2d(&tmC, b, col0, rbase);
-          else tma_store_2d(&tmC, b, col0, rbase);
+          else tma_store_2d_hint(&tmC, b, col0, rbase, polC);
           bulk_commit();
         }
         if (epi.colsum_part && !epi.out_f32) {
@@ -991,6 +995,18 @@ static int launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMa
     const double a_tot = (double)M * K * 2, b_tot = (double)N * K * 2;
     if (raster == 1 && num_n <= slots && b_tot <= 40e6) l2hints = 1;
     else if (raster == -1 && num_m <= slots && a_tot <= 40e6) l2hints = 1 << 2;
+  }
+  // Epilogue streams written or read exactly once, evict_first so they stop displacing the
+  // mainloop's re-read operand blocks: the saved activations (SwiGLU gate|up, GELU
+  // pre-activation / gelu'), the aux inputs of the backward epilogues, dgu, and C when it is
+  // far larger than L2 (the LM-head logits). Measured on the Llama-1B SwiGLU backward:
+  // 521 -> 483 us. B2S_GEMM_EPI_HINT=0 disables them (A/B runs).
+  static const bool epi_hints_on = !(getenv("B2S_GEMM_EPI_HINT") && atoi(getenv("B2S_GEMM_EPI_HINT")) == 0);
+  if (epi_hints_on) {
+    const double c_bytes = (double)M * N * (e.out_f32 ? 4 : 2);
+    const bool c_stream = e.act == 3 || e.act == 4 || (!e.accumulate && c_bytes >= 512e6);
+    const bool x_stream = e.act == 1 || e.act == 2 || e.act == 4 || e.act == 5 || e.act == 6;
+    l2hints |= (c_stream ? 1 << 4 : 0) | (x_stream ? 1 << 6 : 0);
   }
   cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, tx, M, N, K, splits, raster, l2hints, e, sched);
   return check_launch("gemm");
