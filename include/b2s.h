@@ -148,7 +148,9 @@ int b2s_unpack_windows(const void* d_windows, int width, int batch, int64_t seq_
 /* C[M,N] = epi( sum_k A(m,k) B(n,k) ), bf16 operands, fp32 accumulation.
  * A: a_mn_major=0 -> row-major [M][lda] (K contiguous); 1 -> [K][lda] (M contiguous).
  * B: b_mn_major=0 -> row-major [N][ldb];                 1 -> [K][ldb] (N contiguous).
- * C: row-major [M][ldc], fp32 if c_f32 else bf16; accumulate!=0 adds into C.
+ * C: row-major [M][ldc], fp32 if c_f32 else bf16; accumulate=1 adds into C; accumulate=2
+ *    (fp32 C, act 0, no bias) overwrites C whatever it held -- a plain store, or when the
+ *    host splits K a memset of C then the add-reduce (weight gradients written once per step).
  * d_bias: optional bf16 [N] added before the activation.
  * act: 0 none; 1 GELU-tanh (pre-activation written to d_aux as bf16);
  *      2 multiply by GELU-tanh'(d_aux) (fused activation backward);

@@ -1083,7 +1083,18 @@ int gemm_run(const void* d_A, int a_mn_major, int64_t lda, const void* d_B, int 
               B2S_EINVAL, "gemm: activation epilogue needs an aligned bf16 aux buffer and bf16 output");
   B2S_REQUIRE(!(accumulate && (act == 1 || act == 3 || act == 4 || act == 5 || act == 7)), B2S_EINVAL,
               "gemm: accumulate with a GELU / SwiGLU epilogue is not supported");
+  B2S_REQUIRE(accumulate != 2 || (c_f32 && act == 0 && !d_bias), B2S_EINVAL,
+              "gemm: overwrite mode (accumulate=2) needs an fp32 C without bias / activation");
   gemm::Choice ch = gemm::choose(M, N, K, accumulate && !d_bias && act == 0);
+  if (accumulate == 2) {  // overwrite: a store when K is not split, else zero C and add-reduce the splits
+    if (ch.splits == 1) {
+      accumulate = 0;
+    } else {
+      if (cudaMemset2DAsync(d_C, (size_t)ldc * 4, 0, (size_t)N * 4, (size_t)M, st) != cudaSuccess)
+        return check_launch("gemm overwrite memset");
+      accumulate = 1;
+    }
+  }
   if (act == 3) ch = gemm::Choice{256, 2, 1};  // the gate / up interleave needs CTA-pair 256-wide tiles
   if (act == 4) ch = gemm::Choice{256, 2, 1};
   if (act == 7) ch = gemm::Choice{256, 2, 1};  // a 256-wide tile holds whole heads (dh 64 / 128)

@@ -131,6 +131,7 @@ class FlatParams:
         sizes = [_padded_numel(g, world) for g in groups]
         self.gall = torch.zeros(sum(sizes), device=device, dtype=torch.float32)
         offs = [sum(sizes[:i]) for i in range(len(sizes))]
+        self._gall_offs = offs
         self.flat = [FlatUnit(g, rank, world, device, dtype, gfull=self.gall[o:o + n])
                      for g, o, n in zip(groups, offs, sizes)]
         self.owner = {}
@@ -144,6 +145,26 @@ class FlatParams:
                 mi += 1
             self.last_model_unit[fi] = mi - 1
         self._views = [UnitView(self.flat[self.owner[i]], s.name) for i, s in enumerate(unit_specs)]
+
+    def grad_zero_ranges(self, overwritten=None) -> list:
+        """(start, length) element ranges of gall a step must zero before its backward: all of
+        it except the gradients named in ``overwritten`` (written whole by their single writer)."""
+        total = self.gall.numel()
+        if not overwritten:
+            return [(0, total)]
+        keep = []
+        for f, base in zip(self.flat, self._gall_offs):
+            for (_, p), (o, shape, _) in f.offsets.items():
+                if p in overwritten:
+                    keep.append((base + o, base + o + int(torch.Size(shape).numel())))
+        ranges, cur = [], 0
+        for a, b in sorted(keep):
+            if a > cur:
+                ranges.append((cur, a - cur))
+            cur = max(cur, b)
+        if cur < total:
+            ranges.append((cur, total - cur))
+        return ranges
 
     def unit(self, i: int) -> UnitView:
         return self._views[i]
@@ -192,8 +213,10 @@ class Engine:
     backward, its gradient reduce-scatter is queued on the comm stream.
     """
 
-    def __init__(self, params: FlatParams, group=None, world: int = 1, prefetch: int = 2):
+    def __init__(self, params: FlatParams, group=None, world: int = 1, prefetch: int = 2, overwritten=None):
         self.P = params
+        # gradient ranges zeroed at the start of each step (the model overwrites the rest)
+        self.zero_ranges = params.grad_zero_ranges(overwritten)
         self.group = group
         self.world = world
         self.prefetch = prefetch
@@ -214,7 +237,8 @@ class Engine:
     # ------------------------------------------------------------------ step
     def begin_step(self) -> None:
         if self.P.gall.is_cuda:
-            ops.zero_(self.P.gall)
+            for o, n in self.zero_ranges:
+                ops.zero_(self.P.gall[o:o + n])
         else:  # the gloo host-logic tests (tests/test_fsdp_cpu.py) run the engine without a GPU
             self.P.gall.zero_()
         if self.world > 1 and self._prefetched == len(self.P.flat):

@@ -323,6 +323,14 @@ class DecoderLM(torch.nn.Module):
     def attach(self, flat_params) -> None:
         self.params = flat_params
 
+    def overwritten_grads(self) -> set:
+        """Parameter names whose gradient one weight-gradient GEMM writes whole each step
+        (``ops.OVERWRITE``), so the step need not zero them first (fsdp.FlatParams.grad_zero_ranges).
+        The tied GPT-2 wte is written by the head's wgrad before the embedding backward adds to it."""
+        names = {"qkv_w", "proj_w", "fc_w", "fc2_w"} if self.cfg.arch == "gpt2" else {"wqkv", "wo", "w13", "w2"}
+        names.add("wte" if self.cfg.tie_embeddings else "lm_head")
+        return names
+
     def acts(self, B, T, device) -> _Acts:
         key = (B, T)
         if key not in self._acts:
@@ -389,8 +397,9 @@ class DecoderLM(torch.nn.Module):
     def forward_backward(self, tokens, targets, hooks=None, compute_grad: bool = True):
         """One training forward + backward over int64 tokens/targets [B, T].
 
-        Writes fp32 parameter gradients into the flat grad buffers (accumulated;
-        the caller zeroes them) and returns the device scalar mean loss.
+        Writes fp32 parameter gradients into the flat grad buffers -- the weight matrices'
+        (overwritten_grads()) whole, the rest accumulated into buffers the caller zeroed -- and
+        returns the device scalar mean loss.
         ``hooks`` (fsdp.Engine) is told when each unit's parameters are needed
         and when each unit's gradients are complete. With activation
         checkpointing each block's forward is re-run (into the shared slot)
@@ -437,7 +446,7 @@ class DecoderLM(torch.nn.Module):
         # ---------------- backward
         # head: dlogits (in A.logits) -> d ln_f, dW_head
         g_head = E.g("wte") if cfg.tie_embeddings else Hd.g("lm_head")
-        ops.linear_wgrad(A.logits, A.ln_f, out=g_head, accumulate=True)
+        ops.linear_wgrad(A.logits, A.ln_f, out=g_head, accumulate=ops.OVERWRITE)  # first writer (tied wte too)
         ops.linear_dgrad(A.logits, w_head, out=A.dln)
         ops.zero_(A.dx)
         if gpt2:
@@ -454,15 +463,15 @@ class DecoderLM(torch.nn.Module):
                 self._block_forward(i, S, T, rope, with_output=False)
             # --- MLP (its output gradient is the residual gradient dx, bf16 copy in dxb)
             if gpt2:  # fc2_b's grad was summed by the norm backward that produced dx
-                ops.linear_wgrad(A.dxb, S.h, out=U.g("fc2_w"), accumulate=True)
+                ops.linear_wgrad(A.dxb, S.h, out=U.g("fc2_w"), accumulate=ops.OVERWRITE)
                 # fc_b's gradient = colsum(dh), from the dgrad epilogue's per-32-row partials
                 ops.linear_dgrad(A.dxb, U.p("fc2_w"), out=A.dh, act=self._act_bwd, aux=S.hpre, colsum_out=U.g("fc_b"))
-                ops.linear_wgrad(A.dh, S.ln_b, out=U.g("fc_w"), accumulate=True)
+                ops.linear_wgrad(A.dh, S.ln_b, out=U.g("fc_w"), accumulate=ops.OVERWRITE)
                 ops.linear_dgrad(A.dh, U.p("fc_w"), out=A.dln)
                 ops.layernorm_bwd(S.xb, A.dln, U.p("ln2_g"), S.mean_b, S.rstd_b, A.dx, A.dxb,
                                   U.g("ln2_g"), U.g("ln2_b"), dxsum=U.g("proj_b"))
             else:
-                ops.linear_wgrad(A.dxb, S.h, out=U.g("w2"), accumulate=True)
+                ops.linear_wgrad(A.dxb, S.h, out=U.g("w2"), accumulate=ops.OVERWRITE)
                 if self.dtype == torch.bfloat16 and cfg.d_ff % 128 == 0:
                     # dh = dy W2 with the SwiGLU backward in the epilogue (gate / up tiles by TMA):
                     # dh never reaches HBM (0.68 -> 0.61 ms per Llama-1B layer)
@@ -470,12 +479,12 @@ class DecoderLM(torch.nn.Module):
                 else:
                     ops.linear_dgrad(A.dxb, U.p("w2"), out=A.dh)
                     ops.swiglu_bwd(S.gu, A.dh, A.dgu)
-                ops.linear_wgrad(A.dgu, S.ln_b, out=U.g("w13"), accumulate=True)
+                ops.linear_wgrad(A.dgu, S.ln_b, out=U.g("w13"), accumulate=ops.OVERWRITE)
                 ops.linear_dgrad(A.dgu, U.p("w13"), out=A.dln)
                 ops.rmsnorm_bwd(S.xb, A.dln, U.p("mlp_norm"), S.rstd_b, A.dx, A.dxb, U.g("mlp_norm"))
             # --- attention
             wo = "proj_w" if gpt2 else "wo"
-            ops.linear_wgrad(A.dxb, S.o, out=U.g(wo), accumulate=True)
+            ops.linear_wgrad(A.dxb, S.o, out=U.g(wo), accumulate=ops.OVERWRITE)
             ops.linear_dgrad(A.dxb, U.p(wo), out=A.do)
             if not gpt2 and self.dtype == torch.bfloat16:  # dq / dk rotated back inside (b2s_attn_bwd_rope)
                 ops.attn_bwd(S.qkv, S.o, A.do, S.lse, B, T, H, Hkv, dh, dqkv=A.dqkv, work=A.attn_work, rope=rope)
@@ -486,7 +495,7 @@ class DecoderLM(torch.nn.Module):
             wq = "qkv_w" if gpt2 else "wqkv"
             if gpt2:
                 ops.colsum_accumulate(A.dqkv, U.g("qkv_b"))
-            ops.linear_wgrad(A.dqkv, S.ln_a, out=U.g(wq), accumulate=True)
+            ops.linear_wgrad(A.dqkv, S.ln_a, out=U.g(wq), accumulate=ops.OVERWRITE)
             ops.linear_dgrad(A.dqkv, U.p(wq), out=A.dln)
             if gpt2:
                 prev_fc2_b = P.unit(i).g("fc2_b") if i > 0 else None

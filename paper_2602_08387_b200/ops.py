@@ -135,7 +135,8 @@ def _gemm_f32(a, b, *, a_mn, b_mn, M, N, K, out=None, accumulate=False, bias=Non
     ld_aux = aux.stride(0) if aux is not None else 0
     _timed("gemm", 2.0 * M * N * K, lambda: _call(
         "b2s_gemm_f32", a.data_ptr(), int(a_mn), a.stride(0), b.data_ptr(), int(b_mn), b.stride(0), out.data_ptr(),
-        out.stride(0), M, N, K, int(accumulate), _ptr(bias), act, _ptr(aux), ld_aux, _sp()))
+        out.stride(0), M, N, K, int(accumulate == 1 or accumulate is True), _ptr(bias), act, _ptr(aux), ld_aux,
+        _sp()))
     return out
 
 
@@ -227,8 +228,14 @@ def linear_dgrad_swiglu(dy, w2, gu, dgu):
     return dgu
 
 
+OVERWRITE = 2  # gemm accumulate mode: C is written whatever it held (see b2s_gemm)
+
+
 def linear_wgrad(dy, x, out=None, accumulate=False, out_f32=True):
-    """dw = dy^T @ x: dy [M,N], x [M,K] -> [N,K] (fp32 by default)."""
+    """dw = dy^T @ x: dy [M,N], x [M,K] -> [N,K] (fp32 by default).
+
+    accumulate: False (store), True (add into out) or OVERWRITE (fp32: store, or zero + split-K
+    add-reduce -- a weight gradient's single writer in a step needs no pre-zeroed buffer)."""
     M, N = dy.shape
     K = x.shape[1]
     return gemm(dy, x, a_mn=True, b_mn=True, M=N, N=K, K=M, out=out, out_f32=out_f32,

@@ -126,7 +126,7 @@ class SPMDTrainer:
         init_dev = "cpu" if self.init_device == "cpu" else self.device
         self.params.load(param_initializer(cfg, self.seed, init_dev))
         self.model.attach(self.params)
-        self.engine = Engine(self.params, self.group, self.world)
+        self.engine = Engine(self.params, self.group, self.world, overwritten=self.model.overwritten_grads())
         self.optimizer = FusedAdamW(self.opt_cfg)
         self.dataloader.bind(self.rank, self.world, self.device, vocab_size=cfg.vocab_size)
         if self.dataloader.seq_len > cfg.max_seq_len:

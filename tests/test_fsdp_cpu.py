@@ -104,3 +104,27 @@ def test_fsdp_sharding_gloo_2ranks(bpu):
     assert out[0]["master_ok"] and out[1]["master_ok"]
     assert out[0]["units"] == (2 + (2 + bpu - 1) // bpu)
     assert out[0]["steps"] > 0
+
+
+def test_grad_zero_ranges_complement():
+    """The per-step gradient zeroing covers exactly what the model does not overwrite."""
+    from paper_2602_08387_b200.fsdp import FlatParams
+    from paper_2602_08387_b200.model import PRESETS, DecoderLM
+
+    for name in ("tiny-llama", "tiny-gpt2"):
+        model = DecoderLM(PRESETS[name], precision="fp32")
+        P = FlatParams(model.units, 0, 1, "cpu", blocks_per_unit=2)
+        over = model.overwritten_grads()
+        ranges = P.grad_zero_ranges(over)
+        zeroed = torch.zeros(P.gall.numel(), dtype=torch.bool)
+        for o, n in ranges:
+            assert n > 0 and not zeroed[o:o + n].any()
+            zeroed[o:o + n] = True
+        written = torch.zeros_like(zeroed)
+        for f, base in zip(P.flat, P._gall_offs):
+            for (_, p), (o, shape, _) in f.offsets.items():
+                if p in over:
+                    written[base + o:base + o + int(torch.Size(shape).numel())] = True
+        assert written.any() and torch.equal(zeroed, ~written)
+        assert P.grad_zero_ranges(None) == [(0, P.gall.numel())]
+

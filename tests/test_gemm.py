@@ -112,6 +112,28 @@ def test_gemm_split_k(cuda, monkeypatch, force_split):
     torch.testing.assert_close(c, ref, rtol=1e-4, atol=5e-2)
 
 
+@pytest.mark.parametrize("force", ["", "256,2,1", "256,2,4", "128,1,8"])
+def test_gemm_overwrite_mode(cuda, monkeypatch, force):
+    """accumulate=OVERWRITE writes the product whatever C held: a plain store unsplit, a memset
+    then the split-K add-reduce when split (the weight-gradient path; C starts as garbage)."""
+    from paper_2602_08387_b200 import ops
+
+    if force:
+        monkeypatch.setenv("B2S_GEMM_FORCE", force)
+    M, N, K = 768, 2304, 4096
+    a = torch.randn(K, M, device=cuda).bfloat16()
+    b = torch.randn(K, N, device=cuda).bfloat16()
+    c = torch.full((M, N), float("nan"), device=cuda)
+    ref = a.float().t() @ b.float()
+    ops.gemm(a, b, a_mn=True, b_mn=True, M=M, N=N, K=K, out=c, accumulate=ops.OVERWRITE)
+    torch.testing.assert_close(c, ref, rtol=1e-4, atol=5e-2)
+    # a strided destination (rows of a wider buffer): the memset must touch only the view
+    big = torch.full((M, N + 64), 7.0, device=cuda)
+    ops.gemm(a, b, a_mn=True, b_mn=True, M=M, N=N, K=K, out=big[:, :N], accumulate=ops.OVERWRITE)
+    torch.testing.assert_close(big[:, :N], ref, rtol=1e-4, atol=5e-2)
+    assert torch.all(big[:, N:] == 7.0)
+
+
 @pytest.mark.parametrize("M,F,K", [(2048, 512, 256), (1000, 384, 200), (16384, 8192, 2048)])
 def test_swiglu_fused_gemms_match_unfused(cuda, M, F, K):
     """The SwiGLU forward / backward fused into the GEMM epilogues give the unfused chain's bits."""
