@@ -138,16 +138,16 @@ def step_gemms(cfg, M):
     else:
         g += [("swiglu_fwd", M, f, d), (M, d, f, 0, 0, "bf16", 0, 0, 0)]
     g += [(M, V, d, 0, 0, "bf16", 0, 0, 0)]
-    # backward: head wgrad / dgrad, then per block
-    g += [(V, d, M, 1, 1, "f32", 1, 0, 0), (M, d, V, 0, 1, "bf16", 0, 0, 0)]
+    # backward: head wgrad / dgrad, then per block (weight gradients in overwrite mode: acc 2)
+    g += [(V, d, M, 1, 1, "f32", 2, 0, 0), (M, d, V, 0, 1, "bf16", 0, 0, 0)]
     if gpt2:
-        g += [(d, f, M, 1, 1, "f32", 1, 0, 0), ("colsum", M, f, d, 6), (f, d, M, 1, 1, "f32", 1, 0, 0),
+        g += [(d, f, M, 1, 1, "f32", 2, 0, 0), ("colsum", M, f, d, 6), (f, d, M, 1, 1, "f32", 2, 0, 0),
               (M, d, f, 0, 1, "bf16", 0, 0, 0)]
     else:
-        g += [(d, f, M, 1, 1, "f32", 1, 0, 0), ("swiglu_bwd", M, f, d), (2 * f, d, M, 1, 1, "f32", 1, 0, 0),
+        g += [(d, f, M, 1, 1, "f32", 2, 0, 0), ("swiglu_bwd", M, f, d), (2 * f, d, M, 1, 1, "f32", 2, 0, 0),
               (M, d, 2 * f, 0, 1, "bf16", 0, 0, 0)]
-    g += [(d, hd, M, 1, 1, "f32", 1, 0, 0), (M, hd, d, 0, 1, "bf16", 0, 0, 0),
-          (qkv, d, M, 1, 1, "f32", 1, 0, 0), (M, d, qkv, 0, 1, "bf16", 0, 0, 0)]
+    g += [(d, hd, M, 1, 1, "f32", 2, 0, 0), (M, hd, d, 0, 1, "bf16", 0, 0, 0),
+          (qkv, d, M, 1, 1, "f32", 2, 0, 0), (M, d, qkv, 0, 1, "bf16", 0, 0, 0)]
     out = []
     for x in g:
         if x not in out:
@@ -226,9 +226,9 @@ def test_step_gemm_headline(cuda, name, shape):
     if dt == "f32":
         init = torch.randn(M, N, device=cuda) if acc else None
         out = init.clone() if acc else torch.empty(M, N, device=cuda)
-        ops.gemm(a, b, a_mn=bool(a_mn), b_mn=bool(b_mn), M=M, N=N, K=K, out=out, accumulate=bool(acc), bias=bv)
-        want = ref + init if acc else ref
-        assert _rel(out, want) < 2e-5, _rel(out, want)
+        ops.gemm(a, b, a_mn=bool(a_mn), b_mn=bool(b_mn), M=M, N=N, K=K, out=out, accumulate=acc, bias=bv)
+        want = ref + init if acc == 1 else ref  # acc 2 (overwrite): whatever C held is replaced
+        assert _rel(out, want) < (2e-5 if acc == 1 else 5e-5), _rel(out, want)  # acc 2: relative to the bare product
         return
     if act == 5:  # bias + GELU(tanh); aux = gelu'(z)
         aux = torch.empty(M, N, device=cuda, dtype=torch.bfloat16)
