@@ -107,6 +107,7 @@ __device__ unsigned long long g_trace[kTraceCtas][18][kTraceRecs][2];
 template <int DH>
 struct Fwd {
   static constexpr bool ALIAS = DH == 128;      // P over S (dh 128: O takes 2 x 128 columns)
+  static constexpr bool kFusedMax = DH == 128;  // block max inside the exponential loop (see below)
   // K / V stages: the K load of block j + KVS waits for both tiles' PV(j); two stages leave it
   // about one softmax period of TMA latency, which is not enough at dh 64 (dh 128 has no room)
   static constexpr int KVS = DH == 64 ? 4 : 2;
@@ -155,6 +156,35 @@ __device__ __forceinline__ float exp_pack_regs(const uint32_t* v, int r, float s
 #pragma unroll
     for (int i = 0; i < 4; ++i) out[k8 * 4 + i] = pack_bf16x2(e[2 * i], e[2 * i + 1]);
   }
+  return (rs4[0] + rs4[1]) + (rs4[2] + rs4[3]);
+}
+
+// Same, against the running max m of the previous blocks, without a separate row-max pass:
+// xmax returns max(s*sl2 - m) over the row's unmasked columns. When it is <= kRescaleThresh the
+// P values are <= 2^8 exactly as if the row max had been taken first (lazy rescale); otherwise
+// the caller shifts m by an integer k >= xmax and scales P, the sum and O by 2^-k (exact in
+// bf16 / fp32). P <= 2^xmax meanwhile: finite for xmax < 128 (log2 units).
+template <bool DIAG>
+__device__ __forceinline__ float exp_pack_regs_mx(const uint32_t* v, int r, float sl2, float m, uint32_t* out,
+                                                  float& xmax) {
+  float rs4[4] = {0.f, 0.f, 0.f, 0.f};
+  float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+  for (int k8 = 0; k8 < BKV / 8; ++k8) {
+    float e[8], x[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      x[i] = fmaf(__uint_as_float(v[k8 * 8 + i]), sl2, -m);
+      if (DIAG && k8 * 8 + i > r) x[i] = -INFINITY;  // masked: exp 0, not in the max
+      e[i] = ex2(x[i]);
+    }
+    mx4[k8 & 3] = fmax3(mx4[k8 & 3], fmax3(x[0], x[1], x[2]), fmax3(x[3], x[4], x[5]));
+    mx4[k8 & 3] = fmax3(mx4[k8 & 3], x[6], x[7]);
+    rs4[k8 & 3] += ((e[0] + e[1]) + (e[2] + e[3])) + ((e[4] + e[5]) + (e[6] + e[7]));
+#pragma unroll
+    for (int i = 0; i < 4; ++i) out[k8 * 4 + i] = pack_bf16x2(e[2 * i], e[2 * i + 1]);
+  }
+  xmax = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
   return (rs4[0] + rs4[1]) + (rs4[2] + rs4[3]);
 }
 
@@ -395,51 +425,96 @@ __global__ void __launch_bounds__(Fwd<DH>::kThreads, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(&s_empty[t]);  // S(j) is in registers: QK^T(j+1) may overwrite it
         TRACE(32, ns);
-        // row max over 8 independent partial maxima (short dependency chains)
-        float mx8[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) mx8[u] = -INFINITY;
-        if (diag) {
-#pragma unroll
-          for (int i = 0; i < BKV; ++i)
-            if (i <= r) mx8[i & 7] = fmaxf(mx8[i & 7], __uint_as_float(v[i]));
-        } else {  // three-input max (FMNMX3): two new elements per instruction
-#pragma unroll
-          for (int i = 0; i < BKV / 2; ++i)
-            mx8[i & 7] = fmax3(mx8[i & 7], __uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
-        }
-        const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
-                               fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
-        const float m_cand = mx * sl2;
-        // lazy rescale: keep the old max unless the new one exceeds it by > 2^8
-        float m_use = m;
-        bool resc = false;
-        if (m_cand > m + kRescaleThresh) { m_use = m_cand; resc = (j > 0); }
-        const float alpha = ex2(m - m_use);  // 0 on the first block (m = -inf)
-        if (__any_sync(0xffffffffu, resc)) {
-          // O must not be in flight: wait for the previous PV of this tile, then O *= alpha
-          mbar_wait(&pv_done[t], (ns - 1) & 1);
-          tc_fence_after();
-#pragma unroll
-          for (int c = 0; c < DH / 16; ++c) {
-            uint32_t o[16];
-            tmem_ld16(tO + c * 16, o);
-            tmem_wait_ld();
-#pragma unroll
-            for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * (resc ? alpha : 1.f));
-            tmem_st16(tO + c * 16, o);
-          }
-          tmem_wait_st();
-        }
-        // exponentials first (bf16 pairs packed over the S registers), then wait for PV(j-1)
-        // to release this tile's TMEM P block, then one TMEM store round
+        // P = 2^(S*scale*log2e - m) as bf16 pairs over the S registers
         uint32_t* pk = v;
-        TRACE(33, ns);
-        named_sync(my_turn, 256);
-        TRACE(37, ns);
-        const float rs = diag ? exp_pack_regs<true>(v, r, sl2, m_use, pk) : exp_pack_regs<false>(v, r, sl2, m_use, pk);
-        named_arrive(other_turn, 256);
-        TRACE(34, ns);
+        float m_use, alpha, rs;
+        // dh 128: after the first block, no separate row-max pass (its max is tracked inside the
+        // exponential loop; 282 -> 273 us at the Llama-8B shape). dh 64 keeps the max pass:
+        // there the fused loop lengthened the MUFU turn (443 -> 453 us at the 1B shape).
+        if (j == 0 || !C::kFusedMax) {
+          // the row max first (8 independent partial maxima)
+          float mx8[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) mx8[u] = -INFINITY;
+          if (diag) {
+#pragma unroll
+            for (int i = 0; i < BKV; ++i)
+              if (i <= r) mx8[i & 7] = fmaxf(mx8[i & 7], __uint_as_float(v[i]));
+          } else {  // three-input max (FMNMX3): two new elements per instruction
+#pragma unroll
+            for (int i = 0; i < BKV / 2; ++i)
+              mx8[i & 7] = fmax3(mx8[i & 7], __uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
+          }
+          const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                                 fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
+          const float m_cand = mx * sl2;
+          // lazy rescale: keep the old max unless the new one exceeds it by > 2^8
+          m_use = m;
+          bool resc = false;
+          if (m_cand > m + kRescaleThresh) { m_use = m_cand; resc = (j > 0); }
+          alpha = ex2(m - m_use);  // 0 on the first block (m = -inf)
+          if (__any_sync(0xffffffffu, resc)) {
+            // O must not be in flight: wait for the previous PV of this tile, then O *= alpha
+            mbar_wait(&pv_done[t], (ns - 1) & 1);
+            tc_fence_after();
+#pragma unroll
+            for (int c = 0; c < DH / 16; ++c) {
+              uint32_t o[16];
+              tmem_ld16(tO + c * 16, o);
+              tmem_wait_ld();
+#pragma unroll
+              for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * (resc ? alpha : 1.f));
+              tmem_st16(tO + c * 16, o);
+            }
+            tmem_wait_st();
+          }
+          TRACE(33, ns);
+          named_sync(my_turn, 256);
+          TRACE(37, ns);
+          rs = diag ? exp_pack_regs<true>(v, r, sl2, m_use, pk) : exp_pack_regs<false>(v, r, sl2, m_use, pk);
+          named_arrive(other_turn, 256);
+          TRACE(34, ns);
+        } else {
+          // later blocks: exponentials against the running max straight away, the block max
+          // tracked inside the same loop (no separate max pass ahead of the MUFU turn)
+          TRACE(33, ns);
+          named_sync(my_turn, 256);
+          TRACE(37, ns);
+          float xmax;
+          rs = diag ? exp_pack_regs_mx<true>(v, r, sl2, m, pk, xmax) : exp_pack_regs_mx<false>(v, r, sl2, m, pk, xmax);
+          named_arrive(other_turn, 256);
+          TRACE(34, ns);
+          m_use = m;
+          alpha = 1.f;
+          // lazy rescale: only when the block max exceeds the running one by > 2^8
+          const bool resc = xmax > kRescaleThresh;
+          if (__any_sync(0xffffffffu, resc)) {
+            if (resc) {  // shift the max by an integer k: P, the sum and O scale by 2^-k exactly
+              const float k = ceilf(xmax);
+              alpha = ex2(-k);
+              m_use = m + k;
+              rs *= alpha;
+#pragma unroll
+              for (int i = 0; i < BKV / 2; ++i) {
+                const float lo = __uint_as_float(pk[i] << 16), hi = __uint_as_float(pk[i] & 0xffff0000u);
+                pk[i] = pack_bf16x2(lo * alpha, hi * alpha);
+              }
+            }
+            // O must not be in flight: wait for the previous PV of this tile, then O *= alpha
+            mbar_wait(&pv_done[t], (ns - 1) & 1);
+            tc_fence_after();
+#pragma unroll
+            for (int c = 0; c < DH / 16; ++c) {
+              uint32_t o[16];
+              tmem_ld16(tO + c * 16, o);
+              tmem_wait_ld();
+#pragma unroll
+              for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * (resc ? alpha : 1.f));
+              tmem_st16(tO + c * 16, o);
+            }
+            tmem_wait_st();
+          }
+        }
         if (ns > 0) mbar_wait(&p_empty[t], (ns - 1) & 1);
         TRACE(35, ns);
         tc_fence_after();
