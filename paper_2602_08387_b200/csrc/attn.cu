@@ -720,10 +720,10 @@ __device__ __forceinline__ void p_ds(uint32_t* sv, uint32_t* dv, int q0, int r, 
     dv[e] = __float_as_uint(pv * fmaf(__uint_as_float(dv[e]), scale, -ds[e]));
   }
 }
-// dh = 64: dQ fused (TMEM S^T 128 + dP^T 128 + dV 64 + dK 64 + dQ 2x64 = 512
-// columns) and Q / dO double-buffered. dh = 128: dV + dK take 256 columns, so
-// this kernel computes dK / dV only (single-buffered Q / dO to fit 227 KB of
-// smem) and attn_bwd_q_kernel produces dQ per query tile.
+// dh = 64: dQ fused (TMEM S^T 128 + dP^T 128 + dV 64 + dK 64 + dQ 64 + P^T 64 = 512
+// columns). dh = 128 launches attn_bwd128_kernel (dK / dV, P^T and dS^T in TMEM) and
+// attn_bwd_q_kernel (dQ per query tile) instead; this template's non-DQ branches are the
+// round-1 dh-128 form (P^T / dS^T in shared memory, one Q / dO stage), kept compilable.
 template <int DH>
 struct Bwd {
   static constexpr bool DQ = DH == 64;  // dQ fused into the key-tile kernel
@@ -1066,6 +1066,275 @@ __global__ void __launch_bounds__(320, 1)
 }
 
 // -------------------------------------------------------------------------------------
+// dK / dV at dh 128 (attn_bwd128_kernel; dQ comes from attn_bwd_q_kernel). CTA = (batch, kv
+// head, 128-key tile) in the block order of attn_bwd_kernel. TMEM holds S^T, dP^T, dV and dK
+// (4 x 128 columns), so P^T and dS^T go back into TMEM over the S^T / dP^T columns their warp
+// just read (pass qq of warp half h: columns 64h + 32qq + [0, 16) of each block, bf16 pairs):
+// no P^T / dS^T shared-memory tiles, which leaves room for two Q / dO stages -- with one, every
+// step waited for its Q / dO reload (~3000 clk) behind the previous step's MMAs -- and dV / dK
+// run in the TMEM-A MMA form. MMA order per step t: dV(t) S(t+1) dK(t) dP(t+1): the tensor pipe
+// runs one thread's MMAs in order, so S(t+1) overwrites P^T(t) after dV(t) read it and dP(t+1)
+// overwrites dS^T(t) after dK(t), while the compute warps start P(t+1) as soon as S(t+1) lands.
+struct Bwd128 {
+  static constexpr int DH = 128, kTileQ = BQ * DH * 2, QS = 2, LS = 4;
+  static constexpr int kSmem = 1024 + 2 * kTileQ /*K, V*/ + 2 * QS * kTileQ /*Q, dO*/ + 2 * LS * BQ * 4 + 256;
+  static_assert(kSmem <= 232448, "backward tiles exceed shared memory");
+};
+
+__global__ void __launch_bounds__(320, 1)
+    attn_bwd128_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
+                       const __grid_constant__ CUtensorMap tm_dkv, Params p) {
+  constexpr int DH = Bwd128::DH, kTQ = Bwd128::kTileQ, QS = Bwd128::QS, LS = Bwd128::LS, NA = DH / 64;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sK = align1024(smem_raw);
+  uint8_t* sV = sK + kTQ;
+  uint8_t* sQ = sV + kTQ;        // [QS]
+  uint8_t* sdO = sQ + QS * kTQ;  // [QS]
+  float* sLse = reinterpret_cast<float*>(sdO + QS * kTQ);  // [LS][128]
+  float* sD = sLse + LS * BQ;                              // [LS][128]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sD + LS * BQ);
+  uint64_t* kv_full = bars;
+  uint64_t* qd_full = bars + 1;           // [QS]
+  uint64_t* qd_empty = qd_full + QS;      // [QS]
+  uint64_t* s_full = qd_empty + QS;
+  uint64_t* dp_full = s_full + 1;
+  uint64_t* pds_full = s_full + 2;
+  uint64_t* done = s_full + 3;
+  uint64_t* st_ld_full = s_full + 4;        // [LS]
+  uint64_t* st_ld_empty = st_ld_full + LS;  // [LS]
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(st_ld_empty + LS);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // block order: see attn_bwd_kernel
+  const int nbk = p.B * p.Hkv;
+  const int gc = nbk < kBwdGroups ? nbk : kBwdGroups;
+  const int chunk = (int)(blockIdx.x / (gc * p.nqt));
+  const int in_chunk = (int)(blockIdx.x - chunk * gc * p.nqt);
+  const int gcur = min(gc, nbk - chunk * gc);
+  const int kt = in_chunk / gcur;
+  const int bk = chunk * gc + in_chunk % gcur;
+  const int b = bk / p.Hkv, kvh = bk % p.Hkv;
+  const int G = p.Hq / p.Hkv;
+  const int nq = p.nqt - kt;
+  const int nsteps = G * nq;
+  const int krow0 = b * p.T + kt * BKV;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tm_qkv);
+    tma_prefetch(&tm_do);
+    mbar_init(kv_full, 1);
+    for (int s = 0; s < QS; ++s) { mbar_init(&qd_full[s], 1); mbar_init(&qd_empty[s], 1); }
+    mbar_init(s_full, 1);
+    mbar_init(dp_full, 1);
+    mbar_init(pds_full, 8);
+    mbar_init(done, 1);
+    for (int s = 0; s < LS; ++s) { mbar_init(&st_ld_full[s], 1); mbar_init(&st_ld_empty[s], 8); }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tslot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tslot;
+  const uint32_t tS = tbase, tdP = tbase + 128, tdV = tbase + 256, tdK = tbase + 384;
+
+  if (warp == 0) {
+    // ------------------------------------------------ TMA producer
+    if (lane == 0) {
+      mbar_arrive_expect_tx(kv_full, 2 * kTQ);
+      for (int a = 0; a < NA; ++a) {
+        tma_load_2d(sK + a * kTile, &tm_qkv, kv_full, (p.Hq + kvh) * DH + a * 64, krow0);
+        tma_load_2d(sV + a * kTile, &tm_qkv, kv_full, (p.Hq + p.Hkv + kvh) * DH + a * 64, krow0);
+      }
+      for (int t = 0; t < nsteps; ++t) {
+        const int h = kvh * G + t / nq, i = kt + t % nq;
+        const int s = t % LS;
+        mbar_wait(&st_ld_empty[s], ((t / LS) & 1) ^ 1);
+        const size_t off = ((size_t)b * p.Hq + h) * p.T + (size_t)i * BQ;
+        mbar_arrive_expect_tx(&st_ld_full[s], 2 * BQ * 4);
+        bulk_load_1d(sLse + s * BQ, p.lse + off, BQ * 4, &st_ld_full[s]);
+        bulk_load_1d(sD + s * BQ, p.dsum + off, BQ * 4, &st_ld_full[s]);
+        const int qs = t % QS;
+        mbar_wait(&qd_empty[qs], ((t / QS) & 1) ^ 1);
+        mbar_arrive_expect_tx(&qd_full[qs], 2 * kTQ);
+        for (int a = 0; a < NA; ++a) {
+          tma_load_2d(sQ + qs * kTQ + a * kTile, &tm_qkv, &qd_full[qs], h * DH + a * 64, b * p.T + i * BQ);
+          tma_load_2d(sdO + qs * kTQ + a * kTile, &tm_do, &qd_full[qs], h * DH + a * 64, b * p.T + i * BQ);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ------------------------------------------------ MMA issuer (whole warp, one lane elected per op)
+    constexpr uint32_t idSS = make_idesc_bf16(128, 128, false, false);  // S^T, dP^T
+    constexpr uint32_t idKM = make_idesc_bf16(128, DH, false, true);    // dV, dK (B = dO / Q, MN-major)
+    const uint32_t aK = smem_u32(sK), aV = smem_u32(sV), aQ = smem_u32(sQ), adO = smem_u32(sdO);
+    auto issue_S = [&](int t) {  // S^T(t) = K Q(t)^T
+      const int qs = t % QS;
+      mbar_wait(&qd_full[qs], (t / QS) & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int kk = 0; kk < DH / 16; ++kk) {
+        const uint32_t ko = (kk >> 2) * kTile + (kk & 3) * 32;
+        mma_bf16_ss_w(tS, make_sdesc(aK + ko, 16, 1024), make_sdesc(aQ + qs * kTQ + ko, 16, 1024), idSS, kk > 0);
+      }
+      mma_commit_w(s_full);
+    };
+    auto issue_dP = [&](int t) {  // dP^T(t) = V dO(t)^T
+      const int qs = t % QS;
+      mbar_wait(&qd_full[qs], (t / QS) & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int kk = 0; kk < DH / 16; ++kk) {
+        const uint32_t ko = (kk >> 2) * kTile + (kk & 3) * 32;
+        mma_bf16_ss_w(tdP, make_sdesc(aV + ko, 16, 1024), make_sdesc(adO + qs * kTQ + ko, 16, 1024), idSS, kk > 0);
+      }
+      mma_commit_w(dp_full);
+    };
+    mbar_wait(kv_full, 0);
+    issue_S(0);
+    issue_dP(0);
+    for (int t = 0; t < nsteps; ++t) {
+      const int qs = t % QS;
+      const uint32_t q_ = aQ + qs * kTQ, do_ = adO + qs * kTQ;
+      mbar_wait(pds_full, t & 1);
+      tc_fence_after();
+      // K step kk = queries 16kk.. : warp half kk >> 2, pass (kk >> 1) & 1, 8 packed columns
+#pragma unroll
+      for (int kk = 0; kk < BQ / 16; ++kk) {
+        const uint32_t col = 64 * (kk >> 2) + 32 * ((kk >> 1) & 1) + (kk & 1) * 8;
+        mma_bf16_ts_w(tdV, tS + col, make_sdesc(do_ + kk * 2048, kTile, 1024), idKM, (t > 0 || kk > 0));
+      }
+      if (t + 1 < nsteps) issue_S(t + 1);  // after dV(t) read P^T(t) from these columns
+#pragma unroll
+      for (int kk = 0; kk < BQ / 16; ++kk) {
+        const uint32_t col = 64 * (kk >> 2) + 32 * ((kk >> 1) & 1) + (kk & 1) * 8;
+        mma_bf16_ts_w(tdK, tdP + col, make_sdesc(q_ + kk * 2048, kTile, 1024), idKM, (t > 0 || kk > 0));
+      }
+      mma_commit_w(&qd_empty[qs]);
+      if (t + 1 < nsteps) issue_dP(t + 1);  // after dK(t) read dS^T(t)
+    }
+    mma_commit_w(done);
+    __syncwarp();
+  } else {
+    // ------------------------------------------------ compute warps
+    const int q4 = warp & 3;
+    const int half = (warp - 2) >> 2;
+    const int r = q4 * 32 + lane;  // key row
+    const uint32_t lrow = (uint32_t)(q4 * 32) << 16;
+    for (int t = 0; t < nsteps; ++t) {
+      const int i = kt + t % nq;
+      const bool diag = (i == kt);
+      mbar_wait(&st_ld_full[t % LS], (t / LS) & 1);
+      const float* lse2 = sLse + (t % LS) * BQ;
+      const float* dd = sD + (t % LS) * BQ;
+      mbar_wait(s_full, t & 1);
+      tc_fence_after();
+      // P^T = 2^(s scale log2e - lse2[q]) for this warp's 64 query columns: fp32 kept for dS,
+      // bf16 pairs stored over the S^T columns just read
+      float pf[2][32];
+#pragma unroll
+      for (int qq = 0; qq < 2; ++qq) {
+        uint32_t sv[32], pw[16];
+        tmem_ld32(tS + lrow + half * 64 + qq * 32, sv);
+        tmem_wait_ld();
+        const int q0 = half * 64 + qq * 32;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const float4 l4 = *reinterpret_cast<const float4*>(lse2 + q0 + 4 * k);
+          const float ls[4] = {l4.x, l4.y, l4.z, l4.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int j = 4 * k + e;
+            float pv = ex2(fmaf(__uint_as_float(sv[j]), p.scale_log2, -ls[e]));
+            if (diag && q0 + j < r) pv = 0.f;  // query index below key index: masked
+            pf[qq][j] = pv;
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < 16; ++k) pw[k] = pack_bf16x2(pf[qq][2 * k], pf[qq][2 * k + 1]);
+        tmem_st16(tS + lrow + half * 64 + qq * 32, pw);
+      }
+      // dS^T = P^T (scale dP^T - D') once dP(t) lands, bf16 pairs over the dP^T columns just read
+      mbar_wait(dp_full, t & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int qq = 0; qq < 2; ++qq) {
+        uint32_t dv[32], zw[16];
+        tmem_ld32(tdP + lrow + half * 64 + qq * 32, dv);
+        tmem_wait_ld();
+        const int q0 = half * 64 + qq * 32;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const float4 d4 = *reinterpret_cast<const float4*>(dd + q0 + 4 * k);
+          const float ds[4] = {d4.x, d4.y, d4.z, d4.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int j = 4 * k + e;
+            dv[j] = __float_as_uint(pf[qq][j] * fmaf(__uint_as_float(dv[j]), p.scale, -ds[e]));
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < 16; ++k) zw[k] = pack_bf16x2(__uint_as_float(dv[2 * k]), __uint_as_float(dv[2 * k + 1]));
+        tmem_st16(tdP + lrow + half * 64 + qq * 32, zw);
+      }
+      tmem_wait_st();  // P^T / dS^T are in TMEM before the MMA warp is told
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(pds_full);
+        mbar_arrive(&st_ld_empty[t % LS]);
+      }
+    }
+    // dK (from the pre-scaled dS) and dV -> bf16 -> smem (the Q / dO stages are free) -> TMA store
+    mbar_wait(done, 0);
+    tc_fence_after();
+    uint8_t* sdK_out = sQ;
+    uint8_t* sdV_out = sdO;
+#pragma unroll
+    for (int cc = 0; cc < 2; ++cc) {  // this warp's 64 of the 128 columns, 32 at a time
+      const int col0 = half * 64 + cc * 32;
+      uint32_t kv[32], vv[32];
+      tmem_ld32(tdK + lrow + col0, kv);
+      tmem_ld32(tdV + lrow + col0, vv);
+      tmem_wait_ld();
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint4 w, z;
+        w.x = pack_bf16x2(__uint_as_float(kv[8 * c + 0]), __uint_as_float(kv[8 * c + 1]));
+        w.y = pack_bf16x2(__uint_as_float(kv[8 * c + 2]), __uint_as_float(kv[8 * c + 3]));
+        w.z = pack_bf16x2(__uint_as_float(kv[8 * c + 4]), __uint_as_float(kv[8 * c + 5]));
+        w.w = pack_bf16x2(__uint_as_float(kv[8 * c + 6]), __uint_as_float(kv[8 * c + 7]));
+        z.x = pack_bf16x2(__uint_as_float(vv[8 * c + 0]), __uint_as_float(vv[8 * c + 1]));
+        z.y = pack_bf16x2(__uint_as_float(vv[8 * c + 2]), __uint_as_float(vv[8 * c + 3]));
+        z.z = pack_bf16x2(__uint_as_float(vv[8 * c + 4]), __uint_as_float(vv[8 * c + 5]));
+        z.w = pack_bf16x2(__uint_as_float(vv[8 * c + 6]), __uint_as_float(vv[8 * c + 7]));
+        const int chunk16 = col0 / 8 + c;  // 16-byte chunk of the row: atom chunk16 / 8, position % 8
+        *reinterpret_cast<uint4*>(sdK_out + (chunk16 >> 3) * kTile + swz(r, chunk16 & 7)) = w;
+        *reinterpret_cast<uint4*>(sdV_out + (chunk16 >> 3) * kTile + swz(r, chunk16 & 7)) = z;
+      }
+    }
+    fence_proxy_async_smem();
+    named_sync(1, 256);
+    if (threadIdx.x == 64) {
+      for (int a = 0; a < NA; ++a) {
+        tma_store_2d(&tm_dkv, sdK_out + a * kTile, (p.Hq + kvh) * DH + a * 64, krow0);
+        tma_store_2d(&tm_dkv, sdV_out + a * kTile, (p.Hq + p.Hkv + kvh) * DH + a * 64, krow0);
+      }
+      bulk_commit();
+      bulk_wait_read<0>();
+    }
+    __syncwarp();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<512>(tbase);
+  }
+}
+
+// -------------------------------------------------------------------------------------
 // dQ for dh = 128: CTA = (batch, q head, 128-query tile), looping over the causal key
 // tiles j <= i. S = Q K_j^T and dP = dO V_j^T into TMEM, thread = query row:
 // dS = P (dP - D) -> bf16 -> smem, dQ += dS K_j (TMEM accumulator across the loop,
@@ -1353,14 +1622,20 @@ int attn_bwd_dh(const void* d_qkv, const void* d_o, const void* d_do, const floa
                  dsum, dq_acc, nullptr};
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(attn::attn_bwd_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+    if constexpr (DH == 128)
+      cudaFuncSetAttribute(attn::attn_bwd128_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, attn::Bwd128::kSmem);
+    else
+      cudaFuncSetAttribute(attn::attn_bwd_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
     if constexpr (!C::DQ)
       cudaFuncSetAttribute(attn::attn_bwd_q_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            attn::BwdQ<DH>::kSmem);
     attr = true;
   }
   const unsigned grid = (unsigned)(B * Hkv * (T / attn::BQ));
-  attn::attn_bwd_kernel<DH><<<grid, attn::kBwdThreads, C::kSmem, st>>>(tq, tdo, tdq, tdkv, p);
+  if constexpr (DH == 128)
+    attn::attn_bwd128_kernel<<<grid, attn::kBwdThreads, attn::Bwd128::kSmem, st>>>(tq, tdo, tdkv, p);
+  else
+    attn::attn_bwd_kernel<DH><<<grid, attn::kBwdThreads, C::kSmem, st>>>(tq, tdo, tdq, tdkv, p);
   rc = check_launch("attn_bwd");
   if (rc) return rc;
   if constexpr (C::DQ) {
