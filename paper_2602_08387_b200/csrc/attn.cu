@@ -1337,13 +1337,13 @@ __global__ void __launch_bounds__(320, 1)
 // -------------------------------------------------------------------------------------
 // dQ for dh = 128: CTA = (batch, q head, 128-query tile), looping over the causal key
 // tiles j <= i. S = Q K_j^T and dP = dO V_j^T into TMEM, thread = query row:
-// dS = P (dP - D) -> bf16 -> smem, dQ += dS K_j (TMEM accumulator across the loop,
+// dS = P (dP - D) -> bf16 -> TMEM (columns 384..447), dQ += dS K_j (TMEM-A MMA form, TMEM accumulator across the loop,
 // K_j as an MN-major operand) -> x scale -> bf16 -> TMA store into dqkv.
-// smem 224 KB: Q, dO (32 KB each), K / V 2 stages (128 KB), dS (32 KB).
+// smem 192 KB: Q, dO (32 KB each), K / V 2 stages (128 KB).
 template <int DH>
 struct BwdQ {
   static constexpr int kTileQ = BQ * DH * 2;
-  static constexpr int kSmem = 1024 + 2 * kTileQ + 2 * kStages * kTileQ + kPBuf + 256;
+  static constexpr int kSmem = 1024 + 2 * kTileQ + 2 * kStages * kTileQ + 256;
   static_assert(kSmem <= 232448, "dQ tiles exceed shared memory");
 };
 
@@ -1357,8 +1357,7 @@ __global__ void __launch_bounds__(320, 1)
   uint8_t* sdO = sQ + kTQ;
   uint8_t* sK = sdO + kTQ;              // [kStages]
   uint8_t* sV = sK + kStages * kTQ;     // [kStages]
-  uint8_t* sdS = sV + kStages * kTQ;    // dS [128 q][128 keys], two 64-key atoms
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sdS + kPBuf);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + kStages * kTQ);
   uint64_t* qd_full = bars;
   uint64_t* k_full = bars + 1;          // [kStages]
   uint64_t* v_full = k_full + kStages;  // [kStages]
@@ -1396,7 +1395,8 @@ __global__ void __launch_bounds__(320, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tslot;
-  const uint32_t tS = tbase, tdP = tbase + 128, tdQ = tbase + 256;
+  // dS (bf16 pairs, 64 columns) in TMEM [384, 448): the dQ MMA takes it in the TMEM-A form
+  const uint32_t tS = tbase, tdP = tbase + 128, tdQ = tbase + 256, tDS = tbase + 384;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -1423,7 +1423,6 @@ __global__ void __launch_bounds__(320, 1)
       constexpr uint32_t idSS = make_idesc_bf16(BQ, BKV, false, false);  // S, dP
       constexpr uint32_t idQ = make_idesc_bf16(BQ, DH, false, true);     // dQ += dS K (K MN-major)
       const uint32_t aQ = smem_u32(sQ), adO = smem_u32(sdO), aK = smem_u32(sK), aV = smem_u32(sV);
-      const uint32_t adS = smem_u32(sdS);
       auto issue_S = [&](int j) {
         const int s = j % kStages;
         mbar_wait(&k_full[s], (j / kStages) & 1);
@@ -1451,9 +1450,9 @@ __global__ void __launch_bounds__(320, 1)
         mbar_wait(pds_full, j & 1);
         tc_fence_after();
 #pragma unroll
-        for (int kk = 0; kk < BKV / 16; ++kk)
-          mma_bf16_ss_w(tdQ, make_sdesc(adS + (kk >> 2) * kTile + (kk & 3) * 32, 16, 1024),
-                        make_sdesc(aK + s * kTQ + kk * 2048, kTile, 1024), idQ, (j > 0 || kk > 0) ? 1u : 0u);
+        for (int kk = 0; kk < BKV / 16; ++kk)  // K step kk = keys 16kk.. = packed dS columns 8kk..
+          mma_bf16_ts_w(tdQ, tDS + kk * 8, make_sdesc(aK + s * kTQ + kk * 2048, kTile, 1024), idQ,
+                        (j > 0 || kk > 0) ? 1u : 0u);
         mma_commit_w(pds_empty);
         mma_commit_w(&kv_empty[s]);
       }
@@ -1492,18 +1491,14 @@ __global__ void __launch_bounds__(320, 1)
           if (diag && k0 + e > r) pv = 0.f;  // key after query: masked
           dv[e] = __float_as_uint(pv * fmaf(__uint_as_float(dv[e]), p.scale, -dd));  // scaled dS
         }
-        if (qq == 0 && j > 0) mbar_wait(pds_empty, (j - 1) & 1);
+        if (qq == 0 && j > 0) mbar_wait(pds_empty, (j - 1) & 1);  // dQ(j-1) has read dS(j-1)
+        uint32_t zw[16];
 #pragma unroll
-        for (int k8 = 0; k8 < 4; ++k8) {
-          uint4 z;
-          z.x = pack_bf16x2(__uint_as_float(dv[8 * k8 + 0]), __uint_as_float(dv[8 * k8 + 1]));
-          z.y = pack_bf16x2(__uint_as_float(dv[8 * k8 + 2]), __uint_as_float(dv[8 * k8 + 3]));
-          z.z = pack_bf16x2(__uint_as_float(dv[8 * k8 + 4]), __uint_as_float(dv[8 * k8 + 5]));
-          z.w = pack_bf16x2(__uint_as_float(dv[8 * k8 + 6]), __uint_as_float(dv[8 * k8 + 7]));
-          *reinterpret_cast<uint4*>(sdS + half * kTile + swz(r, qq * 4 + k8)) = z;
-        }
+        for (int e = 0; e < 16; ++e) zw[e] = pack_bf16x2(__uint_as_float(dv[2 * e]), __uint_as_float(dv[2 * e + 1]));
+        tmem_st16(tDS + lrow + half * 32 + qq * 16, zw);
       }
-      fence_proxy_async_smem();
+      tmem_wait_st();  // dS is in TMEM before the MMA warp is told
+      tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(pds_full);
     }
