@@ -30,7 +30,6 @@ constexpr int BQ = 128, BKV = 128;
 
 constexpr int kTile = BQ * 64 * 2;  // 16 KB: one 128-row x 64-column bf16 swizzle atom
 constexpr int kPBuf = BQ * BKV * 2; // 32 KB: a 128 x 128 bf16 P tile (two atoms)
-constexpr int kStages = 2;
 constexpr float kLog2e = 1.4426950408889634f;
 
 // byte offset of 16-B chunk c of row r in a 128B-swizzled tile of 128-B rows
@@ -1343,7 +1342,10 @@ __global__ void __launch_bounds__(320, 1)
 template <int DH>
 struct BwdQ {
   static constexpr int kTileQ = BQ * DH * 2;
-  static constexpr int kSmem = 1024 + 2 * kTileQ + 2 * kStages * kTileQ + 256;
+  // K / V stages: a K stage is freed when dQ(j) retires, a V stage as soon as dP(j) does; the
+  // reload takes ~3000 clk under load, so with two K stages S(j+2) waited on it every block
+  static constexpr int KS = 3, VS = 2;
+  static constexpr int kSmem = 1024 + 2 * kTileQ + (KS + VS) * kTileQ + 256;
   static_assert(kSmem <= 232448, "dQ tiles exceed shared memory");
 };
 
@@ -1355,21 +1357,28 @@ __global__ void __launch_bounds__(320, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sQ = align1024(smem_raw);
   uint8_t* sdO = sQ + kTQ;
-  uint8_t* sK = sdO + kTQ;              // [kStages]
-  uint8_t* sV = sK + kStages * kTQ;     // [kStages]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + kStages * kTQ);
+  constexpr int KS = BwdQ<DH>::KS, VS = BwdQ<DH>::VS;
+  uint8_t* sK = sdO + kTQ;              // [KS]
+  uint8_t* sV = sK + KS * kTQ;          // [VS]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + VS * kTQ);
   uint64_t* qd_full = bars;
-  uint64_t* k_full = bars + 1;          // [kStages]
-  uint64_t* v_full = k_full + kStages;  // [kStages]
-  uint64_t* kv_empty = v_full + kStages;
-  uint64_t* st_full = kv_empty + kStages;
-  uint64_t* st_empty = st_full + 1;
-  uint64_t* pds_full = st_empty + 1;
-  uint64_t* pds_empty = pds_full + 1;
+  uint64_t* k_full = bars + 1;          // [KS]
+  uint64_t* k_empty = k_full + KS;      // [KS]
+  uint64_t* v_full = k_empty + KS;      // [VS]
+  uint64_t* v_empty = v_full + VS;      // [VS]
+  uint64_t* s_full = v_empty + VS;
+  uint64_t* s_empty = s_full + 1;
+  uint64_t* dp_full = s_full + 2;
+  uint64_t* dp_empty = s_full + 3;
+  uint64_t* pds_full = s_full + 4;
+  uint64_t* pds_empty = s_full + 5;
   uint64_t* done = pds_empty + 1;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(done + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#ifdef B2S_ATTN_TRACE
+  int tr_n = 0;
+#endif
   const int nbh = p.B * p.Hq;
   const int i = p.nqt - 1 - (int)(blockIdx.x / nbh);  // heaviest query tiles first
   const int bh = blockIdx.x % nbh;
@@ -1382,9 +1391,12 @@ __global__ void __launch_bounds__(320, 1)
     tma_prefetch(&tm_qkv);
     tma_prefetch(&tm_do);
     mbar_init(qd_full, 1);
-    for (int s = 0; s < kStages; ++s) { mbar_init(&k_full[s], 1); mbar_init(&v_full[s], 1); mbar_init(&kv_empty[s], 1); }
-    mbar_init(st_full, 1);
-    mbar_init(st_empty, 8);
+    for (int s = 0; s < KS; ++s) { mbar_init(&k_full[s], 1); mbar_init(&k_empty[s], 1); }
+    for (int s = 0; s < VS; ++s) { mbar_init(&v_full[s], 1); mbar_init(&v_empty[s], 1); }
+    mbar_init(s_full, 1);
+    mbar_init(s_empty, 8);
+    mbar_init(dp_full, 1);
+    mbar_init(dp_empty, 8);
     mbar_init(pds_full, 8);
     mbar_init(pds_empty, 1);
     mbar_init(done, 1);
@@ -1406,15 +1418,16 @@ __global__ void __launch_bounds__(320, 1)
         tma_load_2d(sdO + a * kTile, &tm_do, qd_full, h * DH + a * 64, qrow0);
       }
       for (int j = 0; j < nkv; ++j) {
-        const int s = j % kStages;
-        mbar_wait(&kv_empty[s], ((j / kStages) & 1) ^ 1);
         const int r = b * p.T + j * BKV;
-        mbar_arrive_expect_tx(&k_full[s], kTQ);
+        const int sk = j % KS, sv = j % VS;
+        mbar_wait(&k_empty[sk], ((j / KS) & 1) ^ 1);
+        mbar_arrive_expect_tx(&k_full[sk], kTQ);
         for (int a = 0; a < NA; ++a)
-          tma_load_2d(sK + s * kTQ + a * kTile, &tm_qkv, &k_full[s], (p.Hq + kvh) * DH + a * 64, r);
-        mbar_arrive_expect_tx(&v_full[s], kTQ);
+          tma_load_2d(sK + sk * kTQ + a * kTile, &tm_qkv, &k_full[sk], (p.Hq + kvh) * DH + a * 64, r);
+        mbar_wait(&v_empty[sv], ((j / VS) & 1) ^ 1);
+        mbar_arrive_expect_tx(&v_full[sv], kTQ);
         for (int a = 0; a < NA; ++a)
-          tma_load_2d(sV + s * kTQ + a * kTile, &tm_qkv, &v_full[s], (p.Hq + p.Hkv + kvh) * DH + a * 64, r);
+          tma_load_2d(sV + sv * kTQ + a * kTile, &tm_qkv, &v_full[sv], (p.Hq + p.Hkv + kvh) * DH + a * 64, r);
       }
     }
     __syncwarp();
@@ -1423,38 +1436,54 @@ __global__ void __launch_bounds__(320, 1)
       constexpr uint32_t idSS = make_idesc_bf16(BQ, BKV, false, false);  // S, dP
       constexpr uint32_t idQ = make_idesc_bf16(BQ, DH, false, true);     // dQ += dS K (K MN-major)
       const uint32_t aQ = smem_u32(sQ), adO = smem_u32(sdO), aK = smem_u32(sK), aV = smem_u32(sV);
+      // S(j) and dP(j) are released separately (the compute warps read all of S first), so S(j+1)
+      // runs while block j's dS is still being formed
       auto issue_S = [&](int j) {
-        const int s = j % kStages;
-        mbar_wait(&k_full[s], (j / kStages) & 1);
-        mbar_wait(&v_full[s], (j / kStages) & 1);
-        if (j > 0) mbar_wait(st_empty, (j - 1) & 1);
+        const int sk = j % KS;
+        mbar_wait(&k_full[sk], (j / KS) & 1);
+        if (j > 0) mbar_wait(s_empty, (j - 1) & 1);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < DH / 16; ++kk) {
           const uint32_t ko = (kk >> 2) * kTile + (kk & 3) * 32;
-          mma_bf16_ss_w(tS, make_sdesc(aQ + ko, 16, 1024), make_sdesc(aK + s * kTQ + ko, 16, 1024), idSS, kk > 0);
+          mma_bf16_ss_w(tS, make_sdesc(aQ + ko, 16, 1024), make_sdesc(aK + sk * kTQ + ko, 16, 1024), idSS, kk > 0);
         }
+        mma_commit_w(s_full);
+        TRACE(50, j);
+      };
+      auto issue_dP = [&](int j) {
+        const int sv = j % VS;
+        mbar_wait(&v_full[sv], (j / VS) & 1);
+        if (j > 0) mbar_wait(dp_empty, (j - 1) & 1);
+        tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < DH / 16; ++kk) {
           const uint32_t ko = (kk >> 2) * kTile + (kk & 3) * 32;
-          mma_bf16_ss_w(tdP, make_sdesc(adO + ko, 16, 1024), make_sdesc(aV + s * kTQ + ko, 16, 1024), idSS,
+          mma_bf16_ss_w(tdP, make_sdesc(adO + ko, 16, 1024), make_sdesc(aV + sv * kTQ + ko, 16, 1024), idSS,
                         kk > 0);
         }
-        mma_commit_w(st_full);
+        mma_commit_w(dp_full);
+        mma_commit_w(&v_empty[sv]);  // V(j) is read by dP(j) only
       };
       mbar_wait(qd_full, 0);
       issue_S(0);
+      issue_dP(0);
       for (int j = 0; j < nkv; ++j) {
-        const int s = j % kStages;
-        if (j + 1 < nkv) issue_S(j + 1);
+        const int s = j % KS;
+        if (j + 1 < nkv) {
+          issue_S(j + 1);
+          issue_dP(j + 1);
+        }
         mbar_wait(pds_full, j & 1);
+        TRACE(51, j);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < BKV / 16; ++kk)  // K step kk = keys 16kk.. = packed dS columns 8kk..
           mma_bf16_ts_w(tdQ, tDS + kk * 8, make_sdesc(aK + s * kTQ + kk * 2048, kTile, 1024), idQ,
                         (j > 0 || kk > 0) ? 1u : 0u);
         mma_commit_w(pds_empty);
-        mma_commit_w(&kv_empty[s]);
+        mma_commit_w(&k_empty[s]);
+        TRACE(52, j);
       }
       mma_commit_w(done);
     }
@@ -1471,27 +1500,47 @@ __global__ void __launch_bounds__(320, 1)
     const float sl2 = p.scale_log2;
     for (int j = 0; j < nkv; ++j) {
       const bool diag = (j == i);
-      mbar_wait(st_full, j & 1);
+      mbar_wait(s_full, j & 1);
+      TRACE(60, j);
       tc_fence_after();
+      // all of this warp's S columns first, then S(j+1) may overwrite them
+      uint32_t sv[2][32];
+      tmem_ld32(tS + lrow + half * 64, sv[0]);
+      tmem_ld32(tS + lrow + half * 64 + 32, sv[1]);
+      tmem_wait_ld();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(s_empty);
+      TRACE(61, j);
 #pragma unroll
       for (int qq = 0; qq < 2; ++qq) {
-        uint32_t sv[32], dv[32];
-        tmem_ld32(tS + lrow + half * 64 + qq * 32, sv);
-        tmem_ld32(tdP + lrow + half * 64 + qq * 32, dv);
-        tmem_wait_ld();
-        if (qq == 1) {
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(st_empty);
-        }
         const int k0 = half * 64 + qq * 32;
 #pragma unroll
         for (int e = 0; e < 32; ++e) {
-          float pv = ex2(fmaf(__uint_as_float(sv[e]), sl2, -lse2));
+          float pv = ex2(fmaf(__uint_as_float(sv[qq][e]), sl2, -lse2));
           if (diag && k0 + e > r) pv = 0.f;  // key after query: masked
-          dv[e] = __float_as_uint(pv * fmaf(__uint_as_float(dv[e]), p.scale, -dd));  // scaled dS
+          sv[qq][e] = __float_as_uint(pv);
         }
+      }
+      mbar_wait(dp_full, j & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int qq = 0; qq < 2; ++qq) {
+        uint32_t dv[32];
+        tmem_ld32(tdP + lrow + half * 64 + qq * 32, dv);
+        tmem_wait_ld();
+        TRACE(61 + 3 * qq, j);
+        if (qq == 1) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(dp_empty);
+        }
+#pragma unroll
+        for (int e = 0; e < 32; ++e)  // scaled dS
+          dv[e] = __float_as_uint(__uint_as_float(sv[qq][e]) * fmaf(__uint_as_float(dv[e]), p.scale, -dd));
+        TRACE(62 + 3 * qq, j);
         if (qq == 0 && j > 0) mbar_wait(pds_empty, (j - 1) & 1);  // dQ(j-1) has read dS(j-1)
+        if (qq == 0) TRACE(63, j);
         uint32_t zw[16];
 #pragma unroll
         for (int e = 0; e < 16; ++e) zw[e] = pack_bf16x2(__uint_as_float(dv[2 * e]), __uint_as_float(dv[2 * e + 1]));
@@ -1501,6 +1550,7 @@ __global__ void __launch_bounds__(320, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(pds_full);
+      TRACE(66, j);
     }
     // dQ (TMEM) * scale -> bf16 -> smem (Q / dO are free once every MMA retired) -> TMA store
     mbar_wait(done, 0);

@@ -15,7 +15,7 @@ sys.path.insert(0, ROOT)
 from paper_2602_08387_b200 import _lib, ops  # noqa: E402
 
 B, T, Hq, Hkv = (int(x) for x in sys.argv[1:5])
-dh = 64
+dh = int(os.environ.get("DH", "64"))  # 128: traces the dQ kernel (attn_bwd_q_kernel)
 qkv = torch.randn(B * T, (Hq + 2 * Hkv) * dh, device="cuda").bfloat16()
 o, lse = ops.attn_fwd(qkv, B, T, Hq, Hkv, dh)
 do = torch.randn_like(o)
@@ -27,7 +27,7 @@ buf = np.zeros((CTAS, WARPS, RECS, 2), dtype=np.uint64)
 lib = _lib.load()
 lib.b2s_attn_trace_read.argtypes = [ctypes.c_void_p, ctypes.c_int64]
 assert lib.b2s_attn_trace_read(buf.ctypes.data, buf.nbytes) == 0
-NAMES = {50: "S_issued", 51: "pds_full_seen", 52: "dVdKdQ_issued", 60: "st_full_seen", 61: "ld0_done",
+NAMES = {50: "S_issued", 51: "pds_full_seen", 52: "dQ_issued" if dh == 128 else "dVdKdQ_issued", 60: "st_full_seen", 61: "ld0_done",
          62: "pds0_done", 63: "pds_empty_seen", 64: "ld1_done", 65: "pds1_done", 66: "pds_arrived",
          67: "dq_full_seen", 68: "drain_done", 70: "Q_load_issued", 71: "qd_full_seen", 72: "st_empty_seen"}
 t0 = 0
