@@ -1,0 +1,91 @@
+// TMEM store throughput by tcgen05.st shape (32x32b.x16 / .x32 / .x64 / .x128, 16x256b.x8 / .x16),
+// W warps each storing its lane quarter then tcgen05.wait::st, in a loop; bytes per clock per SM.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tmem_st tmem_st.cu && ./tmem_st
+#include <cstdint>
+#include <cstdio>
+#include <cuda_runtime.h>
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+template <int OP>
+__device__ __forceinline__ void st(uint32_t taddr, const uint32_t* r) {
+  if constexpr (OP == 0)
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
+                 ::"r"(taddr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+                 "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]) : "memory");
+  if constexpr (OP == 1)
+    asm volatile("tcgen05.st.sync.aligned.16x256b.x4.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
+                 ::"r"(taddr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+                 "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]) : "memory");
+  if constexpr (OP == 2)
+    asm volatile("tcgen05.st.sync.aligned.16x128b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
+                 ::"r"(taddr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+                 "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]) : "memory");
+  if constexpr (OP == 3)
+    asm volatile("tcgen05.st.sync.aligned.16x64b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
+                 ::"r"(taddr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+                 "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]) : "memory");
+}
+
+// every variant stores 16 registers per thread = 2 KB per warp per instruction
+template <int OP, int NST>
+__global__ void k(uint32_t* out, long long* cyc, int iters) {
+  __shared__ uint32_t slot;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t base = slot + ((uint32_t)((warp & 3) * 32) << 16) + (warp >> 2) * 128;
+  uint32_t r[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) r[i] = lane * 16 + i;
+  __syncthreads();
+  long long t0 = clock64();
+  for (int it = 0; it < iters; ++it) {
+    r[it & 15] += 1;
+#pragma unroll
+    for (int s = 0; s < NST; ++s) st<OP>(base + s * 16, r);
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  }
+  long long t1 = clock64();
+  __syncthreads();
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+  out[blockIdx.x * blockDim.x + threadIdx.x] = r[0];
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(slot));
+}
+
+template <int OP, int NST>
+void run(const char* name, int warps) {
+  const int blocks = 148, iters = 2048;
+  uint32_t* out;
+  long long* cyc;
+  cudaMalloc(&out, blocks * 1024 * 4);
+  cudaMalloc(&cyc, blocks * 8);
+  k<OP, NST><<<blocks, warps * 32>>>(out, cyc, 16);
+  k<OP, NST><<<blocks, warps * 32>>>(out, cyc, iters);
+  cudaError_t e = cudaDeviceSynchronize();
+  long long h[148];
+  cudaMemcpy(h, cyc, sizeof(h), cudaMemcpyDeviceToHost);
+  double m = 0;
+  for (int i = 0; i < blocks; ++i) m += h[i];
+  m /= blocks;
+  const double bytes = (double)warps * 2048 * NST * iters;
+  printf("%-22s x%d per wait  warps %2d: %6.1f B/clk/SM (%s)\n", name, NST, warps, bytes / m, cudaGetErrorString(e));
+  cudaFree(out);
+  cudaFree(cyc);
+}
+
+int main() {
+  for (int w : {4, 8}) run<0, 1>("32x32b.x16", w);
+  for (int w : {4, 8}) run<0, 4>("32x32b.x16", w);
+  for (int w : {4, 8}) run<1, 4>("16x256b.x4", w);
+  for (int w : {4, 8}) run<2, 4>("16x128b.x8", w);
+  for (int w : {4, 8}) run<3, 4>("16x64b.x16", w);
+  return 0;
+}
