@@ -27,7 +27,17 @@ __device__ __forceinline__ void st(uint32_t taddr, const uint32_t* r) {
                  "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]) : "memory");
 }
 
-// every variant stores 16 registers per thread = 2 KB per warp per instruction
+template <int OP>
+__device__ __forceinline__ void st32(uint32_t taddr, const uint32_t* r) {  // 32x32b.x32: 4 KB per warp
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+               "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};"
+               ::"r"(taddr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+               "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]),
+               "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+               "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]) : "memory");
+}
+
+// every variant stores 16 registers per thread = 2 KB per warp per instruction (OP 9: x32, 4 KB)
 template <int OP, int NST>
 __global__ void k(uint32_t* out, long long* cyc, int iters) {
   __shared__ uint32_t slot;
@@ -48,7 +58,10 @@ __global__ void k(uint32_t* out, long long* cyc, int iters) {
   for (int it = 0; it < iters; ++it) {
     r[it & 15] += 1;
 #pragma unroll
-    for (int s = 0; s < NST; ++s) st<OP>(base + s * 16, r);
+    for (int s = 0; s < NST; ++s) {
+      if constexpr (OP == 9) st32<0>(base + s * 32, r);
+      else st<OP>(base + s * 16, r);
+    }
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
   }
   long long t1 = clock64();
@@ -75,7 +88,7 @@ void run(const char* name, int warps) {
   double m = 0;
   for (int i = 0; i < blocks; ++i) m += h[i];
   m /= blocks;
-  const double bytes = (double)warps * 2048 * NST * iters;
+  const double bytes = (double)warps * (OP == 9 ? 4096 : 2048) * NST * iters;
   printf("%-22s x%d per wait  warps %2d: %6.1f B/clk/SM (%s)\n", name, NST, warps, bytes / m, cudaGetErrorString(e));
   cudaFree(out);
   cudaFree(cyc);
@@ -84,6 +97,8 @@ void run(const char* name, int warps) {
 int main() {
   for (int w : {4, 8}) run<0, 1>("32x32b.x16", w);
   for (int w : {4, 8}) run<0, 4>("32x32b.x16", w);
+  for (int w : {4, 8}) run<9, 2>("32x32b.x32", w);
+  for (int w : {4, 8}) run<9, 1>("32x32b.x32", w);
   for (int w : {4, 8}) run<1, 4>("16x256b.x4", w);
   for (int w : {4, 8}) run<2, 4>("16x128b.x8", w);
   for (int w : {4, 8}) run<3, 4>("16x64b.x16", w);
