@@ -1109,6 +1109,9 @@ __global__ void __launch_bounds__(320, 1)
   uint32_t* tslot = reinterpret_cast<uint32_t*>(st_ld_empty + LS);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#ifdef B2S_ATTN_TRACE
+  int tr_n = 0;
+#endif
   // block order: see attn_bwd_kernel
   const int nbk = p.B * p.Hkv;
   const int gc = nbk < kBwdGroups ? nbk : kBwdGroups;
@@ -1202,6 +1205,7 @@ __global__ void __launch_bounds__(320, 1)
       const int qs = t % QS;
       const uint32_t q_ = aQ + qs * kTQ, do_ = adO + qs * kTQ;
       mbar_wait(pds_full, t & 1);
+      TRACE(51, t);
       tc_fence_after();
       // K step kk = queries 16kk.. : warp half kk >> 2, pass (kk >> 1) & 1, 8 packed columns
 #pragma unroll
@@ -1210,6 +1214,7 @@ __global__ void __launch_bounds__(320, 1)
         mma_bf16_ts_w(tdV, tS + col, make_sdesc(do_ + kk * 2048, kTile, 1024), idKM, (t > 0 || kk > 0));
       }
       if (t + 1 < nsteps) issue_S(t + 1);  // after dV(t) read P^T(t) from these columns
+      TRACE(50, t + 1);
 #pragma unroll
       for (int kk = 0; kk < BQ / 16; ++kk) {
         const uint32_t col = 64 * (kk >> 2) + 32 * ((kk >> 1) & 1) + (kk & 1) * 8;
@@ -1217,6 +1222,7 @@ __global__ void __launch_bounds__(320, 1)
       }
       mma_commit_w(&qd_empty[qs]);
       if (t + 1 < nsteps) issue_dP(t + 1);  // after dK(t) read dS^T(t)
+      TRACE(52, t);
     }
     mma_commit_w(done);
     __syncwarp();
@@ -1233,6 +1239,7 @@ __global__ void __launch_bounds__(320, 1)
       const float* lse2 = sLse + (t % LS) * BQ;
       const float* dd = sD + (t % LS) * BQ;
       mbar_wait(s_full, t & 1);
+      TRACE(60, t);
       tc_fence_after();
       // P^T = 2^(s scale log2e - lse2[q]) for this warp's 64 query columns: fp32 kept for dS,
       // bf16 pairs stored over the S^T columns just read
@@ -1260,7 +1267,9 @@ __global__ void __launch_bounds__(320, 1)
         tmem_st16(tS + lrow + half * 64 + qq * 32, pw);
       }
       // dS^T = P^T (scale dP^T - D') once dP(t) lands, bf16 pairs over the dP^T columns just read
+      TRACE(62, t);
       mbar_wait(dp_full, t & 1);
+      TRACE(63, t);
       tc_fence_after();
 #pragma unroll
       for (int qq = 0; qq < 2; ++qq) {
@@ -1289,6 +1298,7 @@ __global__ void __launch_bounds__(320, 1)
         mbar_arrive(pds_full);
         mbar_arrive(&st_ld_empty[t % LS]);
       }
+      TRACE(66, t);
     }
     // dK (from the pre-scaled dS) and dV -> bf16 -> smem (the Q / dO stages are free) -> TMA store
     mbar_wait(done, 0);
@@ -1381,8 +1391,13 @@ __global__ void __launch_bounds__(320, 1)
   uint32_t* tslot = reinterpret_cast<uint32_t*>(done + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-#ifdef B2S_ATTN_TRACE
+#if defined(B2S_ATTN_TRACE) && !defined(B2S_TRACE_KV)
   int tr_n = 0;
+#else
+#undef TRACE
+#define TRACE(ev, aux) \
+  do {                 \
+  } while (0)
 #endif
   const int nbh = p.B * p.Hq;
   const int i = p.nqt - 1 - (int)(blockIdx.x / nbh);  // heaviest query tiles first

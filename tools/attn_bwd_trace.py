@@ -15,7 +15,8 @@ sys.path.insert(0, ROOT)
 from paper_2602_08387_b200 import _lib, ops  # noqa: E402
 
 B, T, Hq, Hkv = (int(x) for x in sys.argv[1:5])
-dh = int(os.environ.get("DH", "64"))  # 128: traces the dQ kernel (attn_bwd_q_kernel)
+dh = int(os.environ.get("DH", "64"))  # 128: traces the dQ kernel (attn_bwd_q_kernel), or with
+# B2S_TRACE_KV=1 the dK / dV kernel (attn_bwd128_kernel; build the trace variant with -DB2S_TRACE_KV)
 qkv = torch.randn(B * T, (Hq + 2 * Hkv) * dh, device="cuda").bfloat16()
 o, lse = ops.attn_fwd(qkv, B, T, Hq, Hkv, dh)
 do = torch.randn_like(o)
