@@ -1076,7 +1076,8 @@ __global__ void __launch_bounds__(320, 1)
 // just read (pass qq of warp half h: columns 64h + 32qq + [0, 16) of each block, bf16 pairs):
 // no P^T / dS^T shared-memory tiles, which leaves room for two Q / dO stages -- with one, every
 // step waited for its Q / dO reload (~3000 clk) behind the previous step's MMAs -- and dV / dK
-// run in the TMEM-A MMA form. MMA order per step t: dV(t) S(t+1) dK(t) dP(t+1): the tensor pipe
+// run in the TMEM-A MMA form. MMA order per step t: dV(t) S(t+1) dK(t) dP(t+1), dV(t) as soon as
+// P^T(t) is stored (p_full), so dV(t) and S(t+1) run while dS(t) is formed: the tensor pipe
 // runs one thread's MMAs in order, so S(t+1) overwrites P^T(t) after dV(t) read it and dP(t+1)
 // overwrites dS^T(t) after dK(t), while the compute warps start P(t+1) as soon as S(t+1) lands.
 struct Bwd128 {
@@ -1102,9 +1103,10 @@ __global__ void __launch_bounds__(320, 1)
   uint64_t* qd_empty = qd_full + QS;      // [QS]
   uint64_t* s_full = qd_empty + QS;
   uint64_t* dp_full = s_full + 1;
-  uint64_t* pds_full = s_full + 2;
-  uint64_t* done = s_full + 3;
-  uint64_t* st_ld_full = s_full + 4;        // [LS]
+  uint64_t* p_full = s_full + 2;   // P^T(t) written over the S^T columns (dV(t), then S(t+1) may go)
+  uint64_t* ds_full = s_full + 3;  // dS^T(t) written over the dP^T columns (dK(t), then dP(t+1))
+  uint64_t* done = s_full + 4;
+  uint64_t* st_ld_full = s_full + 5;        // [LS]
   uint64_t* st_ld_empty = st_ld_full + LS;  // [LS]
   uint32_t* tslot = reinterpret_cast<uint32_t*>(st_ld_empty + LS);
 
@@ -1133,7 +1135,8 @@ __global__ void __launch_bounds__(320, 1)
     for (int s = 0; s < QS; ++s) { mbar_init(&qd_full[s], 1); mbar_init(&qd_empty[s], 1); }
     mbar_init(s_full, 1);
     mbar_init(dp_full, 1);
-    mbar_init(pds_full, 8);
+    mbar_init(p_full, 8);
+    mbar_init(ds_full, 8);
     mbar_init(done, 1);
     for (int s = 0; s < LS; ++s) { mbar_init(&st_ld_full[s], 1); mbar_init(&st_ld_empty[s], 8); }
     fence_barrier_init();
@@ -1204,7 +1207,7 @@ __global__ void __launch_bounds__(320, 1)
     for (int t = 0; t < nsteps; ++t) {
       const int qs = t % QS;
       const uint32_t q_ = aQ + qs * kTQ, do_ = adO + qs * kTQ;
-      mbar_wait(pds_full, t & 1);
+      mbar_wait(p_full, t & 1);  // dV(t) and S(t+1) overlap the dS phase of step t
       TRACE(51, t);
       tc_fence_after();
       // K step kk = queries 16kk.. : warp half kk >> 2, pass (kk >> 1) & 1, 8 packed columns
@@ -1215,6 +1218,8 @@ __global__ void __launch_bounds__(320, 1)
       }
       if (t + 1 < nsteps) issue_S(t + 1);  // after dV(t) read P^T(t) from these columns
       TRACE(50, t + 1);
+      mbar_wait(ds_full, t & 1);
+      tc_fence_after();
 #pragma unroll
       for (int kk = 0; kk < BQ / 16; ++kk) {
         const uint32_t col = 64 * (kk >> 2) + 32 * ((kk >> 1) & 1) + (kk & 1) * 8;
@@ -1267,6 +1272,10 @@ __global__ void __launch_bounds__(320, 1)
         tmem_st16(tS + lrow + half * 64 + qq * 32, pw);
       }
       // dS^T = P^T (scale dP^T - D') once dP(t) lands, bf16 pairs over the dP^T columns just read
+      tmem_wait_st();  // P^T is in TMEM before the MMA warp is told
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p_full);
       TRACE(62, t);
       mbar_wait(dp_full, t & 1);
       TRACE(63, t);
@@ -1291,11 +1300,11 @@ __global__ void __launch_bounds__(320, 1)
         for (int k = 0; k < 16; ++k) zw[k] = pack_bf16x2(__uint_as_float(dv[2 * k]), __uint_as_float(dv[2 * k + 1]));
         tmem_st16(tdP + lrow + half * 64 + qq * 32, zw);
       }
-      tmem_wait_st();  // P^T / dS^T are in TMEM before the MMA warp is told
+      tmem_wait_st();  // dS^T is in TMEM before the MMA warp is told
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
-        mbar_arrive(pds_full);
+        mbar_arrive(ds_full);
         mbar_arrive(&st_ld_empty[t % LS]);
       }
       TRACE(66, t);
