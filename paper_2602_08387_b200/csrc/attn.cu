@@ -15,9 +15,13 @@
 //
 // Backward CTA = (batch, kv head, 128-key tile), looping over the q heads of
 // its group and the causal query tiles: S^T = K Q^T, dP^T = V dO^T (TMEM),
-// P^T and dS^T = P^T (dP^T - D) to smem (thread = key row), then
-// dV += P^T dO, dK += dS^T Q (TMEM accumulators across the loop) and
-// dQ_i = dS K (TMEM) -> fp32 smem -> TMA add-reduce into a dQ accumulator.
+// P^T and dS^T = P^T (dP^T - D) (thread = key row), then dV += P^T dO, dK += dS^T Q
+// (TMEM accumulators across the loop).
+//   dh 64 (attn_bwd_kernel): P^T to TMEM (TMEM-A dV), dS^T to smem, and dQ_i = dS K fused
+//   (TMEM) -> fp32 smem -> TMA add-reduce into a dQ accumulator.
+//   dh 128 (attn_bwd128_kernel + attn_bwd_q_kernel): the key-tile kernel writes P^T / dS^T back
+//   over the S^T / dP^T columns (TMEM-A dV and dK), and a query-tile kernel recomputes S / dP
+//   and accumulates dQ in TMEM (dS in TMEM, TMEM-A dQ MMA).
 #include <mutex>
 #include "common.cuh"
 #include "sm100.cuh"
