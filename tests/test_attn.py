@@ -21,7 +21,9 @@ def _ref(qkv, B, T, Hq, Hkv, dh):
     return o.transpose(1, 2).reshape(B * T, Hq * dh), lse
 
 
-CASES = [(1, 128, 1, 1), (2, 256, 4, 2), (1, 512, 3, 3), (2, 384, 8, 2)]
+# the last two wrap the kernels' stage rings many times (Q / dO x3, lse / D x4, K x3 / V x2 at
+# dh 128) and cover an 8:1 GQA group and three sequences
+CASES = [(1, 128, 1, 1), (2, 256, 4, 2), (1, 512, 3, 3), (2, 384, 8, 2), (3, 1024, 8, 1), (1, 2048, 2, 2)]
 
 
 @pytest.mark.parametrize("dh", [64, 128])
