@@ -112,11 +112,11 @@ def _optimizer(lr=3e-4, beta1=0.9, beta2=0.95, eps=1e-8, weight_decay=0.1, grad_
 
 
 def _trainer(model, optimizer, dataloader, steps=20, seed=0, blocks_per_unit=1, init_device="cpu",
-             log_every=0):
+             log_every=0, metrics_path=None):
     from .trainer import SPMDTrainer
 
     return SPMDTrainer(model, optimizer, dataloader, steps=steps, seed=seed, blocks_per_unit=blocks_per_unit,
-                       init_device=init_device, log_every=log_every)
+                       init_device=init_device, log_every=log_every, metrics_path=metrics_path)
 
 
 def _planner(model, dp, alpha=1e-5, bandwidth=7.7e11, memory_cap_bytes=1 << 30):
@@ -197,7 +197,8 @@ def default_registry() -> Registry:
          P("dataloader", "dependency", interface="dataloader"), P("steps", "int", required=False, default=20),
          P("seed", "int", required=False, default=0), P("blocks_per_unit", "int", required=False, default=1),
          P("init_device", "string", required=False, default="cpu"),
-         P("log_every", "int", required=False, default=0)), _trainer))
+         P("log_every", "int", required=False, default=0),
+         P("metrics_path", "string", required=False, default=None)), _trainer))
     r.register_component(FactoryDescriptor(
         "planner", "fsdp_comm",
         (P("model", "dependency", interface="model"), P("dp", "int"),

@@ -17,6 +17,7 @@ collectives. A step is:
 from __future__ import annotations
 
 import atexit
+import json
 import os
 import time
 import weakref
@@ -29,6 +30,10 @@ from .data import PackedDataLoader
 from .fsdp import Engine, FlatParams
 from .model import DecoderLM, param_initializer
 from .optim import AdamWConfig, FusedAdamW
+
+# dense bf16 peak the per-step MFU is quoted against: the burst figure measured on this pool's
+# B200s (MEASURED_PEAKS.json, which bench.py reads; 2.25 PF/s is the nominal datasheet number)
+BF16_PEAK_FLOPS = 1639.2e12
 
 
 def init_distributed():
@@ -98,7 +103,7 @@ class _NativeGraph:
 class SPMDTrainer:
     def __init__(self, model: DecoderLM, optimizer, dataloader: PackedDataLoader, steps: int = 20,
                  seed: int = 0, blocks_per_unit: int = 1, init_device: str = "cpu", log_every: int = 0,
-                 cuda_graph: bool = True):
+                 cuda_graph: bool = True, metrics_path: str | None = None):
         self.model = model
         self.opt_cfg = optimizer if isinstance(optimizer, AdamWConfig) else optimizer.cfg
         self.dataloader = dataloader
@@ -107,6 +112,9 @@ class SPMDTrainer:
         self.blocks_per_unit = blocks_per_unit
         self.init_device = init_device
         self.log_every = log_every
+        # rank 0 appends one JSON line per step of run(): loss, step ms, tokens/s/GPU, MFU, lr,
+        # and at W > 1 the FSDP bytes all-gathered / reduce-scattered per step
+        self.metrics_path = metrics_path
         # single GPU: after two eager steps the forward+backward (~350 launches) is
         # captured once as a CUDA graph and replayed (optimizer stays eager: its
         # learning rate / bias corrections are per-step host scalars)
@@ -158,7 +166,8 @@ class SPMDTrainer:
             if multi:
                 with torch.cuda.graph(g):
                     self.engine.in_graph = True
-                    ops.zero_(self.engine.P.gall)
+                    for o, n in self.engine.zero_ranges:  # the ranges begin_step zeroes
+                        ops.zero_(self.engine.P.gall[o:o + n])
                     self._gloss = self.model.forward_backward(self._gx, self._gy, hooks=self.engine)
                     self.engine.end_backward()  # joins the comm stream back into the capture
                     self.engine.in_graph = False
@@ -231,10 +240,28 @@ class SPMDTrainer:
         self.setup()
         losses = []
         t0 = time.perf_counter()
-        for g in range(self.steps):
-            loss = self.train_step(g)
-            losses.append(float(loss.item()))
-            if self.log_every and self.rank == 0 and (g % self.log_every == 0 or g == self.steps - 1):
-                print(f"step {g:5d}  loss {losses[-1]:.4f}  {time.perf_counter() - t0:.1f}s", flush=True)
+        mf = open(self.metrics_path, "a") if (self.metrics_path and self.rank == 0) else None
+        cfg, B, T = self.model.cfg, self.dataloader.batch_size, self.dataloader.seq_len
+        try:
+            for g in range(self.steps):
+                ts = time.perf_counter()
+                loss = self.train_step(g)
+                losses.append(float(loss.item()))  # synchronises: the step's wall time is complete
+                dt = time.perf_counter() - ts
+                if mf is not None:
+                    tps = B * T / dt
+                    rec = {"step": g, "loss": losses[-1], "step_ms": round(dt * 1e3, 3),
+                           "tokens_per_s_per_gpu": round(tps, 1),
+                           "mfu": round(tps * cfg.flops_per_token(T) / BF16_PEAK_FLOPS, 4),
+                           "lr": self.opt_cfg.lr_at(g + 1), "world": self.world}
+                    if self.world > 1:
+                        rec.update(ag_bytes=self.engine.bytes_ag, rs_bytes=self.engine.bytes_rs)
+                    mf.write(json.dumps(rec) + "\n")
+                    mf.flush()
+                if self.log_every and self.rank == 0 and (g % self.log_every == 0 or g == self.steps - 1):
+                    print(f"step {g:5d}  loss {losses[-1]:.4f}  {time.perf_counter() - t0:.1f}s", flush=True)
+        finally:
+            if mf is not None:
+                mf.close()
         self.close()  # a later run() re-captures; the process group can be torn down now
         return losses

@@ -24,7 +24,9 @@ def test_yaml_trainer_run_matches_oracle(cuda, tmp_path):
 
     text = open(os.path.join(ROOT, "configs", "tiny_llama_parity.yaml")).read()
     data = str(tmp_path / "markov.cfpk")
-    graph = cg.load(text, default_registry(), roots=["trainer"], overrides=[f"data.config.path={data}"])
+    metrics = str(tmp_path / "metrics.jsonl")
+    graph = cg.load(text, default_registry(), roots=["trainer"],
+                    overrides=[f"data.config.path={data}", f"trainer.config.metrics_path={metrics}"])
     tr = graph["trainer"]
     assert isinstance(tr, SPMDTrainer)
     # fan-in: the trainer's dataloader is the graph's single `loader` instance
@@ -47,3 +49,10 @@ def test_yaml_trainer_run_matches_oracle(cuda, tmp_path):
     rel = [abs(a - b) / b for a, b in zip(losses, ref)]
     assert max(rel) < 0.02, list(zip(losses, ref))
     assert losses[-1] < losses[0] - 0.3
+    # the per-step metrics log: one JSON line per step, losses as returned
+    import json
+
+    recs = [json.loads(line) for line in open(metrics)]
+    assert [r["step"] for r in recs] == list(range(tr.steps))
+    assert all(abs(r["loss"] - lo) < 1e-6 for r, lo in zip(recs, losses))
+    assert all(r["step_ms"] > 0 and r["tokens_per_s_per_gpu"] > 0 and 0 < r["mfu"] < 1 for r in recs)
