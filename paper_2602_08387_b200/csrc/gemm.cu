@@ -103,8 +103,12 @@ struct Epi {
   int rope_T, rope_dh, rope_cols;
 };
 
+// sigmoid as MUFU.EX2 + MUFU.RCP (approximate reciprocal, ~1 ulp): the IEEE __frcp_rn adds
+// Newton steps and a special-case subroutine call per element to the SwiGLU epilogues
 __device__ __forceinline__ float silu_sig(float g, float& sg) {
-  sg = __frcp_rn(1.f + __expf(-g));
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(1.f + __expf(-g)));
+  sg = y;
   return g * sg;
 }
 
