@@ -78,6 +78,26 @@ __device__ __forceinline__ void from_f(__nv_bfloat16& d, float v) { d = f2bf(v);
 __device__ __forceinline__ void from_f(float& d, float v) { d = v; }
 
 
+// Four elements loaded without conversion (bf16: one 8-byte load), converted at first use, so
+// the load can stay in flight across other work.
+template <typename T>
+struct Raw4;
+template <>
+struct Raw4<__nv_bfloat16> {
+  uint2 v;
+  __device__ __forceinline__ void ld(const __nv_bfloat16* p) { v = *reinterpret_cast<const uint2*>(p); }
+  __device__ __forceinline__ void get(float* f) const {
+    f[0] = __uint_as_float(v.x << 16); f[1] = __uint_as_float(v.x & 0xffff0000u);
+    f[2] = __uint_as_float(v.y << 16); f[3] = __uint_as_float(v.y & 0xffff0000u);
+  }
+};
+template <>
+struct Raw4<float> {
+  float4 v;
+  __device__ __forceinline__ void ld(const float* p) { v = ld4(p); }
+  __device__ __forceinline__ void get(float* f) const { f[0] = v.x; f[1] = v.y; f[2] = v.z; f[3] = v.w; }
+};
+
 // ------------------------------------------------------------------ norms
 // y = (x - mean) * rstd * g (+ b)  [LayerNorm]   or   y = x * rstd * g  [RMSNorm]
 // x fp32 [M, D] (the residual stream), y bf16; optional x_copy (forward the
@@ -111,8 +131,12 @@ __device__ __forceinline__ float row_sum(float v, float* scratch, int& toggle) {
 // res (optional): the sublayer output y_prev [M, D] (activation type) to add to x
 // first -- the residual add of the previous GEMM; x_copy then receives x + res
 // (the new residual stream), which is what gets normalised.
+// Block-per-row form (TPR 256, D >= 2048): the next row's loads are prefetched and the kernel
+// is held to 64 registers (4 blocks per SM): Llama-1B RMSNorm 62.1 -> 56.1 us (0.82 -> 0.91 of
+// HBM), with the residual add 68.5 -> 67.1 us. The warp-per-row form (D <= 1024) loads the
+// current row as before: prefetching there measured slower (GPT-2 LayerNorm 23.6 -> 29.5 us).
 template <int D, int TPR, bool RMS, typename T = __nv_bfloat16>
-__global__ void __launch_bounds__(kRowThreads) norm_fwd_kernel(
+__global__ void __launch_bounds__(kRowThreads, TPR >= 256 ? 4 : 1) norm_fwd_kernel(
     const float* __restrict__ x, const T* __restrict__ g, const T* __restrict__ b,
     T* __restrict__ y, float* __restrict__ mean_out, float* __restrict__ rstd_out,
     float* __restrict__ x_copy, int64_t M, float eps, const T* __restrict__ res) {
@@ -129,20 +153,34 @@ __global__ void __launch_bounds__(kRowThreads) norm_fwd_kernel(
     ld_v4(g + t * 4 + j * TPR * 4, gv[j]);
     if (!RMS) ld_v4(b + t * 4 + j * TPR * 4, bv[j]);
   }
+  // PF: the next row's x / res loads are issued before this row's reductions and stores (kept
+  // raw in registers until then), so a block keeps HBM reads in flight through its two row syncs
+  constexpr bool PF = TPR >= 256;
+  float4 xn[V];
+  Raw4<T> rn[V];
+  auto fetch = [&](int64_t row) {
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      xn[j] = ld4(x + row * D + t * 4 + j * TPR * 4);
+      if (res) rn[j].ld(res + row * D + t * 4 + j * TPR * 4);
+    }
+  };
+  if (PF && r0 < M) fetch(r0);
   for (int64_t row = r0; row < M; row += nr) {
-    const float* xr = x + row * D;
+    if (!PF) fetch(row);
     float4 xv[V];
     float s = 0.f, ss = 0.f;
 #pragma unroll
     for (int j = 0; j < V; ++j) {
-      xv[j] = ld4(xr + t * 4 + j * TPR * 4);
+      xv[j] = xn[j];
       if (res) {
         float r4[4];
-        ld_v4(res + row * D + t * 4 + j * TPR * 4, r4);
+        rn[j].get(r4);
         xv[j].x += r4[0]; xv[j].y += r4[1]; xv[j].z += r4[2]; xv[j].w += r4[3];
       }
       s += xv[j].x + xv[j].y + xv[j].z + xv[j].w;
     }
+    if (PF && row + nr < M) fetch(row + nr);
     if (x_copy) {
 #pragma unroll
       for (int j = 0; j < V; ++j) st4(x_copy + row * D + t * 4 + j * TPR * 4, xv[j]);

@@ -41,6 +41,9 @@ for D, M in ((768, 16384), (2048, 16384)):
             M * D * (4 + 2 + 4 + 4 + 2))
     else:
         rec(f"rmsnorm_fwd D={D}", time_it(lambda: ops.rmsnorm_fwd(x, g, 1e-5, y, rstd, x_copy=xc)), M * D * (4 + 2 + 4))
+        yr = torch.randn(M, D, device=dev).bfloat16()
+        rec(f"rmsnorm_fwd+res D={D}", time_it(lambda: ops.rmsnorm_fwd_res(x, yr, g, 1e-5, y, rstd, xc)),
+            M * D * (4 + 2 + 4 + 2))
         rec(f"rmsnorm_bwd D={D}", time_it(lambda: ops.rmsnorm_bwd(x, dy, g, rstd, dx, dxb, dg, ds)),
             M * D * (4 + 2 + 4 + 4 + 2))
 cfg = PRESETS["llama-1b"]
