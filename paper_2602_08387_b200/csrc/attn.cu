@@ -620,14 +620,18 @@ __global__ void attn_bwd_prep_kernel(const __nv_bfloat16* __restrict__ o, const 
                                      const float* __restrict__ lse, float* __restrict__ dsum,
                                      float* __restrict__ lse2, float* __restrict__ dq_acc, int B, int T, int Hq,
                                      float scale) {
-  // DH/8 lanes per (row, head): each lane a 16-byte vector of o and dO
+  // DH/8 lanes per (row, head): each lane a 16-byte vector of o and dO. Work items run in the
+  // [b, h, t] order of lse / D' (t fastest), so those 4-byte reads and writes coalesce across
+  // consecutive items; each item's o / dO / dQ slices are whole 128 / 256-byte lines either way.
   constexpr int LPR = DH / 8;
   const int sub = threadIdx.x & (LPR - 1);
   const int64_t nrows = (int64_t)B * T * Hq;
   for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / LPR; w < nrows;
        w += ((int64_t)gridDim.x * blockDim.x) / LPR) {
-    const int64_t row = (int64_t)((uint32_t)w / (uint32_t)Hq);  // B*T*Hq < 2^32 (host-checked)
-    const int h = (int)(w - row * Hq);
+    const uint32_t bh = (uint32_t)w / (uint32_t)T;  // B*T*Hq < 2^32 (host-checked)
+    const int64_t t = (int64_t)((uint32_t)w - bh * (uint32_t)T);
+    const uint32_t b = bh / (uint32_t)Hq, h = bh - b * (uint32_t)Hq;
+    const int64_t row = (int64_t)b * T + t;
     const int64_t off = row * Hq * DH + h * DH + sub * 8;
     float a[8], g[8];
     unpack8(*reinterpret_cast<const bf16x8*>(o + off), a);
@@ -642,10 +646,8 @@ __global__ void attn_bwd_prep_kernel(const __nv_bfloat16* __restrict__ o, const 
       *reinterpret_cast<float4*>(dq_acc + off + 4) = make_float4(0.f, 0.f, 0.f, 0.f);
     }
     if (sub == 0) {
-      const int64_t b = (int64_t)((uint32_t)row / (uint32_t)T), t = row - b * T;
-      const int64_t i = (b * Hq + h) * T + t;
-      dsum[i] = acc * scale;
-      lse2[i] = lse[i] * kLog2e;
+      dsum[w] = acc * scale;  // w = (b * Hq + h) * T + t
+      lse2[w] = lse[w] * kLog2e;
     }
   }
 }
