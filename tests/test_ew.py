@@ -55,6 +55,52 @@ def test_norm_fwd_bwd(cuda, D, rms):
     torch.testing.assert_close(dg, gr.grad, rtol=1e-4, atol=1e-3)
 
 
+@pytest.mark.parametrize("D", [2048, 4096])
+@pytest.mark.parametrize("rms", [False, True])
+@pytest.mark.parametrize("res", [False, True])
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+def test_norm_fwd_many_rows_per_block(cuda, D, rms, res, dtype):
+    """The block-per-row forward (D >= 2048) prefetches the next row of its grid stride: M well
+    above the 4-blocks-per-SM grid, not a multiple of it, so blocks run 3-5 rows and the last
+    stride is ragged; with and without the fused residual add."""
+    from paper_2602_08387_b200 import ops
+
+    torch.manual_seed(D + 2 * rms + res)
+    M = 3 * 1184 + 517
+    x = torch.randn(M, D, device=cuda) * 2 + 0.5
+    r = (torch.randn(M, D, device=cuda)).to(dtype)
+    g = (1 + 0.1 * torch.randn(D, device=cuda)).to(dtype)
+    b = (0.1 * torch.randn(D, device=cuda)).to(dtype)
+    y = torch.empty(M, D, device=cuda, dtype=dtype)
+    rstd = torch.empty(M, device=cuda)
+    mean = torch.empty(M, device=cuda)
+    xo = torch.empty_like(x)
+    if res:
+        if rms:
+            ops.rmsnorm_fwd_res(x, r, g, 1e-5, y, rstd, xo)
+        else:
+            ops.layernorm_fwd_res(x, r, g, b, 1e-5, y, mean, rstd, xo)
+        xs = x + r.float()
+        assert torch.equal(xo, xs)
+    else:
+        if rms:
+            ops.rmsnorm_fwd(x, g, 1e-5, y, rstd, x_copy=xo)
+        else:
+            ops.layernorm_fwd(x, g, b, 1e-5, y, mean, rstd, x_copy=xo)
+        xs = x
+        assert torch.equal(xo, x)
+    if rms:
+        want_rstd = torch.rsqrt(xs.pow(2).mean(-1) + 1e-5)
+        ref = xs * want_rstd[:, None] * g.float()
+    else:
+        want_rstd = torch.rsqrt(xs.var(-1, unbiased=False) + 1e-5)
+        torch.testing.assert_close(mean, xs.mean(-1), rtol=1e-5, atol=1e-5)
+        ref = F.layer_norm(xs, (D,), g.float(), b.float(), 1e-5)
+    torch.testing.assert_close(rstd, want_rstd, rtol=1e-5, atol=1e-6)
+    tol = 1e-2 if dtype == torch.bfloat16 else 1e-5
+    torch.testing.assert_close(y.float(), ref, rtol=tol, atol=2 * tol)
+
+
 @pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
 @pytest.mark.parametrize("M,N,ld", [(16384, 2304, 2304), (16384, 3072, 3072), (777, 520, 1040), (1, 8, 8),
                                     (4096, 16384, 16384)])
