@@ -81,6 +81,33 @@ constexpr int UMMA_K = 16;
 // costs one smem pipeline stage; 8 otherwise.
 constexpr int kStageSlot = 4096;  // one 32x32 fp32 (or bf16) staging sub-tile
 
+// Wait accounting of one launch (experiment builds, -DB2S_GEMM_PROF; tools/gemm_prof.py): per CTA,
+// role 0 = the MMA issuer [total, waits for a free accumulator, for a loaded stage, for the first
+// stage of a tile], role 1 = epilogue warp 2 [total, waits for a finished accumulator, -, tiles],
+// role 2 = the TMA producer [total, tile-index step, waits for a free stage, tiles, of which the
+// leader's wait for a free tile-ring slot]; [4] of role 0 is the first-stage wait.
+#ifdef B2S_GEMM_PROF
+__device__ unsigned long long g_gprof[148][3][5];
+#define GPROF_DECL long long gp_start = clock64(), gp_t0 = 0, gp_w[3] = {0, 0, 0}; int gp_tiles = 0;
+#define GPROF_T0 gp_t0 = clock64();
+#define GPROF_ACC(i) gp_w[i] += clock64() - gp_t0;
+#define GPROF_TILE ++gp_tiles;
+#define GPROF_END(role)                                                                              \
+  if ((threadIdx.x & 31) == 0 && (role != 1 || warp == 2) && blockIdx.x < 148) {                     \
+    g_gprof[blockIdx.x][role][0] = clock64() - gp_start;                                             \
+    g_gprof[blockIdx.x][role][1] = gp_w[1];                                                          \
+    g_gprof[blockIdx.x][role][2] = gp_w[2];                                                          \
+    g_gprof[blockIdx.x][role][3] = gp_tiles;                                                         \
+    g_gprof[blockIdx.x][role][4] = gp_w[0];                                                          \
+  }
+#else
+#define GPROF_DECL
+#define GPROF_T0
+#define GPROF_ACC(i)
+#define GPROF_TILE
+#define GPROF_END(role)
+#endif
+
 constexpr int kRing = 8;  // tile-index ring depth (producer runs ahead of MMA + 2 epilogue buffers)
 
 struct Epi {
@@ -336,24 +363,43 @@ __global__ void __launch_bounds__(Cfg<BN, CG, EW>::kThreads, 1)
       // tile i+1 is issued when tile i starts loading, so its latency is hidden
       const int tstride = gridDim.x / CG;
       int next = blockIdx.x / CG;
+      GPROF_DECL
       for (int it = 0;; ++it) {
         int tile;
+        GPROF_T0
         if (leader) {  // publish the next tile (to the peer CTA too)
           const int slot = it % kRing;
+#ifdef B2S_GEMM_PROF
+          const long long gp_r0 = clock64();
+#endif
           mbar_wait(&rempty[slot], ((it / kRing) & 1) ^ 1);
+#ifdef B2S_GEMM_PROF
+          gp_w[0] += clock64() - gp_r0;
+#endif
           tile = next < num_tiles ? next : num_tiles;  // num_tiles = sentinel: no more work
           ring[slot] = tile;
           mbar_arrive(&rfull[slot]);
           if constexpr (CG == 2) {
+            // to the peer: an asynchronous remote store that completes the transaction count of the
+            // peer's rfull[slot] (whose one arrival is the peer producer's expect_tx) -- no release
+            // fence, so the producer goes straight on to the next tile's loads (a st.shared::cluster
+            // + release-arrive cost ~1000 clk here, in front of every tile's first load)
             const uint32_t peer_slot = mapa_shared(smem_u32(&ring[slot]), 1);
-            asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(peer_slot), "r"(tile) : "memory");
-            mbar_arrive_cluster(mapa_shared(smem_u32(&rfull[slot]), 1));
+            asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.u32 [%0], %1, [%2];" ::"r"(peer_slot),
+                         "r"(tile), "r"(mapa_shared(smem_u32(&rfull[slot]), 1))
+                         : "memory");
           }
         } else {
+          mbar_arrive_expect_tx(&rfull[it % kRing], 4);  // the peer's one arrival; the leader's st.async the bytes
           tile = ring_get(it);
           ring_release(it, tile);
         }
-        if (tile >= num_tiles) break;
+        GPROF_ACC(1)
+        if (tile >= num_tiles) {
+          GPROF_END(2)
+          break;
+        }
+        GPROF_TILE
         if (leader) next = sched ? tstride + atomicAdd(sched, 1) : tile + tstride;
         const int mn = tile % (num_m * num_n), ks = tile / (num_m * num_n);
         int mi, ni;
@@ -364,7 +410,9 @@ __global__ void __launch_bounds__(Cfg<BN, CG, EW>::kThreads, 1)
         const int n0 = SPEC == 3 ? (rank ? epi.glu_F : 0) + ni * (BN / 2) : ni * BN + rank * BNc;
         const int kb0 = ks * kb_per, kb1 = min(num_kb_all, kb0 + kb_per);
         for (int kb = kb0; kb < kb1; ++kb) {
+          GPROF_T0
           mbar_wait(&empty[stage], phase ^ 1);
+          GPROF_ACC(2)
           uint8_t* sa = smem + stage * C_::kStageBytes;
           uint8_t* sb = sa + C_::kABytes;
           const int k0 = kb * BK;
@@ -410,17 +458,25 @@ __global__ void __launch_bounds__(Cfg<BN, CG, EW>::kThreads, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
+      GPROF_DECL
       for (int it = 0;; ++it) {
         const int tile = ring_get(it);
         ring_release(it, tile);
         if (tile >= num_tiles) break;
+        GPROF_T0
         mbar_wait(&tempty[acc], acc_phase ^ 1);
+        GPROF_ACC(1)
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
         const int ks = tile / (num_m * num_n);
         const int kb0 = ks * kb_per, kb1 = min(num_kb_all, kb0 + kb_per);
         for (int kb = kb0; kb < kb1; ++kb) {
+          GPROF_T0
           mbar_wait(&full[stage], phase);
+          GPROF_ACC(2)
+#ifdef B2S_GEMM_PROF
+          if (kb == kb0) gp_w[0] += clock64() - gp_t0;
+#endif
           tc_fence_after();
           const uint32_t sa = smem_u32(smem + stage * C_::kStageBytes);
           const uint32_t sb = sa + C_::kABytes;
@@ -443,7 +499,9 @@ __global__ void __launch_bounds__(Cfg<BN, CG, EW>::kThreads, 1)
         if constexpr (CG == 2) mma_commit_pair(&tfull[acc], 0x3);
         else mma_commit(&tfull[acc]);
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        GPROF_TILE
       }
+      GPROF_END(0)
     }
     __syncwarp();
   } else {
@@ -512,17 +570,24 @@ __global__ void __launch_bounds__(Cfg<BN, CG, EW>::kThreads, 1)
       ++aux_used;
       __syncwarp();  // every lane has read the slot before its next TMA load is issued
     };
+    GPROF_DECL
     for (int it = 0;; ++it) {
       const int tile = ring_get(it);
       __syncwarp();
       if (lane == 0) ring_release(it, tile);
-      if (tile >= num_tiles) break;
+      if (tile >= num_tiles) {
+        GPROF_END(1)
+        break;
+      }
+      GPROF_TILE
       load_aux(tile, half);  // first two chunks' aux tiles: in flight while the MMAs finish
       if (half + kEG < BN / 32) load_aux(tile, half + kEG);
       int mi, ni;
       tile_mn(tile % (num_m * num_n), num_m, num_n, raster, mi, ni);
       const int m0 = mi * BM * CG + rank * BM, n0 = ni * BN;
+      GPROF_T0
       mbar_wait(&tfull[acc], acc_phase);
+      GPROF_ACC(1)
       tc_fence_after();
       const int rbase = m0 + q * 32;
       if constexpr (SPEC == 3) {  // SwiGLU forward: gate chunk c with up chunk c + BN/64 of the same rows
@@ -1064,6 +1129,12 @@ static Choice choose(int M, int N, int K, bool can_split) {
 
 }  // namespace gemm
 }  // namespace b2s
+
+#ifdef B2S_GEMM_PROF
+extern "C" int b2s_gemm_prof_read(unsigned long long* host) {
+  return cudaMemcpyFromSymbol(host, b2s::gemm::g_gprof, sizeof(b2s::gemm::g_gprof)) == cudaSuccess ? 0 : -1;
+}
+#endif
 
 namespace {
 // Shared host path. glu_F / c_width: SwiGLU epilogues (act 3: N = 2F, aux = h [M, F];
