@@ -364,31 +364,35 @@ __global__ void __launch_bounds__(Cfg<BN, CG, EW>::kThreads, 1)
       const int tstride = gridDim.x / CG;
       int next = blockIdx.x / CG;
       GPROF_DECL
+      // leader: tile i -> ring slot i (local readers: rfull arrive; the peer: see below)
+      auto publish = [&](int i, int t) {
+        const int slot = i % kRing;
+#ifdef B2S_GEMM_PROF
+        const long long gp_r0 = clock64();
+#endif
+        mbar_wait(&rempty[slot], ((i / kRing) & 1) ^ 1);
+#ifdef B2S_GEMM_PROF
+        gp_w[0] += clock64() - gp_r0;
+#endif
+        ring[slot] = t;
+        mbar_arrive(&rfull[slot]);
+        if constexpr (CG == 2) {
+          // to the peer: an asynchronous remote store that completes the transaction count of the
+          // peer's rfull[slot] (whose one arrival is the peer producer's expect_tx) -- no release
+          // fence, so the producer goes straight on to the next tile's loads (a st.shared::cluster
+          // + release-arrive cost ~1000 clk here, in front of every tile's first load)
+          const uint32_t peer_slot = mapa_shared(smem_u32(&ring[slot]), 1);
+          asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.u32 [%0], %1, [%2];" ::"r"(peer_slot),
+                       "r"(t), "r"(mapa_shared(smem_u32(&rfull[slot]), 1))
+                       : "memory");
+        }
+      };
       for (int it = 0;; ++it) {
         int tile;
         GPROF_T0
-        if (leader) {  // publish the next tile (to the peer CTA too)
-          const int slot = it % kRing;
-#ifdef B2S_GEMM_PROF
-          const long long gp_r0 = clock64();
-#endif
-          mbar_wait(&rempty[slot], ((it / kRing) & 1) ^ 1);
-#ifdef B2S_GEMM_PROF
-          gp_w[0] += clock64() - gp_r0;
-#endif
+        if (leader) {
           tile = next < num_tiles ? next : num_tiles;  // num_tiles = sentinel: no more work
-          ring[slot] = tile;
-          mbar_arrive(&rfull[slot]);
-          if constexpr (CG == 2) {
-            // to the peer: an asynchronous remote store that completes the transaction count of the
-            // peer's rfull[slot] (whose one arrival is the peer producer's expect_tx) -- no release
-            // fence, so the producer goes straight on to the next tile's loads (a st.shared::cluster
-            // + release-arrive cost ~1000 clk here, in front of every tile's first load)
-            const uint32_t peer_slot = mapa_shared(smem_u32(&ring[slot]), 1);
-            asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.u32 [%0], %1, [%2];" ::"r"(peer_slot),
-                         "r"(tile), "r"(mapa_shared(smem_u32(&rfull[slot]), 1))
-                         : "memory");
-          }
+          publish(it, tile);
         } else {
           mbar_arrive_expect_tx(&rfull[it % kRing], 4);  // the peer's one arrival; the leader's st.async the bytes
           tile = ring_get(it);
