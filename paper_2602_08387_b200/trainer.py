@@ -252,7 +252,9 @@ class SPMDTrainer:
                     tps = B * T / dt
                     rec = {"step": g, "loss": losses[-1], "step_ms": round(dt * 1e3, 3),
                            "tokens_per_s_per_gpu": round(tps, 1),
-                           "mfu": round(tps * cfg.flops_per_token(T) / BF16_PEAK_FLOPS, 4),
+                           # 4 significant digits (a tiny model's first, eager / capturing steps
+                           # are below 1e-4 MFU and would round to 0)
+                           "mfu": float(f"{tps * cfg.flops_per_token(T) / BF16_PEAK_FLOPS:.4g}"),
                            "lr": self.opt_cfg.lr_at(g + 1), "world": self.world}
                     if self.world > 1:
                         rec.update(ag_bytes=self.engine.bytes_ag, rs_bytes=self.engine.bytes_rs)
