@@ -1,5 +1,6 @@
 # GEMM tile indices published one tile ahead (-DB2S_GEMM_PUBLISH_AHEAD) vs the default build (st.async
 # publication at the tile boundary): wait accounting, GEMM parity, shape timings, step A/B via B2S_LIB
+# (the B2S_GEMM_PUBLISH_AHEAD #ifdef was removed after this measurement)
 O=gpurun_out/r2ahead; mkdir -p $O
 for v in staprof aheadprof; do
   timeout 300 env B2S_LIB=paper_2602_08387_b200/csrc/build/var_$v/libb2s.so python tools/gemm_prof.py 16384 3072 768 16384 8192 2048 2>&1 | sed "s/^/$v /"
